@@ -1,0 +1,232 @@
+/*
+ * rnn.h -- C ABI of librnn.so, the B200-native lifted join-aggregate (LJA) of RelaNN's
+ * Neuro-Relational Algebra (arxiv 2605.24207; PAPER.md = /root/reference/PAPER.md).
+ *
+ * The LJA is the NRA expression a join rule compiles to (sec 3.1):
+ *
+ *     Out(t; alpha(c(z_s, z_e, z_t))) :- E(s, t; z_e), S(s; z_s), T(t; z_t)
+ *     ==  U_{alpha,t}( T_c( E |><| S |><| T ) )
+ *
+ * - E is the edge / incidence relation (n_edge_rows tuples, content (s, t)), S the gathered
+ *   "source" relation keyed by s, T the group-side relation keyed by t.  Each relation is a
+ *   set: duplicate keys in S or T are an error.  Rows of E whose s (or t) has
+ *   no partner are dropped (natural join).
+ * - The join pairs tuples and concatenates embeddings; the combine c is
+ *   the per-row transformation T_tau; the projected union groups by t and
+ *   aggregates the multiset once.
+ * - The paper's physical plan realises this with cuDF merge/groupby index tensors,
+ *   torch.index_select and torch_scatter (Fig. 3); this library replaces
+ *   them with a key-grouped CSR join index (built once and reused -- "content caching") and
+ *   fused gather-combine-reduce kernels, forward and backward (gradients flow through
+ *   embeddings only).
+ *
+ * Conventions (apply to every entry point):
+ * - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA memory) unless noted.
+ * - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All calls are
+ *   asynchronous on `stream` except those marked SYNC.
+ * - Ownership: the caller allocates and owns every buffer, including scratch `workspace`
+ *   sized by a query; the library never allocates device memory and keeps no global state
+ *   besides a thread-local error string.  Inputs are never written.  Outputs must not alias
+ *   inputs.  A workspace must not be shared by concurrent calls.
+ * - Errors: every function returns rnn_status; nothing throws across the ABI.  Host-side
+ *   argument checks are always on.  On error, rnn_last_error() describes it (thread-local,
+ *   valid until the next call on the thread).  CUDA launch failures map to RNN_ERR_CUDA.
+ * - Embedding operands are fp32, row-major, leading dimension `ld` in elements with
+ *   ld % 4 == 0 and a 16-byte aligned base (128-bit loads); 1 <= dim <= 512.
+ * - Keys are signed int64 (any value).  Row ids are int32 (relations < 2^31 rows); join-row
+ *   counts and CSR pointers are int64.
+ * - Determinism: identical inputs give bit-identical outputs (no floating-point atomics on
+ *   any path; every reduction has a fixed order).
+ */
+#ifndef RNN_H
+#define RNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RNN_ABI_VERSION 1
+
+typedef enum {
+  RNN_OK = 0,
+  RNN_ERR_INVALID_ARGUMENT = 1,   /* null/misaligned pointer, bad size or flag            */
+  RNN_ERR_SHAPE_MISMATCH = 2,     /* operand widths inconsistent      */
+  RNN_ERR_INDEX_OUT_OF_RANGE = 3, /* device-side validation found an index out of range  */
+  RNN_ERR_DUPLICATE_KEY = 4,      /* S or T is not a set                   */
+  RNN_ERR_UNSUPPORTED = 5,        /* valid request outside this build's limits            */
+  RNN_ERR_WORKSPACE_TOO_SMALL = 6,
+  RNN_ERR_CUDA = 7                /* a CUDA runtime call failed (detail in last error)    */
+} rnn_status;
+
+const char* rnn_status_string(rnn_status s); /* static string, never NULL */
+const char* rnn_last_error(void);            /* thread-local detail, never NULL */
+int rnn_abi_version(void);
+
+/* ===================================================================================== */
+/* A1. Join index (replaces cuDF merge + groupby)                    */
+/* ===================================================================================== */
+
+/* Key-grouped CSR of the join rows.  POD; every array is CALLER-owned device memory and is
+ * immutable once built, so one index is reused across iterations and streams.
+ *   Group-major order: join rows sorted by (group, edge row) -- or (group, S key, edge row)
+ *   with RNN_IDX_WITHIN_GROUP_BY_SRC_KEY (DHN adjacency lists).  Groups are the distinct t of
+ *   the join rows in ascending signed order (compact output: absent keys have no group).
+ *   Source-major order: positions p sorted by (src_row[p], p).
+ *   Work schedules: contiguous ranges of positions, each either a run of whole segments
+ *   (total <= 2 * rows_per_item rows) or one piece (<= rows_per_item rows) of a longer
+ *   segment; they load-balance the kernels over power-law degree skew.                   */
+typedef struct {
+  int64_t n_edge_rows, n_join_rows, n_groups, n_src_rows, n_dst_rows;
+  int64_t* group_ptr;     /* [G+1]  rows of group g are positions [group_ptr[g], group_ptr[g+1])  */
+  int64_t* group_key;     /* [G]    t key of group g, strictly ascending                          */
+  int32_t* group_dst_row; /* [G]    row of T holding key group_key[g] (-1 when T absent)          */
+  int32_t* src_row;       /* [E']   S row of join row p (-1 when S absent)                        */
+  int32_t* edge_row;      /* [E']   E row of join row p                                           */
+  int64_t* src_ptr;       /* [n_src+1] source-major CSR over all S rows (empty rows included)     */
+  int32_t* src_pos;       /* [E']   group-major position of the q-th source-major entry           */
+  int32_t* src_group;     /* [E']   group of position src_pos[q]                                  */
+  int64_t n_work;         /* number of group-major work items                                     */
+  int64_t* work_ptr;      /* [n_work+1] item boundaries (positions)                               */
+  int64_t n_src_work;     /* number of source-major work items                                    */
+  int64_t* src_work_ptr;  /* [n_src_work+1]                                                       */
+} rnn_join_index;
+
+enum {
+  RNN_IDX_VALIDATE = 1,                /* check S/T duplicate keys (RNN_ERR_DUPLICATE_KEY)      */
+  RNN_IDX_WITHIN_GROUP_BY_SRC_KEY = 2, /* DHN adjacency variant (needs S and T)                 */
+  RNN_IDX_NO_TRANSPOSE = 4             /* skip src_ptr/src_pos/src_group/src_work_ptr           */
+};
+
+/* Build the canonical join index of E(s,t) |><| S(s) |><| T(t) grouped by t.
+ *   e_src_key[n_edge_rows], e_dst_key[n_edge_rows] : content columns of E (device).
+ *   src_key[n_src] : keys of S, row i <-> embedding row i; NULL => S absent (every E row is
+ *                    a join row w.r.t. s and src_row = -1).
+ *   dst_key[n_dst] : keys of T; NULL => T absent (groups = distinct e_dst_key).
+ *   rows_per_item  : work-schedule granularity (0 => 32).
+ * Two phases (SYNC in phase 1):
+ *   (1) idx->group_ptr == NULL: computes idx->n_join_rows, idx->n_groups, idx->n_work,
+ *       idx->n_src_work and the other counts, and *workspace_bytes; blocks on `stream`.
+ *       If workspace == NULL only *workspace_bytes is set (host-only query, no device work).
+ *   (2) with every array allocated to those sizes: fills them.  Deterministic: the same
+ *       inputs give identical bytes.  Duplicate S/T keys are always detected in phase 1. */
+rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64_t* e_dst_key,
+                                int64_t n_edge_rows, const int64_t* src_key, int64_t n_src,
+                                const int64_t* dst_key, int64_t n_dst, int flags,
+                                int64_t rows_per_item, rnn_join_index* idx, void* workspace,
+                                size_t* workspace_bytes, void* stream);
+
+/* ===================================================================================== */
+/* A3/A4. Fused gather - combine - segmented reduce, forward                             */
+/* ===================================================================================== */
+
+typedef enum { RNN_AGG_SUM = 0, RNN_AGG_MEAN = 1, RNN_AGG_SOFTMAX = 2 } rnn_agg;
+typedef enum {
+  RNN_COMBINE_SRC = 0,   /* w * z_s ; w = scalar edge operand (dim 1) or 1 (GCN norm, a*v)  */
+  RNN_COMBINE_MUL = 1,   /* z_s (.) z_e (.) z_t of the present operands (q*k, DHN product)  */
+  RNN_COMBINE_ADD = 2,   /* z_s + z_e + z_t of the present operands ("+ z3")   */
+  RNN_COMBINE_CONCAT = 3 /* z_s (+) z_e (+) z_t (join default)               */
+} rnn_combine;
+
+/* An embedding operand.  data == NULL => absent.
+ * mode RNN_BY_ROW: src rows via src_row[p], edge rows via edge_row[p], dst rows via
+ *                  group_dst_row[g];  mode RNN_BY_POSITION: edge row = join position p,
+ *                  dst row = group id g (src operands must use RNN_BY_ROW).
+ * A dim-1 edge operand broadcasts as a scalar (per-row weight). */
+enum { RNN_BY_ROW = 0, RNN_BY_POSITION = 1 };
+typedef struct {
+  const float* data;
+  int64_t ld;
+  int32_t dim;
+  int32_t mode;
+} rnn_operand;
+
+typedef struct {
+  rnn_combine combine;
+  rnn_agg agg;
+  int32_t heads;   /* SOFTMAX: number of heads h (dim/h in {4,8,16,32,64}); else 1          */
+  float scale;     /* SOFTMAX: score scale (e.g. mu / sqrt(d/h)); else ignored               */
+  rnn_operand src;     /* gathered by src_row: values                                         */
+  rnn_operand src_key; /* SOFTMAX: keys gathered by src_row                                   */
+  rnn_operand edge;    /* gathered by edge_row (or position): edge embedding or scalar weight */
+  rnn_operand dst;     /* per group via group_dst_row (or g): group-side factor / queries     */
+} rnn_lifted_query;
+
+/* Supported (combine, agg) in this build:
+ *   SUM/MEAN x {SRC (edge dim 1 or absent, no dst), MUL, ADD (dims equal, edge may be 1),
+ *               CONCAT (total width <= 512)};
+ *   SOFTMAX with combine SRC: src/src_key/dst present, edge absent, dim <= 128.
+ * out[G, ld_out]: row g = aggregate of group g.  beta = 0 overwrites, beta = 1 accumulates
+ * (union over relations, PAPER.md:451-460 / HGT H_tilda sum over phi; SUM/SOFTMAX only).
+ * lse[G, heads] (SOFTMAX only, required there): log-sum-exp per group and head, saved for
+ * the backward.  workspace: partial states of split groups; size via rnn_lja_workspace_size. */
+rnn_status rnn_lja_workspace_size(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                  size_t* fwd_bytes, size_t* bwd_bytes);
+rnn_status rnn_join_aggregate_fwd(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                  float* out, int64_t ld_out, float beta, float* lse,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* ===================================================================================== */
+/* A5. Backward                                                                          */
+/* ===================================================================================== */
+/* Gradients are WRITTEN (not accumulated) into dense full-relation buffers with ld = dim:
+ *   d_src[n_src_rows, src.dim], d_src_key[n_src_rows, src_key.dim],
+ *   d_edge[(n_edge_rows or E' for RNN_BY_POSITION), edge.dim],
+ *   d_dst[(n_dst_rows or G), dst.dim].  Any may be NULL (not computed).  Rows never
+ *   referenced by a join row get 0.  out/lse are the forward's outputs (SOFTMAX only).
+ * The source-major pass uses the transposed CSR (no atomics); d_src requires it. */
+rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                  const float* out, int64_t ld_out, const float* lse,
+                                  const float* d_out, int64_t ld_dout, float* d_src,
+                                  float* d_src_key, float* d_edge, float* d_dst,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* Standalone grouped softmax over materialised scores [E', heads] in group-major order (the
+ * ATT relation of Fig. 4), and its backward ds = p (dp - sum_q p dp). */
+rnn_status rnn_group_softmax(const rnn_join_index* idx, const float* scores, int32_t heads,
+                             float* probs, void* stream);
+rnn_status rnn_group_softmax_bwd(const rnn_join_index* idx, const float* probs,
+                                 const float* d_probs, int32_t heads, float* d_scores,
+                                 void* stream);
+
+/* ===================================================================================== */
+/* A2. Dense per-relation projection on tcgen05 tensor cores                             */
+/* ===================================================================================== */
+/* The transformation pushed below the join so it runs once per node, not once per edge
+ * (PAPER.md:1032).  Y[M, N] = X[M, K] . W^T + b, W laid out [N, K] (torch.nn.Linear).
+ * X: ldx % 4 == 0; W: ldw % 4 == 0; Y: ldy % 4 == 0; 16-byte aligned; M < 2^31, K <= 8192,
+ * N <= 256.  Precision:
+ *   RNN_PREC_TF32   : one kind::tf32 MMA per tile (operands truncated to tf32).
+ *   RNN_PREC_3XTF32 : split-operand 3xTF32 (hi*hi + hi*lo + lo*hi), ~fp32 accuracy.
+ * Backward: dX = dY . W (may be NULL), dW = dY^T . X (required), db = colsum(dY) (may be NULL),
+ * all written.  workspace: dW partials (deterministic split-M reduction). */
+typedef enum { RNN_PREC_TF32 = 0, RNN_PREC_3XTF32 = 1 } rnn_precision;
+rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t ldx, const float* W,
+                       int32_t N, int64_t ldw, const float* bias, float* Y, int64_t ldy,
+                       rnn_precision prec, void* stream);
+rnn_status rnn_project_bwd_workspace_size(int64_t M, int32_t K, int32_t N, size_t* bytes);
+rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, const float* W,
+                           int32_t N, int64_t ldw, const float* dY, int64_t lddy, float* dX,
+                           int64_t lddx, float* dW, float* db, rnn_precision prec,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* ===================================================================================== */
+/* Program helpers                                                                       */
+/* ===================================================================================== */
+/* GCN normalisation as a per-join-position weight (use with RNN_BY_POSITION):
+ * w[p] = deg(s_p)^-1/2 * deg(t_g)^-1/2 with deg = group size of the node (in-degree of the
+ * self-looped edge relation, PyG gcn_norm reading).  S and T must be the same node relation
+ * (n_src_rows == n_dst_rows). */
+rnn_status rnn_gcn_norm(const rnn_join_index* idx, float* w, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* Multi-GPU ownership of group keys: owner[i] = splitmix64(keys[i] ^ seed) mod P. */
+rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed,
+                              int32_t* owner, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNN_H */

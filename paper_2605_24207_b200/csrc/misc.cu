@@ -1,0 +1,76 @@
+// misc.cu -- program helpers: GCN normalisation weights and the multi-GPU hash partition.
+#include "common.cuh"
+
+namespace rnn {
+namespace {
+
+__global__ void deg_kernel(const int64_t* __restrict__ gp, const int32_t* __restrict__ dst_row,
+                           int64_t G, int32_t* deg, int* bad) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  const int32_t r = dst_row[g];
+  if (r < 0) { *bad = 1; return; }
+  deg[r] = (int32_t)(gp[g + 1] - gp[g]);
+}
+
+// w[p] = deg(s_p)^-1/2 deg(t_g)^-1/2 ; warp per group
+__global__ void norm_kernel(const int64_t* __restrict__ gp, const int32_t* __restrict__ src_row,
+                            int64_t G, const int32_t* __restrict__ deg, float* __restrict__ w) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= G) return;
+  const int64_t b = gp[g], e = gp[g + 1];
+  const float rt = 1.f / sqrtf((float)(e - b));
+  for (int64_t p = b + (threadIdx.x & 31); p < e; p += 32) {
+    const int32_t ds = deg[src_row[p]];
+    w[p] = ds > 0 ? rt * (1.f / sqrtf((float)ds)) : 0.f;
+  }
+}
+
+__global__ void partition_kernel(const int64_t* __restrict__ keys, int64_t n, uint32_t P,
+                                 uint64_t seed, int32_t* __restrict__ owner) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) owner[i] = (int32_t)(splitmix64((uint64_t)keys[i] ^ seed) % P);
+}
+
+}  // namespace
+}  // namespace rnn
+
+using namespace rnn;
+
+extern "C" rnn_status rnn_gcn_norm(const rnn_join_index* idx, float* w, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(idx && idx->group_ptr, RNN_ERR_INVALID_ARGUMENT, "index required");
+  RNN_REQUIRE(idx->n_src_rows == idx->n_dst_rows && idx->n_src_rows > 0, RNN_ERR_INVALID_ARGUMENT,
+              "GCN normalisation needs S and T to be the same node relation");
+  const size_t need = sizeof(int32_t) * (size_t)idx->n_dst_rows + 256;
+  if (!workspace) {
+    RNN_REQUIRE(workspace_bytes == 0, RNN_ERR_INVALID_ARGUMENT, "workspace NULL");
+  }
+  RNN_REQUIRE(workspace && workspace_bytes >= need, RNN_ERR_WORKSPACE_TOO_SMALL,
+              "workspace needs %zu bytes", need);
+  RNN_REQUIRE(w || idx->n_join_rows == 0, RNN_ERR_INVALID_ARGUMENT, "w required");
+  cudaStream_t st = as_stream(stream);
+  int32_t* deg = static_cast<int32_t*>(workspace);
+  int* bad = reinterpret_cast<int*>(static_cast<char*>(workspace) + need - 256);
+  RNN_CUDA(cudaMemsetAsync(workspace, 0, need, st));
+  const int64_t G = idx->n_groups;
+  if (G == 0) return RNN_OK;
+  deg_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(idx->group_ptr, idx->group_dst_row, G,
+                                                          deg, bad);
+  norm_kernel<<<(unsigned)ceil_div(G, 8), 256, 0, st>>>(idx->group_ptr, idx->src_row, G, deg, w);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed,
+                                         int32_t* owner, void* stream) {
+  clear_error();
+  RNN_REQUIRE(P >= 1 && n >= 0 && (n == 0 || (keys && owner)), RNN_ERR_INVALID_ARGUMENT,
+              "bad argument");
+  if (n == 0) return RNN_OK;
+  partition_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(keys, n, (uint32_t)P,
+                                                                              seed, owner);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}

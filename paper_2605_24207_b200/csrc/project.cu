@@ -1,0 +1,587 @@
+// project.cu -- A2: the dense per-relation projection Y = X W^T + b on tcgen05 tensor cores.
+//
+// This is the transformation T_tau pushed below the join so it runs once per node instead of
+// once per edge (the paper's physical plan applies nn.Linear).
+//
+// Kernel anatomy (one 128-row output tile per CTA, 192 threads, warp-specialised):
+//   warp 0      : TMA producer -- cp.async.bulk.tensor 2D boxes into a STAGES-deep ring of
+//                 128B-swizzled shared-memory tiles, signalling `full` mbarriers (complete_tx).
+//   warp 1      : allocates TMEM, one elected lane issues tcgen05.mma.kind::tf32 (M=128,
+//                 N=BN, K=8 per instruction) from smem descriptors, accumulating in TMEM;
+//                 tcgen05.commit frees each stage (`empty`) and finally signals `acc_full`.
+//   warps 2..5  : 3xTF32 only: split every landed tile into hi = tf32(x) and lo = x - hi
+//                 (so the MMA computes hi*hi + hi*lo + lo*hi ~ fp32 accuracy); then the
+//                 epilogue: tcgen05.ld 32x32b TMEM -> registers, + bias, store.
+// Operands may be K-major (row-major [rows, K]) or MN-major (row-major [K, rows]) -- the
+// latter gives dW = dY^T X without materialising transposes (smem descriptor major bit).
+// Split-K over z with partial tiles reduced in a fixed order keeps dW deterministic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace rnn {
+namespace {
+
+constexpr int BM = 128;   // UMMA_M (cta_group::1): accumulator row i <-> TMEM lane i
+constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row
+constexpr int THREADS = 192;
+constexpr int MAX_STAGES = 4;
+
+struct GemmParams {
+  int64_t M;        // output rows
+  int N;            // output cols
+  int BN;           // tile cols (multiple of 16 (K-major B) or 32 (MN-major B))
+  int64_t Kred;     // reduction length
+  int64_t k_split;  // reduction elements per blockIdx.z (multiple of BK)
+  int stages;
+  float* out; int64_t ldo;
+  const float* bias;
+  int mode;         // 0: out = acc + bias ; 1: partial[z] = acc
+  float* partial; int64_t ldp; int64_t part_stride;
+  uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor (sm_100 version bits = 1).
+//  K-major : SWIZZLE_128B (layout type 2): 8-row x 128B atoms stacked every 1024B (SBO); the
+//            K step of 8 tf32 elements is a 32-byte advance of the start address.
+//  MN-major: tf32 (32-bit) MN-major operands only support SWIZZLE_128B_BASE32B (layout type
+//            1): atoms of 32 MN elements (128B) x 4 K-rows with 32-byte chunks swizzled by
+//            the K row (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B); 32-wide MN chunks every
+//            `lbo` bytes (LBO), 4-row K groups every 512B (SBO); the K step of 8 rows is a
+//            1024-byte advance.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, bool mn_major, int kk, uint32_t lbo) {
+  const uint32_t start = saddr + (mn_major ? kk * 1024u : kk * 32u);
+  const uint64_t LBO = mn_major ? (lbo >> 4) : 1u;
+  const uint64_t SBO = mn_major ? (512u >> 4) : (1024u >> 4);
+  const uint64_t layout = mn_major ? 1ull : 2ull;
+  return (uint64_t)((start >> 4) & 0x3FFFu) | ((LBO & 0x3FFFull) << 16) |
+         ((SBO & 0x3FFFull) << 32) | (1ull << 46) | (layout << 61);
+}
+
+// Instruction descriptor for kind::tf32: D=F32, A=B=TF32, M=128, N=bn.
+__device__ __forceinline__ uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+template <bool A_MN, bool B_MN, bool SPLIT3>
+__global__ void __launch_bounds__(THREADS, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                   GemmParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte align the carve (swizzle atoms)
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t A_BYTES = BM * BK * 4;
+  const uint32_t B_BYTES = (uint32_t)p.BN * BK * 4;
+  const uint32_t STAGE = (A_BYTES + B_BYTES) * (SPLIT3 ? 2u : 1u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE);
+  uint64_t* empty = full + MAX_STAGES;
+  uint64_t* conv = empty + MAX_STAGES;
+  uint64_t* acc_full = conv + MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * p.BN;
+  const int64_t kbeg = (int64_t)blockIdx.z * p.k_split;
+  const int64_t kend = kbeg + p.k_split < p.Kred ? kbeg + p.k_split : p.Kred;
+  const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < MAX_STAGES; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], 1);
+        mbar_init(&conv[s], 128);
+      }
+      mbar_init(acc_full, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto a_hi = [&](int s) { return smem + s * STAGE; };
+  auto b_hi = [&](int s) { return smem + s * STAGE + A_BYTES; };
+  auto a_lo = [&](int s) { return smem + s * STAGE + A_BYTES + B_BYTES; };
+  auto b_lo = [&](int s) { return smem + s * STAGE + 2 * A_BYTES + B_BYTES; };
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % p.stages;
+        const uint32_t ph = (kb / p.stages) & 1;
+        if (kb >= p.stages) mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        const int k = (int)(kbeg + (int64_t)kb * BK);
+        if (!A_MN) {
+          tma_load_2d(&ta, a_hi(s), &full[s], k, (int)m0);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BM / 32; ++j)
+            tma_load_2d(&ta, a_hi(s) + j * 4096, &full[s], (int)m0 + 32 * j, k);
+        }
+        if (!B_MN) {
+          tma_load_2d(&tb, b_hi(s), &full[s], k, n0);
+        } else {
+          for (int j = 0; j < p.BN / 32; ++j)
+            tma_load_2d(&tb, b_hi(s) + j * 4096, &full[s], n0 + 32 * j, k);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = make_idesc(p.BN, A_MN, B_MN);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % p.stages;
+      const uint32_t ph = (kb / p.stages) & 1;
+      mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+      tc_fence_after();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t ad = make_desc(smem_u32(a_hi(s)), A_MN, kk, 4096);
+          const uint64_t bd = make_desc(smem_u32(b_hi(s)), B_MN, kk, 4096);
+          tc_mma_tf32(tmem, ad, bd, idesc, (kb | kk) != 0);
+          if (SPLIT3) {
+            const uint64_t al = make_desc(smem_u32(a_lo(s)), A_MN, kk, 4096);
+            const uint64_t bl = make_desc(smem_u32(b_lo(s)), B_MN, kk, 4096);
+            tc_mma_tf32(tmem, ad, bl, idesc, 1u);
+            tc_mma_tf32(tmem, al, bd, idesc, 1u);
+          }
+        }
+        tc_commit(&empty[s]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) tc_commit(acc_full);
+    __syncwarp();
+  } else {
+    // ---------------- converters (3xTF32) + epilogue: warps 2..5 ----------------
+    const int et = threadIdx.x - 64;  // 0..127
+    if (SPLIT3) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % p.stages;
+        const uint32_t ph = (kb / p.stages) & 1;
+        mbar_wait(&full[s], ph);
+        float4* ah = reinterpret_cast<float4*>(a_hi(s));
+        float4* al = reinterpret_cast<float4*>(a_lo(s));
+        for (uint32_t i = et; i < A_BYTES / 16; i += 128) {
+          float4 x = ah[i], h, l;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
+          ah[i] = h; al[i] = l;
+        }
+        float4* bh = reinterpret_cast<float4*>(b_hi(s));
+        float4* bl = reinterpret_cast<float4*>(b_lo(s));
+        for (uint32_t i = et; i < B_BYTES / 16; i += 128) {
+          float4 x = bh[i], h, l;
+          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
+          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
+          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
+          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
+          bh[i] = h; bl[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&conv[s]);
+      }
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) belong to this warp
+    const int64_t row = m0 + quad * 32 + lane;
+    const bool row_ok = row < p.M;
+    for (int c0 = 0; c0 < p.BN; c0 += 16) {
+      uint32_t r[16];
+      tc_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, r);
+      if (!row_ok) continue;
+      const int col0 = n0 + c0;
+      if (p.mode == 0) {
+        float* dst = p.out + row * p.ldo + col0;
+        const bool vec = col0 + 16 <= p.N && (p.ldo % 4 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          v[j] = __uint_as_float(r[j]) + ((p.bias && col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f);
+        if (vec) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (col0 + j < p.N) dst[j] = v[j];
+        }
+      } else {
+        float* dst = p.partial + blockIdx.z * p.part_stride + row * p.ldp + col0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (col0 + j < p.N) dst[j] = __uint_as_float(r[j]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(p.tmem_cols));
+  }
+}
+
+// out[r, c] = sum_z partial[z, r, c]   (fixed order => deterministic split-K)
+__global__ void splitk_reduce(const float* __restrict__ part, int64_t splits, int64_t stride,
+                              int64_t rows, int cols, int64_t ldp, float* __restrict__ out,
+                              int64_t ldo) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i / cols;
+  const int c = (int)(i % cols);
+  float acc = 0.f;
+  for (int64_t z = 0; z < splits; ++z) acc += part[z * stride + r * ldp + c];
+  out[r * ldo + c] = acc;
+}
+
+// column sums db[c] = sum_m dY[m, c]: stage 1 (per row-chunk partials), stage 2 (ordered sum)
+__global__ void colsum_partial(const float* __restrict__ Y, int64_t M, int N, int64_t ld,
+                               int64_t rows_per, float* __restrict__ part) {
+  const int c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int w = threadIdx.x >> 5;  // 8 warps
+  __shared__ float red[8][32];
+  const int64_t r0 = blockIdx.y * rows_per;
+  const int64_t r1 = r0 + rows_per < M ? r0 + rows_per : M;
+  float acc = 0.f;
+  if (c < N)
+    for (int64_t r = r0 + w; r < r1; r += 8) acc += Y[r * ld + c];
+  red[w][threadIdx.x & 31] = acc;
+  __syncthreads();
+  if (w == 0) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x & 31];
+    if (c < N) part[blockIdx.y * (int64_t)N + c] = s;
+  }
+}
+__global__ void colsum_final(const float* __restrict__ part, int64_t chunks, int N,
+                             float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= N) return;
+  float s = 0.f;
+  for (int64_t k = 0; k < chunks; ++k) s += part[k * N + c];
+  out[c] = s;
+}
+
+__global__ void transpose_kernel(const float* __restrict__ W, int N, int K, int64_t ldw,
+                                 float* __restrict__ Wt, int64_t ldt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)N * K) return;
+  const int n = (int)(i / K), k = (int)(i % K);
+  Wt[(int64_t)k * ldt + n] = W[(int64_t)n * ldw + k];
+}
+
+// ------------------------------------------------------------------------------------------
+// host side
+// ------------------------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2D fp32 tensor [rows, inner] with row stride ld (elements); box {box_inner, box_rows}
+rnn_status make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t rows, int64_t ld,
+                    uint32_t box_inner, uint32_t box_rows, bool mn_major = false) {
+  auto fn = encode_fn();
+  RNN_REQUIRE(fn, RNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  RNN_REQUIRE(aligned16(base) && (ld * 4) % 16 == 0, RNN_ERR_INVALID_ARGUMENT,
+              "TMA operands need a 16-byte aligned base and ld %% 4 == 0");
+  cuuint64_t dims[2] = {(cuuint64_t)(inner > 0 ? inner : 1), (cuuint64_t)(rows > 0 ? rows : 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RNN_REQUIRE(r == CUDA_SUCCESS, RNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return RNN_OK;
+}
+
+uint32_t pow2_cols(int bn) {
+  uint32_t c = 32;
+  while ((int)c < bn) c <<= 1;
+  return c;
+}
+
+template <bool A_MN, bool B_MN, bool SPLIT3>
+rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int splits,
+                       cudaStream_t st) {
+  const uint32_t stage = (uint32_t)(BM * BK * 4 + p.BN * BK * 4) * (SPLIT3 ? 2u : 1u);
+  const int64_t nkb_max = ceil_div(p.k_split, BK);
+  int stages = (int)((200 * 1024) / stage);
+  if (!SPLIT3 && stages > 3 && stage * 3 <= 100 * 1024) stages = 3;  // 2 CTAs / SM
+  if (stages > MAX_STAGES) stages = MAX_STAGES;
+  if (stages > nkb_max) stages = (int)nkb_max;
+  if (stages < 1) stages = 1;
+  p.stages = stages;
+  p.tmem_cols = pow2_cols(p.BN);
+  const size_t smem = (size_t)stages * stage + 1024 + 8 * (3 * MAX_STAGES + 2) + 64;
+  auto kern = tc_gemm_kernel<A_MN, B_MN, SPLIT3>;
+  RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)ceil_div(p.M, BM), (unsigned)ceil_div(p.N, p.BN), (unsigned)splits);
+  kern<<<grid, THREADS, smem, st>>>(ta, tb, p);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+template <bool A_MN, bool B_MN>
+rnn_status gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits,
+                rnn_precision prec, cudaStream_t st) {
+  if (prec == RNN_PREC_3XTF32) return launch_gemm<A_MN, B_MN, true>(ta, tb, p, splits, st);
+  return launch_gemm<A_MN, B_MN, false>(ta, tb, p, splits, st);
+}
+
+__global__ void bias_fill(float* Y, int64_t M, int N, int64_t ldy, const float* b) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < M * N) Y[(i / N) * ldy + i % N] = b ? b[i % N] : 0.f;
+}
+
+// Y[M, N] = A[M, Kred] B[N, Kred]^T (+bias), both K-major
+rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const float* B, int N,
+                   int64_t ldb, const float* bias, float* Y, int64_t ldy, rnn_precision prec,
+                   cudaStream_t st) {
+  if (M == 0 || N == 0) return RNN_OK;
+  if (Kred == 0) {
+    bias_fill<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(Y, M, N, ldy, bias);
+    RNN_LAUNCH_CHECK();
+    return RNN_OK;
+  }
+  GemmParams p{};
+  p.M = M; p.N = N;
+  p.BN = N <= 256 ? (int)((N + 15) / 16 * 16) : 256;
+  p.Kred = Kred; p.k_split = ceil_div(Kred, BK) * BK;
+  p.out = Y; p.ldo = ldy; p.bias = bias; p.mode = 0;
+  CUtensorMap ta, tb;
+  RNN_TRY(make_map(&ta, A, Kred, M, lda, BK, BM));
+  RNN_TRY(make_map(&tb, B, Kred, N, ldb, BK, (uint32_t)p.BN));
+  return gemm<false, false>(ta, tb, p, 1, prec, st);
+}
+
+}  // namespace
+}  // namespace rnn
+
+using namespace rnn;
+
+extern "C" rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t ldx,
+                                  const float* W, int32_t N, int64_t ldw, const float* bias,
+                                  float* Y, int64_t ldy, rnn_precision prec, void* stream) {
+  clear_error();
+  RNN_REQUIRE(X && W && Y, RNN_ERR_INVALID_ARGUMENT, "X, W, Y required");
+  RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 0 && K <= 8192 && N >= 1 && N <= 256,
+              RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, K <= 8192, 1 <= N <= 256");
+  RNN_REQUIRE(ldx >= K && ldw >= K && ldy >= N, RNN_ERR_INVALID_ARGUMENT, "ld too small");
+  RNN_REQUIRE(prec == RNN_PREC_TF32 || prec == RNN_PREC_3XTF32, RNN_ERR_INVALID_ARGUMENT,
+              "precision");
+  return gemm_kk(X, M, K, ldx, W, N, ldw, bias, Y, ldy, prec, as_stream(stream));
+}
+
+namespace {
+struct BwdWs {
+  float* Wt; float* part; float* cpart;
+  size_t bytes;
+  int splits; int64_t chunks;
+};
+BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
+  BwdWs w{};
+  Carve c(base);
+  const int64_t ldt = (N + 3) / 4 * 4;
+  w.Wt = c.take<float>((size_t)K * ldt);
+  const int64_t tiles = ceil_div(N, BM) * ceil_div(K, 256);
+  int64_t splits = ceil_div(M, 8 * BK);
+  const int64_t cap = (2 * 148 + tiles - 1) / tiles;
+  if (splits > cap) splits = cap;
+  if (splits < 1) splits = 1;
+  w.splits = (int)splits;
+  w.part = c.take<float>((size_t)splits * N * K);
+  w.chunks = ceil_div(M > 0 ? M : 1, 4096);
+  w.cpart = c.take<float>((size_t)w.chunks * N);
+  w.bytes = c.used + 1024;
+  return w;
+}
+}  // namespace
+
+extern "C" rnn_status rnn_project_bwd_workspace_size(int64_t M, int32_t K, int32_t N,
+                                                     size_t* bytes) {
+  clear_error();
+  RNN_REQUIRE(bytes && M >= 0 && K >= 0 && N >= 1, RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  *bytes = bwd_ws(M, K, N, nullptr).bytes;
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx,
+                                      const float* W, int32_t N, int64_t ldw, const float* dY,
+                                      int64_t lddy, float* dX, int64_t lddx, float* dW, float* db,
+                                      rnn_precision prec, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(X && W && dY && dW, RNN_ERR_INVALID_ARGUMENT, "X, W, dY, dW required");
+  RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 1 && K <= 8192 && N >= 1 && N <= 256,
+              RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, 1 <= K <= 8192, 1 <= N <= 256");
+  RNN_REQUIRE(ldx >= K && ldw >= K && lddy >= N && (!dX || lddx >= K), RNN_ERR_INVALID_ARGUMENT,
+              "ld too small");
+  cudaStream_t st = as_stream(stream);
+  BwdWs w = bwd_ws(M, K, N, workspace);
+  RNN_REQUIRE(workspace && workspace_bytes >= w.bytes, RNN_ERR_WORKSPACE_TOO_SMALL,
+              "workspace %zu < %zu bytes", workspace_bytes, w.bytes);
+  const int64_t ldt = (N + 3) / 4 * 4;
+  // dX = dY W : K-major A = dY [M, N], K-major B = W^T [K, N]
+  if (dX) {
+    transpose_kernel<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, st>>>(W, N, K, ldw, w.Wt,
+                                                                             ldt);
+    RNN_LAUNCH_CHECK();
+    RNN_TRY(gemm_kk(dY, M, N, lddy, w.Wt, K, ldt, nullptr, dX, lddx, prec, st));
+  }
+  // dW = dY^T X : both operands MN-major, split over M, ordered reduction
+  if (M == 0) {
+    RNN_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * K, st));
+  } else {
+    GemmParams p{};
+    p.M = N; p.N = K;
+    p.BN = K <= 256 ? (int)((K + 31) / 32 * 32) : 256;
+    p.Kred = M;
+    p.k_split = ceil_div(ceil_div(M, w.splits), BK) * BK;
+    const int splits = (int)ceil_div(M, p.k_split);
+    p.mode = 1; p.partial = w.part; p.ldp = K; p.part_stride = (int64_t)N * K;
+    CUtensorMap ta, tb;
+    RNN_TRY(make_map(&ta, dY, N, M, lddy, 32, BK, true));
+    RNN_TRY(make_map(&tb, X, K, M, ldx, 32, BK, true));
+    RNN_TRY((gemm<true, true>(ta, tb, p, splits, prec, st)));
+    splitk_reduce<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, st>>>(
+        w.part, splits, p.part_stride, N, K, K, dW, K);
+    RNN_LAUNCH_CHECK();
+  }
+  if (db) {
+    if (M == 0) {
+      RNN_CUDA(cudaMemsetAsync(db, 0, sizeof(float) * N, st));
+    } else {
+      dim3 g1((unsigned)ceil_div(N, 32), (unsigned)w.chunks);
+      colsum_partial<<<g1, 256, 0, st>>>(dY, M, N, lddy, 4096, w.cpart);
+      colsum_final<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(w.cpart, w.chunks, N, db);
+      RNN_LAUNCH_CHECK();
+    }
+  }
+  return RNN_OK;
+}
+
+// Internal test hook (not part of include/rnn.h): C[M, N] = A . B with A given K-major
+// ([M, Kred] row-major) or MN-major ([Kred, M] row-major), likewise B ([N, Kred] or [Kred, N]).
+extern "C" rnn_status rnn_internal_gemm(int a_mn, int b_mn, const float* A, int64_t lda,
+                                        const float* B, int64_t ldb, int64_t M, int N,
+                                        int64_t Kred, float* Cout, int64_t ldc, int prec,
+                                        void* stream) {
+  clear_error();
+  GemmParams p{};
+  p.M = M; p.N = N;
+  p.BN = N <= 256 ? (int)((N + 31) / 32 * 32) : 256;
+  p.Kred = Kred; p.k_split = ceil_div(Kred, BK) * BK;
+  p.out = Cout; p.ldo = ldc; p.mode = 0;
+  CUtensorMap ta, tb;
+  if (a_mn) RNN_TRY(make_map(&ta, A, M, Kred, lda, 32, BK, true));
+  else RNN_TRY(make_map(&ta, A, Kred, M, lda, BK, BM));
+  if (b_mn) RNN_TRY(make_map(&tb, B, N, Kred, ldb, 32, BK, true));
+  else RNN_TRY(make_map(&tb, B, Kred, N, ldb, BK, (uint32_t)p.BN));
+  const rnn_precision pr = (rnn_precision)prec;
+  cudaStream_t st = as_stream(stream);
+  if (a_mn && b_mn) return gemm<true, true>(ta, tb, p, 1, pr, st);
+  if (a_mn) return gemm<true, false>(ta, tb, p, 1, pr, st);
+  if (b_mn) return gemm<false, true>(ta, tb, p, 1, pr, st);
+  return gemm<false, false>(ta, tb, p, 1, pr, st);
+}

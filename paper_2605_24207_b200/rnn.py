@@ -1,0 +1,365 @@
+"""Thin Python binding of librnn.so (include/rnn.h): argument marshalling only.
+
+Every step of the path runs in librnn.so's CUDA kernels; this module only turns torch CUDA
+tensors into (pointer, size, stride) arguments, allocates caller-owned outputs/workspaces
+with torch (PyTorch is device memory + streams here) and raises on a non-OK status.
+There is no CPU fallback: if the extension or a GPU is missing, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librnn.so")
+
+# enums (include/rnn.h)
+RNN_OK = 0
+AGG = {"sum": 0, "mean": 1, "softmax": 2}
+COMBINE = {"src": 0, "mul": 1, "add": 2, "concat": 3}
+BY_ROW, BY_POSITION = 0, 1
+IDX_VALIDATE, IDX_WITHIN_GROUP_BY_SRC_KEY, IDX_NO_TRANSPOSE = 1, 2, 4
+PREC = {"tf32": 0, "3xtf32": 1}
+
+
+class RnnError(RuntimeError):
+    def __init__(self, status: int, name: str, detail: str):
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+        self.name = name
+
+
+class JoinIndexC(C.Structure):
+    _fields_ = [("n_edge_rows", C.c_int64), ("n_join_rows", C.c_int64), ("n_groups", C.c_int64),
+                ("n_src_rows", C.c_int64), ("n_dst_rows", C.c_int64),
+                ("group_ptr", C.c_void_p), ("group_key", C.c_void_p),
+                ("group_dst_row", C.c_void_p), ("src_row", C.c_void_p), ("edge_row", C.c_void_p),
+                ("src_ptr", C.c_void_p), ("src_pos", C.c_void_p), ("src_group", C.c_void_p),
+                ("n_work", C.c_int64), ("work_ptr", C.c_void_p),
+                ("n_src_work", C.c_int64), ("src_work_ptr", C.c_void_p)]
+
+
+class OperandC(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("ld", C.c_int64), ("dim", C.c_int32), ("mode", C.c_int32)]
+
+
+class QueryC(C.Structure):
+    _fields_ = [("combine", C.c_int), ("agg", C.c_int), ("heads", C.c_int32), ("scale", C.c_float),
+                ("src", OperandC), ("src_key", OperandC), ("edge", OperandC), ("dst", OperandC)]
+
+
+_lib = None
+
+
+def lib():
+    """Load librnn.so (never builds implicitly; run __graft_entry__.build() first)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32, sz = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+        L.rnn_status_string.restype = C.c_char_p
+        L.rnn_status_string.argtypes = [C.c_int]
+        L.rnn_last_error.restype = C.c_char_p
+        L.rnn_abi_version.restype = C.c_int
+        L.rnn_build_join_index.argtypes = [vp, vp, i64, vp, i64, vp, i64, C.c_int, i64,
+                                           C.POINTER(JoinIndexC), vp, C.POINTER(sz), vp]
+        L.rnn_lja_workspace_size.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC),
+                                             C.POINTER(sz), C.POINTER(sz)]
+        L.rnn_join_aggregate_fwd.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp, i64,
+                                             C.c_float, vp, vp, sz, vp]
+        L.rnn_join_aggregate_bwd.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp, i64, vp,
+                                             vp, i64, vp, vp, vp, vp, vp, sz, vp]
+        L.rnn_group_softmax.argtypes = [C.POINTER(JoinIndexC), vp, i32, vp, vp]
+        L.rnn_group_softmax_bwd.argtypes = [C.POINTER(JoinIndexC), vp, vp, i32, vp, vp]
+        L.rnn_project.argtypes = [vp, i64, i32, i64, vp, i32, i64, vp, vp, i64, C.c_int, vp]
+        L.rnn_project_bwd_workspace_size.argtypes = [i64, i32, i32, C.POINTER(sz)]
+        L.rnn_project_bwd.argtypes = [vp, i64, i32, i64, vp, i32, i64, vp, i64, vp, i64, vp, vp,
+                                      C.c_int, vp, sz, vp]
+        L.rnn_gcn_norm.argtypes = [C.POINTER(JoinIndexC), vp, vp, sz, vp]
+        L.rnn_hash_partition.argtypes = [vp, i64, i32, C.c_uint64, vp, vp]
+        for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
+                  "rnn_join_aggregate_bwd", "rnn_group_softmax", "rnn_group_softmax_bwd",
+                  "rnn_project", "rnn_project_bwd_workspace_size", "rnn_project_bwd",
+                  "rnn_gcn_norm", "rnn_hash_partition"):
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != RNN_OK:
+        L = lib()
+        raise RnnError(st, L.rnn_status_string(st).decode(), L.rnn_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _cuda(t, dtype, name):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == dtype):
+        raise TypeError(f"{name} must be a CUDA {dtype} tensor")
+    return t
+
+
+def _ws(nbytes, device):
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+# ------------------------------------------------------------------------------------------
+# A1 join index
+# ------------------------------------------------------------------------------------------
+class JoinIndex:
+    """Key-grouped CSR of the join rows of E(s,t) |><| S(s) |><| T(t), grouped by t.
+
+    Immutable once built (content caching): reuse it for every iteration.  Arrays are torch
+    tensors owned by this object; ``c`` is the POD handed to the C ABI.
+    """
+
+    def __init__(self, c: JoinIndexC, arrays: dict):
+        self.c = c
+        self.arrays = arrays
+        for k, v in arrays.items():
+            setattr(self, k, v)
+
+    @property
+    def n_join_rows(self):
+        return self.c.n_join_rows
+
+    @property
+    def n_groups(self):
+        return self.c.n_groups
+
+    @property
+    def n_src_rows(self):
+        return self.c.n_src_rows
+
+    @property
+    def n_dst_rows(self):
+        return self.c.n_dst_rows
+
+
+def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, validate=False,
+                     within_group_by_src_key=False, transpose=True, rows_per_item=0,
+                     stream=None) -> JoinIndex:
+    """rnn_build_join_index: phase 1 (sizes, SYNC), allocate, phase 2 (fill)."""
+    L = lib()
+    e_dst_key = _cuda(e_dst_key, torch.int64, "e_dst_key").contiguous()
+    dev = e_dst_key.device
+    e_src_key = None if e_src_key is None else _cuda(e_src_key, torch.int64, "e_src_key").contiguous()
+    src_key = None if src_key is None else _cuda(src_key, torch.int64, "src_key").contiguous()
+    dst_key = None if dst_key is None else _cuda(dst_key, torch.int64, "dst_key").contiguous()
+    flags = (IDX_VALIDATE if validate else 0) | (IDX_WITHIN_GROUP_BY_SRC_KEY if within_group_by_src_key else 0) \
+        | (0 if transpose else IDX_NO_TRANSPOSE)
+    n_e = e_dst_key.numel()
+    n_s = 0 if src_key is None else src_key.numel()
+    n_t = 0 if dst_key is None else dst_key.numel()
+    # an EMPTY relation is not an ABSENT one: hand the C ABI a non-NULL pointer for it
+    if src_key is not None and n_s == 0:
+        src_key = torch.zeros(1, dtype=torch.int64, device=dev)
+    if dst_key is not None and n_t == 0:
+        dst_key = torch.zeros(1, dtype=torch.int64, device=dev)
+    if e_src_key is not None and n_e == 0:
+        e_src_key = torch.zeros(1, dtype=torch.int64, device=dev)
+    if n_e == 0:
+        e_dst_key = torch.zeros(1, dtype=torch.int64, device=dev)
+    idx = JoinIndexC()
+    wsb = C.c_size_t(0)
+    args = (_ptr(e_src_key), _ptr(e_dst_key), n_e, _ptr(src_key), n_s, _ptr(dst_key), n_t, flags,
+            rows_per_item)
+    _check(L.rnn_build_join_index(*args, C.byref(idx), None, C.byref(wsb), _stream(stream)))
+    ws = _ws(wsb.value, dev)
+    _check(L.rnn_build_join_index(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
+    nj, ng = idx.n_join_rows, idx.n_groups
+    i64 = dict(dtype=torch.int64, device=dev)
+    i32 = dict(dtype=torch.int32, device=dev)
+    has_t = src_key is not None and transpose
+    arrays = {
+        "group_ptr": torch.empty(ng + 1, **i64), "group_key": torch.empty(max(ng, 1), **i64),
+        "group_dst_row": torch.empty(max(ng, 1), **i32), "src_row": torch.empty(max(nj, 1), **i32),
+        "edge_row": torch.empty(max(nj, 1), **i32),
+        "work_ptr": torch.empty(idx.n_work + 1, **i64),
+    }
+    if has_t:
+        arrays.update({"src_ptr": torch.empty(n_s + 1, **i64), "src_pos": torch.empty(max(nj, 1), **i32),
+                       "src_group": torch.empty(max(nj, 1), **i32),
+                       "src_work_ptr": torch.empty(idx.n_src_work + 1, **i64)})
+    for k, v in arrays.items():
+        setattr(idx, k, v.data_ptr())
+    _check(L.rnn_build_join_index(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
+    arrays["group_key"] = arrays["group_key"][:ng]
+    arrays["group_dst_row"] = arrays["group_dst_row"][:ng]
+    for k in ("src_row", "edge_row", "src_pos", "src_group"):
+        if k in arrays:
+            arrays[k] = arrays[k][:nj]
+    return JoinIndex(idx, arrays)
+
+
+# ------------------------------------------------------------------------------------------
+# A3/A4/A5 lifted join-aggregate
+# ------------------------------------------------------------------------------------------
+def _operand(t, mode=BY_ROW):
+    if t is None:
+        return OperandC(None, 0, 0, 0)
+    t = _cuda(t, torch.float32, "operand")
+    if t.dim() == 1:
+        t = t.view(-1, 1)
+    if t.stride(1) != 1:
+        raise ValueError("operands must be row-major (stride(1) == 1)")
+    return OperandC(t.data_ptr(), t.stride(0), t.shape[1], mode)
+
+
+def make_query(combine="src", agg="sum", src=None, src_key=None, edge=None, dst=None, heads=1,
+               scale=1.0, edge_mode=BY_ROW, dst_mode=BY_ROW) -> QueryC:
+    q = QueryC(COMBINE[combine], AGG[agg], heads, scale, _operand(src), _operand(src_key),
+               _operand(edge, edge_mode), _operand(dst, dst_mode))
+    # the struct holds raw pointers: keep the operand tensors alive as long as the query
+    q.keep = (src, src_key, edge, dst)
+    return q
+
+
+def out_width(q: QueryC) -> int:
+    if q.agg == AGG["softmax"] or q.combine == COMBINE["src"]:
+        return q.src.dim
+    dims = [o.dim for o in (q.src, q.edge, q.dst) if o.data]
+    return sum(dims) if q.combine == COMBINE["concat"] else max(dims)
+
+
+class Workspace:
+    """Grow-only device scratch buffer (reused across calls; never shared by concurrent calls)."""
+
+    def __init__(self, device="cuda"):
+        self.buf = None
+        self.device = device
+
+    def get(self, nbytes):
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def lja_workspace_size(idx: JoinIndex, q: QueryC):
+    f, b = C.c_size_t(0), C.c_size_t(0)
+    _check(lib().rnn_lja_workspace_size(C.byref(idx.c), C.byref(q), C.byref(f), C.byref(b)))
+    return f.value, b.value
+
+
+def join_aggregate_fwd(idx: JoinIndex, q: QueryC, out=None, beta=0.0, lse=None, ws=None,
+                       stream=None, ld_out=None):
+    dev = idx.group_ptr.device
+    D = out_width(q)
+    if out is None:
+        ldo = ld_out or (D + 3) // 4 * 4
+        out = torch.empty(idx.n_groups, ldo, dtype=torch.float32, device=dev)[:, :D]
+    if q.agg == AGG["softmax"] and lse is None:
+        lse = torch.empty(max(idx.n_groups, 1), q.heads, dtype=torch.float32, device=dev)
+    fb, _ = lja_workspace_size(idx, q)
+    w = ws.get(fb) if ws is not None else _ws(fb, dev)
+    _check(lib().rnn_join_aggregate_fwd(C.byref(idx.c), C.byref(q), _ptr(out), out.stride(0),
+                                        float(beta), _ptr(lse), _ptr(w), w.numel(), _stream(stream)))
+    return (out, lse) if q.agg == AGG["softmax"] else out
+
+
+def _grad_like(op: OperandC, rows, dev):
+    if not op.data:
+        return None
+    return torch.empty(max(rows, 1), op.ld, dtype=torch.float32, device=dev)[:rows, :op.dim]
+
+
+def join_aggregate_bwd(idx: JoinIndex, q: QueryC, d_out, *, out=None, lse=None, want_src=True,
+                       want_src_key=True, want_edge=True, want_dst=True, n_src_rows=None,
+                       n_edge_rows=None, n_dst_rows=None, ws=None, stream=None):
+    """Returns dict of gradient tensors (same ld as the operands; rows never referenced = 0)."""
+    dev = idx.group_ptr.device
+    ns = idx.n_src_rows if n_src_rows is None else n_src_rows
+    ne = (idx.c.n_edge_rows if q.edge.mode == BY_ROW else idx.n_join_rows) if n_edge_rows is None else n_edge_rows
+    nt = (idx.n_dst_rows if q.dst.mode == BY_ROW else idx.n_groups) if n_dst_rows is None else n_dst_rows
+    g = {"src": _grad_like(q.src, ns, dev) if want_src else None,
+         "src_key": _grad_like(q.src_key, ns, dev) if want_src_key else None,
+         "edge": _grad_like(q.edge, ne, dev) if want_edge else None,
+         "dst": _grad_like(q.dst, nt, dev) if want_dst else None}
+    _, bb = lja_workspace_size(idx, q)
+    w = ws.get(bb) if ws is not None else _ws(bb, dev)
+    _check(lib().rnn_join_aggregate_bwd(C.byref(idx.c), C.byref(q), _ptr(out),
+                                        0 if out is None else out.stride(0), _ptr(lse), _ptr(d_out),
+                                        d_out.stride(0), _ptr(g["src"]), _ptr(g["src_key"]),
+                                        _ptr(g["edge"]), _ptr(g["dst"]), _ptr(w), w.numel(),
+                                        _stream(stream)))
+    return g
+
+
+def group_softmax(idx: JoinIndex, scores, heads, stream=None):
+    scores = _cuda(scores, torch.float32, "scores").contiguous()
+    probs = torch.empty_like(scores)
+    _check(lib().rnn_group_softmax(C.byref(idx.c), _ptr(scores), heads, _ptr(probs), _stream(stream)))
+    return probs
+
+
+def group_softmax_bwd(idx: JoinIndex, probs, d_probs, heads, stream=None):
+    ds = torch.empty_like(probs)
+    _check(lib().rnn_group_softmax_bwd(C.byref(idx.c), _ptr(probs.contiguous()),
+                                       _ptr(d_probs.contiguous()), heads, _ptr(ds), _stream(stream)))
+    return ds
+
+
+# ------------------------------------------------------------------------------------------
+# A2 projection
+# ------------------------------------------------------------------------------------------
+def project(X, W, bias=None, out=None, prec="3xtf32", stream=None):
+    """Y = X W^T + b on tcgen05 (W is [N, K] like nn.Linear.weight)."""
+    M, K = X.shape
+    N = W.shape[0]
+    if out is None:
+        out = torch.empty(M, (N + 3) // 4 * 4, dtype=torch.float32, device=X.device)[:, :N]
+    _check(lib().rnn_project(_ptr(X), M, K, X.stride(0), _ptr(W), N, W.stride(0), _ptr(bias),
+                             _ptr(out), out.stride(0), PREC[prec], _stream(stream)))
+    return out
+
+
+def project_bwd(X, W, dY, want_dx=True, want_db=False, prec="3xtf32", ws=None, stream=None,
+                dx_out=None, dw_out=None):
+    M, K = X.shape
+    N = W.shape[0]
+    dev = X.device
+    dX = None
+    if want_dx:
+        dX = dx_out if dx_out is not None else torch.empty(M, (K + 3) // 4 * 4, dtype=torch.float32, device=dev)[:, :K]
+    dW = dw_out if dw_out is not None else torch.empty(N, K, dtype=torch.float32, device=dev)
+    db = torch.empty(N, dtype=torch.float32, device=dev) if want_db else None
+    nb = C.c_size_t(0)
+    _check(lib().rnn_project_bwd_workspace_size(M, K, N, C.byref(nb)))
+    w = ws.get(nb.value) if ws is not None else _ws(nb.value, dev)
+    _check(lib().rnn_project_bwd(_ptr(X), M, K, X.stride(0), _ptr(W), N, W.stride(0), _ptr(dY),
+                                 dY.stride(0), _ptr(dX), 0 if dX is None else dX.stride(0), _ptr(dW),
+                                 _ptr(db), PREC[prec], _ptr(w), w.numel(), _stream(stream)))
+    return dX, dW, db
+
+
+# ------------------------------------------------------------------------------------------
+# helpers
+# ------------------------------------------------------------------------------------------
+def gcn_norm(idx: JoinIndex, stream=None):
+    dev = idx.group_ptr.device
+    w = torch.empty(max(idx.n_join_rows, 1), dtype=torch.float32, device=dev)
+    nb = 4 * idx.n_dst_rows + 256
+    ws = _ws(nb, dev)
+    _check(lib().rnn_gcn_norm(C.byref(idx.c), _ptr(w), _ptr(ws), ws.numel(), _stream(stream)))
+    return w[:idx.n_join_rows]
+
+
+def hash_partition(keys, P, seed, stream=None):
+    keys = _cuda(keys, torch.int64, "keys").contiguous()
+    owner = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
+    _check(lib().rnn_hash_partition(_ptr(keys), keys.numel(), P, seed, _ptr(owner), _stream(stream)))
+    return owner

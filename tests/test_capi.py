@@ -1,0 +1,59 @@
+"""CPU tests of the boundary: librnn.so loads and exports every symbol include/rnn.h declares,
+and host-side argument checks reject bad calls without touching a GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    with open(os.path.join(ROOT, "include", "rnn.h")) as f:
+        src = f.read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(rnn_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_24207_b200 import build as b
+    b.build()
+    from paper_2605_24207_b200 import rnn
+    return rnn.lib()
+
+
+def test_every_declared_symbol_is_exported(lib):
+    names = declared_functions()
+    assert len(names) >= 14
+    for n in names:
+        assert hasattr(lib, n), n
+
+
+def test_status_strings_and_version(lib):
+    assert lib.rnn_abi_version() == 1
+    assert lib.rnn_status_string(0) == b"RNN_OK"
+    assert lib.rnn_status_string(4) == b"RNN_ERR_DUPLICATE_KEY"
+    assert lib.rnn_status_string(99) == b"RNN_ERR_UNKNOWN"
+
+
+def test_host_side_checks_without_gpu(lib):
+    from paper_2605_24207_b200 import rnn
+    # NULL index pointer -> invalid argument, detail in last error
+    assert lib.rnn_join_aggregate_fwd(None, None, None, 0, C.c_float(0), None, None, 0, None) == 1
+    assert b"required" in lib.rnn_last_error()
+    # workspace size query is host-only
+    idx = rnn.JoinIndexC()
+    wsb = C.c_size_t(0)
+    st = lib.rnn_build_join_index(C.c_void_p(16), C.c_void_p(16), 1000, C.c_void_p(16), 10, None,
+                                  0, 0, 0, C.byref(idx), None, C.byref(wsb), None)
+    assert st == 0 and wsb.value > 0
+    # S given without the E column that joins it
+    st = lib.rnn_build_join_index(None, C.c_void_p(16), 1000, C.c_void_p(16), 10, None, 0, 0, 0,
+                                  C.byref(idx), None, C.byref(wsb), None)
+    assert st == 1 and b"e_src_key" in lib.rnn_last_error()
+    # bad projection shapes are rejected before any launch
+    assert lib.rnn_project(C.c_void_p(16), 10, 10, 10, C.c_void_p(16), 300, 10, None,
+                           C.c_void_p(16), 300, 0, None) == 5
+    assert lib.rnn_hash_partition(None, 10, 0, 0, None, None) == 1
