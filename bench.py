@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""bench.py -- lifted join-aggregate join-rows/s (fwd+bwd) on B200 (BASELINE.json metric).
+
+A step is one pass of the whole hot path over one batch of synthetic input: for every layer
+of the program the tcgen05 projection, the fused gather-combine-reduce forward, the
+transposed-CSR backward and the projection backward (the join index is built once before
+timing -- content caching, PAPER.md comment :737).  Default workload: BASELINE.json
+configs[1], the 3-layer GCN on synthetic ogbn-arxiv-shaped relations (169,343 nodes,
+1,166,243 edges + self-loops, d = 128).
+
+Contract: `python bench.py --gpus N --steps K --warmup W [--impl reference]` prints ONE JSON
+line on rank 0.  Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA
+events on the launching stream with L2 flushed (a 256 MiB write) between steps outside the
+events; barrier + synchronize on both sides; the max over ranks.  `--impl reference` times
+the fp64 CPU oracle (the reference arm of this tier) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "lifted join-aggregate join-rows/s (fwd+bwd)"
+UNIT = "join-rows/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="arxiv", choices=["arxiv", "cora"])
+    ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-launches", action="store_true",
+                    help="count kernel launches with torch.profiler (untimed pass)")
+    return ap.parse_args()
+
+
+def make_graph(cfg, seed):
+    import synth
+    if cfg == "arxiv":
+        return synth.arxiv_like(seed)
+    return synth.cora_like(seed)
+
+
+WORKLOAD = {
+    "arxiv": "3-layer GCN as lifted query on synthetic ogbn-arxiv-shaped relations "
+             "(169,343 node tuples, 1,166,243 edge tuples + self-loops, 128-dim)",
+    "cora": "2-layer GCN as lifted query on synthetic Cora-shaped relations "
+            "(2,708 node tuples, 10,556 edge tuples + self-loops, 1,433->16->7)",
+}
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampled DURING the timed region (B200_PROFILING.md recipe)
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = None
+
+    def start(self):
+        def run():
+            while not self.stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self.stop.wait(0.2)
+        self.th = threading.Thread(target=run, daemon=True)
+        self.th.start()
+
+    def finish(self):
+        self.stop.set()
+        if self.th:
+            self.th.join(timeout=10)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_24207_b200 import programs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+
+    graph = make_graph(args.config, args.seed)
+    # multi-GPU: replicas of the single-GPU step (weak scaling)
+    prog = programs.GCNProgram(graph, device=dev, prec=args.prec)
+    rows = prog.join_rows_per_step
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        prog.step()
+    barrier()
+
+    # ---- timed region ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    prog.timers = {}
+    starts, ends = [], []
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)                      # L2 flush outside the step's events
+        s = torch.cuda.Event(enable_timing=True)
+        e = torch.cuda.Event(enable_timing=True)
+        s.record()
+        prog.step()
+        e.record()
+        starts.append(s)
+        ends.append(e)
+    barrier()
+    clocks = sampler.finish()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    timers = prog.timers
+    prog.timers = None
+    t_step = float(np.mean(step_ms))
+    if world > 1:
+        t = torch.tensor([t_step], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_step = float(t.item())
+    value = world * rows / (t_step * 1e-3)
+
+    def kernel_ms(name):
+        a, b = timers.get(name, []), timers.get(name + "_end", [])
+        return float(np.mean([x.elapsed_time(y) for x, y in zip(a, b)])) if a else None
+
+    per = {k: kernel_ms(k) for k in ("proj_fwd", "lja_fwd", "lja_bwd", "proj_bwd")}
+
+    # ---- roofline of the dominant hot-path kernel (the fused LJA) ----
+    peak, peak_src = peaks()
+    d = prog.dims[1:]
+    # algorithmic bytes per LJA launch (gather model):
+    #   fwd: per join row  src_row 4 + weight 4 + gathered row 4d ; per group  out row 4d + ptr 8
+    #   bwd: per join row  src_group 4 + src_pos 4 + weight 4 + gathered dOut row 4d ;
+    #        per source  d_src row 4d + ptr 8
+    Ep, G = prog.idx1.n_join_rows, prog.G
+    fwd_bytes = float(np.mean([Ep * (8 + 4 * dd) + G * (4 * dd + 8) for dd in d]))
+    bwd_bytes = float(np.mean([Ep * (12 + 4 * dd) + G * (4 * dd + 8) for dd in d]))
+    cand = {"lja_fwd": (per["lja_fwd"], fwd_bytes), "lja_bwd": (per["lja_bwd"], bwd_bytes)}
+    dom = max(cand, key=lambda k: cand[k][0] or 0)
+    ms, byt = cand[dom]
+    achieved = byt / (ms * 1e-3) / 1e9
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "algorithmic_bytes_per_launch": int(byt), "avg_launch_ms": round(ms, 5),
+            "traffic": None,
+            "kernel_ms": {k: (round(v, 5) if v else None) for k, v in per.items()}}
+    tr = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tr):
+        with open(tr) as f:
+            roof["traffic"] = json.load(f).get(dom)
+
+    launches = None
+    if args.profile_launches or True:
+        launches = count_launches(prog)
+
+    # ---- end to end through the C-ABI with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(prog, args, world, dev)
+
+    result = None
+    if rank == 0:
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded; shapes of BASELINE.json configs, see DESIGN.md)",
+            "config": {"workload": WORKLOAD[args.config], "config": args.config,
+                       "join_rows_per_step": rows, "layers": prog.L, "dims": prog.dims,
+                       "projection_precision": args.prec, "l2": "flushed between timed steps",
+                       "parallelism": f"replica x{world}" if world > 1 else "single"},
+            "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return result
+
+
+def count_launches(prog):
+    """Kernels launched by librnn.so in one step, counted by the CUDA profiler (CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as p:
+        prog.step()
+        torch.cuda.synchronize()
+    names = [e.name for e in p.events() if e.device_type.name == "CUDA"]
+    ours = [n for n in names if "rnn::" in n or "seg_kernel" in n or "tc_gemm" in n]
+    return len(ours)
+
+
+def run_e2e(prog, args, world, dev):
+    """Same metric through the public API with HOST buffers: every step copies its inputs
+    (node features X0 and the upstream gradient) from pinned host memory and reads the
+    parameter gradients dW back, inside the timed region."""
+    import torch
+    X_host = prog.X0.cpu().pin_memory()
+    D_host = prog.d_out.cpu().pin_memory()
+    dW_host = [torch.empty(w.shape, dtype=torch.float32).pin_memory() for w in prog.dW]
+    h2d = X_host.numel() * 4 + D_host.numel() * 4
+    d2h = sum(w.numel() * 4 for w in dW_host)
+    steps = max(3, args.steps // 2)
+
+    def one():
+        prog.X0.copy_(X_host, non_blocking=True)
+        prog.d_out.copy_(D_host, non_blocking=True)
+        prog.step()
+        for a, b in zip(dW_host, prog.dW):
+            a.copy_(b, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    s = torch.cuda.Event(enable_timing=True)
+    e = torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        one()
+    e.record()
+    torch.cuda.synchronize()
+    t = s.elapsed_time(e) / steps
+    return {"value": world * prog.join_rows_per_step / (t * 1e-3), "unit": UNIT,
+            "ms_per_step": t, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+
+# ------------------------------------------------------------------------------------------
+# the oracle (CPU, fp64): cpu_baseline and the --impl reference arm
+# ------------------------------------------------------------------------------------------
+def oracle_timing(args, steps=1):
+    import oracle
+    from oracle import programs as op
+    oracle.build()
+    graph = make_graph(args.config, args.seed)
+    L = len(graph["W"])
+    rows = None
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        op.gcn_step(graph)
+        times.append(time.perf_counter() - t0)
+    import oracle as O
+    o = O.build_join_index(graph["edges"]["src"], graph["edges"]["dst"], graph["nodes"]["key"],
+                           graph["nodes"]["key"])
+    rows = o["n_join_rows"] * L
+    t = float(np.median(times))
+    return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"full {args.config} step (all {L} layers, fwd+bwd incl. projections), "
+                      f"{steps} step(s), fp64 single-threaded C, median {t:.2f} s"}, t, rows
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and rank != 0:
+        return None
+    steps = max(1, min(args.steps, 2))
+    cb, t, rows = oracle_timing(args, steps)
+    return {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+            "steps": steps, "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[args.config], "config": args.config,
+                       "join_rows_per_step": rows},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        res = run_reference(args)
+    else:
+        res = run_ours(args)
+        if res is not None and not args.no_cpu_baseline:
+            res["cpu_baseline"] = oracle_timing(args, 1)[0]
+    if res is not None:
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()
