@@ -85,13 +85,17 @@ typedef struct {
   int32_t* group_dst_row; /* [G]    row of T holding key group_key[g] (-1 when T absent)          */
   int32_t* src_row;       /* [E']   S row of join row p (-1 when S absent)                        */
   int32_t* edge_row;      /* [E']   E row of join row p                                           */
+  int32_t* pos_group;     /* [E']   group of group-major position p                               */
   int64_t* src_ptr;       /* [n_src+1] source-major CSR over all S rows (empty rows included)     */
   int32_t* src_pos;       /* [E']   group-major position of the q-th source-major entry           */
   int32_t* src_group;     /* [E']   group of position src_pos[q]                                  */
+  int32_t* src_seg;       /* [E']   S row of the q-th source-major entry (= src_row[src_pos[q]])  */
   int64_t n_work;         /* number of group-major work items                                     */
   int64_t* work_ptr;      /* [n_work+1] item boundaries (positions)                               */
+  int32_t* work_seg;      /* [n_work] first group an item touches (the one holding work_ptr[i])   */
   int64_t n_src_work;     /* number of source-major work items                                    */
   int64_t* src_work_ptr;  /* [n_src_work+1]                                                       */
+  int32_t* src_work_seg;  /* [n_src_work] first source an item touches (empty sources included)   */
 } rnn_join_index;
 
 enum {
@@ -105,7 +109,7 @@ enum {
  *   src_key[n_src] : keys of S, row i <-> embedding row i; NULL => S absent (every E row is
  *                    a join row w.r.t. s and src_row = -1).
  *   dst_key[n_dst] : keys of T; NULL => T absent (groups = distinct e_dst_key).
- *   rows_per_item  : work-schedule granularity (0 => 32).
+ *   rows_per_item  : work-schedule granularity (0 => 128).
  * Two phases (SYNC in phase 1):
  *   (1) idx->group_ptr == NULL: computes idx->n_join_rows, idx->n_groups, idx->n_work,
  *       idx->n_src_work and the other counts, and *workspace_bytes; blocks on `stream`.

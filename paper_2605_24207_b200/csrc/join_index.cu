@@ -182,9 +182,14 @@ __global__ void transpose_input(const int32_t* __restrict__ src_row, int64_t n, 
 }
 
 __global__ void src_group_kernel(const int32_t* __restrict__ src_pos, int64_t n,
-                                 const int32_t* __restrict__ pos_group, int32_t* src_group) {
+                                 const int32_t* __restrict__ pos_group,
+                                 const uint32_t* __restrict__ sorted_src, int32_t* src_group,
+                                 int32_t* src_seg) {
   int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q < n) src_group[q] = pos_group[src_pos[q]];
+  if (q < n) {
+    src_group[q] = pos_group[src_pos[q]];
+    src_seg[q] = (int32_t)sorted_src[q];
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -255,7 +260,7 @@ struct Sched {
     auto add = [&](size_t x) { b = ((b + 255) & ~size_t(255)) + x; };
     const int64_t cap = n_blocks + 2 + 2 * ceil_div(E > 0 ? E : 1, C) + E / (C + 1) + 2;
     add(sizeof(int64_t) * (n_seg + 1));     // long counts / offsets
-    add(scan_workspace_bytes(n_seg));
+    add(scan_workspace_bytes(std::max<int64_t>(n_seg, cap)));
     add(sizeof(uint64_t) * cap);            // candidates
     add(sizeof(int32_t) * cap);             // dummy values for the sort
     add(sizeof(int64_t) * (cap + 1));       // unique heads
@@ -264,9 +269,21 @@ struct Sched {
   }
 };
 
-// host: returns the number of items; writes work_ptr[n+1] when out != nullptr.
+// first segment an item touches: the segment holding position work_ptr[i] (or, when empty
+// segments start exactly there, the first of them)
+__global__ void sched_seg_kernel(const int64_t* __restrict__ ptr, int64_t n_seg,
+                                 const int64_t* __restrict__ wp, int64_t n_items, int32_t* seg) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_items) return;
+  const int64_t b = wp[i];
+  int64_t s = lower_bound_dev(ptr, 0, n_seg + 1, b);
+  if (s > n_seg || ptr[s] > b) s -= 1;
+  seg[i] = (int32_t)s;
+}
+
+// host: returns the number of items; writes work_ptr[n+1] (and work_seg[n]) when out != nullptr.
 rnn_status build_schedule(const int64_t* ptr, int64_t n_seg, int64_t E, int64_t C, void* ws,
-                          int64_t* out, int64_t* n_items, cudaStream_t st) {
+                          int64_t* out, int32_t* seg_out, int64_t* n_items, cudaStream_t st) {
   if (E <= 0) {
     *n_items = 0;
     if (out) RNN_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t), st));
@@ -274,10 +291,10 @@ rnn_status build_schedule(const int64_t* ptr, int64_t n_seg, int64_t E, int64_t 
   }
   const int64_t n_blocks = ceil_div(E, C);
   Carve c(ws);
-  int64_t* cnt = c.take<int64_t>(n_seg + 1);
-  void* sws = c.take<char>(scan_workspace_bytes(n_seg));
   // long-segment boundary counts: sum over long segs of (ceil(len/C)+1) <= 2E/C + ... bound
   const int64_t cap = n_blocks + 2 + 2 * ceil_div(E, C) + E / (C + 1) + 2;
+  int64_t* cnt = c.take<int64_t>(n_seg + 1);
+  void* sws = c.take<char>(scan_workspace_bytes(std::max<int64_t>(n_seg, cap)));
   uint64_t* cand = c.take<uint64_t>(cap);
   int32_t* dummy = c.take<int32_t>(cap);
   int64_t* head = c.take<int64_t>(cap + 1);
@@ -312,6 +329,10 @@ rnn_status build_schedule(const int64_t* ptr, int64_t n_seg, int64_t E, int64_t 
   if (out) {
     unique_emit<<<blocks_for(n_cand), T256, 0, st>>>(cand, n_cand, head, out);
     RNN_LAUNCH_CHECK();
+    if (seg_out && *n_items > 0) {
+      sched_seg_kernel<<<blocks_for(*n_items), T256, 0, st>>>(ptr, n_seg, out, *n_items, seg_out);
+      RNN_LAUNCH_CHECK();
+    }
   }
   return RNN_OK;
 }
@@ -428,7 +449,7 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
   P.n_e = n_edge_rows; P.n_s = src_key ? n_src : 0; P.n_t = dst_key ? n_dst : 0;
   P.has_s = src_key != nullptr; P.has_t = dst_key != nullptr;
   P.cap_s = pow2_at_least(2 * P.n_s + 2); P.cap_t = pow2_at_least(2 * P.n_t + 2);
-  P.C = rows_per_item > 0 ? rows_per_item : 32;
+  P.C = rows_per_item > 0 ? rows_per_item : 128;
   P.transpose = P.has_s && !(flags & RNN_IDX_NO_TRANSPOSE);
   P.by_key = by_key;
   if (by_key)
@@ -502,19 +523,21 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
     out_er = reinterpret_cast<int32_t*>(s.key) + (n_e > 0 ? n_e : 1);
   } else {
     RNN_REQUIRE(idx->group_key && idx->group_dst_row && idx->src_row && idx->edge_row &&
-                    idx->work_ptr,
+                    idx->pos_group && idx->work_ptr && idx->work_seg,
                 RNN_ERR_INVALID_ARGUMENT, "phase 2 needs every group-major array");
-    RNN_REQUIRE(!P.transpose || (idx->src_ptr && idx->src_pos && idx->src_group && idx->src_work_ptr),
+    RNN_REQUIRE(!P.transpose || (idx->src_ptr && idx->src_pos && idx->src_group &&
+                                 idx->src_seg && idx->src_work_ptr && idx->src_work_seg),
                 RNN_ERR_INVALID_ARGUMENT, "phase 2 needs the transposed arrays");
     out_gp = idx->group_ptr; out_gk = idx->group_key; out_gd = idx->group_dst_row;
     out_sr = idx->src_row; out_er = idx->edge_row;
   }
   // sorted edge rows are in s.val; the emit kernel reads them before out_sr/out_er (which may
   // alias s.key in phase 1) are written -- s.val and s.key are distinct buffers.
+  int32_t* pos_group = phase1 ? s.pos_group : idx->pos_group;
   if (n_join > 0) {
     IndexOut o{out_gp, out_gk, out_gd, out_sr, out_er};
     emit_groups<<<blocks_for(n_join), T256, 0, st>>>(s.head, n_join, s.val, e_dst_key,
-                                                     s.s_row_of, s.t_row_of, o, s.pos_group);
+                                                     s.s_row_of, s.t_row_of, o, pos_group);
     RNN_LAUNCH_CHECK();
   } else {
     RNN_CUDA(cudaMemsetAsync(out_gp, 0, sizeof(int64_t), st));
@@ -535,18 +558,20 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
       RNN_LAUNCH_CHECK();
       RNN_TRY(radix_sort_u32(tk, idx->src_pos, n_join,
                              bits_for((uint64_t)(P.n_s > 0 ? P.n_s - 1 : 0)), s.rsort_ws, st));
-      src_group_kernel<<<blocks_for(n_join), T256, 0, st>>>(idx->src_pos, n_join, s.pos_group,
-                                                            idx->src_group);
+      src_group_kernel<<<blocks_for(n_join), T256, 0, st>>>(idx->src_pos, n_join, pos_group, tk,
+                                                            idx->src_group, idx->src_seg);
       RNN_LAUNCH_CHECK();
     }
   }
   // 5. schedules
   int64_t n_work = 0, n_src_work = 0;
   RNN_TRY(build_schedule(out_gp, n_groups, n_join, P.C, s.sched_ws,
-                         phase1 ? nullptr : idx->work_ptr, &n_work, st));
+                         phase1 ? nullptr : idx->work_ptr, phase1 ? nullptr : idx->work_seg,
+                         &n_work, st));
   if (P.transpose)
     RNN_TRY(build_schedule(out_sp, P.n_s, n_join, P.C, s.sched_ws,
-                           phase1 ? nullptr : idx->src_work_ptr, &n_src_work, st));
+                           phase1 ? nullptr : idx->src_work_ptr,
+                           phase1 ? nullptr : idx->src_work_seg, &n_src_work, st));
   idx->n_work = n_work;
   idx->n_src_work = P.transpose ? n_src_work : 0;
   if (!phase1) RNN_CUDA(cudaStreamSynchronize(st));

@@ -34,6 +34,9 @@ struct QueryInfo {
 
 inline OpndD opnd(const rnn_operand& o) { return OpndD{o.data, o.ld, o.dim, o.mode}; }
 
+// floats per partial state: the flat kernel (widths > 64) stores 32 lanes x VEC float4
+inline int64_t flat_pstride(int D) { return D > 64 ? (D + 127) / 128 * 128 : (D + 3) / 4 * 4; }
+
 // 1,2,4,8,16,32 lanes per row (one float4 each), or 64 / 128 float4 columns (VEC 2 / 4)
 inline int lane_config(int D) {
   const int n4 = (D + 3) / 4;
@@ -130,7 +133,7 @@ inline rnn_status check_query(const rnn_join_index* idx, const rnn_lifted_query*
       RNN_FAIL(RNN_ERR_INVALID_ARGUMENT, "combine invalid");
   }
   RNN_REQUIRE(lane_config(qi->D) != 0, RNN_ERR_UNSUPPORTED, "width %d > 512", qi->D);
-  qi->pstride = (qi->D + 3) / 4 * 4;
+  qi->pstride = flat_pstride(qi->D);
   return RNN_OK;
 }
 

@@ -11,7 +11,7 @@
 // SOFTMAX (flash-style, two passes): pass 1 (group-major) recomputes a = exp(e - lse) and
 // writes (a, de) per row and head, de = a (<dOut, M'_s> - <dOut, Out>), plus dQ; pass 2
 // (source-major) gathers dM'_s = sum a dOut_t and dK'_s = scale sum de Q_t.
-#include "lja.cuh"
+#include "rowsplit.cuh"
 
 namespace rnn {
 namespace {
@@ -123,6 +123,107 @@ struct BwdSrc {
     }
   }
 };
+
+// row-split version of the transposed gather (rows wider than 64 floats)
+template <int VEC, bool EV>  // EV: vector edge factor (MUL with an edge embedding)
+struct BwdRS {
+  SrcArgs a;
+  int n4e;
+  struct Meta { int g, e; float c; };
+  __device__ __forceinline__ Meta meta(int64_t q, int) const {
+    Meta m{a.src_group[q], 0, 1.f};
+    const int p = a.src_pos[q];
+    if (a.edge.p) {
+      m.e = a.edge.mode ? p : a.edge_row[p];
+      if (!EV) m.c = __ldg(a.edge.p + (int64_t)m.e * a.edge.ld);
+    }
+    if (a.mean) m.c *= 1.f / (float)(a.group_ptr[m.g + 1] - a.group_ptr[m.g]);
+    return m;
+  }
+  __device__ __forceinline__ Meta shfl(const Meta& m, int src) const {
+    Meta o;
+    o.g = __shfl_sync(FULL, m.g, src);
+    o.e = EV ? __shfl_sync(FULL, m.e, src) : 0;
+    o.c = __shfl_sync(FULL, m.c, src);
+    return o;
+  }
+  __device__ __forceinline__ float4 load(const Meta& m, bool ok, int w) const {
+    const int k = lane_id() + 32 * w;
+    return ld_row4(a.Y, m.g, a.ldy, k, ok && k < a.n4y);
+  }
+  __device__ __forceinline__ float4 load_f(const Meta& m, bool ok, int w) const {
+    if (!EV) return f4_zero();
+    const int k = lane_id() + 32 * w;
+    return ld_row4(a.edge.p, m.e, a.edge.ld, k, ok && k < n4e);
+  }
+  __device__ __forceinline__ float4 add(float4 acc, const Meta& m, float4 x, float4 f) const {
+    return f4_fma(m.c, EV ? f4_mul(x, f) : x, acc);
+  }
+  __device__ __forceinline__ void finish(const float4 (&acc)[4], int64_t seg) const {
+    const int lane = lane_id();
+    const int n4 = (a.D + 3) / 4;
+#pragma unroll
+    for (int w = 0; w < VEC; ++w) {
+      const int k = lane + 32 * w;
+      if (k < n4) store4_clip(a.d, seg, a.ldd, k, a.D, acc[w]);
+    }
+  }
+  __device__ __forceinline__ void zero(int64_t seg) const {
+    const int lane = lane_id();
+    const int n4 = (a.D + 3) / 4;
+#pragma unroll
+    for (int w = 0; w < VEC; ++w) {
+      const int k = lane + 32 * w;
+      if (k < n4) store4_clip(a.d, seg, a.ldd, k, a.D, f4_zero());
+    }
+  }
+};
+
+template <int VEC, bool EV>
+rnn_status launch_src_rs(const SrcArgs& a, const RSCtx& cx, cudaStream_t st) {
+  BwdRS<VEC, EV> pol;
+  pol.a = a;
+  pol.n4e = a.edge.p ? (a.edge.dim + 3) / 4 : 0;
+  return launch_rowsplit<BwdRS<VEC, EV>, VEC>(pol, cx, st);
+}
+
+// metadata of the lean kernel: idx = group of the position, c = w_p (/|g| for MEAN)
+struct LeanBwdMeta {
+  const int32_t* src_group;
+  const int32_t* src_pos;
+  const int32_t* edge_row;
+  const int64_t* group_ptr;
+  const float* w;  // scalar edge weight (nullptr: 1)
+  int64_t ldw;
+  int w_by_pos;
+  int mean;
+  struct Meta { int idx; float c; };
+  __device__ __forceinline__ Meta meta(int64_t q, int) const {
+    Meta m{src_group[q], 1.f};
+    if (w) {
+      const int p = src_pos[q];
+      m.c = __ldg(w + (w_by_pos ? (int64_t)p : (int64_t)edge_row[p]) * ldw);
+    }
+    if (mean) m.c *= 1.f / (float)(group_ptr[m.idx + 1] - group_ptr[m.idx]);
+    return m;
+  }
+};
+
+rnn_status dispatch_src_rs(const SrcArgs& a, const RSCtx& cx, cudaStream_t st) {
+  const int lc = lane_config(a.D);
+  const bool ev = a.edge.p && a.edge.dim > 1;
+  if (!ev && a.D == 4 * lc && a.ldd % 4 == 0 && a.ldy % 4 == 0) {
+    LeanBwdMeta mp{a.src_group, a.src_pos, a.edge_row, a.group_ptr, a.edge.p, a.edge.ld,
+                   a.edge.mode, a.mean};
+    LeanOut o{a.Y, a.ldy, a.d, a.ldd, 0.f};
+    if (lc == 32) return launch_lean<LeanBwdMeta, 1>(mp, cx, o, st);
+    if (lc == 64) return launch_lean<LeanBwdMeta, 2>(mp, cx, o, st);
+    return launch_lean<LeanBwdMeta, 4>(mp, cx, o, st);
+  }
+  if (lc == 32) return ev ? launch_src_rs<1, true>(a, cx, st) : launch_src_rs<1, false>(a, cx, st);
+  if (lc == 64) return ev ? launch_src_rs<2, true>(a, cx, st) : launch_src_rs<2, false>(a, cx, st);
+  return ev ? launch_src_rs<4, true>(a, cx, st) : launch_src_rs<4, false>(a, cx, st);
+}
 
 // U[g] = dOut[g] (.) z_t[g]  (MUL with a group-side factor), ld = ldu
 __global__ void mul_dst_kernel(const float* __restrict__ dO, int64_t ld_do, OpndD dst,
@@ -484,7 +585,7 @@ BwdLayout bwd_layout(const rnn_join_index* idx, const rnn_lifted_query* q, const
   Carve c(ws);
   BwdLayout L{};
   const int64_t ld4 = (qi.D + 3) / 4 * 4;
-  const int64_t ps = q->agg == RNN_AGG_SOFTMAX ? 2 * ld4 : ld4;
+  const int64_t ps = q->agg == RNN_AGG_SOFTMAX ? 2 * ld4 : flat_pstride(qi.D);
   L.part_src = c.take<float>((size_t)idx->n_src_work * ps);
   L.cnt_src = c.take<int>((size_t)idx->n_src_work);
   L.Ubuf = c.take<float>((size_t)idx->n_groups * ld4);
@@ -646,8 +747,14 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
     }
     if (q->combine == RNN_COMBINE_CONCAT) s.edge = OpndD{nullptr, 0, 0, 0};
     SegCtx cx{idx->src_ptr, n_s, idx->src_work_ptr, idx->n_src_work, Lw.part_src,
-              (int64_t)((s.D + 3) / 4 * 4), Lw.cnt_src};
-    RNN_TRY(dispatch_src(s, cx, st));
+              flat_pstride(s.D), Lw.cnt_src};
+    if (lane_config(s.D) >= 32 && idx->src_seg) {
+      RSCtx rx{idx->src_seg, idx->src_ptr, n_s, idx->n_join_rows, idx->src_work_ptr,
+               idx->n_src_work, Lw.part_src, flat_pstride(s.D), Lw.cnt_src, 1};
+      RNN_TRY(dispatch_src_rs(s, rx, st));
+    } else {
+      RNN_TRY(dispatch_src(s, cx, st));
+    }
   }
   if (q->combine == RNN_COMBINE_CONCAT) {
     if (d_edge || d_dst) {

@@ -11,7 +11,7 @@
 // SOFTMAX (HGT, Fig. 4): per group and head an online (running max / sum)
 // softmax over the rows' scores scale * <K'[s], Q[t]>, weighting the gathered values M'[s];
 // the log-sum-exp is saved for the backward.
-#include "lja.cuh"
+#include "rowsplit.cuh"
 
 namespace rnn {
 namespace {
@@ -243,6 +243,127 @@ struct FwdSoftmax {
 };
 
 // ------------------------------------------------------------------------------------------
+// SUM / MEAN, row-split hot loop (rows wider than 64 floats; src operand present)
+// ------------------------------------------------------------------------------------------
+// MODE 0: row value = c * z_s          (SRC with/without weight, MUL with a scalar or no edge)
+// MODE 1: row value = c * (z_s op z_e)  (MUL / ADD with a vector edge embedding)
+// MODE 2: row value = c * (z_s + w)     (ADD with a scalar edge)
+// c folds the edge weight and, for MEAN, 1/|g| (so the finish never reloads group sizes).
+template <int VEC, int MODE>
+struct FwdRS {
+  LjaArgs a;
+  int n4s, n4e, n4t, n4o;
+  bool has_dst;
+  struct Meta { int idx, e; float c, wa; };
+
+  __device__ __forceinline__ Meta meta(int64_t r, int g) const {
+    Meta m{a.src_row[r], 0, 1.f, 0.f};
+    if (a.edge.p) {
+      m.e = a.edge.mode ? (int)r : a.edge_row[r];
+      if (a.edge.dim == 1) {
+        const float w = __ldg(a.edge.p + (int64_t)m.e * a.edge.ld);
+        if (MODE == 2) m.wa = w; else m.c = w;
+      }
+    }
+    if (a.mean) m.c *= 1.f / (float)(a.group_ptr[g + 1] - a.group_ptr[g]);
+    return m;
+  }
+  __device__ __forceinline__ Meta shfl(const Meta& m, int src) const {
+    Meta o;
+    o.idx = __shfl_sync(FULL, m.idx, src);
+    o.e = MODE == 1 ? __shfl_sync(FULL, m.e, src) : 0;
+    o.c = __shfl_sync(FULL, m.c, src);
+    o.wa = MODE == 2 ? __shfl_sync(FULL, m.wa, src) : 0.f;
+    return o;
+  }
+  __device__ __forceinline__ float4 load(const Meta& m, bool ok, int w) const {
+    const int k = lane_id() + 32 * w;
+    return ld_row4(a.src.p, m.idx, a.src.ld, k, ok && k < n4s);
+  }
+  __device__ __forceinline__ float4 load_f(const Meta& m, bool ok, int w) const {
+    if (MODE != 1) return f4_zero();
+    const int k = lane_id() + 32 * w;
+    return ld_row4(a.edge.p, m.e, a.edge.ld, k, ok && k < n4e);
+  }
+  __device__ __forceinline__ float4 add(float4 acc, const Meta& m, float4 x, float4 f) const {
+    if (MODE == 1) x = a.combine == RNN_COMBINE_MUL ? f4_mul(x, f) : f4_add(x, f);
+    if (MODE == 2) x = f4_add(x, make_float4(m.wa, m.wa, m.wa, m.wa));
+    return f4_fma(m.c, x, acc);
+  }
+  __device__ __forceinline__ void finish(const float4 (&acc)[4], int64_t g) const {
+    const int lane = lane_id();
+    int64_t t = 0;
+    float n = 1.f;
+    if (has_dst) {
+      t = a.dst.mode ? g : (int64_t)a.dst_row[g];
+      if (a.combine == RNN_COMBINE_ADD && !a.mean) n = (float)(a.group_ptr[g + 1] - a.group_ptr[g]);
+    }
+#pragma unroll
+    for (int w = 0; w < VEC; ++w) {
+      const int k = lane + 32 * w;
+      if (k >= n4o) continue;
+      float4 x = acc[w];
+      if (has_dst) {
+        float4 z;
+        if (a.dst.dim == 1) { const float z0 = __ldg(a.dst.p + t * a.dst.ld); z = make_float4(z0, z0, z0, z0); }
+        else z = load4(a.dst.p, t, a.dst.ld, k, n4t);
+        if (a.combine == RNN_COMBINE_MUL) x = f4_mul(x, z);
+        else if (a.combine == RNN_COMBINE_ADD) x = f4_add(x, f4_scale(n, z));  // mean folded: + z
+      }
+      if (a.beta != 0.f) x = f4_add(x, f4_scale(a.beta, load4_clip(a.out, g, a.ld_out, k, a.D)));
+      store4_clip(a.out, g, a.ld_out, k, a.D, x);
+    }
+  }
+  __device__ __forceinline__ void zero(int64_t) const {}
+};
+
+template <int VEC, int MODE>
+rnn_status launch_rs(const LjaArgs& a, const RSCtx& cx, cudaStream_t st) {
+  FwdRS<VEC, MODE> pol;
+  pol.a = a;
+  pol.n4s = (a.src.dim + 3) / 4;
+  pol.n4e = a.edge.p ? (a.edge.dim + 3) / 4 : 0;
+  pol.n4t = a.dst.p ? (a.dst.dim + 3) / 4 : 0;
+  pol.n4o = (a.D + 3) / 4;
+  pol.has_dst = a.dst.p != nullptr;
+  return launch_rowsplit<FwdRS<VEC, MODE>, VEC>(pol, cx, st);
+}
+
+// metadata of the lean kernel (rowsplit.cuh): idx = src_row[r], c = w_r (/|g| for MEAN)
+struct LeanFwdMeta {
+  const int32_t* src_row;
+  const int32_t* edge_row;
+  const int64_t* group_ptr;
+  const float* w;  // scalar edge weight (nullptr: 1)
+  int64_t ldw;
+  int w_by_pos;
+  int mean;
+  struct Meta { int idx; float c; };
+  __device__ __forceinline__ Meta meta(int64_t r, int g) const {
+    Meta m{src_row[r], 1.f};
+    if (w) m.c = __ldg(w + (w_by_pos ? r : (int64_t)edge_row[r]) * ldw);
+    if (mean) m.c *= 1.f / (float)(group_ptr[g + 1] - group_ptr[g]);
+    return m;
+  }
+};
+
+template <int VEC>
+rnn_status launch_rs_mode(const LjaArgs& a, const RSCtx& cx, cudaStream_t st) {
+  // lean path: full-width rows, row value = c * z_s, no group-side factor
+  const bool scaled = a.combine == RNN_COMBINE_SRC ||
+                      (a.combine == RNN_COMBINE_MUL && (!a.edge.p || a.edge.dim == 1));
+  if (scaled && !a.dst.p && a.D == 128 * VEC && a.ld_out % 4 == 0) {
+    LeanFwdMeta mp{a.src_row, a.edge_row, a.group_ptr, a.edge.p, a.edge.ld, a.edge.mode, a.mean};
+    LeanOut o{a.src.p, a.src.ld, a.out, a.ld_out, a.beta};
+    return launch_lean<LeanFwdMeta, VEC>(mp, cx, o, st);
+  }
+  const bool ev = a.edge.p && a.edge.dim > 1;
+  if (ev) return launch_rs<VEC, 1>(a, cx, st);
+  if (a.combine == RNN_COMBINE_ADD && a.edge.p) return launch_rs<VEC, 2>(a, cx, st);
+  return launch_rs<VEC, 0>(a, cx, st);
+}
+
+// ------------------------------------------------------------------------------------------
 // CONCAT (and any width layout): one warp per group, lanes stride over output columns
 // ------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) fwd_concat_kernel(LjaArgs a, int64_t n_groups) {
@@ -334,6 +455,14 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
   cx.partial = c.take<float>((size_t)idx->n_work * qi.pstride);
   cx.counter = c.take<int>((size_t)idx->n_work);
   RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * idx->n_work, st));
+  const int lc = lane_config(qi.D);
+  if (q->agg != RNN_AGG_SOFTMAX && lc >= 32 && q->src.data && idx->pos_group) {
+    RSCtx rx{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
+             idx->n_work, cx.partial, cx.pstride, cx.counter, 0};
+    if (lc == 32) return launch_rs_mode<1>(a, rx, st);
+    if (lc == 64) return launch_rs_mode<2>(a, rx, st);
+    return launch_rs_mode<4>(a, rx, st);
+  }
   if (q->agg == RNN_AGG_SOFTMAX) {
     switch (qi.D / 4) {
       case 1: return launch_softmax<Lanes<1, 1>>(a, q->heads, q->scale, cx, st);

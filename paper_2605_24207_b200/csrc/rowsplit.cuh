@@ -1,0 +1,332 @@
+// rowsplit.cuh -- the lifted join-aggregate hot loop as a row-split segmented gather-reduce.
+//
+// One warp per work item (a contiguous run of positions of a key-grouped CSR: group-major for
+// the forward, source-major for the transposed backward).  Every position carries its segment
+// id (pos_group / src_seg, built once with the index), so segment ends are found lane-parallel
+// -- 32 rows of metadata (segment id, gather row, coefficient) per coalesced load -- and the
+// inner loop is the bare gather: U independent 128-bit row loads in flight per warp, an FMA
+// per row, and a predicated flush when a row closes its segment.  A segment that starts before
+// or continues after the item (a power-law hub split by the schedule) is a piece: its partial
+// goes to workspace and the warp holding the last ticket merges the pieces in item order, so
+// the summation order is fixed by the schedule (bit-reproducible, no float atomics).
+#pragma once
+#include "lja.cuh"
+
+namespace rnn {
+
+struct RSCtx {
+  const int32_t* seg;       // [E] segment id of every position
+  const int64_t* ptr;       // [n_seg + 1]
+  int64_t n_seg, E;
+  const int64_t* work_ptr;  // [n_work + 1]
+  int64_t n_work;
+  float* partial;           // [n_work, pstride]
+  int64_t pstride;
+  int* counter;             // [n_work], zero on entry
+  int zero_empty;           // write zero rows for empty segments (source-major CSR)
+};
+
+// Sum the partial states of items [i0, i1) in item order.  Loads are issued 8 at a time so a
+// hub split into many pieces costs a few memory latencies, not one per piece; the additions
+// still run strictly in item order (deterministic).
+template <int VEC>
+__device__ __forceinline__ void merge_pieces(const RSCtx& cx, int64_t i0, int64_t i1,
+                                             float4 (&tot)[4]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int v = 0; v < 4; ++v) tot[v] = f4_zero();
+  constexpr int B = 8;
+  for (int64_t i = i0; i < i1; i += B) {
+    float4 x[B][VEC];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int64_t k = i + u < i1 ? i + u : i;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) x[u][v] = ld_f4_cg(cx.partial + k * cx.pstride + 4 * (lane + 32 * v));
+    }
+#pragma unroll
+    for (int u = 0; u < B; ++u)
+      if (i + u < i1) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) tot[v] = f4_add(tot[v], x[u][v]);
+      }
+  }
+}
+
+// Pol provides (row width <= 128 * VEC floats, lane owns float4 columns lane + 32 v):
+//   struct Meta;  Meta meta(int64_t pos, int seg);  Meta shfl(const Meta&, int lane);
+//   float4 load(const Meta&, bool ok, int v) ;  float4 load_f(const Meta&, bool ok, int v);
+//   float4 add(float4 acc, const Meta&, float4 x, float4 f);
+//   void finish(const float4 (&acc)[VEC], int64_t seg);   void zero(int64_t seg);
+template <class Pol, int VEC>
+__device__ __noinline__ void rs_piece(const Pol& pol, const RSCtx& cx, int64_t item, int64_t g,
+                                      float4 a0, float4 a1, float4 a2, float4 a3) {
+  const int lane = lane_id();
+  const float4 acc[4] = {a0, a1, a2, a3};
+  float* mine = cx.partial + item * cx.pstride;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) __stcg(reinterpret_cast<float4*>(mine + 4 * (lane + 32 * v)), acc[v]);
+  __threadfence();
+  __syncwarp();
+  int64_t i0 = 0, i1 = 0;
+  int last = 0;
+  if (lane == 0) {
+    i0 = lower_bound_dev(cx.work_ptr, 0, cx.n_work + 1, cx.ptr[g]);
+    i1 = lower_bound_dev(cx.work_ptr, 0, cx.n_work + 1, cx.ptr[g + 1]);
+    last = atomicAdd(&cx.counter[i0], 1) == (int)(i1 - i0 - 1);
+  }
+  last = __shfl_sync(FULL, last, 0);
+  if (!last) return;
+  i0 = __shfl_sync(FULL, i0, 0);
+  i1 = __shfl_sync(FULL, i1, 0);
+  __threadfence();
+  float4 tot[4];
+  merge_pieces<VEC>(cx, i0, i1, tot);
+  pol.finish(tot, g);
+}
+
+template <class Pol>
+__device__ __noinline__ void rs_zero_range(const Pol& pol, int64_t g0, int64_t g1) {
+  for (int64_t g = g0; g < g1; ++g) pol.zero(g);
+}
+
+template <class Pol, int VEC, int U>
+__global__ void __launch_bounds__(256) rowsplit_kernel(Pol pol, RSCtx cx) {
+  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (item >= cx.n_work) return;
+  const int lane = lane_id();
+  const int64_t b = cx.work_ptr[item], e = cx.work_ptr[item + 1];
+  // does the first segment start before b? (then its first flush is a piece)
+  bool head_piece = b > 0 && cx.seg[b - 1] == cx.seg[b];
+  float4 acc[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) acc[v] = f4_zero();
+  bool pending = false;  // rows accumulated into a segment not flushed yet
+  int g_tail = -1;
+  for (int64_t r0 = b; r0 < e; r0 += 32) {
+    const int P = (int)((e - r0) < 32 ? (e - r0) : 32);
+    typename Pol::Meta m{};
+    int gl = -1;
+    bool endf = false;
+    if (lane < P) {
+      const int64_t r = r0 + lane;
+      gl = cx.seg[r];
+      m = pol.meta(r, gl);
+      const int gn = r + 1 < cx.E ? cx.seg[r + 1] : -1;
+      endf = gl != gn;
+    }
+    if (cx.zero_empty) {
+      // empty segments between this position and the previous one (or before position 0)
+      // get zero rows here; trailing ones are written by the last item
+      const int gprev = lane < P ? (r0 + lane > 0 ? cx.seg[r0 + lane - 1] : -1) : 0;
+      unsigned gaps = __ballot_sync(FULL, lane < P && gl > gprev + 1);
+      while (gaps) {
+        const int j = __ffs(gaps) - 1;
+        gaps &= gaps - 1;
+        const int g1 = __shfl_sync(FULL, gl, j), g0 = __shfl_sync(FULL, gprev, j) + 1;
+        rs_zero_range(pol, g0, g1);
+      }
+    }
+    const unsigned ends = __ballot_sync(FULL, endf);
+    for (int j0 = 0; j0 < P; j0 += U) {
+      float4 v[U][VEC], f[U][VEC];
+      typename Pol::Meta mu[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = j0 + u < P;
+        mu[u] = pol.shfl(m, (j0 + u) & 31);
+#pragma unroll
+        for (int w = 0; w < VEC; ++w) {
+          v[u][w] = pol.load(mu[u], ok, w);
+          f[u][w] = pol.load_f(mu[u], ok, w);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        if (j < P) {
+#pragma unroll
+          for (int w = 0; w < VEC; ++w) acc[w] = pol.add(acc[w], mu[u], v[u][w], f[u][w]);
+          pending = true;
+          if ((ends >> j) & 1u) {
+            const int g = __shfl_sync(FULL, gl, j);
+            if (head_piece) rs_piece<Pol, VEC>(pol, cx, item, g, acc[0], acc[1], acc[2], acc[3]);
+            else pol.finish(acc, g);
+            head_piece = false;
+            pending = false;
+#pragma unroll
+            for (int w = 0; w < VEC; ++w) acc[w] = f4_zero();
+          }
+        }
+      }
+    }
+    g_tail = __shfl_sync(FULL, gl, P - 1);
+  }
+  if (pending)  // the last segment continues past e
+    rs_piece<Pol, VEC>(pol, cx, item, g_tail, acc[0], acc[1], acc[2], acc[3]);
+  if (cx.zero_empty && item == cx.n_work - 1) rs_zero_range(pol, cx.seg[cx.E - 1] + 1, cx.n_seg);
+}
+
+template <class Pol, int VEC>
+rnn_status launch_rowsplit(const Pol& pol, RSCtx cx, cudaStream_t st) {
+  if (cx.n_work <= 0) return RNN_OK;
+  constexpr int U = VEC == 1 ? 8 : (VEC == 2 ? 4 : 2);
+  RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * cx.n_work, st));
+  rowsplit_kernel<Pol, VEC, U><<<(unsigned)ceil_div(cx.n_work, 8), 256, 0, st>>>(pol, cx);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// Lean variant for the dominant case -- out[seg] = beta*out[seg] + sum_rows c_r * V[idx_r]
+// with full-width rows (D = 128*VEC): GCN / hypergraph forward (SRC, weights by position or
+// row, MEAN folded into c) and every transposed source-gradient gather.  Only the metadata
+// policy MP varies (how idx_r and c_r are derived); the per-row path is shuffle, 128-bit
+// load, 4 FMAs and a segment-end bit test.
+//   MP: struct Meta { int idx; float c; };  Meta meta(int64_t pos, int seg) const;
+// ------------------------------------------------------------------------------------------
+struct LeanOut {
+  const float* V;  // gathered matrix
+  int64_t ldv;
+  float* out;      // [n_seg, ldo]
+  int64_t ldo;
+  float beta;
+};
+
+template <int VEC>
+__device__ __forceinline__ void lean_store(const LeanOut& o, int64_t g, const float4 (&acc)[4]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int w = 0; w < VEC; ++w) {
+    float4* p = reinterpret_cast<float4*>(o.out + g * o.ldo) + lane + 32 * w;
+    float4 x = acc[w];
+    if (o.beta != 0.f) x = f4_fma(o.beta, *p, x);
+    *p = x;
+  }
+}
+
+template <int VEC>
+__device__ __noinline__ void lean_piece(const LeanOut& o, const RSCtx& cx, int64_t item, int64_t g,
+                                        float4 a0, float4 a1, float4 a2, float4 a3) {
+  const int lane = lane_id();
+  const float4 acc[4] = {a0, a1, a2, a3};
+  float* mine = cx.partial + item * cx.pstride;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) __stcg(reinterpret_cast<float4*>(mine + 4 * (lane + 32 * v)), acc[v]);
+  __threadfence();
+  __syncwarp();
+  int64_t i0 = 0, i1 = 0;
+  int last = 0;
+  if (lane == 0) {
+    i0 = lower_bound_dev(cx.work_ptr, 0, cx.n_work + 1, cx.ptr[g]);
+    i1 = lower_bound_dev(cx.work_ptr, 0, cx.n_work + 1, cx.ptr[g + 1]);
+    last = atomicAdd(&cx.counter[i0], 1) == (int)(i1 - i0 - 1);
+  }
+  last = __shfl_sync(FULL, last, 0);
+  if (!last) return;
+  i0 = __shfl_sync(FULL, i0, 0);
+  i1 = __shfl_sync(FULL, i1, 0);
+  __threadfence();
+  float4 tot[4];
+  merge_pieces<VEC>(cx, i0, i1, tot);
+  lean_store<VEC>(o, g, tot);
+}
+
+template <int VEC>
+__device__ __noinline__ void lean_zero(const LeanOut& o, int64_t g0, int64_t g1) {
+  float4 z[4] = {f4_zero(), f4_zero(), f4_zero(), f4_zero()};
+  LeanOut o0 = o;
+  o0.beta = 0.f;
+  for (int64_t g = g0; g < g1; ++g) lean_store<VEC>(o0, g, z);
+}
+
+template <class MP, int VEC, int U>
+__global__ void __launch_bounds__(256) lean_kernel(MP mp, RSCtx cx, LeanOut o) {
+  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (item >= cx.n_work) return;
+  const int lane = lane_id();
+  const int64_t b = cx.work_ptr[item], e = cx.work_ptr[item + 1];
+  bool head_piece = b > 0 && cx.seg[b - 1] == cx.seg[b];
+  float4 acc[4];
+#pragma unroll
+  for (int v = 0; v < 4; ++v) acc[v] = f4_zero();
+  bool pending = false;
+  int g_tail = -1;
+  for (int64_t r0 = b; r0 < e; r0 += 32) {
+    const int P = (int)((e - r0) < 32 ? (e - r0) : 32);
+    int mi = 0, gl = -1;
+    float mc = 0.f;
+    bool endf = false;
+    if (lane < P) {
+      const int64_t r = r0 + lane;
+      gl = cx.seg[r];
+      const typename MP::Meta m = mp.meta(r, gl);
+      mi = m.idx;
+      mc = m.c;
+      endf = r + 1 >= cx.E || cx.seg[r + 1] != gl;
+    }
+    if (cx.zero_empty) {
+      const int gprev = lane < P ? (r0 + lane > 0 ? cx.seg[r0 + lane - 1] : -1) : 0;
+      unsigned gaps = __ballot_sync(FULL, lane < P && gl > gprev + 1);
+      while (gaps) {
+        const int j = __ffs(gaps) - 1;
+        gaps &= gaps - 1;
+        lean_zero<VEC>(o, __shfl_sync(FULL, gprev, j) + 1, __shfl_sync(FULL, gl, j));
+      }
+    }
+    const unsigned ends = __ballot_sync(FULL, endf);
+    for (int j0 = 0; j0 < P; j0 += U) {
+      float4 v[U][VEC];
+      float c[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int s = __shfl_sync(FULL, mi, (j0 + u) & 31);  // rows >= P read row mi = 0
+        c[u] = __shfl_sync(FULL, mc, (j0 + u) & 31);
+#pragma unroll
+        for (int w = 0; w < VEC; ++w)
+          v[u][w] = __ldg(reinterpret_cast<const float4*>(o.V + (int64_t)s * o.ldv) + lane + 32 * w);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        if (j < P) {
+#pragma unroll
+          for (int w = 0; w < VEC; ++w) acc[w] = f4_fma(c[u], v[u][w], acc[w]);
+          pending = true;
+          if ((ends >> j) & 1u) {
+            const int g = __shfl_sync(FULL, gl, j);
+            if (head_piece) lean_piece<VEC>(o, cx, item, g, acc[0], acc[1], acc[2], acc[3]);
+            else lean_store<VEC>(o, g, acc);
+            head_piece = false;
+            pending = false;
+#pragma unroll
+            for (int w = 0; w < VEC; ++w) acc[w] = f4_zero();
+          }
+        }
+      }
+    }
+    g_tail = __shfl_sync(FULL, gl, P - 1);
+  }
+  if (pending) lean_piece<VEC>(o, cx, item, g_tail, acc[0], acc[1], acc[2], acc[3]);
+  if (cx.zero_empty && item == cx.n_work - 1) lean_zero<VEC>(o, cx.seg[cx.E - 1] + 1, cx.n_seg);
+}
+
+template <class MP, int VEC>
+rnn_status launch_lean(const MP& mp, RSCtx cx, const LeanOut& o, cudaStream_t st) {
+  if (cx.n_work <= 0) return RNN_OK;
+  constexpr int U = VEC == 1 ? 8 : (VEC == 2 ? 4 : 2);
+  RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * cx.n_work, st));
+  lean_kernel<MP, VEC, U><<<(unsigned)ceil_div(cx.n_work, 8), 256, 0, st>>>(mp, cx, o);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+// branch-free masked float4 load: an inactive lane/row reads a valid dummy address
+__device__ __forceinline__ float4 ld_row4(const float* base, int64_t row, int64_t ld, int k,
+                                          bool active) {
+  const float4* p = reinterpret_cast<const float4*>(base + (active ? row * ld : 0)) + (active ? k : 0);
+  const float4 x = __ldg(p);
+  return active ? x : f4_zero();
+}
+
+}  // namespace rnn

@@ -36,9 +36,12 @@ class JoinIndexC(C.Structure):
                 ("n_src_rows", C.c_int64), ("n_dst_rows", C.c_int64),
                 ("group_ptr", C.c_void_p), ("group_key", C.c_void_p),
                 ("group_dst_row", C.c_void_p), ("src_row", C.c_void_p), ("edge_row", C.c_void_p),
+                ("pos_group", C.c_void_p),
                 ("src_ptr", C.c_void_p), ("src_pos", C.c_void_p), ("src_group", C.c_void_p),
-                ("n_work", C.c_int64), ("work_ptr", C.c_void_p),
-                ("n_src_work", C.c_int64), ("src_work_ptr", C.c_void_p)]
+                ("src_seg", C.c_void_p),
+                ("n_work", C.c_int64), ("work_ptr", C.c_void_p), ("work_seg", C.c_void_p),
+                ("n_src_work", C.c_int64), ("src_work_ptr", C.c_void_p),
+                ("src_work_seg", C.c_void_p)]
 
 
 class OperandC(C.Structure):
@@ -188,19 +191,22 @@ def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, valida
     arrays = {
         "group_ptr": torch.empty(ng + 1, **i64), "group_key": torch.empty(max(ng, 1), **i64),
         "group_dst_row": torch.empty(max(ng, 1), **i32), "src_row": torch.empty(max(nj, 1), **i32),
-        "edge_row": torch.empty(max(nj, 1), **i32),
+        "edge_row": torch.empty(max(nj, 1), **i32), "pos_group": torch.empty(max(nj, 1), **i32),
         "work_ptr": torch.empty(idx.n_work + 1, **i64),
+        "work_seg": torch.empty(max(idx.n_work, 1), **i32),
     }
     if has_t:
         arrays.update({"src_ptr": torch.empty(n_s + 1, **i64), "src_pos": torch.empty(max(nj, 1), **i32),
                        "src_group": torch.empty(max(nj, 1), **i32),
-                       "src_work_ptr": torch.empty(idx.n_src_work + 1, **i64)})
+                       "src_seg": torch.empty(max(nj, 1), **i32),
+                       "src_work_ptr": torch.empty(idx.n_src_work + 1, **i64),
+                       "src_work_seg": torch.empty(max(idx.n_src_work, 1), **i32)})
     for k, v in arrays.items():
         setattr(idx, k, v.data_ptr())
     _check(L.rnn_build_join_index(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
     arrays["group_key"] = arrays["group_key"][:ng]
     arrays["group_dst_row"] = arrays["group_dst_row"][:ng]
-    for k in ("src_row", "edge_row", "src_pos", "src_group"):
+    for k in ("src_row", "edge_row", "pos_group", "src_pos", "src_group", "src_seg"):
         if k in arrays:
             arrays[k] = arrays[k][:nj]
     return JoinIndex(idx, arrays)
