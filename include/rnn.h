@@ -101,7 +101,11 @@ typedef struct {
 enum {
   RNN_IDX_VALIDATE = 1,                /* check S/T duplicate keys (RNN_ERR_DUPLICATE_KEY)      */
   RNN_IDX_WITHIN_GROUP_BY_SRC_KEY = 2, /* DHN adjacency variant (needs S and T)                 */
-  RNN_IDX_NO_TRANSPOSE = 4             /* skip src_ptr/src_pos/src_group/src_work_ptr           */
+  RNN_IDX_NO_TRANSPOSE = 4,            /* skip src_ptr/src_pos/src_group/src_work_ptr           */
+  RNN_IDX_DENSE_GROUPS = 8             /* every T row is a group (key order), empty ones too:   */
+                                       /* outputs are dense [n_dst, d] in T-key order, so the   */
+                                       /* union over several relations with one T is a beta=1   */
+                                       /* accumulation; needs T              */
 };
 
 /* Build the canonical join index of E(s,t) |><| S(s) |><| T(t) grouped by t.
@@ -201,7 +205,8 @@ rnn_status rnn_group_softmax_bwd(const rnn_join_index* idx, const float* probs,
 /* The transformation pushed below the join so it runs once per node, not once per edge
  * (PAPER.md:1032).  Y[M, N] = X[M, K] . W^T + b, W laid out [N, K] (torch.nn.Linear).
  * X: ldx % 4 == 0; W: ldw % 4 == 0; Y: ldy % 4 == 0; 16-byte aligned; M < 2^31, K <= 8192,
- * N <= 256.  Precision:
+ * N <= 8192 (tiles of 256 columns; several per-relation projections of one node relation
+ * are one GEMM with their weights stacked).  Precision:
  *   RNN_PREC_TF32   : one kind::tf32 MMA per tile (operands truncated to tf32).
  *   RNN_PREC_3XTF32 : split-operand 3xTF32 (hi*hi + hi*lo + lo*hi), ~fp32 accuracy.
  * Backward: dX = dY . W (may be NULL), dW = dY^T . X (required), db = colsum(dY) (may be NULL),
@@ -225,6 +230,12 @@ rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, co
  * (n_src_rows == n_dst_rows). */
 rnn_status rnn_gcn_norm(const rnn_join_index* idx, float* w, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* Union over relations of materialised per-relation results that share a head relation
+ * (PAPER.md:451-460, e.g. HGT's H_tilda = sum over relation types, :1408-1409):
+ * y[r, c] = beta * y[r, c] + x[r, c] for r < rows, c < cols (fp32, row-major, any ld). */
+rnn_status rnn_accumulate(float* y, int64_t ldy, const float* x, int64_t ldx, int64_t rows,
+                          int32_t cols, float beta, void* stream);
 
 /* Multi-GPU ownership of group keys: owner[i] = splitmix64(keys[i] ^ seed) mod P. */
 rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed,

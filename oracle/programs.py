@@ -35,3 +35,41 @@ def gcn_step(graph, layers=None):
         dX, dW[l], _ = oracle.project_bwd(H[l], graph["W"][l], dZ, want_db=False)
         dY = dX
     return H, dW, dY
+
+
+def hypergraph_step(hg):
+    """O8: two-hop node -> hyperedge -> node (hop 1 SUM by hyperedge, hop 2 MEAN by node),
+    after the projection Z = X Theta^T; backward with dOut = hg['d_out'][:G2]."""
+    nk, hk = hg["nodes"]["key"], hg["hyperedges"]["key"]
+    iv, ih = hg["inc"]["node"], hg["inc"]["hyper"]
+    o1 = oracle.build_join_index(iv, ih, nk, hk)
+    o2 = oracle.build_join_index(ih, iv, o1["group_key"], nk)
+    X = np.asarray(hg["nodes"]["x"], np.float64)
+    Z = oracle.project(X, hg["theta"])
+    Eh = oracle.lja_fwd(o1, "src", "sum", src=Z)[0]
+    Xo = oracle.lja_fwd(o2, "src", "mean", src=Eh)[0]
+    dXo = np.asarray(hg["d_out"][: o2["n_groups"]], np.float64)
+    dEh = oracle.lja_bwd(o2, dXo, "src", "mean", src=Eh, want=("src",))["src"]
+    dZ = oracle.lja_bwd(o1, dEh, "src", "sum", src=Z, want=("src",))["src"]
+    dX, dTheta, _ = oracle.project_bwd(X, hg["theta"], dZ, want_db=False)
+    return {"Xo": Xo, "dTheta": dTheta, "dX": dX, "o1": o1, "o2": o2}
+
+
+def hgt_relation(H_src, H_dst, Wk, Wm, Wq, src_keys, dst_keys, e_src, e_dst, heads, d_out_dense):
+    """One relation phi of the HGT layer (Fig. 4): K' = H_s Wk^T (scale folded),
+    M' = H_s Wm^T, Q = H_t Wq^T, O = per-target per-head softmax-weighted sum.  Returns the
+    compact oracle outputs, the key-sorted dense placement and the gradients."""
+    K = oracle.project(H_src, Wk)
+    M = oracle.project(H_src, Wm)
+    Q = oracle.project(H_dst, Wq)
+    o = oracle.build_join_index(e_src, e_dst, src_keys, dst_keys)
+    out, lse = oracle.lja_fwd(o, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
+    # dense rows in T-key order: rank of every T key
+    order = np.argsort(dst_keys, kind="stable")
+    rank = np.empty(len(dst_keys), np.int64)
+    rank[order] = np.arange(len(dst_keys))
+    dense_rows = rank[o["group_dst_row"]]
+    dO = np.asarray(d_out_dense, np.float64)[dense_rows]
+    g = oracle.lja_bwd(o, dO, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
+    return {"index": o, "out": out, "lse": lse, "dense_rows": dense_rows,
+            "dK": g["src_key"], "dM": g["src"], "dQ": g["dst"], "K": K, "M": M, "Q": Q}

@@ -170,6 +170,31 @@ __global__ void emit_groups(const int64_t* __restrict__ head_scan /*exclusive, [
   if (pos_group) pos_group[p] = (int32_t)g;
 }
 
+// dense groups (RNN_IDX_DENSE_GROUPS): group = rank of the T key; count group sizes
+__global__ void emit_dense(const uint32_t* __restrict__ rank_t, int64_t n,
+                           const int32_t* __restrict__ sorted_j,
+                           const int32_t* __restrict__ s_row_of,
+                           const int32_t* __restrict__ t_row_of, IndexOut o, int32_t* pos_group) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int32_t j = sorted_j[p];
+  const int64_t g = rank_t[t_row_of[j]];
+  o.src_row[p] = s_row_of[j];
+  o.edge_row[p] = j;
+  pos_group[p] = (int32_t)g;
+  atomicAdd(reinterpret_cast<unsigned long long*>(&o.group_ptr[g]), 1ull);
+}
+
+__global__ void dense_groups(const uint32_t* __restrict__ rank_t, int64_t n_t,
+                             const int64_t* __restrict__ dst_key, int64_t* group_key,
+                             int32_t* group_dst_row) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_t) return;
+  const uint32_t g = rank_t[i];
+  group_key[g] = dst_key[i];
+  group_dst_row[g] = (int32_t)i;
+}
+
 __global__ void count_src(const int32_t* __restrict__ src_row, int64_t n, int64_t* cnt) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p < n) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[src_row[p]]), 1ull);
@@ -361,6 +386,7 @@ size_t plan_bytes(const Plan& P) {
   add(sizeof(uint64_t) * n); add(sizeof(int32_t) * n);      // sort key / val
   add(sizeof(int64_t) * (n + 1));                           // head scan
   add(sizeof(int32_t) * n);                                 // pos_group
+  add(sizeof(int64_t) * (P.n_t + 1));                       // dense group_ptr (phase 1)
   add(sizeof(uint32_t) * (P.n_t + 1)); add(sizeof(uint32_t) * (P.n_s + 1));  // ranks
   int64_t big = std::max<int64_t>(n, std::max(P.n_s, P.n_t));
   add(sizeof(uint64_t) * big); add(sizeof(int32_t) * big);  // rank sort scratch
@@ -379,6 +405,7 @@ struct Scratch {
   uint64_t* key; int32_t* val;
   int64_t* head;
   int32_t* pos_group;
+  int64_t* gp_dense;
   uint32_t *rank_t, *rank_s;
   uint64_t* rk; int32_t* rv;
   void* rsort_ws; void* scan_ws;
@@ -400,6 +427,7 @@ Scratch carve(const Plan& P, void* ws) {
   s.key = c.take<uint64_t>(n); s.val = c.take<int32_t>(n);
   s.head = c.take<int64_t>(n + 1);
   s.pos_group = c.take<int32_t>(n);
+  s.gp_dense = c.take<int64_t>(P.n_t + 1);
   s.rank_t = c.take<uint32_t>(P.n_t + 1); s.rank_s = c.take<uint32_t>(P.n_s + 1);
   int64_t big = std::max<int64_t>(n, std::max(P.n_s, P.n_t));
   s.rk = c.take<uint64_t>(big); s.rv = c.take<int32_t>(big);
@@ -442,6 +470,8 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
                   n_dst < (int64_t(1) << 31),
               RNN_ERR_UNSUPPORTED, "relations must have < 2^31 rows");
   const bool by_key = flags & RNN_IDX_WITHIN_GROUP_BY_SRC_KEY;
+  const bool dense = flags & RNN_IDX_DENSE_GROUPS;
+  RNN_REQUIRE(!dense || dst_key, RNN_ERR_INVALID_ARGUMENT, "RNN_IDX_DENSE_GROUPS needs T");
   RNN_REQUIRE(!by_key || (src_key && dst_key), RNN_ERR_UNSUPPORTED,
               "RNN_IDX_WITHIN_GROUP_BY_SRC_KEY needs S and T");
   RNN_REQUIRE(rows_per_item >= 0, RNN_ERR_INVALID_ARGUMENT, "rows_per_item < 0");
@@ -510,6 +540,7 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
   int64_t n_groups = 0;
   RNN_CUDA(cudaMemcpyAsync(&n_groups, s.head + n_join, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   RNN_CUDA(cudaStreamSynchronize(st));
+  if (dense) n_groups = P.n_t;  // every T row is a group (key order), empty ones included
 
   idx->n_edge_rows = n_e; idx->n_join_rows = n_join; idx->n_groups = n_groups;
   idx->n_src_rows = P.n_s; idx->n_dst_rows = P.n_t;
@@ -534,7 +565,22 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
   // sorted edge rows are in s.val; the emit kernel reads them before out_sr/out_er (which may
   // alias s.key in phase 1) are written -- s.val and s.key are distinct buffers.
   int32_t* pos_group = phase1 ? s.pos_group : idx->pos_group;
-  if (n_join > 0) {
+  if (dense) {
+    // groups = all T rows in key order; sizes counted (exact integers), then scanned
+    if (phase1) out_gp = s.gp_dense;
+    RNN_CUDA(cudaMemsetAsync(out_gp, 0, sizeof(int64_t) * (P.n_t + 1), st));
+    IndexOut o{out_gp, out_gk, out_gd, out_sr, out_er};
+    if (n_join > 0) {
+      emit_dense<<<blocks_for(n_join), T256, 0, st>>>(s.rank_t, n_join, s.val, s.s_row_of,
+                                                      s.t_row_of, o, pos_group);
+      RNN_LAUNCH_CHECK();
+    }
+    if (P.n_t > 0) {
+      dense_groups<<<blocks_for(P.n_t), T256, 0, st>>>(s.rank_t, P.n_t, dst_key, out_gk, out_gd);
+      RNN_LAUNCH_CHECK();
+    }
+    RNN_TRY(exclusive_scan_i64(out_gp, out_gp, P.n_t, s.scan_ws, st));
+  } else if (n_join > 0) {
     IndexOut o{out_gp, out_gk, out_gd, out_sr, out_er};
     emit_groups<<<blocks_for(n_join), T256, 0, st>>>(s.head, n_join, s.val, e_dst_key,
                                                      s.s_row_of, s.t_row_of, o, pos_group);

@@ -316,7 +316,7 @@ __global__ void bwd_dst_kernel(const float* __restrict__ dO, int64_t ld_do,
   if (g >= G) return;
   const int lane = lane_id();
   const float n = (float)(group_ptr[g + 1] - group_ptr[g]);
-  const float cg = mean ? 1.f / n : 1.f;
+  const float cg = mean ? (n > 0.f ? 1.f / n : 0.f) : 1.f;
   const int64_t t = dst.mode ? g : (int64_t)dst_row[g];
   float sum = 0.f;
   for (int c = lane; c < D; c += 32) {
@@ -687,14 +687,19 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
   const int64_t n_s = idx->n_src_rows;
   RNN_REQUIRE(!d_src || vec_ok, RNN_ERR_INVALID_ARGUMENT,
               "source gradients need d_out 16-byte aligned with ld_dout %% 4 == 0");
-  if (d_src && idx->n_join_rows == 0)
-    RNN_CUDA(cudaMemsetAsync(d_src, 0, sizeof(float) * n_s * q->src.ld, st));
+  // (2D memsets: a gradient buffer may be a column block of a wider matrix)
+  auto zero2d = [&](float* p, int64_t ld, int dim, int64_t rows) -> rnn_status {
+    if (rows > 0)
+      RNN_CUDA(cudaMemset2DAsync(p, sizeof(float) * ld, 0, sizeof(float) * dim, rows, st));
+    return RNN_OK;
+  };
+  if (d_src && idx->n_join_rows == 0) RNN_TRY(zero2d(d_src, q->src.ld, q->src.dim, n_s));
   if (d_src_key && idx->n_join_rows == 0)
-    RNN_CUDA(cudaMemsetAsync(d_src_key, 0, sizeof(float) * n_s * q->src_key.ld, st));
+    RNN_TRY(zero2d(d_src_key, q->src_key.ld, q->src_key.dim, n_s));
   if (d_edge && q->edge.mode == RNN_BY_ROW)
-    RNN_CUDA(cudaMemsetAsync(d_edge, 0, sizeof(float) * idx->n_edge_rows * q->edge.ld, st));
-  if (d_dst && q->dst.mode == RNN_BY_ROW)
-    RNN_CUDA(cudaMemsetAsync(d_dst, 0, sizeof(float) * idx->n_dst_rows * q->dst.ld, st));
+    RNN_TRY(zero2d(d_edge, q->edge.ld, q->edge.dim, idx->n_edge_rows));
+  if (d_dst && q->dst.mode == RNN_BY_ROW && idx->n_groups < idx->n_dst_rows)
+    RNN_TRY(zero2d(d_dst, q->dst.ld, q->dst.dim, idx->n_dst_rows));
   if (idx->n_groups == 0) return RNN_OK;
   LjaArgs a = make_args(idx, q, nullptr, 0, 0.f, nullptr, qi.D);
   const int64_t ld4 = (qi.D + 3) / 4 * 4;

@@ -114,7 +114,8 @@ struct FwdSum {
         if (a.combine == RNN_COMBINE_MUL) x = f4_mul(x, z);
         else if (a.combine == RNN_COMBINE_ADD) x = f4_add(x, f4_scale((float)n, z));
       }
-      if (a.mean) x = f4_scale(1.f / (float)n, x);
+      if (a.mean) x = f4_scale(n > 0 ? 1.f / (float)n : 0.f, x);
+      if (n == 0) x = f4_zero();  // empty group (dense index): aggregate of {} is 0
       if (a.beta != 0.f) x = f4_add(x, f4_scale(a.beta, load4_clip(a.out, g, a.ld_out, k, a.D)));
       store4_clip(a.out, g, a.ld_out, k, a.D, x);
     }
@@ -219,10 +220,11 @@ struct FwdSoftmax {
   __device__ __forceinline__ void finish(State& s, int64_t g) const {
     if (L::slot() != 0) return;
     const int k = L::sub();
-    float4 x = f4_scale(1.f / s.l, s.acc);
+    const bool empty = s.l == 0.f;  // empty group (dense index): out 0, lse -inf
+    float4 x = empty ? f4_zero() : f4_scale(1.f / s.l, s.acc);
     if (a.beta != 0.f) x = f4_add(x, f4_scale(a.beta, ld_f4(a.out + g * a.ld_out + 4 * k)));
     st_f4(a.out + g * a.ld_out + 4 * k, x);
-    if (k % LH == 0) a.lse[g * heads + k / LH] = (s.m + log2f(s.l)) * LN2;
+    if (k % LH == 0) a.lse[g * heads + k / LH] = empty ? -INFINITY : (s.m + log2f(s.l)) * LN2;
   }
   __device__ __forceinline__ void save(const State& s, float* dst) const {
     if (L::slot() != 0) return;
@@ -314,7 +316,15 @@ struct FwdRS {
       store4_clip(a.out, g, a.ld_out, k, a.D, x);
     }
   }
-  __device__ __forceinline__ void zero(int64_t) const {}
+  __device__ __forceinline__ void zero(int64_t g) const {
+    if (a.beta != 0.f) return;  // empty group: out = beta*out + 0
+    const int lane = lane_id();
+#pragma unroll
+    for (int w = 0; w < VEC; ++w) {
+      const int k = lane + 32 * w;
+      if (k < n4o) store4_clip(a.out, g, a.ld_out, k, a.D, f4_zero());
+    }
+  }
 };
 
 template <int VEC, int MODE>
@@ -385,7 +395,7 @@ __global__ void __launch_bounds__(256) fwd_concat_kernel(LjaArgs a, int64_t n_gr
     } else {
       acc = (float)(e - b) * __ldg(a.dst.p + t * a.dst.ld + (c - ds - de));
     }
-    if (a.mean) acc *= 1.f / (float)(e - b);
+    if (a.mean) acc *= e > b ? 1.f / (float)(e - b) : 0.f;
     float* o = a.out + g * a.ld_out + c;
     *o = a.beta != 0.f ? acc + a.beta * *o : acc;
   }
@@ -458,7 +468,7 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
   const int lc = lane_config(qi.D);
   if (q->agg != RNN_AGG_SOFTMAX && lc >= 32 && q->src.data && idx->pos_group) {
     RSCtx rx{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
-             idx->n_work, cx.partial, cx.pstride, cx.counter, 0};
+             idx->n_work, cx.partial, cx.pstride, cx.counter, 1};
     if (lc == 32) return launch_rs_mode<1>(a, rx, st);
     if (lc == 64) return launch_rs_mode<2>(a, rx, st);
     return launch_rs_mode<4>(a, rx, st);

@@ -74,3 +74,31 @@ extern "C" rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t
   RNN_LAUNCH_CHECK();
   return RNN_OK;
 }
+
+namespace rnn {
+namespace {
+__global__ void accumulate_kernel(float* __restrict__ y, int64_t ldy, const float* __restrict__ x,
+                                  int64_t ldx, int64_t rows, int cols, float beta) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  const int64_t r = i / cols;
+  const int c = (int)(i % cols);
+  float v = x[r * ldx + c];
+  if (beta != 0.f) v += beta * y[r * ldy + c];
+  y[r * ldy + c] = v;
+}
+}  // namespace
+}  // namespace rnn
+
+extern "C" rnn_status rnn_accumulate(float* y, int64_t ldy, const float* x, int64_t ldx,
+                                     int64_t rows, int32_t cols, float beta, void* stream) {
+  clear_error();
+  RNN_REQUIRE(rows >= 0 && cols >= 0 && (rows == 0 || cols == 0 || (x && y)) && ldy >= cols &&
+                  ldx >= cols,
+              RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  if (rows == 0 || cols == 0) return RNN_OK;
+  accumulate_kernel<<<(unsigned)ceil_div(rows * cols, 256), 256, 0, as_stream(stream)>>>(
+      y, ldy, x, ldx, rows, cols, beta);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}

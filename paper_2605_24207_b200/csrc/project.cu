@@ -465,8 +465,8 @@ extern "C" rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t 
                                   float* Y, int64_t ldy, rnn_precision prec, void* stream) {
   clear_error();
   RNN_REQUIRE(X && W && Y, RNN_ERR_INVALID_ARGUMENT, "X, W, Y required");
-  RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 0 && K <= 8192 && N >= 1 && N <= 256,
-              RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, K <= 8192, 1 <= N <= 256");
+  RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 0 && K <= 8192 && N >= 1 && N <= 8192,
+              RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, K <= 8192, 1 <= N <= 8192");
   RNN_REQUIRE(ldx >= K && ldw >= K && ldy >= N, RNN_ERR_INVALID_ARGUMENT, "ld too small");
   RNN_REQUIRE(prec == RNN_PREC_TF32 || prec == RNN_PREC_3XTF32, RNN_ERR_INVALID_ARGUMENT,
               "precision");
@@ -513,8 +513,8 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
                                       size_t workspace_bytes, void* stream) {
   clear_error();
   RNN_REQUIRE(X && W && dY && dW, RNN_ERR_INVALID_ARGUMENT, "X, W, dY, dW required");
-  RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 1 && K <= 8192 && N >= 1 && N <= 256,
-              RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, 1 <= K <= 8192, 1 <= N <= 256");
+  RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 1 && K <= 8192 && N >= 1 && N <= 8192,
+              RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, 1 <= K <= 8192, 1 <= N <= 8192");
   RNN_REQUIRE(ldx >= K && ldw >= K && lddy >= N && (!dX || lddx >= K), RNN_ERR_INVALID_ARGUMENT,
               "ld too small");
   cudaStream_t st = as_stream(stream);

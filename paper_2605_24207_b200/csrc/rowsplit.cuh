@@ -232,12 +232,12 @@ __device__ __noinline__ void lean_piece(const LeanOut& o, const RSCtx& cx, int64
   lean_store<VEC>(o, g, tot);
 }
 
+// empty segments: the aggregate of an empty multiset is 0, so out = beta*out (+0)
 template <int VEC>
 __device__ __noinline__ void lean_zero(const LeanOut& o, int64_t g0, int64_t g1) {
+  if (o.beta != 0.f) return;
   float4 z[4] = {f4_zero(), f4_zero(), f4_zero(), f4_zero()};
-  LeanOut o0 = o;
-  o0.beta = 0.f;
-  for (int64_t g = g0; g < g1; ++g) lean_store<VEC>(o0, g, z);
+  for (int64_t g = g0; g < g1; ++g) lean_store<VEC>(o, g, z);
 }
 
 template <class MP, int VEC, int U>

@@ -127,3 +127,184 @@ class GCNProgram:
         self.forward()
         return self.backward()
 
+
+
+class HypergraphProgram:
+    """HyGNN-style two-hop incidence join (config 4, reading 13):
+
+        Z = X Theta^T                                          (A2)
+        E_h(e; sum(z))  :- Inc(v, e), Z(v; z)                  hop 1, grouped by hyperedge
+        X'(v; mean(z))  :- Inc(v, e), E_h(e; z)                hop 2, grouped by node
+    """
+
+    def __init__(self, hg: dict, device="cuda", prec="3xtf32", rows_per_item=0):
+        dev = self.device = torch.device(device)
+        self.prec = prec
+        nk = torch.as_tensor(hg["nodes"]["key"]).to(dev)
+        hk = torch.as_tensor(hg["hyperedges"]["key"]).to(dev)
+        iv = torch.as_tensor(hg["inc"]["node"]).to(dev)
+        ih = torch.as_tensor(hg["inc"]["hyper"]).to(dev)
+        self.idx1 = rnn.build_join_index(iv, ih, nk, hk, rows_per_item=rows_per_item)
+        self.idx2 = rnn.build_join_index(ih, iv, self.idx1.group_key.clone(), nk,
+                                         rows_per_item=rows_per_item)
+        d = hg["nodes"]["x"].shape[1]
+        self.d = d
+        self.X = _dev_f32(hg["nodes"]["x"], dev)
+        self.theta = _dev_f32(hg["theta"], dev)
+        n = len(hg["nodes"]["key"])
+        self.Z = _empty(n, d, dev)
+        self.Eh = _empty(self.idx1.n_groups, d, dev)
+        self.Xo = _empty(self.idx2.n_groups, d, dev)
+        self.dEh = _empty(self.idx1.n_groups, d, dev)
+        self.dZ = _empty(n, d, dev)
+        self.dX = _empty(n, d, dev)
+        self.dTheta = torch.empty(d, d, dtype=torch.float32, device=dev)
+        self.d_out = _dev_f32(hg["d_out"][: self.idx2.n_groups], dev)
+        self.q1 = rnn.make_query("src", "sum", src=self.Z)
+        self.q2 = rnn.make_query("src", "mean", src=self.Eh)
+        self.ws = rnn.Workspace(dev)
+        self.ws_p = rnn.Workspace(dev)
+
+    @property
+    def join_rows_per_step(self):
+        return self.idx1.n_join_rows + self.idx2.n_join_rows
+
+    def forward(self):
+        rnn.project(self.X, self.theta, out=self.Z, prec=self.prec)
+        rnn.join_aggregate_fwd(self.idx1, self.q1, out=self.Eh, ws=self.ws)
+        rnn.join_aggregate_fwd(self.idx2, self.q2, out=self.Xo, ws=self.ws)
+        return self.Xo
+
+    def backward(self):
+        _lja_src_grad(self.idx2, self.q2, self.d_out, self.dEh, self.ws)
+        _lja_src_grad(self.idx1, self.q1, self.dEh, self.dZ, self.ws)
+        rnn.project_bwd(self.X, self.theta, self.dZ, want_dx=True, prec=self.prec, ws=self.ws_p,
+                        dx_out=self.dX, dw_out=self.dTheta)
+        return self.dTheta, self.dX
+
+    def step(self):
+        self.forward()
+        return self.backward()
+
+
+def _lja_src_grad(idx, q, d_out, d_src, ws):
+    """rnn_join_aggregate_bwd writing only the source-embedding gradient into d_src."""
+    import ctypes as C
+    _, bb = rnn.lja_workspace_size(idx, q)
+    w = ws.get(bb)
+    rnn._check(rnn.lib().rnn_join_aggregate_bwd(
+        C.byref(idx.c), C.byref(q), None, 0, None, rnn._ptr(d_out), d_out.stride(0),
+        rnn._ptr(d_src), None, None, None, rnn._ptr(w), w.numel(), rnn._stream()))
+    return d_src
+
+
+class HGTProgram:
+    """One HGT attention layer over a heterogeneous schema (config 3; Fig. 4, PAPER.md:905-936,
+    appendix :1343-1409; SURVEY sec 8c reading 3/12).
+
+    Per relation phi = (tau_s -> tau_t), with the transformations pushed below the join:
+        K'_phi = H_{tau_s} Wk_phi^T      (KLin . W_ATT . mu / sqrt(d/h) folded)
+        M'_phi = H_{tau_s} Wm_phi^T      (MLin . W_MSG folded)
+        Q_phi  = H_{tau_t} Wq_{tau_t}^T
+        O_phi(t; softmax-weighted sum) :- phi(s, t), K'(s), M'(s), Q(t)     (A4, per head)
+        H_tilda_{tau_t} = sum_phi O_phi                                      (A7 union)
+    All projections of one node type are ONE tcgen05 GEMM (weights stacked); every relation's
+    index has dense groups over its target type, so outputs share the target's key order.
+    """
+
+    def __init__(self, mag: dict, device="cuda", prec="3xtf32", rows_per_item=0, seed=7):
+        dev = self.device = torch.device(device)
+        self.prec = prec
+        self.d, self.h = mag["d"], mag["heads"]
+        d = self.d
+        rng = np.random.default_rng(seed)
+        types = list(mag["n"].keys())
+        self.keys = {t: torch.as_tensor(mag["key"][t]).to(dev) for t in types}
+        self.H = {t: _dev_f32(mag["h"][t], dev) for t in types}
+        self.n = dict(mag["n"])
+        rels = mag["rels"]
+        # column blocks of each type's stacked projection
+        blocks = {t: [] for t in types}
+        for name, r in rels.items():
+            blocks[r["src_type"]] += [("k", name), ("m", name)]
+            blocks[r["dst_type"]] += [("q", name)]
+        self.blocks = {t: b for t, b in blocks.items() if b}
+        scale = 1.0 / np.sqrt(d / self.h)
+        self.W, self.Y, self.dY, self.dW, self.dH = {}, {}, {}, {}, {}
+        wq = {t: rng.standard_normal((d, d)) / np.sqrt(d) for t in types}
+        for t, b in self.blocks.items():
+            ws = []
+            for kind, name in b:
+                w = rng.standard_normal((d, d)) / np.sqrt(d)
+                if kind == "k":
+                    w = w * scale            # mu / sqrt(d/h) folded into K'
+                if kind == "q":
+                    w = wq[t]                # Q shared by every relation into t
+                ws.append(w)
+            self.W[t] = _dev_f32(np.concatenate(ws, 0).astype(np.float32), dev)
+            nb = len(b)
+            self.Y[t] = _empty(self.n[t], nb * d, dev)
+            self.dY[t] = _empty(self.n[t], nb * d, dev)
+            self.dW[t] = torch.empty(nb * d, d, dtype=torch.float32, device=dev)
+            self.dH[t] = _empty(self.n[t], d, dev)
+        self.col = {(kind, name): (t, i) for t, b in self.blocks.items() for i, (kind, name) in enumerate(b)}
+        self.idx, self.q, self.O, self.lse, self.dO = {}, {}, {}, {}, {}
+        self.targets = sorted({r["dst_type"] for r in rels.values()})
+        self.Ht = {t: _empty(self.n[t], d, dev) for t in self.targets}
+        self.d_out = {t: _dev_f32(rng.standard_normal((self.n[t], d)).astype(np.float32), dev)
+                      for t in self.targets}
+        for name, r in rels.items():
+            ts, tt = r["src_type"], r["dst_type"]
+            self.idx[name] = rnn.build_join_index(
+                torch.as_tensor(r["src"]).to(dev), torch.as_tensor(r["dst"]).to(dev),
+                self.keys[ts], self.keys[tt], dense_groups=True, rows_per_item=rows_per_item)
+            self.q[name] = rnn.make_query("src", "softmax", src=self._blk("m", name),
+                                          src_key=self._blk("k", name), dst=self._blk("q", name),
+                                          heads=self.h, scale=1.0)
+            self.O[name] = _empty(self.n[tt], d, dev)
+            self.lse[name] = torch.empty(max(self.n[tt], 1), self.h, dtype=torch.float32, device=dev)
+        self.rels = rels
+        self.ws = rnn.Workspace(dev)
+        self.ws_p = rnn.Workspace(dev)
+
+    def _blk(self, kind, name, grad=False):
+        t, i = self.col[(kind, name)]
+        buf = self.dY[t] if grad else self.Y[t]
+        return buf[:, i * self.d:(i + 1) * self.d]
+
+    @property
+    def join_rows_per_step(self):
+        return sum(ix.n_join_rows for ix in self.idx.values())
+
+    def forward(self):
+        for t in self.blocks:
+            rnn.project(self.H[t], self.W[t], out=self.Y[t], prec=self.prec)
+        first = {t: True for t in self.targets}
+        for name, r in self.rels.items():
+            tt = r["dst_type"]
+            rnn.join_aggregate_fwd(self.idx[name], self.q[name], out=self.O[name],
+                                   lse=self.lse[name], ws=self.ws)
+            rnn.accumulate(self.Ht[tt], self.O[name], beta=0.0 if first[tt] else 1.0)
+            first[tt] = False
+        return self.Ht
+
+    def backward(self):
+        import ctypes as C
+        for name, r in self.rels.items():
+            idx, q = self.idx[name], self.q[name]
+            dO = self.d_out[r["dst_type"]]
+            _, bb = rnn.lja_workspace_size(idx, q)
+            w = self.ws.get(bb)
+            dm, dk, dq = self._blk("m", name, True), self._blk("k", name, True), self._blk("q", name, True)
+            rnn._check(rnn.lib().rnn_join_aggregate_bwd(
+                C.byref(idx.c), C.byref(q), rnn._ptr(self.O[name]), self.O[name].stride(0),
+                rnn._ptr(self.lse[name]), rnn._ptr(dO), dO.stride(0), rnn._ptr(dm), rnn._ptr(dk),
+                None, rnn._ptr(dq), rnn._ptr(w), w.numel(), rnn._stream()))
+        for t in self.blocks:
+            rnn.project_bwd(self.H[t], self.W[t], self.dY[t], want_dx=True, prec=self.prec,
+                            ws=self.ws_p, dx_out=self.dH[t], dw_out=self.dW[t])
+        return self.dW, self.dH
+
+    def step(self):
+        self.forward()
+        return self.backward()

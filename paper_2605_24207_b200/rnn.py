@@ -20,7 +20,7 @@ RNN_OK = 0
 AGG = {"sum": 0, "mean": 1, "softmax": 2}
 COMBINE = {"src": 0, "mul": 1, "add": 2, "concat": 3}
 BY_ROW, BY_POSITION = 0, 1
-IDX_VALIDATE, IDX_WITHIN_GROUP_BY_SRC_KEY, IDX_NO_TRANSPOSE = 1, 2, 4
+IDX_VALIDATE, IDX_WITHIN_GROUP_BY_SRC_KEY, IDX_NO_TRANSPOSE, IDX_DENSE_GROUPS = 1, 2, 4, 8
 PREC = {"tf32": 0, "3xtf32": 1}
 
 
@@ -84,6 +84,8 @@ def lib():
                                       C.c_int, vp, sz, vp]
         L.rnn_gcn_norm.argtypes = [C.POINTER(JoinIndexC), vp, vp, sz, vp]
         L.rnn_hash_partition.argtypes = [vp, i64, i32, C.c_uint64, vp, vp]
+        L.rnn_accumulate.argtypes = [vp, i64, vp, i64, i64, i32, C.c_float, vp]
+        L.rnn_accumulate.restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
                   "rnn_join_aggregate_bwd", "rnn_group_softmax", "rnn_group_softmax_bwd",
                   "rnn_project", "rnn_project_bwd_workspace_size", "rnn_project_bwd",
@@ -154,8 +156,8 @@ class JoinIndex:
 
 
 def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, validate=False,
-                     within_group_by_src_key=False, transpose=True, rows_per_item=0,
-                     stream=None) -> JoinIndex:
+                     within_group_by_src_key=False, transpose=True, dense_groups=False,
+                     rows_per_item=0, stream=None) -> JoinIndex:
     """rnn_build_join_index: phase 1 (sizes, SYNC), allocate, phase 2 (fill)."""
     L = lib()
     e_dst_key = _cuda(e_dst_key, torch.int64, "e_dst_key").contiguous()
@@ -164,7 +166,7 @@ def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, valida
     src_key = None if src_key is None else _cuda(src_key, torch.int64, "src_key").contiguous()
     dst_key = None if dst_key is None else _cuda(dst_key, torch.int64, "dst_key").contiguous()
     flags = (IDX_VALIDATE if validate else 0) | (IDX_WITHIN_GROUP_BY_SRC_KEY if within_group_by_src_key else 0) \
-        | (0 if transpose else IDX_NO_TRANSPOSE)
+        | (0 if transpose else IDX_NO_TRANSPOSE) | (IDX_DENSE_GROUPS if dense_groups else 0)
     n_e = e_dst_key.numel()
     n_s = 0 if src_key is None else src_key.numel()
     n_t = 0 if dst_key is None else dst_key.numel()
@@ -369,3 +371,11 @@ def hash_partition(keys, P, seed, stream=None):
     owner = torch.empty(keys.numel(), dtype=torch.int32, device=keys.device)
     _check(lib().rnn_hash_partition(_ptr(keys), keys.numel(), P, seed, _ptr(owner), _stream(stream)))
     return owner
+
+
+def accumulate(y, x, beta=1.0, stream=None):
+    """y = beta * y + x (union over relations of per-relation results)."""
+    rows, cols = x.shape
+    _check(lib().rnn_accumulate(_ptr(y), y.stride(0), _ptr(x), x.stride(0), rows, cols,
+                                float(beta), _stream(stream)))
+    return y

@@ -54,6 +54,6 @@ def test_host_side_checks_without_gpu(lib):
                                   C.byref(idx), None, C.byref(wsb), None)
     assert st == 1 and b"e_src_key" in lib.rnn_last_error()
     # bad projection shapes are rejected before any launch
-    assert lib.rnn_project(C.c_void_p(16), 10, 10, 10, C.c_void_p(16), 300, 10, None,
-                           C.c_void_p(16), 300, 0, None) == 5
+    assert lib.rnn_project(C.c_void_p(16), 10, 10, 10, C.c_void_p(16), 9000, 10, None,
+                           C.c_void_p(16), 9000, 0, None) == 5
     assert lib.rnn_hash_partition(None, 10, 0, 0, None, None) == 1
