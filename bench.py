@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="arxiv", choices=["arxiv", "cora"])
+    ap.add_argument("--config", default="arxiv", choices=["arxiv", "cora", "hyper", "mag"])
     ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-e2e", action="store_true")
@@ -49,11 +49,28 @@ def parse():
     return ap.parse_args()
 
 
-def make_graph(cfg, seed):
+def make_graph(cfg, seed, sample=False):
+    """Seeded synthetic input of a config; `sample` = the bounded
+    same-structure instance the CPU oracle is timed on (hyper, mag: 1/20)."""
     import synth
     if cfg == "arxiv":
         return synth.arxiv_like(seed)
+    if cfg == "hyper":
+        if sample:
+            return synth.hypergraph_like(seed, n_nodes=50_000, n_hyper=10_000, n_inc=250_000)
+        return synth.hypergraph_like(seed)
+    if cfg == "mag":
+        return synth.mag_like(seed, scale=0.05 if sample else 1.0)
     return synth.cora_like(seed)
+
+
+def make_program(cfg, data, dev, prec):
+    from paper_2605_24207_b200 import programs
+    if cfg == "hyper":
+        return programs.HypergraphProgram(data, device=dev, prec=prec)
+    if cfg == "mag":
+        return programs.HGTProgram(data, device=dev, prec=prec)
+    return programs.GCNProgram(data, device=dev, prec=prec)
 
 
 WORKLOAD = {
@@ -61,6 +78,10 @@ WORKLOAD = {
              "(169,343 node tuples, 1,166,243 edge tuples + self-loops, 128-dim)",
     "cora": "2-layer GCN as lifted query on synthetic Cora-shaped relations "
             "(2,708 node tuples, 10,556 edge tuples + self-loops, 1,433->16->7)",
+    "hyper": "HyGNN two-hop incidence join (node->hyperedge SUM, hyperedge->node MEAN) on "
+             "synthetic power-law hypergraph (1M nodes, 200K hyperedges, 5M incidences, 128-dim)",
+    "mag": "HGT attention layer (4 relations, 8-head grouped softmax, dense target groups) on "
+           "synthetic ogbn-mag-shaped schema (1.94M nodes, 21.1M edges, 128-dim)",
 }
 
 
@@ -126,8 +147,6 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_24207_b200 import programs
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -138,7 +157,8 @@ def run_ours(args):
 
     graph = make_graph(args.config, args.seed)
     # multi-GPU: replicas of the single-GPU step (weak scaling)
-    prog = programs.GCNProgram(graph, device=dev, prec=args.prec)
+    prog = make_program(args.config, graph, dev, args.prec)
+    del graph
     rows = prog.join_rows_per_step
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
@@ -186,15 +206,10 @@ def run_ours(args):
 
     # ---- roofline of the dominant hot-path kernel (the fused LJA) ----
     peak, peak_src = peaks()
-    d = prog.dims[1:]
-    # algorithmic bytes per LJA launch (gather model):
-    #   fwd: per join row  src_row 4 + weight 4 + gathered row 4d ; per group  out row 4d + ptr 8
-    #   bwd: per join row  src_group 4 + src_pos 4 + weight 4 + gathered dOut row 4d ;
-    #        per source  d_src row 4d + ptr 8
-    Ep, G = prog.idx1.n_join_rows, prog.G
-    fwd_bytes = float(np.mean([Ep * (8 + 4 * dd) + G * (4 * dd + 8) for dd in d]))
-    bwd_bytes = float(np.mean([Ep * (12 + 4 * dd) + G * (4 * dd + 8) for dd in d]))
-    cand = {"lja_fwd": (per["lja_fwd"], fwd_bytes), "lja_bwd": (per["lja_bwd"], bwd_bytes)}
+    # algorithmic bytes per LJA launch (gather model, DESIGN.md "Byte model";
+    # programs._sum_bytes / _sum_bwd_bytes / HGTProgram.lja_bytes)
+    byt = prog.lja_bytes()
+    cand = {"lja_fwd": (per["lja_fwd"], byt["lja_fwd"]), "lja_bwd": (per["lja_bwd"], byt["lja_bwd"])}
     dom = max(cand, key=lambda k: cand[k][0] or 0)
     ms, byt = cand[dom]
     achieved = byt / (ms * 1e-3) / 1e9
@@ -225,7 +240,8 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded; shapes of BASELINE.json configs, see DESIGN.md)",
             "config": {"workload": WORKLOAD[args.config], "config": args.config,
-                       "join_rows_per_step": rows, "layers": prog.L, "dims": prog.dims,
+                       "join_rows_per_step": rows,
+                       **({"layers": prog.L, "dims": prog.dims} if hasattr(prog, "dims") else {}),
                        "projection_precision": args.prec, "l2": "flushed between timed steps",
                        "parallelism": f"replica x{world}" if world > 1 else "single"},
             "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
@@ -251,21 +267,21 @@ def count_launches(prog):
 
 def run_e2e(prog, args, world, dev):
     """Same metric through the public API with HOST buffers: every step copies its inputs
-    (node features X0 and the upstream gradient) from pinned host memory and reads the
-    parameter gradients dW back, inside the timed region."""
+    (node features and the upstream gradient, prog.host_io()) from pinned host memory and
+    reads the parameter gradients back, inside the timed region."""
     import torch
-    X_host = prog.X0.cpu().pin_memory()
-    D_host = prog.d_out.cpu().pin_memory()
-    dW_host = [torch.empty(w.shape, dtype=torch.float32).pin_memory() for w in prog.dW]
-    h2d = X_host.numel() * 4 + D_host.numel() * 4
-    d2h = sum(w.numel() * 4 for w in dW_host)
+    ins, outs = prog.host_io()
+    in_host = [x.cpu().pin_memory() for x in ins]
+    out_host = [torch.empty(w.shape, dtype=torch.float32).pin_memory() for w in outs]
+    h2d = sum(x.numel() * 4 for x in in_host)
+    d2h = sum(w.numel() * 4 for w in out_host)
     steps = max(3, args.steps // 2)
 
     def one():
-        prog.X0.copy_(X_host, non_blocking=True)
-        prog.d_out.copy_(D_host, non_blocking=True)
+        for a, b in zip(ins, in_host):
+            a.copy_(b, non_blocking=True)
         prog.step()
-        for a, b in zip(dW_host, prog.dW):
+        for a, b in zip(out_host, outs):
             a.copy_(b, non_blocking=True)
 
     one()
@@ -286,12 +302,15 @@ def run_e2e(prog, args, world, dev):
 # the oracle (CPU, fp64): cpu_baseline and the --impl reference arm
 # ------------------------------------------------------------------------------------------
 def oracle_timing(args, steps=1):
-    """The oracle (fp64, single-threaded C) on a bounded sample of the same workload: the
-    first layer of the program, forward + backward including its projections (about a
-    third of a step; ~10-30 s of CPU on the GPU box).  Rows/s = that layer's join rows / t."""
+    """The oracle (fp64, single-threaded C) on a bounded sample of the same workload (~10-30 s
+    of CPU on the GPU box): arxiv -- the first of the three layers, fwd + bwd incl. its
+    projections; hyper / mag -- the whole step on a same-structure instance scaled down
+    (make_graph sample=True).  Rows/s = the sample's join rows / t."""
     import oracle
     from oracle import programs as op
     oracle.build()
+    if args.config in ("hyper", "mag"):
+        return _oracle_sampled(args, steps, oracle, op)
     graph = make_graph(args.config, args.seed)
     L = len(graph["W"])
     if args.config == "arxiv":
@@ -310,6 +329,39 @@ def oracle_timing(args, steps=1):
     return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{args.config}: first {sample_layers} of {L} layers (fwd+bwd incl. "
                       f"projections, {rows} join rows), {steps} run(s), fp64 single-threaded C, "
+                      f"median {t:.2f} s"}, t, rows
+
+
+def _oracle_sampled(args, steps, oracle, op):
+    data = make_graph(args.config, args.seed, sample=True)
+    times = []
+    if args.config == "hyper":
+        o1 = oracle.build_join_index(data["inc"]["node"], data["inc"]["hyper"],
+                                     data["nodes"]["key"], data["hyperedges"]["key"])
+        rows = 2 * o1["n_join_rows"]
+        what = (f"whole step on a 1/20-scale hypergraph ({len(data['nodes']['key'])} nodes, "
+                f"{len(data['inc']['node'])} incidences)")
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            op.hypergraph_step(data)
+            times.append(time.perf_counter() - t0)
+    else:
+        rng = np.random.default_rng(1)
+        d, h = data["d"], data["heads"]
+        rows = sum(len(r["src"]) for r in data["rels"].values())
+        what = f"whole HGT layer on a 1/20-scale ogbn-mag-shaped schema ({rows} edges)"
+        Ws = {k: rng.standard_normal((d, d)) / np.sqrt(d) for k in ("k", "m", "q")}
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            for r in data["rels"].values():
+                ts, tt = r["src_type"], r["dst_type"]
+                op.hgt_relation(data["h"][ts], data["h"][tt], Ws["k"], Ws["m"], Ws["q"],
+                                data["key"][ts], data["key"][tt], r["src"], r["dst"], h,
+                                rng.standard_normal((data["n"][tt], d)))
+            times.append(time.perf_counter() - t0)
+    t = float(np.median(times))
+    return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{args.config}: {what}, {steps} run(s), fp64 single-threaded C, "
                       f"median {t:.2f} s"}, t, rows
 
 

@@ -222,6 +222,45 @@ rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, co
                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* ===================================================================================== */
+/* A6. Multi-way cyclic joins: DHN closed-walk pattern aggregates                        */
+/* ===================================================================================== */
+/* The deep homomorphism network rules (config 5), read as closed walks
+ * (PAPER.md:1481; Eq. 3 of the appendix, :1500; SURVEY sec 8c reading #9):
+ *
+ *   C_k(n) = f0(n) (.) sum over closed walks n -> v1 -> ... -> v_{k-1} -> n of
+ *                                 f1(v1) (.) f2(v2) (.) ... (.) f_{k-1}(v_{k-1})
+ *   k = 2: the single atom Edge(n, v1) (no closing edge: C2(n) = f0(n) (.) sum_{n->v} f1(v))
+ *   k = 3: Edge(n,v1), Edge(v1,v2), Edge(v2,n)        (triangle rule)
+ *   k = 4: Edge(n,v1), Edge(v1,v2), Edge(v2,v3), Edge(v3,n)   (4-cycle)
+ * with multiplicity: duplicated Edge tuples give distinct join rows (distinct walks).
+ *
+ * adj: the join index of Edge(n, v) |x| Node(v) |x| Node(n) grouped by n, i.e. built with
+ *      e_src_key = v, e_dst_key = n and S = T = the node relation (n_src_rows == n_dst_rows),
+ *      WITH the transposed CSR (not RNN_IDX_NO_TRANSPOSE).  Any other flag is accepted.
+ *      Roots are its groups: out-neighbours of group g are src_row[group_ptr[g] ..], the
+ *      in-neighbours of node row r are src_group[src_ptr[r] ..].
+ * f:   k operands, RNN_BY_ROW over node rows, all of dim d (1 <= d <= 128), any ld.
+ *      f[0].data may be NULL (all ones).
+ * out: [n_groups, ld_out] fp32, C_k of every root in group order (overwritten).
+ *
+ * Closed walks are rotation invariant, so the backward is the same kernel with rotated
+ * operands (d f_j(x) = the walk aggregate rooted at x of (f_{j+1}, ..., g, ..., f_{j-1}),
+ * g = f0 (.) dOut), and d f0 = dOut (.) sum_walks prod f_i.
+ * Work: k = 3 enumerates sum_v deg(v)^2 candidate wedges against a per-root mark array;
+ * k = 4 is factorised through the middle vertex: S3(w) = sum_{w->p->n} f3(p) is scattered
+ * into a per-CTA dense slab, then every 2-path n->v->w reads it.  k = 4 uses fp32 atomics
+ * into the slab, so its rounding order (only) is not deterministic. */
+rnn_status rnn_dhn_workspace_size(const rnn_join_index* adj, int32_t k, int32_t d,
+                                  size_t* bytes);   /* host-only, no device work */
+rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,
+                       int64_t ld_out, void* workspace, size_t workspace_bytes, void* stream);
+/* d_out [n_groups, ld_dout]; d_f[i] [n_src_rows, ld_df] by node row, overwritten (rows that
+ * are on no closed walk get 0); any d_f[i] may be NULL. */
+rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                       const float* d_out, int64_t ld_dout, float* const* d_f, int64_t ld_df,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* ===================================================================================== */
 /* Program helpers                                                                       */
 /* ===================================================================================== */
 /* GCN normalisation as a per-join-position weight (use with RNN_BY_POSITION):

@@ -18,6 +18,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rnn {
@@ -310,6 +312,220 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Persistent projection kernel: Y[M, N] = A[M, K] B[N, K]^T (+ bias), both K-major, for the
+// tall-skinny shapes of the hot path (M = node count, K, N <= a few hundred).  The operand B
+// (the weight tile of this CTA's column block) is loaded ONCE and stays resident in shared
+// memory (split into hi/lo once for 3xTF32); the CTA then streams 128-row tiles of A through a
+// TMA ring, accumulating into one of two TMEM buffers while dedicated epilogue warps drain the
+// other, so loads, MMAs and stores of consecutive tiles overlap.  One CTA per SM; CTA c owns
+// column block c % n_tiles_n and row tiles c / n_tiles_n, + grid / n_tiles_n, ...
+//   warp 0: TMA producer    warp 1: TMEM alloc + MMA issuer
+//   warps 2-5: 3xTF32 hi/lo converters    warps 6-9: epilogue (TMEM -> registers -> HBM)
+// ------------------------------------------------------------------------------------------
+constexpr int PT_THREADS = 320;
+constexpr int PT_MAX_STAGES = 6;
+
+struct ProjParams {
+  int64_t M;
+  int N, BN, n_tiles_n;
+  int64_t n_tiles_m;
+  int nkb;                // K blocks of BK
+  int stages;
+  float* out; int64_t ldo;
+  const float* bias;
+  uint32_t tmem_cols;
+};
+
+__device__ __forceinline__ void split_tile(float4* hi, float4* lo, uint32_t n16, int t) {
+  for (uint32_t i = t; i < n16; i += 128) {
+    float4 x = hi[i], h, l;
+    h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
+    h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
+    h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
+    h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
+    hi[i] = h; lo[i] = l;
+  }
+}
+
+template <bool SPLIT3>
+__global__ void __launch_bounds__(PT_THREADS, 1)
+    tc_proj_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+                   ProjParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  constexpr uint32_t A_BYTES = BM * BK * 4;
+  const uint32_t B_BYTES = (uint32_t)p.BN * BK * 4;            // one K block of B
+  const uint32_t B_RES = B_BYTES * p.nkb;                       // resident B (hi)
+  const uint32_t A_STAGE = A_BYTES * (SPLIT3 ? 2u : 1u);
+  uint8_t* b_hi = smem;
+  uint8_t* b_lo = smem + B_RES;
+  uint8_t* a_base = smem + B_RES * (SPLIT3 ? 2u : 1u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(a_base + p.stages * A_STAGE);
+  uint64_t* a_full = bars;
+  uint64_t* a_conv = a_full + PT_MAX_STAGES;
+  uint64_t* a_empty = a_conv + PT_MAX_STAGES;
+  uint64_t* b_full = a_empty + PT_MAX_STAGES;
+  uint64_t* b_conv = b_full + 1;
+  uint64_t* acc_full = b_conv + 1;     // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = blockIdx.x % p.n_tiles_n;
+  const int n0 = nt * p.BN;
+  const int64_t mt0 = blockIdx.x / p.n_tiles_n;
+  const int64_t mstep = gridDim.x / p.n_tiles_n;
+
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < PT_MAX_STAGES; ++s) {
+        mbar_init(&a_full[s], 1);
+        mbar_init(&a_conv[s], 128);
+        mbar_init(&a_empty[s], 1);
+      }
+      mbar_init(b_full, 1);
+      mbar_init(b_conv, 128);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&acc_full[b], 1);
+        mbar_init(&acc_empty[b], 128);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(p.tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ta)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tb)) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(b_full, B_RES);
+      for (int kb = 0; kb < p.nkb; ++kb) tma_load_2d(&tb, b_hi + kb * B_BYTES, b_full, kb * BK, n0);
+      int64_t it = 0;
+      for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep) {
+        for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+          const int s = (int)(it % p.stages);
+          const uint32_t ph = (uint32_t)((it / p.stages) & 1);
+          if (it >= p.stages) mbar_wait(&a_empty[s], ph ^ 1);
+          mbar_expect_tx(&a_full[s], A_BYTES);
+          tma_load_2d(&ta, a_base + s * A_STAGE, &a_full[s], kb * BK, (int)(mt * BM));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idesc = make_idesc(p.BN, false, false);
+    mbar_wait(SPLIT3 ? b_conv : b_full, 0);
+    tc_fence_after();
+    int64_t it = 0;
+    int j = 0;
+    for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
+      const int buf = j & 1;
+      if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(buf * p.BN);
+      for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+        const int s = (int)(it % p.stages);
+        const uint32_t ph = (uint32_t)((it / p.stages) & 1);
+        mbar_wait(SPLIT3 ? &a_conv[s] : &a_full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ah = smem_u32(a_base + s * A_STAGE);
+          const uint32_t bh = smem_u32(b_hi + kb * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t ad = make_desc(ah, false, kk, 0);
+            const uint64_t bd = make_desc(bh, false, kk, 0);
+            tc_mma_tf32(d, ad, bd, idesc, (kb | kk) != 0);
+            if (SPLIT3) {
+              const uint64_t al = make_desc(ah + A_BYTES, false, kk, 0);
+              const uint64_t bl = make_desc(smem_u32(b_lo + kb * B_BYTES), false, kk, 0);
+              tc_mma_tf32(d, ad, bl, idesc, 1u);
+              tc_mma_tf32(d, al, bd, idesc, 1u);
+            }
+          }
+          tc_commit(&a_empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(&acc_full[buf]);
+      __syncwarp();
+    }
+  } else if (warp < 6) {
+    if (SPLIT3) {
+      const int t = threadIdx.x - 64;
+      mbar_wait(b_full, 0);
+      split_tile(reinterpret_cast<float4*>(b_hi), reinterpret_cast<float4*>(b_lo), B_RES / 16, t);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(b_conv);
+      int64_t it = 0;
+      for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep) {
+        for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+          const int s = (int)(it % p.stages);
+          const uint32_t ph = (uint32_t)((it / p.stages) & 1);
+          mbar_wait(&a_full[s], ph);
+          uint8_t* a = a_base + s * A_STAGE;
+          split_tile(reinterpret_cast<float4*>(a), reinterpret_cast<float4*>(a + A_BYTES),
+                     A_BYTES / 16, t);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&a_conv[s]);
+        }
+      }
+    }
+  } else {
+    // epilogue warps 6..9 -> TMEM lane quadrants 2, 3, 0, 1
+    const int quad = warp & 3;
+    int j = 0;
+    for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
+      const int buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const int64_t row = mt * BM + quad * 32 + lane;
+      const bool row_ok = row < p.M;
+      float* dst_row = p.out + row * p.ldo;
+      for (int c0 = 0; c0 < p.BN; c0 += 16) {
+        uint32_t r[16];
+        tc_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * p.BN + c0), r);
+        const int col0 = n0 + c0;
+        if (!row_ok || col0 >= p.N) continue;
+        float v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          v[q] = __uint_as_float(r[q]) + ((p.bias && col0 + q < p.N) ? __ldg(p.bias + col0 + q) : 0.f);
+        float* dst = dst_row + col0;
+        if (col0 + 16 <= p.N && (p.ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0)) {
+#pragma unroll
+          for (int q = 0; q < 16; q += 4)
+            __stcs(reinterpret_cast<float4*>(dst + q), make_float4(v[q], v[q + 1], v[q + 2], v[q + 3]));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (col0 + q < p.N) dst[q] = v[q];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(p.tmem_cols));
+  }
+}
+
 // out[r, c] = sum_z partial[z, r, c]   (fixed order => deterministic split-K)
 __global__ void splitk_reduce(const float* __restrict__ part, int64_t splits, int64_t stride,
                               int64_t rows, int cols, int64_t ldp, float* __restrict__ out,
@@ -443,6 +659,36 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
     bias_fill<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(Y, M, N, ldy, bias);
     RNN_LAUNCH_CHECK();
     return RNN_OK;
+  }
+  {
+    // persistent resident-B kernel when B's column block fits next to a 2-deep A ring
+    const bool s3 = prec == RNN_PREC_3XTF32;
+    const int nkb = (int)ceil_div(Kred, BK);
+    const int n_tiles_n = (int)ceil_div(N, 128);
+    const int BN = (int)((ceil_div(N, n_tiles_n) + 15) / 16 * 16);
+    const size_t b_res = (size_t)BN * BK * 4 * nkb * (s3 ? 2 : 1);
+    const size_t a_stage = (size_t)BM * BK * 4 * (s3 ? 2 : 1);
+    const size_t budget = 227 * 1024 - 1024 - 256;
+    if (b_res + 2 * a_stage <= budget && n_tiles_n <= num_sms()) {
+      ProjParams q{};
+      q.M = M; q.N = N; q.BN = BN; q.n_tiles_n = n_tiles_n;
+      q.n_tiles_m = ceil_div(M, BM);
+      q.nkb = nkb;
+      q.stages = (int)std::min<size_t>(PT_MAX_STAGES, (budget - b_res) / a_stage);
+      q.out = Y; q.ldo = ldy; q.bias = bias;
+      q.tmem_cols = pow2_cols(2 * BN);
+      CUtensorMap ta, tb;
+      RNN_TRY(make_map(&ta, A, Kred, M, lda, BK, BM));
+      RNN_TRY(make_map(&tb, B, Kred, N, ldb, BK, (uint32_t)BN));
+      const int64_t per_n = std::max<int64_t>(1, std::min<int64_t>(num_sms() / n_tiles_n, q.n_tiles_m));
+      const unsigned grid = (unsigned)(per_n * n_tiles_n);
+      const size_t smem = b_res + q.stages * a_stage + 1024 + 8 * (3 * PT_MAX_STAGES + 6) + 64;
+      auto kern = s3 ? tc_proj_kernel<true> : tc_proj_kernel<false>;
+      RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, PT_THREADS, smem, st>>>(ta, tb, q);
+      RNN_LAUNCH_CHECK();
+      return RNN_OK;
+    }
   }
   GemmParams p{};
   p.M = M; p.N = N;

@@ -37,7 +37,41 @@ def _empty(n, d, device):
     return torch.empty((max(n, 1), ld), dtype=torch.float32, device=device)[:n, :d]
 
 
-class GCNProgram:
+class _Program:
+    """Shared plumbing: optional per-kernel CUDA-event timers (bench.py), the algorithmic
+    byte model of the LJA launches and the step's host I/O."""
+    timers = None  # optional {"lja_fwd": [...], "lja_fwd_end": [...], ...} event lists
+
+    def _t(self, name):
+        if self.timers is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.timers.setdefault(name, []).append(e)
+        return e
+
+    def step(self):
+        self.forward()
+        return self.backward()
+
+
+def _sum_bytes(idx, d, weighted=False, mean=False):
+    """Gather-model bytes of one SUM/MEAN LJA forward launch: per join row the source row id
+    (4), the edge weight (4, if any), the gathered d-vector (4d), the group's extent for MEAN
+    (8); per group the output row (4d) and its CSR pointer (8)."""
+    return idx.n_join_rows * (4 + 4 * d + (4 if weighted else 0) + (8 if mean else 0)) + \
+        idx.n_groups * (4 * d + 8)
+
+
+def _sum_bwd_bytes(idx, d, weighted=False, mean=False):
+    """... backward launch over the transposed CSR: per join row src_pos (4) + group id (4)
+    + weight (4, if any) + gathered upstream d-vector (4d) (+8 MEAN); per source row the
+    gradient row (4d) + pointer (8)."""
+    return idx.n_join_rows * (8 + 4 * d + (4 if weighted else 0) + (8 if mean else 0)) + \
+        idx.n_src_rows * (4 * d + 8)
+
+
+class GCNProgram(_Program):
     """L-layer GCN as lifted queries; step() = forward + backward of every layer."""
 
     def __init__(self, graph: dict, device="cuda", prec="3xtf32", rows_per_item=0):
@@ -75,19 +109,22 @@ class GCNProgram:
             idx, w = (self.idx1, self.w1) if l == 0 else (self.idx2, self.w2)
             self.q.append((idx, rnn.make_query("src", "sum", src=self.Z[l], edge=w,
                                                edge_mode=rnn.BY_POSITION)))
-        self.timers = None  # optional {"lja_fwd": [...], ...} event lists
 
     @property
     def join_rows_per_step(self):
         return self.idx1.n_join_rows + (self.L - 1) * (self.idx2.n_join_rows if self.L > 1 else 0)
 
-    def _t(self, name):
-        if self.timers is None:
-            return None
-        e = torch.cuda.Event(enable_timing=True)
-        e.record()
-        self.timers.setdefault(name, []).append(e)
-        return e
+    def lja_bytes(self):
+        """Average algorithmic bytes per LJA launch {kernel: bytes} (fwd, bwd over layers)."""
+        ix = [self.idx1] + [self.idx2] * (self.L - 1)
+        d = self.dims[1:]
+        return {"lja_fwd": float(np.mean([_sum_bytes(i, dd, True) for i, dd in zip(ix, d)])),
+                "lja_bwd": float(np.mean([_sum_bwd_bytes(i, dd, True) for i, dd in zip(ix, d)]))}
+
+    def host_io(self):
+        """(inputs, outputs) a user's step moves across PCIe: features + upstream gradient in,
+        parameter gradients out."""
+        return [self.X0, self.d_out], list(self.dW)
 
     def forward(self):
         for l in range(self.L):
@@ -123,13 +160,8 @@ class GCNProgram:
             rnn._ptr(d_src), None, None, None, rnn._ptr(w), w.numel(), rnn._stream()))
         return d_src
 
-    def step(self):
-        self.forward()
-        return self.backward()
 
-
-
-class HypergraphProgram:
+class HypergraphProgram(_Program):
     """HyGNN-style two-hop incidence join (config 4, reading 13):
 
         Z = X Theta^T                                          (A2)
@@ -169,22 +201,35 @@ class HypergraphProgram:
     def join_rows_per_step(self):
         return self.idx1.n_join_rows + self.idx2.n_join_rows
 
+    def lja_bytes(self):
+        d = self.d
+        return {"lja_fwd": (_sum_bytes(self.idx1, d) + _sum_bytes(self.idx2, d, mean=True)) / 2,
+                "lja_bwd": (_sum_bwd_bytes(self.idx1, d) + _sum_bwd_bytes(self.idx2, d, mean=True)) / 2}
+
+    def host_io(self):
+        return [self.X, self.d_out], [self.dTheta]
+
     def forward(self):
+        self._t("proj_fwd")
         rnn.project(self.X, self.theta, out=self.Z, prec=self.prec)
-        rnn.join_aggregate_fwd(self.idx1, self.q1, out=self.Eh, ws=self.ws)
-        rnn.join_aggregate_fwd(self.idx2, self.q2, out=self.Xo, ws=self.ws)
+        self._t("proj_fwd_end")
+        for idx, q, out in ((self.idx1, self.q1, self.Eh), (self.idx2, self.q2, self.Xo)):
+            self._t("lja_fwd")
+            rnn.join_aggregate_fwd(idx, q, out=out, ws=self.ws)
+            self._t("lja_fwd_end")
         return self.Xo
 
     def backward(self):
-        _lja_src_grad(self.idx2, self.q2, self.d_out, self.dEh, self.ws)
-        _lja_src_grad(self.idx1, self.q1, self.dEh, self.dZ, self.ws)
+        for idx, q, dout, dsrc in ((self.idx2, self.q2, self.d_out, self.dEh),
+                                   (self.idx1, self.q1, self.dEh, self.dZ)):
+            self._t("lja_bwd")
+            _lja_src_grad(idx, q, dout, dsrc, self.ws)
+            self._t("lja_bwd_end")
+        self._t("proj_bwd")
         rnn.project_bwd(self.X, self.theta, self.dZ, want_dx=True, prec=self.prec, ws=self.ws_p,
                         dx_out=self.dX, dw_out=self.dTheta)
+        self._t("proj_bwd_end")
         return self.dTheta, self.dX
-
-    def step(self):
-        self.forward()
-        return self.backward()
 
 
 def _lja_src_grad(idx, q, d_out, d_src, ws):
@@ -198,7 +243,7 @@ def _lja_src_grad(idx, q, d_out, d_src, ws):
     return d_src
 
 
-class HGTProgram:
+class HGTProgram(_Program):
     """One HGT attention layer over a heterogeneous schema (config 3; Fig. 4, PAPER.md:905-936,
     appendix :1343-1409; SURVEY sec 8c reading 3/12).
 
@@ -276,14 +321,34 @@ class HGTProgram:
     def join_rows_per_step(self):
         return sum(ix.n_join_rows for ix in self.idx.values())
 
+    def lja_bytes(self):
+        """Softmax LJA (per head h): fwd reads per join row src id 4 + K' and M' rows 8d,
+        per group Q row 4d, out 4d, lse 4h, pointer 8.  bwd (two passes) reads per join row
+        src id 4 + group 4 + K', M' rows 8d + the group's Q/O/dO/lse (served from L1 within
+        a group, counted per group) and writes dK', dM' 8d per source row and dQ 4d per group."""
+        d, h = self.d, self.h
+        f, b = [], []
+        for ix in self.idx.values():
+            f.append(ix.n_join_rows * (4 + 8 * d) + ix.n_groups * (8 * d + 4 * h + 8))
+            b.append(ix.n_join_rows * (8 + 8 * d) + ix.n_groups * (16 * d + 4 * h + 8) +
+                     ix.n_src_rows * (8 * d + 8))
+        return {"lja_fwd": float(np.mean(f)), "lja_bwd": float(np.mean(b))}
+
+    def host_io(self):
+        return list(self.H.values()) + list(self.d_out.values()), list(self.dW.values())
+
     def forward(self):
+        self._t("proj_fwd")
         for t in self.blocks:
             rnn.project(self.H[t], self.W[t], out=self.Y[t], prec=self.prec)
+        self._t("proj_fwd_end")
         first = {t: True for t in self.targets}
         for name, r in self.rels.items():
             tt = r["dst_type"]
+            self._t("lja_fwd")
             rnn.join_aggregate_fwd(self.idx[name], self.q[name], out=self.O[name],
                                    lse=self.lse[name], ws=self.ws)
+            self._t("lja_fwd_end")
             rnn.accumulate(self.Ht[tt], self.O[name], beta=0.0 if first[tt] else 1.0)
             first[tt] = False
         return self.Ht
@@ -296,15 +361,15 @@ class HGTProgram:
             _, bb = rnn.lja_workspace_size(idx, q)
             w = self.ws.get(bb)
             dm, dk, dq = self._blk("m", name, True), self._blk("k", name, True), self._blk("q", name, True)
+            self._t("lja_bwd")
             rnn._check(rnn.lib().rnn_join_aggregate_bwd(
                 C.byref(idx.c), C.byref(q), rnn._ptr(self.O[name]), self.O[name].stride(0),
                 rnn._ptr(self.lse[name]), rnn._ptr(dO), dO.stride(0), rnn._ptr(dm), rnn._ptr(dk),
                 None, rnn._ptr(dq), rnn._ptr(w), w.numel(), rnn._stream()))
+            self._t("lja_bwd_end")
+        self._t("proj_bwd")
         for t in self.blocks:
             rnn.project_bwd(self.H[t], self.W[t], self.dY[t], want_dx=True, prec=self.prec,
                             ws=self.ws_p, dx_out=self.dH[t], dw_out=self.dW[t])
+        self._t("proj_bwd_end")
         return self.dW, self.dH
-
-    def step(self):
-        self.forward()
-        return self.backward()

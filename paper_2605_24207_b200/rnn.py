@@ -86,6 +86,12 @@ def lib():
         L.rnn_hash_partition.argtypes = [vp, i64, i32, C.c_uint64, vp, vp]
         L.rnn_accumulate.argtypes = [vp, i64, vp, i64, i64, i32, C.c_float, vp]
         L.rnn_accumulate.restype = C.c_int
+        L.rnn_dhn_workspace_size.argtypes = [C.POINTER(JoinIndexC), i32, i32, C.POINTER(sz)]
+        L.rnn_dhn_fwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64, vp, sz, vp]
+        L.rnn_dhn_bwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
+                                  C.POINTER(vp), i64, vp, sz, vp]
+        for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd"):
+            getattr(L, f).restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
                   "rnn_join_aggregate_bwd", "rnn_group_softmax", "rnn_group_softmax_bwd",
                   "rnn_project", "rnn_project_bwd_workspace_size", "rnn_project_bwd",
@@ -379,3 +385,53 @@ def accumulate(y, x, beta=1.0, stream=None):
     _check(lib().rnn_accumulate(_ptr(y), y.stride(0), _ptr(x), x.stride(0), rows, cols,
                                 float(beta), _stream(stream)))
     return y
+
+
+# ------------------------------------------------------------------------------------------
+# A6 DHN closed-walk aggregates
+# ------------------------------------------------------------------------------------------
+def dhn_workspace_size(adj: JoinIndex, k, d):
+    b = C.c_size_t(0)
+    _check(lib().rnn_dhn_workspace_size(C.byref(adj.c), k, d, C.byref(b)))
+    return b.value
+
+
+def _dhn_ops(f):
+    ops = (OperandC * len(f))(*[_operand(t) for t in f])
+    return ops
+
+
+def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None):
+    """C_k per root (group order) of the closed-walk rule; f = [f0 (or None), f1, ..., f_{k-1}]
+    by node row (rnn_dhn_fwd)."""
+    assert len(f) == k
+    dev = adj.group_ptr.device
+    d = f[1].shape[1]
+    if out is None:
+        out = torch.empty(max(adj.n_groups, 1), (d + 3) // 4 * 4, dtype=torch.float32, device=dev)[:adj.n_groups, :d]
+    nb = dhn_workspace_size(adj, k, d)
+    w = ws.get(nb) if ws is not None else _ws(nb, dev)
+    _check(lib().rnn_dhn_fwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(out), out.stride(0), _ptr(w),
+                             w.numel(), _stream(stream)))
+    return out
+
+
+def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=None):
+    """[d f0, ..., d f_{k-1}] by node row (rnn_dhn_bwd); want[i] False -> None."""
+    dev = adj.group_ptr.device
+    d = f[1].shape[1]
+    n = adj.n_src_rows
+    want = want or [True] * k
+    if d_f is None:
+        d_f = [torch.empty(max(n, 1), (d + 3) // 4 * 4, dtype=torch.float32, device=dev)[:n, :d]
+               if want[i] else None for i in range(k)]
+    lds = {t.stride(0) for t in d_f if t is not None}
+    if len(lds) > 1:
+        raise ValueError("all d_f tensors must share one ld")
+    ld = lds.pop() if lds else d
+    ptrs = (C.c_void_p * k)(*[None if t is None else t.data_ptr() for t in d_f])
+    nb = dhn_workspace_size(adj, k, d)
+    w = ws.get(nb) if ws is not None else _ws(nb, dev)
+    _check(lib().rnn_dhn_bwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out), d_out.stride(0), ptrs,
+                             ld, _ptr(w), w.numel(), _stream(stream)))
+    return d_f

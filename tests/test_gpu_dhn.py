@@ -1,0 +1,137 @@
+"""GPU parity of A6 (DHN closed-walk aggregates C2/C3/C4, rnn_dhn_fwd / rnn_dhn_bwd) against
+the fp64 oracle (ora_dhn_fwd / ora_dhn_bwd, pinned in test_oracle_dhn.py), element by element.
+
+Graphs: directed and undirected, with duplicated Edge tuples (multiplicity), dangling nodes
+(no out-edges) and isolated ones, and a power-law products-shaped instance (synth.products_like,
+config 5 structure) at reduced scale; widths d = 32 (config 5), 7 and 100 (ragged lanes and
+channel slices); both plain and RNN_IDX_DENSE_GROUPS indices."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.util import FP32_TOL, assert_close, np_
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rnn():
+    from paper_2605_24207_b200 import rnn
+    return rnn
+
+
+def random_graph(seed, n, m, directed, dup=0.05, dangling=0.1):
+    rng = np.random.default_rng(seed)
+    keys = (rng.permutation(n).astype(np.int64) * 7 - 1000)
+    s = rng.integers(0, n, m)
+    t = rng.integers(0, n, m)
+    if dangling:   # some nodes get no out-edges
+        dead = rng.random(n) < dangling
+        keep = ~dead[t]
+        s, t = s[keep], t[keep]
+    ok = s != t
+    s, t = s[ok], t[ok]
+    if not directed:
+        s, t = np.concatenate([s, t]), np.concatenate([t, s])
+    nd = int(len(s) * dup)
+    if nd:
+        j = rng.integers(0, len(s), nd)
+        s, t = np.concatenate([s, s[j]]), np.concatenate([t, t[j]])
+    return keys, keys[t], keys[s]      # keys, e_root (n), e_nbr (v): Edge(n, v)
+
+
+def feats(seed, n, d, k):
+    rng = np.random.default_rng(seed + 1)
+    return [rng.standard_normal((n, d)).astype(np.float32) for _ in range(k)]
+
+
+def cu(a):
+    return torch.as_tensor(np.ascontiguousarray(a)).cuda()
+
+
+def build(rnn, keys, e_n, e_v, dense=False):
+    gi = rnn.build_join_index(cu(e_v), cu(e_n), cu(keys), cu(keys), dense_groups=dense)
+    oi = oracle.build_join_index(e_v, e_n, keys, keys, within_by_src_key=True)
+    return gi, oi
+
+
+def run_case(rnn, keys, e_n, e_v, k, d, seed, dense=False, f0_none=False, bwd=True):
+    gi, oi = build(rnn, keys, e_n, e_v, dense)
+    n = len(keys)
+    f = feats(seed, n, d, k)
+    if f0_none:
+        f[0] = np.ones((n, d), np.float32)
+    fg = [None if (i == 0 and f0_none) else cu(x) for i, x in enumerate(f)]
+    out = np_(rnn.dhn_fwd(gi, k, fg))
+    ref = oracle.dhn_fwd(k, oi, keys, f)
+    rows = np.searchsorted(np_(gi.group_key), oi["group_key"])
+    assert_close(out[rows], ref, FP32_TOL, f"C{k} fwd")
+    if dense:    # roots without out-edges are dense groups with no walks -> 0
+        empty = np.setdiff1d(np.arange(gi.n_groups), rows)
+        assert np.all(out[empty] == 0.0)
+    if not bwd:
+        return
+    rng = np.random.default_rng(seed + 2)
+    d_out = rng.standard_normal((gi.n_groups, d)).astype(np.float32)
+    grads = rnn.dhn_bwd(gi, k, fg, cu(d_out))
+    ref_g = oracle.dhn_bwd(k, oi, keys, f, d_out[rows])
+    for i in range(k):
+        assert_close(np_(grads[i]), ref_g[i], FP32_TOL, f"C{k} d f{i}")
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("directed", [False, True])
+def test_random_graph(rnn, k, directed):
+    keys, e_n, e_v = random_graph(10 + k, 300, 2400, directed)
+    run_case(rnn, keys, e_n, e_v, k, 32, seed=k)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+@pytest.mark.parametrize("d", [7, 100])
+def test_ragged_width(rnn, k, d):
+    keys, e_n, e_v = random_graph(20 + d, 200, 1500, directed=False)
+    run_case(rnn, keys, e_n, e_v, k, d, seed=d)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_dense_groups_and_no_f0(rnn, k):
+    keys, e_n, e_v = random_graph(30 + k, 250, 1800, directed=True, dangling=0.3)
+    run_case(rnn, keys, e_n, e_v, k, 32, seed=30 + k, dense=True, f0_none=True)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_products_shaped(rnn, k):
+    """Power-law DC-SBM (config 5 structure), hubs and high clustering, d = 32."""
+    g = synth.products_like(5, scale=0.0004 if k == 4 else 0.002)
+    keys = g["nodes"]["key"]
+    run_case(rnn, keys, g["edges"]["dst"], g["edges"]["src"], k, 32, seed=40 + k)
+
+
+def test_triangle_counts_exact(rnn):
+    """all-ones features, d = 1: C3(n) = (A^3)_nn exactly (integers in fp32)."""
+    keys, e_n, e_v = random_graph(50, 120, 900, directed=True, dup=0.1)
+    gi, oi = build(rnn, keys, e_n, e_v)
+    ones = cu(np.ones((len(keys), 1), np.float32))
+    for k in (2, 3, 4):
+        out = np_(rnn.dhn_fwd(gi, k, [None] + [ones] * (k - 1)))[:, 0]
+        ref = oracle.dhn_fwd(k, oi, keys, [np.ones((len(keys), 1))] * k)[:, 0]
+        np.testing.assert_array_equal(out, ref)
+
+
+def test_empty_and_errors(rnn):
+    keys = np.arange(10, dtype=np.int64)
+    gi = rnn.build_join_index(cu(np.zeros(0, np.int64)), cu(np.zeros(0, np.int64)), cu(keys), cu(keys))
+    f = [cu(np.ones((10, 4), np.float32))] * 3
+    out = rnn.dhn_fwd(gi, 3, f)
+    assert out.shape[0] == 0
+    gs = rnn.dhn_bwd(gi, 3, f, torch.zeros(1, 4, device="cuda"))
+    assert all(float(x.abs().sum()) == 0.0 for x in gs)
+    keys2, e_n, e_v = random_graph(1, 20, 60, directed=False)
+    gi2, _ = build(rnn, keys2, e_n, e_v)
+    with pytest.raises(rnn.RnnError, match="UNSUPPORTED"):
+        rnn.dhn_fwd(gi2, 5, [None] + [cu(np.ones((20, 4), np.float32))] * 4)
+    t = rnn.build_join_index(cu(e_v), cu(e_n), cu(keys2), cu(keys2), transpose=False)
+    with pytest.raises(rnn.RnnError, match="transposed"):
+        rnn.dhn_fwd(t, 3, [None] + [cu(np.ones((20, 4), np.float32))] * 2)

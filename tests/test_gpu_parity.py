@@ -191,7 +191,11 @@ def test_group_softmax_parity(R, ora):
 
 
 @pytest.mark.parametrize("M,K,N", [(300, 128, 128), (2708, 1433, 16), (2708, 16, 7), (1000, 40, 200),
-                                   (129, 32, 48), (5000, 128, 256), (77, 8, 3)])
+                                   (129, 32, 48), (5000, 128, 256), (77, 8, 3),
+                                   # persistent resident-W kernel: many row tiles per CTA,
+                                   # several column blocks, ragged K / N
+                                   (100000, 128, 128), (60001, 128, 384), (40000, 64, 256),
+                                   (3001, 200, 100)])
 @pytest.mark.parametrize("prec", ["3xtf32", "tf32"])
 def test_projection_parity(R, ora, M, K, N, prec):
     rng = np.random.default_rng(M + K + N)
