@@ -39,7 +39,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="arxiv", choices=["arxiv", "cora", "hyper", "mag"])
+    ap.add_argument("--config", default="arxiv", choices=["arxiv", "cora", "hyper", "mag", "dhn"])
+    ap.add_argument("--dhn-scale", type=float, default=0.1,
+                    help="fraction of the ogbn-products-shaped graph for --config dhn")
     ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-e2e", action="store_true")
@@ -61,7 +63,12 @@ def make_graph(cfg, seed, sample=False):
         return synth.hypergraph_like(seed)
     if cfg == "mag":
         return synth.mag_like(seed, scale=0.05 if sample else 1.0)
+    if cfg == "dhn":
+        return synth.products_like(seed, scale=0.0005 if sample else DHN_SCALE[0])
     return synth.cora_like(seed)
+
+
+DHN_SCALE = [0.1]
 
 
 def make_program(cfg, data, dev, prec):
@@ -70,6 +77,8 @@ def make_program(cfg, data, dev, prec):
         return programs.HypergraphProgram(data, device=dev, prec=prec)
     if cfg == "mag":
         return programs.HGTProgram(data, device=dev, prec=prec)
+    if cfg == "dhn":
+        return programs.DHNProgram(data, device=dev, prec=prec)
     return programs.GCNProgram(data, device=dev, prec=prec)
 
 
@@ -80,6 +89,8 @@ WORKLOAD = {
             "(2,708 node tuples, 10,556 edge tuples + self-loops, 1,433->16->7)",
     "hyper": "HyGNN two-hop incidence join (node->hyperedge SUM, hyperedge->node MEAN) on "
              "synthetic power-law hypergraph (1M nodes, 200K hyperedges, 5M incidences, 128-dim)",
+    "dhn": "DHN layer (C2 + C3 triangle + C4 4-cycle closed-walk aggregates, nine 32x32 "
+           "projections) on a synthetic ogbn-products-shaped DC-SBM graph",
     "mag": "HGT attention layer (4 relations, 8-head grouped softmax, dense target groups) on "
            "synthetic ogbn-mag-shaped schema (1.94M nodes, 21.1M edges, 128-dim)",
 }
@@ -131,6 +142,12 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+# fp32 FMA pipe: 148 SMs x 128 lanes x 2 flops x 1.965 GHz (B200_PROFILING.md unit counts and
+# the max SM clock nvidia-smi reports on this pool) -- the ALU roof of the DHN walk kernels
+FP32_ALU_TFLOPS = round(148 * 128 * 2 * 1.965e9 / 1e12, 2)
+FP32_ALU_SRC = "derived: 148 SM x 128 FP32 lanes x 2 flop x 1965 MHz"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -156,10 +173,22 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     graph = make_graph(args.config, args.seed)
-    # multi-GPU: replicas of the single-GPU step (weak scaling)
-    prog = make_program(args.config, graph, dev, args.prec)
+    sharded = world > 1 and args.config in ("arxiv", "cora")
+    if sharded:
+        # multi-GPU: the join relation hash-partitioned by group key, NCCL all-gather of the
+        # source embeddings / reduce-scatter of their gradients per layer
+        from paper_2605_24207_b200.shard import ShardedGCNProgram
+        prog = ShardedGCNProgram(graph, prec=args.prec)
+        r = torch.tensor([prog.join_rows_per_step], dtype=torch.float64, device=dev)
+        dist.all_reduce(r)
+        rows = int(r.item())              # all ranks' join rows = the whole job
+    else:
+        # other configs at N > 1: independent replicas
+        prog = make_program(args.config, graph, dev, args.prec)
+        rows = None
     del graph
-    rows = prog.join_rows_per_step
+    if rows is None:
+        rows = prog.join_rows_per_step
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def barrier():
@@ -196,26 +225,30 @@ def run_ours(args):
         t = torch.tensor([t_step], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         t_step = float(t.item())
-    value = world * rows / (t_step * 1e-3)
+    value = (rows if sharded else world * rows) / (t_step * 1e-3)
 
     def kernel_ms(name):
         a, b = timers.get(name, []), timers.get(name + "_end", [])
         return float(np.mean([x.elapsed_time(y) for x, y in zip(a, b)])) if a else None
 
-    per = {k: kernel_ms(k) for k in ("proj_fwd", "lja_fwd", "lja_bwd", "proj_bwd")}
+    model = prog.roof_model()
+    per = {k: kernel_ms(k) for k in ["proj_fwd", "proj_bwd"] + list(model)}
 
     # ---- roofline of the dominant hot-path kernel (the fused LJA) ----
     peak, peak_src = peaks()
-    # algorithmic bytes per LJA launch (gather model, DESIGN.md "Byte model";
-    # programs._sum_bytes / _sum_bwd_bytes / HGTProgram.lja_bytes)
-    byt = prog.lja_bytes()
-    cand = {"lja_fwd": (per["lja_fwd"], byt["lja_fwd"]), "lja_bwd": (per["lja_bwd"], byt["lja_bwd"])}
-    dom = max(cand, key=lambda k: cand[k][0] or 0)
-    ms, byt = cand[dom]
-    achieved = byt / (ms * 1e-3) / 1e9
-    roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak, 4),
-            "algorithmic_bytes_per_launch": int(byt), "avg_launch_ms": round(ms, 5),
+    # algorithmic bytes (or flops) per launch of each hot-path kernel (
+    # programs._sum_bytes / _sum_bwd_bytes / HGTProgram.lja_bytes / DHNProgram.roof_model)
+    dom = max(model, key=lambda k: per[k] or 0)
+    ms, spec = per[dom], model[dom]
+    if spec["bound"] == "hbm":
+        achieved = spec["amount"] / (ms * 1e-3) / 1e9
+        unit, pk, pk_src = "GB/s", peak, peak_src
+    else:
+        achieved = spec["amount"] / (ms * 1e-3) / 1e12
+        unit, pk, pk_src = "TFLOP/s", FP32_ALU_TFLOPS, FP32_ALU_SRC
+    roof = {"kernel": dom, "bound": spec["bound"], "achieved": round(achieved, 3), "peak": pk,
+            "peak_source": pk_src, "unit": unit, "frac": round(achieved / pk, 4),
+            "algorithmic_per_launch": int(spec["amount"]), "avg_launch_ms": round(ms, 5),
             "traffic": None,
             "kernel_ms": {k: (round(v, 5) if v else None) for k, v in per.items()}}
     tr = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
@@ -230,20 +263,22 @@ def run_ours(args):
     # ---- end to end through the C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(prog, args, world, dev)
+        e2e = run_e2e(prog, args, world, dev, rows if sharded else world * rows)
 
     result = None
     if rank == 0:
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded; shapes of BASELINE.json configs, see DESIGN.md)",
             "config": {"workload": WORKLOAD[args.config], "config": args.config,
                        "join_rows_per_step": rows,
                        **({"layers": prog.L, "dims": prog.dims} if hasattr(prog, "dims") else {}),
                        "projection_precision": args.prec, "l2": "flushed between timed steps",
-                       "parallelism": f"replica x{world}" if world > 1 else "single"},
+                       "parallelism": (f"hash-partition by group key x{world} (NCCL all-gather / "
+                                       f"reduce-scatter per layer)" if sharded else
+                                       f"replica x{world}" if world > 1 else "single")},
             "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
     if world > 1:
@@ -265,7 +300,7 @@ def count_launches(prog):
     return len(ours)
 
 
-def run_e2e(prog, args, world, dev):
+def run_e2e(prog, args, world, dev, job_rows):
     """Same metric through the public API with HOST buffers: every step copies its inputs
     (node features and the upstream gradient, prog.host_io()) from pinned host memory and
     reads the parameter gradients back, inside the timed region."""
@@ -294,7 +329,11 @@ def run_e2e(prog, args, world, dev):
     e.record()
     torch.cuda.synchronize()
     t = s.elapsed_time(e) / steps
-    return {"value": world * prog.join_rows_per_step / (t * 1e-3), "unit": UNIT,
+    if world > 1:
+        tt = torch.tensor([t], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": job_rows / (t * 1e-3), "unit": UNIT,
             "ms_per_step": t, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
 
@@ -384,6 +423,7 @@ def run_reference(args):
 
 def main():
     args = parse()
+    DHN_SCALE[0] = args.dhn_scale
     if args.impl == "reference":
         res = run_reference(args)
     else:

@@ -36,7 +36,8 @@
  * - Keys are signed int64 (any value).  Row ids are int32 (relations < 2^31 rows); join-row
  *   counts and CSR pointers are int64.
  * - Determinism: identical inputs give bit-identical outputs (no floating-point atomics on
- *   any path; every reduction has a fixed order).
+ *   any path; every reduction has a fixed order) -- except the k = 4 DHN aggregate (A6),
+ *   whose slab scatter uses fp32 atomics (rounding order only).
  */
 #ifndef RNN_H
 #define RNN_H
@@ -269,6 +270,14 @@ rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rnn_operand* 
  * (n_src_rows == n_dst_rows). */
 rnn_status rnn_gcn_norm(const rnn_join_index* idx, float* w, void* workspace,
                         size_t workspace_bytes, void* stream);
+
+/* Sharded GCN normalisation (multi-GPU): S is the all-gathered source relation
+ * of every rank, so deg(s) comes from its owner: w[p] = src_deg[src_row[p]]^-1/2 * |g|^-1/2
+ * (0 where src_deg is 0).  src_deg [n_src_rows] int32 (device). */
+rnn_status rnn_gcn_norm_src_deg(const rnn_join_index* idx, const int32_t* src_deg, float* w,
+                                void* stream);
+/* size[g] = number of join rows of group g (int32, device) -- the in-degree a rank owns. */
+rnn_status rnn_group_sizes(const rnn_join_index* idx, int32_t* size, void* stream);
 
 /* Union over relations of materialised per-relation results that share a head relation
  * (PAPER.md:451-460, e.g. HGT's H_tilda = sum over relation types, :1408-1409):

@@ -73,3 +73,30 @@ def hgt_relation(H_src, H_dst, Wk, Wm, Wq, src_keys, dst_keys, e_src, e_dst, hea
     g = oracle.lja_bwd(o, dO, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
     return {"index": o, "out": out, "lse": lse, "dense_rows": dense_rows,
             "dK": g["src_key"], "dM": g["src"], "dQ": g["dst"], "K": K, "M": M, "Q": Q}
+
+
+def dhn_step(g, W, d_out_dense, ks=(2, 3, 4)):
+    """O9: DHN layer: f_{k,i} = h W_{k,i}^T (positions stacked in W, C2 then
+    C3 then C4), C_k closed-walk aggregates, out = C2 (+) C3 (+) C4 placed densely in node-key
+    order (roots without out-edges: 0); backward with d_out_dense [n, 3d]."""
+    keys = np.asarray(g["nodes"]["key"])
+    h = np.asarray(g["nodes"]["x"], np.float64)
+    n, d = h.shape
+    adj = oracle.build_join_index(g["edges"]["src"], g["edges"]["dst"], keys, keys,
+                                  within_by_src_key=True)
+    Y = oracle.project(h, W)
+    rank = np.argsort(np.argsort(keys, kind="stable"), kind="stable")
+    rows = rank[adj["group_dst_row"]]              # dense position of every oracle group
+    out = np.zeros((n, len(ks) * d))
+    dY = np.zeros_like(Y)
+    p = 0
+    for j, k in enumerate(ks):
+        f = [Y[:, (p + i) * d:(p + i + 1) * d] for i in range(k)]
+        out[rows, j * d:(j + 1) * d] = oracle.dhn_fwd(k, adj, keys, f)
+        dO = np.asarray(d_out_dense, np.float64)[rows, j * d:(j + 1) * d]
+        grads = oracle.dhn_bwd(k, adj, keys, f, dO)
+        for i in range(k):
+            dY[:, (p + i) * d:(p + i + 1) * d] = grads[i]
+        p += k
+    dH, dW, _ = oracle.project_bwd(h, W, dY, want_db=False)
+    return {"out": out, "dY": dY, "dW": dW, "dH": dH}

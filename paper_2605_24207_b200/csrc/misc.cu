@@ -26,6 +26,24 @@ __global__ void norm_kernel(const int64_t* __restrict__ gp, const int32_t* __res
   }
 }
 
+// w[p] = src_deg[s_p]^-1/2 |g|^-1/2 ; warp per group (sharded GCN: S spans every rank's rows)
+__global__ void norm_deg_kernel(const int64_t* __restrict__ gp, const int32_t* __restrict__ src_row,
+                                int64_t G, const int32_t* __restrict__ sdeg, float* __restrict__ w) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= G) return;
+  const int64_t b = gp[g], e = gp[g + 1];
+  const float rt = 1.f / sqrtf((float)(e - b));
+  for (int64_t p = b + (threadIdx.x & 31); p < e; p += 32) {
+    const int32_t ds = sdeg[src_row[p]];
+    w[p] = ds > 0 ? rt * (1.f / sqrtf((float)ds)) : 0.f;
+  }
+}
+
+__global__ void group_size_kernel(const int64_t* __restrict__ gp, int64_t G, int32_t* __restrict__ sz) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < G) sz[g] = (int32_t)(gp[g + 1] - gp[g]);
+}
+
 __global__ void partition_kernel(const int64_t* __restrict__ keys, int64_t n, uint32_t P,
                                  uint64_t seed, int32_t* __restrict__ owner) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -59,6 +77,31 @@ extern "C" rnn_status rnn_gcn_norm(const rnn_join_index* idx, float* w, void* wo
   deg_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(idx->group_ptr, idx->group_dst_row, G,
                                                           deg, bad);
   norm_kernel<<<(unsigned)ceil_div(G, 8), 256, 0, st>>>(idx->group_ptr, idx->src_row, G, deg, w);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_group_sizes(const rnn_join_index* idx, int32_t* size, void* stream) {
+  clear_error();
+  RNN_REQUIRE(idx && (idx->n_groups == 0 || (idx->group_ptr && size)), RNN_ERR_INVALID_ARGUMENT,
+              "index / size required");
+  if (idx->n_groups == 0) return RNN_OK;
+  group_size_kernel<<<(unsigned)ceil_div(idx->n_groups, 256), 256, 0, as_stream(stream)>>>(
+      idx->group_ptr, idx->n_groups, size);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_gcn_norm_src_deg(const rnn_join_index* idx, const int32_t* src_deg,
+                                           float* w, void* stream) {
+  clear_error();
+  RNN_REQUIRE(idx && (idx->n_groups == 0 || (idx->group_ptr && idx->src_row)),
+              RNN_ERR_INVALID_ARGUMENT, "index required");
+  RNN_REQUIRE(idx->n_join_rows == 0 || (src_deg && w), RNN_ERR_INVALID_ARGUMENT,
+              "src_deg and w required");
+  if (idx->n_groups == 0) return RNN_OK;
+  norm_deg_kernel<<<(unsigned)ceil_div(idx->n_groups, 8), 256, 0, as_stream(stream)>>>(
+      idx->group_ptr, idx->src_row, idx->n_groups, src_deg, w);
   RNN_LAUNCH_CHECK();
   return RNN_OK;
 }

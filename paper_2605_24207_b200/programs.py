@@ -54,6 +54,10 @@ class _Program:
         self.forward()
         return self.backward()
 
+    def roof_model(self):
+        """{kernel timer name: {"bound": "hbm", "amount": algorithmic bytes per launch}}"""
+        return {k: {"bound": "hbm", "amount": v} for k, v in self.lja_bytes().items()}
+
 
 def _sum_bytes(idx, d, weighted=False, mean=False):
     """Gather-model bytes of one SUM/MEAN LJA forward launch: per join row the source row id
@@ -371,5 +375,120 @@ class HGTProgram(_Program):
         for t in self.blocks:
             rnn.project_bwd(self.H[t], self.W[t], self.dY[t], want_dx=True, prec=self.prec,
                             ws=self.ws_p, dx_out=self.dH[t], dw_out=self.dW[t])
+        self._t("proj_bwd_end")
+        return self.dW, self.dH
+
+
+class DHNProgram(_Program):
+    """Deep homomorphism network layer on one node relation (config 5; PAPER.md:938-950,
+    SURVEY sec 8a A6 and sec 8c readings 9 / 14):
+
+        f_{k,i} = mu_{k,i}(h) = h W_{k,i}^T             (A2: all nine 32x32 maps in ONE GEMM)
+        C_k(n)  = f_{k,0}(n) (.) sum_{closed k-walks} prod_i f_{k,i}(v_i)    k = 2, 3, 4   (A6)
+        out     = C_2 (+) C_3 (+) C_4                    (concat; rho and the readout are OUT)
+
+    The adjacency index has dense groups, so root n of every C_k is node n in key order and
+    out is [n_nodes, 3d] in key order.  Backward: rnn_dhn_bwd per pattern (rotation) into the
+    column blocks of dY, then the projection backward."""
+
+    KS = (2, 3, 4)
+
+    def __init__(self, g: dict, device="cuda", prec="3xtf32", seed=11, ks=KS):
+        dev = self.device = torch.device(device)
+        self.prec = prec
+        self.ks = tuple(ks)
+        keys = torch.as_tensor(g["nodes"]["key"]).to(dev)
+        # Edge(n, v): root n = dst column, neighbour v = src column
+        self.idx = rnn.build_join_index(torch.as_tensor(g["edges"]["src"]).to(dev),
+                                        torch.as_tensor(g["edges"]["dst"]).to(dev), keys, keys,
+                                        dense_groups=True)
+        self.n = len(g["nodes"]["key"])
+        self.d = d = g["nodes"]["x"].shape[1]
+        self.H = _dev_f32(g["nodes"]["x"], dev)
+        rng = np.random.default_rng(seed)
+        self.npos = sum(self.ks)
+        W = rng.standard_normal((self.npos * d, d)) / np.sqrt(d)
+        self.W = _dev_f32(W.astype(np.float32), dev)
+        self.Y = _empty(self.n, self.npos * d, dev)
+        self.dY = _empty(self.n, self.npos * d, dev)
+        self.dW = torch.empty(self.npos * d, d, dtype=torch.float32, device=dev)
+        self.dH = _empty(self.n, d, dev)
+        G = self.idx.n_groups
+        self.out = _empty(G, len(self.ks) * d, dev)
+        self.d_out = _dev_f32(rng.standard_normal((G, len(self.ks) * d)).astype(np.float32), dev)
+        self.ws = rnn.Workspace(dev)
+        self.ws_p = rnn.Workspace(dev)
+        self.pos0 = {}
+        p = 0
+        for k in self.ks:
+            self.pos0[k] = p
+            p += k
+        self._rows = None
+
+    def _f(self, k, buf):
+        p = self.pos0[k]
+        return [buf[:, (p + i) * self.d:(p + i + 1) * self.d] for i in range(k)]
+
+    @property
+    def join_rows_per_step(self):
+        """Rows of the lifted joins: Edge rows for C2, closed 3- / 4-walks for C3 / C4 (the
+        homomorphism counts, measured once with all-ones operands)."""
+        if self._rows is None:
+            tot = 0
+            for k in self.ks:
+                tot += self.idx.n_join_rows if k == 2 else int(self._walks(k))
+            self._rows = tot
+        return self._rows
+
+    def host_io(self):
+        return [self.H, self.d_out], [self.dW]
+
+    def roof_model(self):
+        """The walk kernels are bound by the FP32 pipe and on-chip (L2 / L1) traffic, not HBM:
+        algorithmic flops per launch of the factorised plans:
+          C2: E' d adds;  C3: per closed 3-walk (hit) 2d (scale + multiply-add);
+          C4: per 2-path into the root d adds (S3 scatter) + per 2-path out of the root 2d
+              (f2 * S3 fma) + per root neighbour d (f1 scaling)."""
+        if getattr(self, "_flops", None) is None:
+            deg = np.zeros(self.n)
+            deg[self.idx.group_dst_row.cpu().numpy()] = np.diff(self.idx.group_ptr.cpu().numpy())
+            # Edge is symmetric here (both directions stored): in-degree = out-degree
+            two_paths = float(deg[self.idx.src_row.cpu().numpy()].sum())
+            d = self.d
+            E = float(self.idx.n_join_rows)
+            walks3 = self._walks(3)
+            self._flops = {"dhn2_fwd": E * d, "dhn3_fwd": 2 * d * walks3,
+                           "dhn4_fwd": d * (3 * two_paths + E)}
+            self._flops["dhn2_bwd"] = 2 * self._flops["dhn2_fwd"]
+            self._flops["dhn3_bwd"] = 3 * self._flops["dhn3_fwd"]
+            self._flops["dhn4_bwd"] = 4 * self._flops["dhn4_fwd"]
+        return {k: {"bound": "alu", "amount": v} for k, v in self._flops.items()
+                if int(k[3]) in self.ks}
+
+    def _walks(self, k):
+        ones = torch.ones(self.n, 1, dtype=torch.float32, device=self.device)
+        c = rnn.dhn_fwd(self.idx, k, [None] + [ones] * (k - 1), ws=self.ws)
+        return float(c.double().sum().item())
+
+    def forward(self):
+        self._t("proj_fwd")
+        rnn.project(self.H, self.W, out=self.Y, prec=self.prec)
+        self._t("proj_fwd_end")
+        for j, k in enumerate(self.ks):
+            self._t(f"dhn{k}_fwd")
+            rnn.dhn_fwd(self.idx, k, self._f(k, self.Y), out=self.out[:, j * self.d:(j + 1) * self.d],
+                        ws=self.ws)
+            self._t(f"dhn{k}_fwd_end")
+        return self.out
+
+    def backward(self):
+        for j, k in enumerate(self.ks):
+            self._t(f"dhn{k}_bwd")
+            rnn.dhn_bwd(self.idx, k, self._f(k, self.Y), self.d_out[:, j * self.d:(j + 1) * self.d],
+                        d_f=self._f(k, self.dY), ws=self.ws)
+            self._t(f"dhn{k}_bwd_end")
+        self._t("proj_bwd")
+        rnn.project_bwd(self.H, self.W, self.dY, want_dx=True, prec=self.prec, ws=self.ws_p,
+                        dx_out=self.dH, dw_out=self.dW)
         self._t("proj_bwd_end")
         return self.dW, self.dH

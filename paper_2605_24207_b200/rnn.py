@@ -90,7 +90,10 @@ def lib():
         L.rnn_dhn_fwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64, vp, sz, vp]
         L.rnn_dhn_bwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
                                   C.POINTER(vp), i64, vp, sz, vp]
-        for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd"):
+        L.rnn_gcn_norm_src_deg.argtypes = [C.POINTER(JoinIndexC), vp, vp, vp]
+        L.rnn_group_sizes.argtypes = [C.POINTER(JoinIndexC), vp, vp]
+        for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd", "rnn_gcn_norm_src_deg",
+                  "rnn_group_sizes"):
             getattr(L, f).restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
                   "rnn_join_aggregate_bwd", "rnn_group_softmax", "rnn_group_softmax_bwd",
@@ -370,6 +373,21 @@ def gcn_norm(idx: JoinIndex, stream=None):
     ws = _ws(nb, dev)
     _check(lib().rnn_gcn_norm(C.byref(idx.c), _ptr(w), _ptr(ws), ws.numel(), _stream(stream)))
     return w[:idx.n_join_rows]
+
+
+def gcn_norm_src_deg(idx: JoinIndex, src_deg, stream=None):
+    """w[p] = src_deg[src_row[p]]^-1/2 |g|^-1/2 (sharded GCN: src_deg all-gathered)."""
+    src_deg = _cuda(src_deg, torch.int32, "src_deg").contiguous()
+    w = torch.empty(max(idx.n_join_rows, 1), dtype=torch.float32, device=src_deg.device)
+    _check(lib().rnn_gcn_norm_src_deg(C.byref(idx.c), _ptr(src_deg), _ptr(w), _stream(stream)))
+    return w[:idx.n_join_rows]
+
+
+def group_sizes(idx: JoinIndex, out=None, stream=None):
+    dev = idx.group_ptr.device
+    out = out if out is not None else torch.empty(max(idx.n_groups, 1), dtype=torch.int32, device=dev)
+    _check(lib().rnn_group_sizes(C.byref(idx.c), _ptr(out), _stream(stream)))
+    return out
 
 
 def hash_partition(keys, P, seed, stream=None):

@@ -1,0 +1,285 @@
+"""Multi-GPU sharding of the lifted join-aggregate (BASELINE.json north_star).
+
+The join relation is hash-partitioned by the GROUP BY key: owner(t) = splitmix64(t ^ seed) % P
+(rnn_hash_partition).  Every group is reduced entirely on its owner, in the same within-group
+order as on one GPU.  Per layer of a GCN:
+
+    Z_own  = H_own W^T                                   (A2, owned rows only)
+    Z_all  = all_gather(Z_own)                           (NCCL over NVLink; rank-major blocks)
+    H'_own = LJA_fwd(index_r, src = Z_all, w)            (A3 over the rank's join rows)
+  backward
+    dZ_all = LJA_bwd(index_r, dH'_own)                   (A5: partial over referenced sources)
+    dZ_own = reduce_scatter(dZ_all)                      (sum to the owners)
+    dW     = all_reduce(H_own^T dZ_own),  dH_own = dZ_own W
+
+Layout: rank r's block of the gathered source relation holds its owned node keys in
+ascending order, padded to n_pad = max_r |owned_r| with sentinel keys that match no edge.
+Because a layer's output rows are the owned keys in ascending order (every node has a
+self-loop, so every owned node is a group), the SAME S-key layout serves every layer: one
+join index per rank, built once (content caching).
+
+This module holds the host-side partition plan (numpy, setup time) and the program; the
+collectives are torch.distributed calls on the rank's process group (NCCL on the GPU box;
+gloo works too, which the world-size-2 CPU tests use).
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+class ShardPlan:
+    """Which node keys and which edge rows rank `rank` of `P` owns (host, numpy).
+
+    owner[i] = owning rank of node i (from rnn_hash_partition over the node keys)."""
+
+    def __init__(self, node_keys, e_src, e_dst, owner, P, rank):
+        keys = np.asarray(node_keys, np.int64)
+        owner = np.asarray(owner, np.int64)
+        self.P, self.rank = int(P), int(rank)
+        self.owned_keys = [np.sort(keys[owner == r]) for r in range(self.P)]
+        self.counts = np.array([len(k) for k in self.owned_keys], np.int64)
+        self.n_pad = int(max(1, self.counts.max())) if len(keys) else 1
+        lo = int(keys.min()) if len(keys) else 0
+        n_all = self.P * self.n_pad
+        if lo - n_all - 1 < np.iinfo(np.int64).min + 1:
+            raise ValueError("node keys too close to INT64_MIN for sentinel padding")
+        # sentinel keys (unique, below every real key) pad each rank's block
+        s = np.empty(n_all, np.int64)
+        for r in range(self.P):
+            blk = s[r * self.n_pad:(r + 1) * self.n_pad]
+            c = self.counts[r]
+            blk[:c] = self.owned_keys[r]
+            blk[c:] = lo - 1 - (r * self.n_pad + np.arange(self.n_pad - c))
+        self.s_keys = s                                   # S relation of every layer (all ranks)
+        self.my_keys = self.owned_keys[self.rank]         # T relation (= this rank's groups)
+        # storage rows of this rank's nodes, in key order (to lay out the layer-1 features)
+        order = np.argsort(keys, kind="stable")
+        pos = np.searchsorted(keys[order], self.my_keys)
+        self.my_rows = order[pos]
+        # join rows owned here: the edge's group key (dst) is owned by this rank
+        e_dst = np.asarray(e_dst, np.int64)
+        ks = keys[order]
+        j = np.searchsorted(ks, e_dst)
+        j = np.clip(j, 0, max(len(ks) - 1, 0))
+        present = (len(ks) > 0) & (ks[j] == e_dst) if len(ks) else np.zeros(len(e_dst), bool)
+        e_owner = np.where(present, owner[order[j]] if len(ks) else 0, -1)
+        mine = e_owner == self.rank
+        self.e_src = np.asarray(e_src, np.int64)[mine]
+        self.e_dst = e_dst[mine]
+
+
+def all_gather_rows(out, x, group=None):
+    """out[P * n, d] <- concat over ranks of x[n, d] (contiguous tensors)."""
+    if not dist.is_initialized():
+        out.copy_(x)
+        return
+    try:
+        dist.all_gather_into_tensor(out, x, group=group)
+    except (RuntimeError, NotImplementedError):
+        # backends without the fused variant (gloo + CUDA tensors): list all-gather
+        n = x.shape[0]
+        parts = [out[r * n:(r + 1) * n] for r in range(dist.get_world_size(group))]
+        bufs = [torch.empty_like(x) for _ in parts]
+        dist.all_gather(bufs, x.contiguous(), group=group)
+        for p, b in zip(parts, bufs):
+            p.copy_(b)
+
+
+def reduce_scatter_rows(out, x, group=None):
+    """out[n, d] <- sum over ranks of the rank-th block of x[P * n, d]."""
+    if not dist.is_initialized():
+        out.copy_(x)
+        return
+    try:
+        dist.reduce_scatter_tensor(out, x, group=group)
+    except (RuntimeError, NotImplementedError):
+        # backends without reduce_scatter (gloo + CUDA tensors): all-reduce, keep own block
+        y = x.clone()
+        dist.all_reduce(y, group=group)
+        r = dist.get_rank(group)
+        out.copy_(y[r * out.shape[0]:(r + 1) * out.shape[0]])
+
+
+class ShardedGCNProgram:
+    """L-layer GCN step over P ranks (hash partition by group key, one process per GPU).
+
+    backend: the compute primitives (``RnnBackend`` = librnn.so on this rank's GPU; the CPU
+    tests plug in an fp64 backend built from the oracle to check the sharding logic)."""
+
+    def __init__(self, graph: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32"):
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        be = self.be = backend if backend is not None else RnnBackend(prec=prec)
+        nodes, edges = graph["nodes"], graph["edges"]
+        keys = np.asarray(nodes["key"], np.int64)
+        owner = be.hash_partition(keys, self.P, seed)
+        plan = self.plan = ShardPlan(keys, edges["src"], edges["dst"], owner, self.P, self.rank)
+        self.dims = list(graph["dims"])
+        self.L = len(self.dims) - 1
+        n_pad, P = plan.n_pad, self.P
+        self.n_own = int(plan.counts[self.rank])
+        self.idx = be.build_index(plan.e_src, plan.e_dst, plan.s_keys, plan.my_keys)
+        assert be.n_groups(self.idx) == self.n_own, "every owned node needs a self-loop"
+        # normalisation: deg(s) from its owner (all-gathered group sizes)
+        own_deg = be.zeros_i32(n_pad)
+        be.group_sizes(self.idx, own_deg)
+        all_deg = be.zeros_i32(P * n_pad)
+        all_gather_rows(all_deg, own_deg, group)
+        self.w = be.gcn_norm_src_deg(self.idx, all_deg)
+        # activations (rows >= n_own stay zero: padding of the gathered blocks)
+        x0 = np.zeros((n_pad, self.dims[0]), np.float32)
+        x0[: self.n_own] = np.asarray(nodes["x"], np.float32)[plan.my_rows]
+        self.H = [be.tensor(x0)] + [be.zeros(n_pad, self.dims[l + 1]) for l in range(self.L)]
+        self.W = [be.tensor(np.asarray(w, np.float32)) for w in graph["W"]]
+        self.Z = [be.zeros(n_pad, self.dims[l + 1]) for l in range(self.L)]
+        self.Zall = [be.zeros(P * n_pad, self.dims[l + 1]) for l in range(self.L)]
+        self.dZall = [be.zeros(P * n_pad, self.dims[l + 1]) for l in range(self.L)]
+        self.dZ = [be.zeros(n_pad, self.dims[l + 1]) for l in range(self.L)]
+        self.dH = [be.zeros(n_pad, self.dims[l]) for l in range(self.L)]
+        self.dW = [be.zeros(self.dims[l + 1], self.dims[l]) for l in range(self.L)]
+        # upstream gradient of the owned output rows (the oracle's d_out row of each group)
+        G_all = np.sort(keys)
+        rank_of = np.searchsorted(G_all, plan.my_keys)
+        d_out = np.zeros((n_pad, self.dims[-1]), np.float32)
+        d_out[: self.n_own] = np.asarray(graph["d_out"], np.float32)[rank_of, : self.dims[-1]]
+        self.d_out = be.tensor(d_out)
+        self.timers = None
+
+    @property
+    def join_rows_per_step(self):
+        """Join rows this rank processes per step (all layers)."""
+        return self.L * self.be.n_join_rows(self.idx)
+
+    def roof_model(self):
+        from .programs import _sum_bwd_bytes, _sum_bytes
+        d = self.dims[1:]
+        return {"lja_fwd": {"bound": "hbm", "amount": float(np.mean([_sum_bytes(self.idx, x, True) for x in d]))},
+                "lja_bwd": {"bound": "hbm", "amount": float(np.mean([_sum_bwd_bytes(self.idx, x, True) for x in d]))}}
+
+    def host_io(self):
+        return [self.H[0], self.d_out], list(self.dW)
+
+    def _t(self, name):
+        if self.timers is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.timers.setdefault(name, []).append(e)
+
+    def forward(self):
+        be, g = self.be, self.group
+        for l in range(self.L):
+            self._t("proj_fwd")
+            be.project(self.H[l], self.W[l], self.Z[l])
+            self._t("proj_fwd_end")
+            self._t("allgather")
+            all_gather_rows(self.Zall[l], self.Z[l], g)
+            self._t("allgather_end")
+            self._t("lja_fwd")
+            be.lja_fwd(self.idx, self.Zall[l], self.w, self.H[l + 1])
+            self._t("lja_fwd_end")
+        return self.H[-1]
+
+    def backward(self):
+        be, g = self.be, self.group
+        dY = self.d_out
+        for l in reversed(range(self.L)):
+            self._t("lja_bwd")
+            be.lja_bwd_src(self.idx, self.Zall[l], self.w, dY, self.dZall[l])
+            self._t("lja_bwd_end")
+            self._t("reduce_scatter")
+            reduce_scatter_rows(self.dZ[l], self.dZall[l], g)
+            self._t("reduce_scatter_end")
+            self._t("proj_bwd")
+            be.project_bwd(self.H[l], self.W[l], self.dZ[l], self.dH[l], self.dW[l])
+            self._t("proj_bwd_end")
+            if self.P > 1:
+                dist.all_reduce(self.dW[l], group=g)
+            dY = self.dH[l]
+        return self.dW, self.dH[0]
+
+    def step(self):
+        self.forward()
+        return self.backward()
+
+    # ---- gathering results for checks (host) ----
+    def owned_output(self):
+        return self.be.numpy(self.H[-1])[: self.n_own]
+
+    def owned_dx(self):
+        return self.be.numpy(self.dH[0])[: self.n_own]
+
+
+class RnnBackend:
+    """The product backend: every primitive is a librnn.so call on the current CUDA device."""
+
+    def __init__(self, prec="3xtf32", device=None):
+        from . import rnn
+        self.rnn = rnn
+        self.prec = prec
+        self.dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.ws = rnn.Workspace(self.dev)
+        self.ws_p = rnn.Workspace(self.dev)
+        self._q = {}
+
+    def tensor(self, a):
+        a = np.asarray(a, np.float32)
+        ld = (a.shape[1] + 3) // 4 * 4
+        t = torch.zeros(a.shape[0], ld, dtype=torch.float32, device=self.dev)
+        t[:, : a.shape[1]] = torch.from_numpy(a).to(self.dev)
+        return t[:, : a.shape[1]] if ld != a.shape[1] else t
+
+    def zeros(self, n, d):
+        # collectives need contiguous buffers: keep d a multiple of 4 in the product configs
+        return torch.zeros(n, d, dtype=torch.float32, device=self.dev)
+
+    def zeros_i32(self, n):
+        return torch.zeros(n, dtype=torch.int32, device=self.dev)
+
+    def numpy(self, t):
+        return t.detach().cpu().numpy()
+
+    def hash_partition(self, keys, P, seed):
+        k = torch.as_tensor(np.asarray(keys, np.int64), device=self.dev)
+        return self.rnn.hash_partition(k, P, seed).cpu().numpy()
+
+    def build_index(self, e_src, e_dst, s_keys, t_keys):
+        cu = lambda a: torch.as_tensor(np.asarray(a, np.int64), device=self.dev)
+        return self.rnn.build_join_index(cu(e_src), cu(e_dst), cu(s_keys), cu(t_keys))
+
+    def n_groups(self, idx):
+        return idx.n_groups
+
+    def n_join_rows(self, idx):
+        return idx.n_join_rows
+
+    def group_sizes(self, idx, out):
+        self.rnn.group_sizes(idx, out=out)
+
+    def gcn_norm_src_deg(self, idx, deg):
+        return self.rnn.gcn_norm_src_deg(idx, deg)
+
+    def _query(self, idx, Z, w):
+        key = (id(idx), Z.data_ptr(), w.data_ptr())
+        q = self._q.get(key)
+        if q is None:
+            q = self._q[key] = self.rnn.make_query("src", "sum", src=Z, edge=w,
+                                                   edge_mode=self.rnn.BY_POSITION)
+        return q
+
+    def project(self, X, W, out):
+        self.rnn.project(X, W, out=out, prec=self.prec)
+
+    def lja_fwd(self, idx, Z, w, out):
+        self.rnn.join_aggregate_fwd(idx, self._query(idx, Z, w), out=out, ws=self.ws)
+
+    def lja_bwd_src(self, idx, Z, w, d_out, d_src):
+        from .programs import _lja_src_grad
+        _lja_src_grad(idx, self._query(idx, Z, w), d_out, d_src, self.ws)
+
+    def project_bwd(self, X, W, dY, dX, dW):
+        self.rnn.project_bwd(X, W, dY, want_dx=True, prec=self.prec, ws=self.ws_p, dx_out=dX,
+                             dw_out=dW)

@@ -135,3 +135,25 @@ def test_empty_and_errors(rnn):
     t = rnn.build_join_index(cu(e_v), cu(e_n), cu(keys2), cu(keys2), transpose=False)
     with pytest.raises(rnn.RnnError, match="transposed"):
         rnn.dhn_fwd(t, 3, [None] + [cu(np.ones((20, 4), np.float32))] * 2)
+
+
+def test_dhn_program(rnn):
+    """Config-5 layer (nine stacked 32x32 projections, C2/C3/C4, concat) vs oracle.dhn_step."""
+    from oracle import programs as op
+    from paper_2605_24207_b200 import programs
+    g = synth.products_like(9, scale=0.0003)
+    prog = programs.DHNProgram(g)
+    prog.step()
+    torch.cuda.synchronize()
+    ref = op.dhn_step(g, np_(prog.W), np_(prog.d_out))
+    assert_close(np_(prog.out), ref["out"], FP32_TOL, "out")
+    assert_close(np_(prog.dY), ref["dY"], FP32_TOL, "dY")
+    assert_close(np_(prog.dW), ref["dW"], FP32_TOL, "dW")
+    assert_close(np_(prog.dH), ref["dH"], FP32_TOL, "dH")
+    # join rows: Edge rows + closed 3- and 4-walks (homomorphism counts, exact integers)
+    oi = oracle.build_join_index(g["edges"]["src"], g["edges"]["dst"], g["nodes"]["key"],
+                                 g["nodes"]["key"], within_by_src_key=True)
+    n = len(g["nodes"]["key"])
+    cnt = sum(oracle.dhn_fwd(k, oi, g["nodes"]["key"], [np.ones((n, 1))] * k).sum() for k in (3, 4))
+    ref_rows = oi["n_join_rows"] + int(cnt)
+    assert abs(prog.join_rows_per_step - ref_rows) <= 1e-6 * ref_rows   # fp32 count sums

@@ -1,0 +1,69 @@
+"""GPU parity of the sharded GCN step (paper_2605_24207_b200/shard.py with the librnn.so
+backend) against the oracle GCN step: world size 1, and world size 2 as two processes sharing
+cuda:0 over gloo (the GPU box has one GPU; NCCL needs one device per rank).  Checks the owned
+outputs, the gathered input gradients and the all-reduced weight gradients."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from tests.test_shard_cpu import _free_port, graph_with_weights, reference
+from tests.util import FP32_TOL, assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def arxiv_small():
+    import synth
+    g = synth.arxiv_like(3, n_nodes=6000, n_edges=40000, d=128, layers=2)
+    return g
+
+
+def _run(g):
+    from paper_2605_24207_b200.shard import ShardedGCNProgram
+    prog = ShardedGCNProgram(g)
+    prog.step()
+    torch.cuda.synchronize()
+    return {"keys": prog.plan.my_keys, "rows": prog.plan.my_rows, "out": prog.owned_output(),
+            "dx": prog.owned_dx(), **{f"dW{l}": prog.dW[l].cpu().numpy() for l in range(prog.L)}}
+
+
+def _worker(rank, world, port, path, which):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = graph_with_weights() if which == "small" else arxiv_small()
+        np.savez(os.path.join(path, f"r{rank}.npz"), **_run(g))
+    finally:
+        dist.destroy_process_group()
+
+
+def check(res, g):
+    ref = reference(g)
+    keys = np.concatenate([r["keys"] for r in res])
+    pos = np.searchsorted(ref["out_keys"], keys)
+    assert_close(np.concatenate([r["out"] for r in res]), ref["out"][pos], FP32_TOL, "out")
+    rows = np.concatenate([r["rows"] for r in res])
+    assert_close(np.concatenate([r["dx"] for r in res]), ref["dH0"][rows], FP32_TOL, "dX")
+    for l in range(len(ref["dW"])):
+        for r in res:
+            assert_close(r[f"dW{l}"], ref["dW"][l], FP32_TOL, f"dW{l}")
+
+
+@pytest.mark.parametrize("which", ["small", "arxiv"])
+def test_sharded_world_1(which):
+    g = graph_with_weights() if which == "small" else arxiv_small()
+    check([_run(g)], g)
+
+
+@pytest.mark.parametrize("which", ["small", "arxiv"])
+def test_sharded_world_2(which):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, which), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    check(res, graph_with_weights() if which == "small" else arxiv_small())
