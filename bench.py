@@ -64,7 +64,7 @@ def make_graph(cfg, seed, sample=False):
     if cfg == "mag":
         return synth.mag_like(seed, scale=0.05 if sample else 1.0)
     if cfg == "dhn":
-        return synth.products_like(seed, scale=0.0005 if sample else DHN_SCALE[0])
+        return synth.products_like(seed, scale=0.0001 if sample else DHN_SCALE[0])
     return synth.cora_like(seed)
 
 
@@ -350,6 +350,8 @@ def oracle_timing(args, steps=1):
     oracle.build()
     if args.config in ("hyper", "mag"):
         return _oracle_sampled(args, steps, oracle, op)
+    if args.config == "dhn":
+        return _oracle_dhn(args, steps, oracle, op)
     graph = make_graph(args.config, args.seed)
     L = len(graph["W"])
     if args.config == "arxiv":
@@ -402,6 +404,34 @@ def _oracle_sampled(args, steps, oracle, op):
     return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{args.config}: {what}, {steps} run(s), fp64 single-threaded C, "
                       f"median {t:.2f} s"}, t, rows
+
+
+def _oracle_dhn(args, steps, oracle, op):
+    """DHN layer (C2, C3, C4 fwd + bwd incl. the nine projections) on a 1/10000-scale
+    products-shaped graph: the oracle enumerates closed walks with nested loops, so the full
+    graph (tr(A^4) ~ 1e11 walks) is out of reach; rows = Edge rows + closed 3- and 4-walks,
+    the same unit as the GPU arm."""
+    g = make_graph("dhn", args.seed, sample=True)
+    keys = g["nodes"]["key"]
+    n, d = g["nodes"]["x"].shape
+    rng = np.random.default_rng(11)
+    W = rng.standard_normal((9 * d, d)) / np.sqrt(d)
+    dO = rng.standard_normal((n, 3 * d))
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        op.dhn_step(g, W, dO)
+        times.append(time.perf_counter() - t0)
+    oi = oracle.build_join_index(g["edges"]["src"], g["edges"]["dst"], keys, keys,
+                                 within_by_src_key=True)
+    ones = [np.ones((n, 1))]
+    rows = int(oi["n_join_rows"]) + sum(int(round(oracle.dhn_fwd(k, oi, keys, ones * k).sum()))
+                                        for k in (3, 4))
+    t = float(np.median(times))
+    return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"dhn: whole layer (C2/C3/C4 fwd+bwd, projections) on a {n}-node "
+                      f"products-shaped graph ({len(g['edges']['src'])} Edge rows, {rows} "
+                      f"homomorphisms), {steps} run(s), fp64 single-threaded C, median {t:.2f} s"}, t, rows
 
 
 def run_reference(args):

@@ -11,7 +11,7 @@
 // SOFTMAX (flash-style, two passes): pass 1 (group-major) recomputes a = exp(e - lse) and
 // writes (a, de) per row and head, de = a (<dOut, M'_s> - <dOut, Out>), plus dQ; pass 2
 // (source-major) gathers dM'_s = sum a dOut_t and dK'_s = scale sum de Q_t.
-#include "rowsplit.cuh"
+#include "smsplit.cuh"
 
 namespace rnn {
 namespace {
@@ -717,6 +717,25 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
     s.dv = d_src; s.ld_dv = q->src.ld;
     s.dk = d_src_key; s.ld_dk = q->src_key.ld;
     s.heads = q->heads; s.scale = q->scale;
+    if (sm_rowsplit_ok(idx, q, qi.D) && idx->src_seg) {
+      SmBwd1Pol p1;
+      p1.a = sm_rows(idx, q);
+      p1.out = out; p1.ld_out = ld_out; p1.lse = lse; p1.dO = d_out; p1.ld_do = ld_dout;
+      p1.AD = Lw.AD; p1.dq = d_dst; p1.ld_dq = q->dst.ld;
+      RSCtx c1{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
+               idx->n_work, Lw.part_fwd, qi.pstride, Lw.cnt_fwd, 1};
+      RNN_TRY((launch_st<SmBwd1Pol, 4>(p1, c1, st)));
+      if (d_src || d_src_key) {
+        SmBwd2Pol p2;
+        p2.a = p1.a;
+        p2.dO = d_out; p2.ld_do = ld_dout; p2.AD = Lw.AD;
+        p2.dv = d_src; p2.ld_dv = q->src.ld; p2.dk = d_src_key; p2.ld_dk = q->src_key.ld;
+        RSCtx c2{idx->src_seg, idx->src_ptr, idx->n_src_rows, idx->n_join_rows,
+                 idx->src_work_ptr, idx->n_src_work, Lw.part_src, 2 * ld4, Lw.cnt_src, 1};
+        RNN_TRY((launch_st<SmBwd2Pol, 4>(p2, c2, st)));
+      }
+      return RNN_OK;
+    }
     const int LPR = qi.D / 4;
     s.LH = LPR / q->heads;
     switch (LPR) {

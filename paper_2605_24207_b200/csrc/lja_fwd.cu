@@ -11,7 +11,7 @@
 // SOFTMAX (HGT, Fig. 4): per group and head an online (running max / sum)
 // softmax over the rows' scores scale * <K'[s], Q[t]>, weighting the gathered values M'[s];
 // the log-sum-exp is saved for the backward.
-#include "rowsplit.cuh"
+#include "smsplit.cuh"
 
 namespace rnn {
 namespace {
@@ -472,6 +472,14 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
     if (lc == 32) return launch_rs_mode<1>(a, rx, st);
     if (lc == 64) return launch_rs_mode<2>(a, rx, st);
     return launch_rs_mode<4>(a, rx, st);
+  }
+  if (q->agg == RNN_AGG_SOFTMAX && sm_rowsplit_ok(idx, q, qi.D)) {
+    SmFwdPol pol;
+    pol.a = sm_rows(idx, q);
+    pol.out = out; pol.ld_out = ld_out; pol.beta = beta; pol.lse = lse;
+    RSCtx rx{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
+             idx->n_work, cx.partial, cx.pstride, cx.counter, 1};
+    return launch_st<SmFwdPol, 4>(pol, rx, st);
   }
   if (q->agg == RNN_AGG_SOFTMAX) {
     switch (qi.D / 4) {

@@ -153,7 +153,8 @@ def test_fwd_bwd_parity(R, ora, case):
             assert_close(np_(g[k]), gr[k], FP32_TOL, f"d_{k}")
 
 
-@pytest.mark.parametrize("heads,D", [(8, 128), (1, 4), (2, 16), (4, 32), (2, 64)])
+@pytest.mark.parametrize("heads,D", [(8, 128), (1, 128), (2, 128), (4, 128), (16, 128), (32, 128),
+                                     (1, 4), (2, 16), (4, 32), (2, 64)])
 def test_softmax_attention_parity(R, ora, heads, D):
     rng = np.random.default_rng(D + heads)
     db = make_case(rng, n_s=400, n_t=150, n_e=8000)
@@ -173,6 +174,45 @@ def test_softmax_attention_parity(R, ora, heads, D):
     dO = rng.standard_normal(ref.shape).astype(np.float32)
     g = R.join_aggregate_bwd(gi, q, padded(dO), out=out, lse=lse)
     gr = ora.lja_bwd(oi, dO, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=scale)
+    for k in ("src", "src_key", "dst"):
+        assert_close(np_(g[k]), gr[k], FP32_TOL, f"d_{k}")
+
+
+def test_softmax_dense_groups_beta(R, ora):
+    """Row-split softmax (D = 128) over a dense-group index: T keys with no join row give
+    out 0 / lse -inf / dQ 0; beta = 1 adds onto an existing union (A7); hub pieces merge."""
+    rng = np.random.default_rng(77)
+    db = make_case(rng, n_s=500, n_t=300, n_e=9000)
+    db["e_dst"] = np.where(np.isin(db["e_dst"], db["t_key"][100:140]), db["t_key"][0], db["e_dst"])
+    gi = R.build_join_index(cu(db["e_src"]), cu(db["e_dst"]), cu(db["s_key"]), cu(db["t_key"]),
+                            dense_groups=True, rows_per_item=48)
+    oi = ora.build_join_index(db["e_src"], db["e_dst"], db["s_key"], db["t_key"])
+    D, h = 128, 8
+    K = (rng.standard_normal((500, D)) * 0.5).astype(np.float32)
+    M = rng.standard_normal((500, D)).astype(np.float32)
+    Q = (rng.standard_normal((300, D)) * 0.5).astype(np.float32)
+    q = R.make_query("src", "softmax", src=padded(M), src_key=padded(K), dst=padded(Q), heads=h,
+                     scale=0.25)
+    out, lse = R.join_aggregate_fwd(gi, q)
+    ref, rlse = ora.lja_fwd(oi, agg="softmax", src=M, src_key=K, dst=Q, heads=h, scale=0.25)
+    # dense groups are every T key in ascending key order; present groups sit at their key's rank
+    rows = np.searchsorted(np.sort(db["t_key"]), oi["group_key"])
+    assert gi.n_groups == 300
+    full = np.zeros((300, D)); full[rows] = ref
+    flse = np.full((300, h), -np.inf); flse[rows] = rlse
+    absent = np.setdiff1d(np.arange(300), rows)
+    assert len(absent) >= 40
+    assert_close(np_(out), full, FP32_TOL, "out")
+    got_lse = np_(lse)
+    assert np.all(np.isneginf(got_lse[absent]))
+    assert_close(got_lse[rows], rlse, FP32_TOL, "lse")
+    base = rng.standard_normal((300, D)).astype(np.float32)
+    acc = padded(base)
+    R.join_aggregate_fwd(gi, q, out=acc, lse=torch.empty(300, h, device="cuda"), beta=1.0)
+    assert_close(np_(acc), base + full, FP32_TOL, "beta")
+    dO = rng.standard_normal((300, D)).astype(np.float32)
+    g = R.join_aggregate_bwd(gi, q, padded(dO), out=out, lse=lse)
+    gr = ora.lja_bwd(oi, dO[rows], agg="softmax", src=M, src_key=K, dst=Q, heads=h, scale=0.25)
     for k in ("src", "src_key", "dst"):
         assert_close(np_(g[k]), gr[k], FP32_TOL, f"d_{k}")
 
