@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32"])
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch the step kernel by kernel instead of replaying its CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-launches", action="store_true",
                     help="count kernel launches with torch.profiler (untimed pass)")
@@ -196,30 +198,55 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    graphed = not sharded and not args.eager
+    if graphed:
+        # the step as ONE CUDA graph (programs.CapturedStep): event record nodes around the
+        # step and around every kernel the program brackets give device times per replay
+        from paper_2605_24207_b200.programs import CapturedStep
+        cs = CapturedStep(prog, timed=True)
+        run_step = cs.replay
+    else:
+        run_step = prog.step
     for _ in range(args.warmup):
-        prog.step()
+        run_step()
     barrier()
 
     # ---- timed region ----
     sampler = ClockSampler(local)
     sampler.start()
-    prog.timers = {}
-    starts, ends = [], []
-    barrier()
-    for _ in range(args.steps):
-        flush.fill_(1.0)                      # L2 flush outside the step's events
-        s = torch.cuda.Event(enable_timing=True)
-        e = torch.cuda.Event(enable_timing=True)
-        s.record()
-        prog.step()
-        e.record()
-        starts.append(s)
-        ends.append(e)
-    barrier()
+    step_ms, launches_ms = [], {}
+    if graphed:
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                  # L2 flush outside the step's events
+            cs.replay()
+            torch.cuda.synchronize()          # read this replay's event nodes
+            t, per = cs.times()
+            step_ms.append(t)
+            for k, v in per.items():
+                launches_ms.setdefault(k, []).extend(v)
+        barrier()
+    else:
+        prog.timers = {}
+        starts, ends = [], []
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1.0)                  # L2 flush outside the step's events
+            s = torch.cuda.Event(enable_timing=True)
+            e = torch.cuda.Event(enable_timing=True)
+            s.record()
+            prog.step()
+            e.record()
+            starts.append(s)
+            ends.append(e)
+        barrier()
+        step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+        timers = prog.timers
+        prog.timers = None
+        for k, a in timers.items():
+            if not k.endswith("_end"):
+                launches_ms[k] = [x.elapsed_time(y) for x, y in zip(a, timers.get(k + "_end", []))]
     clocks = sampler.finish()
-    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
-    timers = prog.timers
-    prog.timers = None
     t_step = float(np.mean(step_ms))
     if world > 1:
         t = torch.tensor([t_step], device=dev)
@@ -228,8 +255,8 @@ def run_ours(args):
     value = (rows if sharded else world * rows) / (t_step * 1e-3)
 
     def kernel_ms(name):
-        a, b = timers.get(name, []), timers.get(name + "_end", [])
-        return float(np.mean([x.elapsed_time(y) for x, y in zip(a, b)])) if a else None
+        v = launches_ms.get(name)
+        return float(np.mean(v)) if v else None
 
     model = prog.roof_model()
     per = {k: kernel_ms(k) for k in ["proj_fwd", "proj_bwd"] + list(model)}
@@ -263,7 +290,8 @@ def run_ours(args):
     # ---- end to end through the C-ABI with host buffers ----
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(prog, args, world, dev, rows if sharded else world * rows)
+        e2e = run_e2e(prog, args, world, dev, rows if sharded else world * rows,
+                      cs.replay if graphed else None)
 
     result = None
     if rank == 0:
@@ -276,6 +304,7 @@ def run_ours(args):
                        "join_rows_per_step": rows,
                        **({"layers": prog.L, "dims": prog.dims} if hasattr(prog, "dims") else {}),
                        "projection_precision": args.prec, "l2": "flushed between timed steps",
+                       "step_launch": "one CUDA graph replay" if graphed else "eager launches",
                        "parallelism": (f"hash-partition by group key x{world} (NCCL all-gather / "
                                        f"reduce-scatter per layer)" if sharded else
                                        f"replica x{world}" if world > 1 else "single")},
@@ -300,7 +329,7 @@ def count_launches(prog):
     return len(ours)
 
 
-def run_e2e(prog, args, world, dev, job_rows):
+def run_e2e(prog, args, world, dev, job_rows, replay=None):
     """Same metric through the public API with HOST buffers: every step copies its inputs
     (node features and the upstream gradient, prog.host_io()) from pinned host memory and
     reads the parameter gradients back, inside the timed region."""
@@ -315,7 +344,7 @@ def run_e2e(prog, args, world, dev, job_rows):
     def one():
         for a, b in zip(ins, in_host):
             a.copy_(b, non_blocking=True)
-        prog.step()
+        (replay or prog.step)()
         for a, b in zip(out_host, outs):
             a.copy_(b, non_blocking=True)
 

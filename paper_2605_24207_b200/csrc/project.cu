@@ -526,17 +526,33 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
   }
 }
 
-// out[r, c] = sum_z partial[z, r, c]   (fixed order => deterministic split-K)
+// out[i] = sum_z partial[z, i] over a contiguous [rows * cols] block (fixed z order =>
+// deterministic split-K).  float4 per thread, 8 partials in flight; partials stream (no reuse).
 __global__ void splitk_reduce(const float* __restrict__ part, int64_t splits, int64_t stride,
-                              int64_t rows, int cols, int64_t ldp, float* __restrict__ out,
-                              int64_t ldo) {
+                              int64_t n, float* __restrict__ out) {
+  const int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (4 * i4 >= n) return;
+  const float4* p = reinterpret_cast<const float4*>(part) + i4;
+  const int64_t s4 = stride / 4;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t z = 0;
+  for (; z + 8 <= splits; z += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = __ldcs(p + (z + u) * s4);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = f4_add(acc, x[u]);
+  }
+  for (; z < splits; ++z) acc = f4_add(acc, __ldcs(p + z * s4));
+  reinterpret_cast<float4*>(out)[i4] = acc;
+}
+__global__ void splitk_reduce1(const float* __restrict__ part, int64_t splits, int64_t stride,
+                               int64_t n, float* __restrict__ out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= rows * cols) return;
-  const int64_t r = i / cols;
-  const int c = (int)(i % cols);
+  if (i >= n) return;
   float acc = 0.f;
-  for (int64_t z = 0; z < splits; ++z) acc += part[z * stride + r * ldp + c];
-  out[r * ldo + c] = acc;
+  for (int64_t z = 0; z < splits; ++z) acc += __ldcs(part + z * stride + i);
+  out[i] = acc;
 }
 
 // column sums db[c] = sum_m dY[m, c]: stage 1 (per row-chunk partials), stage 2 (ordered sum)
@@ -732,7 +748,7 @@ BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
   w.Wt = c.take<float>((size_t)K * ldt);
   const int64_t tiles = ceil_div(N, BM) * ceil_div(K, 256);
   int64_t splits = ceil_div(M, 8 * BK);
-  const int64_t cap = (2 * 148 + tiles - 1) / tiles;
+  const int64_t cap = (148 + tiles - 1) / tiles;   // about one wave of CTAs
   if (splits > cap) splits = cap;
   if (splits < 1) splits = 1;
   w.splits = (int)splits;
@@ -790,8 +806,14 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
     RNN_TRY(make_map(&ta, dY, N, M, lddy, 32, BK, true));
     RNN_TRY(make_map(&tb, X, K, M, ldx, 32, BK, true));
     RNN_TRY((gemm<true, true>(ta, tb, p, splits, prec, st)));
-    splitk_reduce<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, st>>>(
-        w.part, splits, p.part_stride, N, K, K, dW, K);
+    // partial tiles and dW are contiguous [N, K]
+    const int64_t nk = (int64_t)N * K;
+    if (nk % 4 == 0 && aligned16(dW))
+      splitk_reduce<<<(unsigned)ceil_div(nk / 4, 128), 128, 0, st>>>(w.part, splits, p.part_stride,
+                                                                    nk, dW);
+    else
+      splitk_reduce1<<<(unsigned)ceil_div(nk, 128), 128, 0, st>>>(w.part, splits, p.part_stride,
+                                                                  nk, dW);
     RNN_LAUNCH_CHECK();
   }
   if (db) {

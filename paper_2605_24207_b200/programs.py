@@ -45,7 +45,10 @@ class _Program:
     def _t(self, name):
         if self.timers is None:
             return None
-        e = torch.cuda.Event(enable_timing=True)
+        # inside a CUDA-graph capture the event becomes a record node of the graph, re-recorded
+        # by every replay (cudaEventRecordExternal)
+        e = torch.cuda.Event(enable_timing=True,
+                             external=torch.cuda.is_current_stream_capturing())
         e.record()
         self.timers.setdefault(name, []).append(e)
         return e
@@ -326,16 +329,18 @@ class HGTProgram(_Program):
         return sum(ix.n_join_rows for ix in self.idx.values())
 
     def lja_bytes(self):
-        """Softmax LJA (per head h): fwd reads per join row src id 4 + K' and M' rows 8d,
-        per group Q row 4d, out 4d, lse 4h, pointer 8.  bwd (two passes) reads per join row
-        src id 4 + group 4 + K', M' rows 8d + the group's Q/O/dO/lse (served from L1 within
-        a group, counted per group) and writes dK', dM' 8d per source row and dQ 4d per group."""
+        """Softmax LJA gather model (h heads).  fwd, per join row: src id 4 +
+        K' and M' rows 8d; per group: Q row 4d, out 4d, lse 4h, pointer 8.  bwd pass 1
+        (group-major), per join row: src id 4 + K', M' rows 8d + (a, de) written 8h; per group:
+        Q, O, dO rows 12d + lse 4h + dQ written 4d + pointer 8.  bwd pass 2 (source-major), per
+        join row: group id + position 8 + (a, de) read 8h + dO[g] and Q[t] rows 8d; per source
+        row: dK', dM' written 8d + pointer 8."""
         d, h = self.d, self.h
         f, b = [], []
         for ix in self.idx.values():
             f.append(ix.n_join_rows * (4 + 8 * d) + ix.n_groups * (8 * d + 4 * h + 8))
-            b.append(ix.n_join_rows * (8 + 8 * d) + ix.n_groups * (16 * d + 4 * h + 8) +
-                     ix.n_src_rows * (8 * d + 8))
+            b.append(ix.n_join_rows * ((4 + 8 * d + 8 * h) + (8 + 8 * h + 8 * d)) +
+                     ix.n_groups * (16 * d + 4 * h + 8) + ix.n_src_rows * (8 * d + 8))
         return {"lja_fwd": float(np.mean(f)), "lja_bwd": float(np.mean(b))}
 
     def host_io(self):
@@ -492,3 +497,53 @@ class DHNProgram(_Program):
                         dx_out=self.dH, dw_out=self.dW)
         self._t("proj_bwd_end")
         return self.dW, self.dH
+
+
+class CapturedStep:
+    """One program step captured once as a CUDA graph and replayed (the step is launch-bound
+    at small sizes: Cora's 14 kernels take ~10 us of GPU time each).  Every buffer the step
+    touches is preallocated by the program, so replays read the current contents of its
+    input tensors (copy new features / upstream gradients into them, then replay).
+
+    timed=True also captures CUDA-event record nodes around the step and around each kernel
+    the program brackets (prog.timers), so per-step and per-kernel device times can be read
+    after every replay (`times()`)."""
+
+    def __init__(self, prog, timed=False, warmup=2):
+        self.prog = prog
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(warmup):       # workspaces reach their final size before capture
+                prog.step()
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        saved = prog.timers
+        prog.timers = {} if timed else None
+        self.t0 = self.t1 = None
+        with torch.cuda.graph(self.graph):
+            if timed:
+                self.t0 = torch.cuda.Event(enable_timing=True, external=True)
+                self.t0.record()
+            prog.step()
+            if timed:
+                self.t1 = torch.cuda.Event(enable_timing=True, external=True)
+                self.t1.record()
+        self.events = prog.timers
+        prog.timers = saved
+
+    def replay(self):
+        self.graph.replay()
+
+    def times(self):
+        """(step ms, {kernel: ms summed over its launches in the step}) of the LAST replay
+        (call after it completed)."""
+        step = self.t0.elapsed_time(self.t1)
+        per = {}
+        for k, ev in self.events.items():
+            if k.endswith("_end"):
+                continue
+            ends = self.events.get(k + "_end", [])
+            per[k] = [a.elapsed_time(b) for a, b in zip(ev, ends)]
+        return step, per
