@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -108,6 +109,20 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tc_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Shared-memory matrix descriptor (sm_100 version bits = 1).
 //  K-major : SWIZZLE_128B (layout type 2): 8-row x 128B atoms stacked every 1024B (SBO); the
 //            K step of 8 tf32 elements is a 32-byte advance of the start address.
@@ -129,6 +144,20 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, bool mn_major, int
 __device__ __forceinline__ uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
          ((uint32_t)(bn >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// lo = x - trunc_tf32(x) only: the tcgen05 tf32 MMA truncates its fp32 inputs itself, so the
+// raw tile is its own hi part
+__device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n16, int t) {
+  for (uint32_t i = t; i < n16; i += 128) {
+    const float4 v = x[i];
+    float4 l;
+    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    lo[i] = l;
+  }
 }
 
 template <bool A_MN, bool B_MN, bool SPLIT3>
@@ -526,24 +555,262 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
   }
 }
 
-// out[i] = sum_z partial[z, i] over a contiguous [rows * cols] block (fixed z order =>
-// deterministic split-K).  float4 per thread, 8 partials in flight; partials stream (no reuse).
-__global__ void splitk_reduce(const float* __restrict__ part, int64_t splits, int64_t stride,
-                              int64_t n, float* __restrict__ out) {
+// ------------------------------------------------------------------------------------------
+// Transposed persistent projection: Y^T[n0:n0+128, tile] = Wb[n0:n0+128, :K] . X_tile^T, i.e.
+// Y[M, N] = X[M, K] W[N, K]^T computed with the WEIGHT block as the MMA A operand resident in
+// TMEM (tcgen05.mma A-from-TMEM: lane = output feature, column = k) and the streamed X row
+// tile as the K-major B operand in shared memory.  Shared memory then holds only the X ring
+// (up to 6 stages of raw 16 KB + its 3xTF32 low part), the accumulator lane is an output
+// FEATURE and its columns are tile ROWS, so the epilogue's tcgen05.ld hands a warp 32
+// consecutive features of one row: every global store is one coalesced 128-byte line.
+// TMEM: [0, 256) two 128-column accumulators, [256, 384) W hi, [384, 512) W lo.
+// Requires K <= 128 (W block hi + lo fit TMEM); N is covered by 128-feature column blocks.
+//   warp 0: TMA producer   warp 1: TMEM alloc + MMA issuer   warps 2-5: X hi/lo split
+//   warps 6-9: W -> TMEM (once), then the epilogue (TMEM -> registers -> HBM)
+// ------------------------------------------------------------------------------------------
+constexpr int PX_STAGES = 6;
+
+struct ProjTParams {
+  int64_t M;            // rows of X / Y
+  int N, K;             // out features, reduction length (K <= 128)
+  int nkb;              // K blocks of BK (the B tile ring steps per row tile)
+  int n_tiles_n;        // 128-feature column blocks
+  int64_t n_tiles_m;
+  int stages;
+  const float* W; int64_t ldw;   // [N, K] row-major
+  float* out; int64_t ldo;
+  const float* bias;
+};
+
+__device__ __forceinline__ void tc_mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+template <bool SPLIT3>
+__global__ void __launch_bounds__(PT_THREADS, 1)
+    tc_projt_kernel(const __grid_constant__ CUtensorMap tx, ProjTParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  constexpr uint32_t X_BYTES = BM * BK * 4;             // one 128-row x 32-k block
+  constexpr uint32_t X_STAGE = X_BYTES * (SPLIT3 ? 2u : 1u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.stages * X_STAGE);
+  uint64_t* x_full = bars;
+  uint64_t* x_conv = x_full + PX_STAGES;
+  uint64_t* x_empty = x_conv + PX_STAGES;
+  uint64_t* w_ready = x_empty + PX_STAGES;
+  uint64_t* acc_full = w_ready + 1;    // [2]
+  uint64_t* acc_empty = acc_full + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nt = blockIdx.x % p.n_tiles_n;
+  const int n0 = nt * 128;
+  const int64_t mt0 = blockIdx.x / p.n_tiles_n;
+  const int64_t mstep = gridDim.x / p.n_tiles_n;
+  constexpr uint32_t W_HI = 256, W_LO = 384;
+
+  if (warp == 1) {
+    if (lane == 0) {
+      for (int s = 0; s < PX_STAGES; ++s) {
+        mbar_init(&x_full[s], 1);
+        mbar_init(&x_conv[s], 128);
+        mbar_init(&x_empty[s], 1);
+      }
+      mbar_init(w_ready, 128);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&acc_full[b], 1);
+        mbar_init(&acc_empty[b], 128);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp == 0 && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tx)) : "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int64_t it = 0;
+      for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep) {
+        for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+          const int s = (int)(it % p.stages);
+          const uint32_t ph = (uint32_t)((it / p.stages) & 1);
+          if (it >= p.stages) mbar_wait(&x_empty[s], ph ^ 1);
+          mbar_expect_tx(&x_full[s], X_BYTES);
+          tma_load_2d(&tx, smem + s * X_STAGE, &x_full[s], kb * BK, (int)(mt * BM));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // A = W block from TMEM (M = 128 features), B = X tile (N = 128 rows, K-major)
+    const uint32_t idesc = make_idesc(BM, false, false);
+    mbar_wait(w_ready, 0);
+    tc_fence_after();
+    int64_t it = 0;
+    int j = 0;
+    for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
+      const int buf = j & 1;
+      if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(buf * 128);
+      for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+        const int s = (int)(it % p.stages);
+        const uint32_t ph = (uint32_t)((it / p.stages) & 1);
+        mbar_wait(SPLIT3 ? &x_conv[s] : &x_full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t xs = smem_u32(smem + s * X_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint64_t bh = make_desc(xs, false, kk, 0);
+            const uint32_t ah = tmem + W_HI + (uint32_t)(kb * BK + kk * 8);
+            tc_mma_tf32_ta(d, ah, bh, idesc, (kb | kk) != 0);
+            if (SPLIT3) {
+              const uint64_t bl = make_desc(xs + X_BYTES, false, kk, 0);
+              tc_mma_tf32_ta(d, ah, bl, idesc, 1u);
+              tc_mma_tf32_ta(d, tmem + W_LO + (uint32_t)(kb * BK + kk * 8), bh, idesc, 1u);
+            }
+          }
+          tc_commit(&x_empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc_commit(&acc_full[buf]);
+      __syncwarp();
+    }
+  } else if (warp < 6) {
+    if (SPLIT3) {
+      const int t = threadIdx.x - 64;
+      int64_t it = 0;
+      for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep) {
+        for (int kb = 0; kb < p.nkb; ++kb, ++it) {
+          const int s = (int)(it % p.stages);
+          const uint32_t ph = (uint32_t)((it / p.stages) & 1);
+          mbar_wait(&x_full[s], ph);
+          uint8_t* x = smem + s * X_STAGE;
+          lo_tile(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(x + X_BYTES),
+                  X_BYTES / 16, t);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(&x_conv[s]);
+        }
+      }
+    }
+  } else {
+    const int quad = warp & 3;                 // TMEM lanes [32 quad, 32 quad + 32)
+    const int f = n0 + quad * 32 + lane;       // this thread's output feature
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    // ---- W block -> TMEM (raw = hi: the MMA truncates fp32 to tf32 itself, profiles/
+    // probe_tf32.py; lo = w - trunc(w)); padding features / k columns are zero.  32 x 32
+    // blocks are read coalesced (lane = k) and transposed through shared memory so that
+    // thread l ends up holding feature row f's k values for tcgen05.st (lane = feature).
+    float* tp = reinterpret_cast<float*>(smem + p.stages * X_STAGE + 1024) + quad * 32 * 33;
+    const int kpad = p.nkb * BK;
+    const int fbase = n0 + quad * 32;
+    for (int k0 = 0; k0 < kpad; k0 += 32) {
+      const int k = k0 + lane;
+      float v[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        v[r] = (fbase + r < p.N && k < p.K) ? __ldg(p.W + (int64_t)(fbase + r) * p.ldw + k) : 0.f;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) tp[r * 33 + lane] = v[r];
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const float w = tp[lane * 33 + h * 16 + q];
+          hi[q] = __float_as_uint(w);
+          lo[q] = __float_as_uint(w - __uint_as_float(__float_as_uint(w) & 0xFFFFE000u));
+        }
+        tc_st16(lane_base + W_HI + (uint32_t)(k0 + 16 * h), hi);
+        if (SPLIT3) tc_st16(lane_base + W_LO + (uint32_t)(k0 + 16 * h), lo);
+      }
+      __syncwarp();
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    tc_fence_before();
+    mbar_arrive(w_ready);
+    // ---- epilogue ----
+    const float bf = (p.bias && f < p.N) ? __ldg(p.bias + f) : 0.f;
+    int j = 0;
+    for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
+      const int buf = j & 1;
+      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const int64_t r0 = mt * BM;
+      for (int c0 = 0; c0 < BM; c0 += 16) {
+        uint32_t r[16];
+        tc_ld16(lane_base + (uint32_t)(buf * 128 + c0), r);
+        if (f < p.N) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int64_t row = r0 + c0 + q;
+            if (row < p.M) __stcs(p.out + row * p.ldo + f, __uint_as_float(r[q]) + bf);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// out[i] = sum_z partial[z, i] over a contiguous [rows * cols] block, two fixed-order stages
+// (deterministic split-K): blockIdx.y = g sums partials [8g, 8g + 8) into tmp[g] (float4 per
+// thread, 8 loads in flight), then splitk_final sums tmp[0..G) in order.
+__global__ void splitk_stage(const float* __restrict__ part, int64_t splits, int64_t stride,
+                            int64_t n, float* __restrict__ tmp) {
   const int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (4 * i4 >= n) return;
+  const int64_t z0 = (int64_t)blockIdx.y * 8;
   const float4* p = reinterpret_cast<const float4*>(part) + i4;
   const int64_t s4 = stride / 4;
+  float4 x[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    x[u] = z0 + u < splits ? __ldcs(p + (z0 + u) * s4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = x[0];
+#pragma unroll
+  for (int u = 1; u < 8; ++u) acc = f4_add(acc, x[u]);
+  reinterpret_cast<float4*>(tmp)[blockIdx.y * (n / 4) + i4] = acc;
+}
+__global__ void splitk_final(const float* __restrict__ tmp, int64_t groups, int64_t n,
+                             float* __restrict__ out) {
+  const int64_t i4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (4 * i4 >= n) return;
+  const float4* t = reinterpret_cast<const float4*>(tmp) + i4;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int64_t z = 0;
-  for (; z + 8 <= splits; z += 8) {
-    float4 x[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = __ldcs(p + (z + u) * s4);
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc = f4_add(acc, x[u]);
-  }
-  for (; z < splits; ++z) acc = f4_add(acc, __ldcs(p + z * s4));
+  for (int64_t g = 0; g < groups; ++g) acc = f4_add(acc, __ldcs(t + g * (n / 4)));
   reinterpret_cast<float4*>(out)[i4] = acc;
 }
 __global__ void splitk_reduce1(const float* __restrict__ part, int64_t splits, int64_t stride,
@@ -676,6 +943,31 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
     RNN_LAUNCH_CHECK();
     return RNN_OK;
   }
+  if (Kred <= 128 && !getenv("RNN_NO_PROJT")) {
+    // weights resident in TMEM as the A operand, X streamed as B (tc_projt_kernel)
+    const bool s3 = prec == RNN_PREC_3XTF32;
+    ProjTParams q{};
+    q.M = M; q.N = N; q.K = (int)Kred;
+    q.nkb = (int)ceil_div(Kred, BK);
+    q.n_tiles_n = (int)ceil_div(N, 128);
+    q.n_tiles_m = ceil_div(M, BM);
+    const size_t x_stage = (size_t)BM * BK * 4 * (s3 ? 2 : 1);
+    const size_t tscratch = 4 * 32 * 33 * sizeof(float) + 1024;   // W transpose tiles
+    const size_t budget = 227 * 1024 - 1024 - 256 - tscratch;
+    q.stages = (int)std::min<size_t>(PX_STAGES, budget / x_stage);
+    q.W = B; q.ldw = ldb; q.out = Y; q.ldo = ldy; q.bias = bias;
+    CUtensorMap tx;
+    RNN_TRY(make_map(&tx, A, Kred, M, lda, BK, BM));
+    const int64_t per_n =
+        std::max<int64_t>(1, std::min<int64_t>(num_sms() / q.n_tiles_n, q.n_tiles_m));
+    const unsigned grid = (unsigned)(per_n * q.n_tiles_n);
+    const size_t smem = q.stages * x_stage + 1024 + tscratch;
+    auto kern = s3 ? tc_projt_kernel<true> : tc_projt_kernel<false>;
+    RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, PT_THREADS, smem, st>>>(tx, q);
+    RNN_LAUNCH_CHECK();
+    return RNN_OK;
+  }
   {
     // persistent resident-B kernel when B's column block fits next to a 2-deep A ring
     const bool s3 = prec == RNN_PREC_3XTF32;
@@ -737,7 +1029,7 @@ extern "C" rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t 
 
 namespace {
 struct BwdWs {
-  float* Wt; float* part; float* cpart;
+  float* Wt; float* part; float* part2; float* cpart;
   size_t bytes;
   int splits; int64_t chunks;
 };
@@ -753,6 +1045,7 @@ BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
   if (splits < 1) splits = 1;
   w.splits = (int)splits;
   w.part = c.take<float>((size_t)splits * N * K);
+  w.part2 = c.take<float>((size_t)ceil_div(splits, 8) * N * K);
   w.chunks = ceil_div(M > 0 ? M : 1, 4096);
   w.cpart = c.take<float>((size_t)w.chunks * N);
   w.bytes = c.used + 1024;
@@ -808,10 +1101,12 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
     RNN_TRY((gemm<true, true>(ta, tb, p, splits, prec, st)));
     // partial tiles and dW are contiguous [N, K]
     const int64_t nk = (int64_t)N * K;
-    if (nk % 4 == 0 && aligned16(dW))
-      splitk_reduce<<<(unsigned)ceil_div(nk / 4, 128), 128, 0, st>>>(w.part, splits, p.part_stride,
-                                                                    nk, dW);
-    else
+    if (nk % 4 == 0 && aligned16(dW)) {
+      const int64_t groups = ceil_div(splits, 8);
+      splitk_stage<<<dim3((unsigned)ceil_div(nk / 4, 128), (unsigned)groups), 128, 0, st>>>(
+          w.part, splits, p.part_stride, nk, w.part2);
+      splitk_final<<<(unsigned)ceil_div(nk / 4, 128), 128, 0, st>>>(w.part2, groups, nk, dW);
+    } else
       splitk_reduce1<<<(unsigned)ceil_div(nk, 128), 128, 0, st>>>(w.part, splits, p.part_stride,
                                                                   nk, dW);
     RNN_LAUNCH_CHECK();

@@ -1,0 +1,35 @@
+"""Micro-benchmark of rnn.project / rnn.project_bwd (CUDA events, median of 20) over shapes and
+precisions: separates MMA-bound from memory-bound behaviour of the projection kernels."""
+import os, sys, json
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2605_24207_b200 import rnn
+
+
+def t(fn, n=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(n):
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record(); torch.cuda.synchronize(); ts.append(a.elapsed_time(b))
+    ts.sort()
+    return ts[len(ts) // 2] * 1e3
+
+
+res = []
+for (M, K, N) in [(169343, 128, 128), (1000000, 128, 128),
+                  (1134649, 128, 512)]:
+    X = torch.randn(M, K, device="cuda"); W = torch.randn(N, K, device="cuda")
+    Y = torch.empty(M, N, device="cuda"); dY = torch.randn(M, N, device="cuda")
+    ws = rnn.Workspace("cuda")
+    for prec in ("3xtf32", "tf32"):
+        f = t(lambda: rnn.project(X, W, out=Y, prec=prec))
+        b = t(lambda: rnn.project_bwd(X, W, dY, want_dx=True, prec=prec, ws=ws))
+        gb = (M * K + M * N) * 4 / 1e9
+        r = dict(M=M, K=K, N=N, prec=prec, fwd_us=round(f, 1), bwd_us=round(b, 1),
+                 fwd_GBps=round(gb / (f * 1e-6)), ideal_fwd_us=round(gb / 6542 * 1e6, 1))
+        print(json.dumps(r), flush=True)
+        res.append(r)
+    del X, W, Y, dY
