@@ -26,10 +26,9 @@
 namespace rnn {
 namespace {
 
-constexpr int DHN_THREADS = 512;
+constexpr int DHN_THREADS = 1024;
 constexpr int DHN_WARPS = DHN_THREADS / 32;
-constexpr int DHN_CTAS_PER_SM = 2;
-constexpr size_t DHN_SLAB_BUDGET = size_t(16) << 30;   // bytes of k=4 slabs across all CTAs
+constexpr int DHN_CTAS_PER_SM = 1;
 
 struct DhnArgs {
   int64_t G;
@@ -51,8 +50,11 @@ struct DhnArgs {
   const int32_t* order;   // roots, heaviest first
   int* counter;
   int* mark;              // k=3: per-CTA [G] int32
-  float* slab;            // k=4: per-CTA [G * ds]
-  int64_t cta_stride;     // elements between consecutive CTAs' mark / slab
+  const uint32_t* wout;   // k=4: out-wedges per root (bound on distinct 2-hop w)
+  float* slab;            // k=4: per-CTA S1 values [H4_CAP][32]
+  const int32_t* nbrh;    // k=4: nbr[] with every group's list sorted by hash partition
+  const int32_t* sgh;     // k=4: src_group[] with every row's list sorted likewise
+  int64_t cta_stride;     // elements between consecutive CTAs' mark
 };
 
 __device__ __forceinline__ void dhn_store(const DhnArgs& a, int64_t n, int c, float v) {
@@ -73,21 +75,65 @@ __device__ __forceinline__ int64_t dhn_next_root(const DhnArgs& a, int* s_root) 
 }
 
 // -------------------------------------------------------------------------------------
-// C3: triangles n -> v -> w -> n
+// shared-memory open-addressing hash sets keyed by group id (linear probing, key -1 = empty)
 // -------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t dhn_hash(uint32_t x) {
+  x ^= x >> 16; x *= 0x7FEB352Du; x ^= x >> 15; x *= 0x846CA68Bu; x ^= x >> 16;
+  return x;
+}
+// slot of key w (inserted if absent); -1 if the table is full
+__device__ __forceinline__ int hs_insert(int* keys, int cap_mask, int w) {
+  uint32_t s = dhn_hash((uint32_t)w) & (uint32_t)cap_mask;
+  for (int t = 0; t <= cap_mask; ++t) {
+    const int prev = atomicCAS(&keys[s], -1, w);
+    if (prev == -1 || prev == w) return (int)s;
+    s = (s + 1) & (uint32_t)cap_mask;
+  }
+  return -1;
+}
+__device__ __forceinline__ int hs_find(const int* keys, int cap_mask, int w) {
+  uint32_t s = dhn_hash((uint32_t)w) & (uint32_t)cap_mask;
+  for (int t = 0; t <= cap_mask; ++t) {
+    const int k = keys[s];
+    if (k == w) return (int)s;
+    if (k == -1) return -1;
+    s = (s + 1) & (uint32_t)cap_mask;
+  }
+  return -1;
+}
+
+// -------------------------------------------------------------------------------------
+// C3: triangles n -> v -> w -> n.  The root's in-neighbours w (with multiplicity = number of
+// closing Edge rows w -> n) go into a shared-memory hash set; the CTA's warps walk the wedges
+// n -> v -> w with lanes over w, probe the set, and the hits gather f1(v) (.) f2(w) with
+// lane = channel.  Roots whose in-degree exceeds the set use a per-CTA global mark array.
+// -------------------------------------------------------------------------------------
+constexpr int H3_CAP = 8192;                 // slots (keys + counts: 64 KB)
+constexpr int H3_MAX_INDEG = 6144;           // load factor <= 0.75
+
 template <int DPL>
-__global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnArgs a) {
+__global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
+  extern __shared__ int h3[];
+  int* keys = h3;
+  int* cnt = h3 + H3_CAP;
+  float* s_acc = reinterpret_cast<float*>(cnt + H3_CAP);   // [DHN_WARPS][DPL * 32]
   __shared__ int s_root;
-  __shared__ float s_acc[DHN_WARPS][DPL * 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* mark = a.mark + (int64_t)blockIdx.x * a.cta_stride;
   const int d = a.d;
+  for (int i = threadIdx.x; i < H3_CAP; i += DHN_THREADS) { keys[i] = -1; cnt[i] = 0; }
   for (;;) {
     const int64_t n = dhn_next_root(a, &s_root);
     if (n < 0) break;
     const int32_t r = a.row_of[n];
     const int64_t ib = a.sp[r], ie = a.sp[r + 1];
-    for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) atomicAdd(&mark[a.sg[q]], 1);
+    const bool hashed = ie - ib <= H3_MAX_INDEG;
+    if (hashed) {
+      for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS)
+        atomicAdd(&cnt[hs_insert(keys, H3_CAP - 1, a.sg[q])], 1);
+    } else {
+      for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) atomicAdd(&mark[a.sg[q]], 1);
+    }
     __syncthreads();
     float acc[DPL];
 #pragma unroll
@@ -106,7 +152,15 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
       for (int64_t i0 = a.gp[v]; i0 < we; i0 += 32) {
         const int64_t i = i0 + lane;
         const int32_t w = i < we ? a.nbr[i] : -1;
-        const int m = w >= 0 ? __ldcg(&mark[w]) : 0;
+        int m = 0;
+        if (w >= 0) {
+          if (hashed) {
+            const int sl = hs_find(keys, H3_CAP - 1, w);
+            m = sl >= 0 ? cnt[sl] : 0;
+          } else {
+            m = __ldcg(&mark[w]);
+          }
+        }
         unsigned bal = __ballot_sync(FULL, m != 0);
         while (bal) {
           // up to 4 hits per round so their row loads are in flight together
@@ -139,78 +193,343 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
       }
     }
 #pragma unroll
-    for (int j = 0; j < DPL; ++j) s_acc[warp][lane + 32 * j] = acc[j];
+    for (int j = 0; j < DPL; ++j) s_acc[warp * DPL * 32 + lane + 32 * j] = acc[j];
     __syncthreads();
     for (int c = threadIdx.x; c < d; c += DHN_THREADS) {
       float s = 0.f;
-#pragma unroll 4
-      for (int w = 0; w < DHN_WARPS; ++w) s += s_acc[w][c];
+      for (int w = 0; w < DHN_WARPS; ++w) s += s_acc[w * DPL * 32 + c];
       dhn_store(a, n, c, s);
     }
-    for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) mark[a.sg[q]] = 0;
+    if (hashed) {
+      for (int i = threadIdx.x; i < H3_CAP; i += DHN_THREADS) { keys[i] = -1; cnt[i] = 0; }
+    } else {
+      for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) mark[a.sg[q]] = 0;
+    }
   }
 }
 
 // -------------------------------------------------------------------------------------
-// C4: 4-cycles n -> v -> w -> p -> n, factorised through w
+// C4: closed 4-walks n -> v -> w -> p -> n, factorised through w:
+//   C4(n) = f0(n) (.) sum_{in-wedges w -> p -> n} f3(p) (.) G(w),
+//   G(w)  = f2(w) (.) S1(w),  S1(w) = sum_{out-wedges n -> v -> w} f1(v).
+// S1 lives in a shared-memory hash table keyed by w holding a 32-channel lane slice per entry
+// (lane = channel: every wedge is ONE conflict-free 128-byte smem atomic).  A root whose
+// out-wedges could name more distinct w than the table holds is processed in P = 2^b
+// partitions of w by the top b bits of hash(w).  Every adjacency list is pre-sorted by that
+// hash (prepare: segmented radix sort), so partition k of a list is a contiguous run that
+// starts where partition k-1 ended: per-neighbour cursors in shared memory make each pass
+// touch only its own entries (no re-scan), lanes test 32 neighbours' cursors at a time.
 // -------------------------------------------------------------------------------------
-template <int DS>
-__global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn4_kernel(DhnArgs a) {
-  constexpr int S = 32 / DS;   // 2-paths processed side by side per warp
-  __shared__ int s_root;
-  __shared__ float s_out[128];
+// phase timing of dhn4_kernel (thread 0's clock between barriers), read by the internal hook
+// rnn_internal_dhn_stats: [0] root setup, [1] out sweep, [2] finalize, [3] in sweep,
+// [4] clear, [5] reduce/store, [6] partitions, [7] roots, [8] chunked partitions
+__device__ unsigned long long g_dhn4_stats[16];
+#define H4_T(slot)                                                                  \
+  do {                                                                              \
+    if (threadIdx.x == 0) {                                                         \
+      const long long t_ = clock64();                                               \
+      atomicAdd(&g_dhn4_stats[slot], (unsigned long long)(t_ - t_last));            \
+      t_last = t_;                                                                  \
+    }                                                                               \
+  } while (0)
+
+constexpr int H4_CAP = 16384;                // key slots in shared memory (64 KB)
+constexpr int H4_PART = 8192;                // target distinct w per partition (load <= 0.5)
+constexpr int H4_DEG_CAP = 8192;             // neighbours with smem cursors (per side)
+constexpr int H4_HBITS = 16;                 // hash bits the lists are sorted by
+
+__device__ __forceinline__ uint32_t h4_top(int32_t w) {   // sort key / partition source
+  return dhn_hash((uint32_t)w ^ 0x5bd1e995u) >> (32 - H4_HBITS);
+}
+
+// first position in [b, e) of list L whose partition (top `bits` of the 16-bit hash) >= k
+__device__ __forceinline__ int64_t h4_lower(const int32_t* L, int64_t b, int64_t e, uint32_t k,
+                                           int sh) {
+  while (b < e) {
+    const int64_t m = b + ((e - b) >> 1);
+    if ((h4_top(L[m]) >> sh) < k) b = m + 1; else e = m;
+  }
+  return b;
+}
+
+constexpr int H4_LONG = 96;                 // runs longer than this are split over all warps
+constexpr int H4_LONG_MAX = 512;             // long runs queued per sweep (overflow: inline)
+
+// One 32-entry chunk of a run: OUT inserts w and adds f1(v) to S1(w) (one 128-byte red per
+// entry); IN finds w and sums G(w) into t (8 slab rows in flight per round).
+// compact id of key w in the C4 table (inserted if absent): the CAS winner draws the next id
+// (so a root's S1 rows are a dense prefix of the CTA's slab and stay L2-resident); a lane
+// that finds w already present waits for the winner to publish the id.
+__device__ __forceinline__ int h4_insert(int* keys, int* ids, int* n_ids, int w) {
+  uint32_t s = dhn_hash((uint32_t)w) & (uint32_t)(H4_CAP - 1);
+  for (int t = 0; t < H4_CAP; ++t) {
+    const int prev = atomicCAS(&keys[s], -1, w);
+    if (prev == -1) {
+      const int id = atomicAdd(n_ids, 1);
+      atomicExch(&ids[s], id);
+      return id;
+    }
+    if (prev == w) {
+      int id;
+      do { id = *((volatile int*)&ids[s]); } while (id < 0);
+      return id;
+    }
+    s = (s + 1) & (uint32_t)(H4_CAP - 1);
+  }
+  return -1;
+}
+
+// One 32-entry chunk of a run: OUT inserts w and adds f1(v) to S1(w) (one 128-byte red per
+// entry); IN finds w and sums G(w) into t (8 slab rows in flight per round).
+template <bool OUT>
+__device__ __forceinline__ void h4_chunk(int* keys, int* ids, int* n_ids, float* S, int32_t w,
+                                         bool in, float fv, float& t, int lane,
+                                         const float* F2c, int d) {
+  if (OUT) {
+    const int sl = (in && w >= 0) ? h4_insert(keys, ids, n_ids, w) : -1;
+    unsigned bal = __ballot_sync(FULL, sl >= 0);
+    while (bal) {
+      const int q = __ffs(bal) - 1;
+      bal &= bal - 1;
+      atomicAdd(&S[__shfl_sync(FULL, sl, q) * 32 + lane], fv);
+    }
+  } else {
+    int sl = (in && w >= 0) ? hs_find(keys, H4_CAP - 1, w) : -1;
+    if (sl >= 0) sl = ids[sl];
+    unsigned bal = __ballot_sync(FULL, sl >= 0);
+    while (bal) {   // G(w) = f2(w) (.) S1(w) formed on the fly, 8 hits in flight
+      float x[8], y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int q = -1;
+        if (bal) { q = __ffs(bal) - 1; bal &= bal - 1; }
+        const int slq = __shfl_sync(FULL, sl, q < 0 ? 0 : q);
+        const int wq = __shfl_sync(FULL, w, q < 0 ? 0 : q);
+        x[u] = q >= 0 ? __ldcg(&S[slq * 32 + lane]) : 0.f;
+        y[u] = q >= 0 ? F2c[(int64_t)wq * d] : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t = fmaf(x[u], y[u], t);
+    }
+  }
+}
+
+struct H4Root {
+  int64_t n, ib, pb;
+  int deg;               // neighbours on this side
+  uint32_t P, part;
+  int sh;
+  bool cur_ok, chunked;
+};
+
+// One side of one partition.  OUT: neighbours v = nbr[pb + i] with lists nbrh over the group
+// CSR; IN: neighbours p = sg[ib + i] with lists sgh over the row CSR.  Phase A: each warp
+// serves neighbours (one per warp, or 32 per step in chunked mode) and walks their runs of
+// this partition; runs longer than H4_LONG are queued.  Phase B: every queued run is split
+// over all warps.  Returns this thread's contribution to the root's accumulator (IN).
+template <bool OUT>
+__device__ float h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids, int* n_ids,
+                          float* S, int* cur, int* q_i, int64_t* q_b, int64_t* q_e, int* q_n,
+                          int* grab, int c, bool cok) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int c = lane % DS, sub = lane / DS;
-  float* slab = a.slab + (int64_t)blockIdx.x * a.cta_stride;
+  const int32_t* L = OUT ? a.nbrh : a.sgh;
+  const float* Fv = OUT ? a.F1 : a.F3;
   const int d = a.d;
+  const float* F2c = a.F2 + (cok ? c : 0);   // f2 column of this lane (rows gathered by w)
+  float acc = 0.f;
+  // phase A: warps grab neighbours dynamically (chunked mode: 32 at a time, lanes in parallel)
+  const int step = R.chunked ? 32 : 1;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(grab, step);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= R.deg) break;
+    const int i = R.chunked ? base + lane : base;
+    int32_t u = -1;
+    int64_t b0 = 0, e0 = 0, s0 = 0;
+    bool has = false;
+    if (i < R.deg && (R.chunked || lane == 0)) {
+      if (OUT) {
+        u = a.nbr[R.pb + i];
+        if (u >= 0) { s0 = a.gp[u]; e0 = a.gp[u + 1]; }
+      } else {
+        u = a.sg[R.ib + i];
+        const int32_t ru = a.row_of[u];
+        s0 = a.sp[ru];
+        e0 = a.sp[ru + 1];
+      }
+      if (u >= 0) {
+        b0 = R.cur_ok ? s0 + cur[i] : h4_lower(L, s0, e0, R.part, R.sh);
+        has = b0 < e0 && (h4_top(L[b0]) >> R.sh) == R.part;
+      }
+    }
+    unsigned hb = __ballot_sync(FULL, has);
+    while (hb) {
+      const int j = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const int32_t uj = __shfl_sync(FULL, u, j);
+      const int64_t bj = __shfl_sync(FULL, b0, j), ej = __shfl_sync(FULL, e0, j);
+      const int64_t sj = __shfl_sync(FULL, s0, j);
+      const int ij = __shfl_sync(FULL, i, j);
+      int64_t re = -1;   // run end when the run is long
+      if (ej - bj > H4_LONG) {
+        re = R.P == 1 ? ej : h4_lower(L, bj, ej, R.part + 1, R.sh);
+        if (re - bj <= H4_LONG) re = -1;
+      }
+      if (re >= 0) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(q_n, 1);
+        slot = __shfl_sync(FULL, slot, 0);
+        if (slot < H4_LONG_MAX) {
+          if (lane == 0) { q_i[slot] = uj; q_b[slot] = bj; q_e[slot] = re; }
+          if (R.cur_ok && lane == 0) cur[ij] = (int)(re - sj);
+          continue;
+        }
+      }
+      const float fv = cok ? Fv[(int64_t)uj * d + c] : 0.f;
+      float t = 0.f;
+      int64_t t0 = bj;
+      for (;;) {
+        const int64_t tt = t0 + lane;
+        const int32_t w = tt < ej ? L[tt] : -1;
+        const bool in = tt < ej && (h4_top(w) >> R.sh) == R.part;
+        const unsigned im = __ballot_sync(FULL, in);
+        h4_chunk<OUT>(keys, ids, n_ids, S, w, in, fv, t, lane, F2c, d);
+        t0 += __popc(im);
+        if (im != FULL) break;
+      }
+      if (!OUT) acc += fv * t;
+      if (R.cur_ok && lane == 0) cur[ij] = (int)(t0 - sj);
+    }
+  }
+  __syncthreads();
+  // phase B: the 32-entry chunks of all queued long runs, grabbed dynamically by the warps
+  const int nq = *q_n < H4_LONG_MAX ? *q_n : H4_LONG_MAX;
+  if (nq > 0) {
+    if (threadIdx.x == 0) *grab = 0;
+    __syncthreads();
+    int k = 0;            // current item (items are walked in order; chunk ids are global)
+    int64_t k_end = 0;    // first global chunk id after item k
+    int64_t k_beg = 0;
+    float fv = 0.f, t = 0.f;
+    int32_t uk = -1;
+    for (;;) {
+      int g = 0;
+      if (lane == 0) g = atomicAdd(grab, 1);
+      g = __shfl_sync(FULL, g, 0);
+      // advance to the item holding chunk g (grabs are increasing per warp)
+      bool done = false;
+      while (g >= k_end) {
+        if (uk >= 0 && !OUT) acc += fv * t;
+        t = 0.f;
+        uk = -1;
+        if (k >= nq) { done = true; break; }
+        k_beg = k_end;
+        k_end += (q_e[k] - q_b[k] + 31) / 32;
+        uk = q_i[k];
+        fv = cok ? Fv[(int64_t)uk * d + c] : 0.f;
+        ++k;
+      }
+      if (done) break;
+      const int64_t qb = q_b[k - 1], qe = q_e[k - 1];
+      const int64_t tt = qb + (g - k_beg) * 32 + lane;
+      const int32_t w = tt < qe ? L[tt] : -1;
+      h4_chunk<OUT>(keys, ids, n_ids, S, w, tt < qe, fv, t, lane, F2c, d);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { *q_n = 0; *grab = 0; }
+  __syncthreads();
+  return acc;
+}
+
+__global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
+  extern __shared__ int h4[];
+  int* keys = h4;
+  int* ids = h4 + H4_CAP;                                  // compact id of each slot
+  float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;  // [H4_CAP][32] by compact id
+  float* s_red = reinterpret_cast<float*>(ids + H4_CAP);   // [DHN_WARPS][32]
+  int* cur_out = reinterpret_cast<int*>(s_red + DHN_WARPS * 32);   // [H4_DEG_CAP]
+  int* cur_in = cur_out + H4_DEG_CAP;                               // [H4_DEG_CAP]
+  int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
+  int64_t* q_e = q_b + H4_LONG_MAX;
+  int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
+  __shared__ int s_root, q_n, n_ids, grab;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = a.d;
+  for (int i = threadIdx.x; i < H4_CAP; i += DHN_THREADS) { keys[i] = -1; ids[i] = -1; }
+  if (threadIdx.x == 0) { q_n = 0; n_ids = 0; grab = 0; }
+  long long t_last = clock64();
   for (;;) {
     const int64_t n = dhn_next_root(a, &s_root);
     if (n < 0) break;
+    if (threadIdx.x == 0) atomicAdd(&g_dhn4_stats[7], 1ull);
     const int32_t r = a.row_of[n];
     const int64_t ib = a.sp[r], ie = a.sp[r + 1];
     const int64_t pb = a.gp[n], pe = a.gp[n + 1];
-    for (int i = threadIdx.x; i < d; i += DHN_THREADS) s_out[i] = 0.f;
-    for (int c0 = 0; c0 < d; c0 += DS) {
-      const int ch = c0 + c;
-      // (A) S3(w) += f3(p) for w -> p -> n
-      for (int64_t q = ib + warp; q < ie; q += DHN_WARPS) {
-        const int32_t p = a.sg[q];
-        const int32_t rp = a.row_of[p];
-        const float f3p = a.F3[(int64_t)p * d + ch];
-        const int64_t e2 = a.sp[rp + 1];
-        for (int64_t q2 = a.sp[rp] + sub; q2 < e2; q2 += S)
-          atomicAdd(&slab[(int64_t)a.sg[q2] * DS + c], f3p);
-      }
-      __syncthreads();
-      // (B) acc += f1(v) f2(w) S3(w) over n -> v -> w
+    const int deg_out = (int)(pe - pb), deg_in = (int)(ie - ib);
+    const bool cur_ok = deg_out <= H4_DEG_CAP && deg_in <= H4_DEG_CAP;
+    const int64_t bound = a.wout[n] < (uint32_t)a.G ? (int64_t)a.wout[n] : a.G;
+    int bits = 0;
+    while (bits < H4_HBITS && ((int64_t)H4_PART << bits) < bound) ++bits;
+    H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
+    // lanes test 32 neighbours per step only when a neighbour's list has under one entry
+    // per partition on average (hubs); otherwise one neighbour per warp
+    R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
+    for (int c0 = 0; c0 < d; c0 += 32) {
+      const int c = c0 + lane;
+      const bool cok = c < d;
       float acc = 0.f;
-      for (int64_t pos = pb + warp; pos < pe; pos += DHN_WARPS) {
-        const int32_t v = a.nbr[pos];
-        if (v < 0) continue;
-        const float f1v = a.F1[(int64_t)v * d + ch];
-        const int64_t we = a.gp[v + 1];
-        float t = 0.f;
-        for (int64_t i = a.gp[v] + sub; i < we; i += S) {
-          const int32_t w = a.nbr[i];
-          if (w >= 0) t += a.F2[(int64_t)w * d + ch] * __ldcg(&slab[(int64_t)w * DS + c]);
+      if (cur_ok) {
+        for (int i = threadIdx.x; i < deg_out; i += DHN_THREADS) cur_out[i] = 0;
+        for (int i = threadIdx.x; i < deg_in; i += DHN_THREADS) cur_in[i] = 0;
+      }
+      __syncthreads();
+      H4_T(0);
+      for (uint32_t part = 0; part < R.P; ++part) {
+        R.part = part;
+        if (threadIdx.x == 0) {
+          atomicAdd(&g_dhn4_stats[6], 1ull);
+          if (R.chunked) atomicAdd(&g_dhn4_stats[8], 1ull);
         }
-        acc += f1v * t;
+        // (1) S1(w) += f1(v) over out-wedges n -> v -> w of this partition
+        R.deg = deg_out;
+        h4_sweep<true>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c, cok);
+        H4_T(1);
+        // (3) acc += f3(p) (.) G(w) over in-wedges w -> p -> n of this partition
+        R.deg = deg_in;
+        acc += h4_sweep<false>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b, q_e, &q_n, &grab, c, cok);
+        H4_T(3);
+        // (4) clear the table for the next partition / root
+        for (int i = threadIdx.x; i < n_ids * 8; i += DHN_THREADS)   // dense prefix, float4
+          __stcg(reinterpret_cast<float4*>(S) + i, make_float4(0.f, 0.f, 0.f, 0.f));
+        for (int i = threadIdx.x; i < H4_CAP; i += DHN_THREADS) { keys[i] = -1; ids[i] = -1; }
+        __syncthreads();
+        if (threadIdx.x == 0) n_ids = 0;
+        __syncthreads();
+        H4_T(4);
       }
-#pragma unroll
-      for (int o = DS; o < 32; o <<= 1) acc += __shfl_xor_sync(FULL, acc, o);
-      if (sub == 0) atomicAdd(&s_out[ch], acc);
+      s_red[warp * 32 + lane] = acc;
       __syncthreads();
-      // (C) re-zero the touched slab entries
-      for (int64_t q = ib + warp; q < ie; q += DHN_WARPS) {
-        const int32_t rp = a.row_of[a.sg[q]];
-        const int64_t e2 = a.sp[rp + 1];
-        for (int64_t q2 = a.sp[rp] + sub; q2 < e2; q2 += S)
-          slab[(int64_t)a.sg[q2] * DS + c] = 0.f;
+      if (warp == 0) {
+        float s = 0.f;
+        for (int w = 0; w < DHN_WARPS; ++w) s += s_red[w * 32 + lane];
+        if (cok) dhn_store(a, n, c, s);
       }
       __syncthreads();
+      H4_T(5);
     }
-    for (int i = threadIdx.x; i < d; i += DHN_THREADS) dhn_store(a, n, i, s_out[i]);
   }
+}
+
+// sort keys of the hash-ordered adjacency lists: (segment << 16) | top 16 bits of hash(w)
+__global__ void h4_keys_kernel(const int32_t* __restrict__ seg, const int32_t* __restrict__ val,
+                               int64_t E, uint64_t* __restrict__ key, int32_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= E) return;
+  const int32_t w = val[i];
+  key[i] = ((uint64_t)(uint32_t)seg[i] << H4_HBITS) | h4_top(w);
+  out[i] = w;
 }
 
 // -------------------------------------------------------------------------------------
@@ -274,7 +593,8 @@ __global__ void to_group_kernel(const float* __restrict__ f, int64_t ldf,
 __global__ void work_kernel(int k, int64_t G, const int64_t* __restrict__ gp,
                             const int32_t* __restrict__ nbr, const int64_t* __restrict__ sp,
                             const int32_t* __restrict__ sg, const int32_t* __restrict__ row_of,
-                            uint32_t* __restrict__ key, int32_t* __restrict__ order) {
+                            uint32_t* __restrict__ key, int32_t* __restrict__ order,
+                            uint32_t* __restrict__ wout) {
   const int64_t n = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (n >= G) return;
   const int lane = threadIdx.x & 31;
@@ -284,6 +604,10 @@ __global__ void work_kernel(int k, int64_t G, const int64_t* __restrict__ gp,
     if (v >= 0) w += gp[v + 1] - gp[v];
   }
   if (k == 4) {
+    int64_t o = w;   // out-wedges n -> v -> w: bound on the distinct w of the S1 table
+#pragma unroll
+    for (int s = 16; s; s >>= 1) o += __shfl_xor_sync(FULL, o, s);
+    if (lane == 0) wout[n] = (uint32_t)(o < (int64_t)UINT32_MAX ? o : UINT32_MAX);
     const int32_t r = row_of[n];
     for (int64_t q = sp[r] + lane; q < sp[r + 1]; q += 32) {
       const int32_t rp = row_of[sg[q]];
@@ -303,22 +627,15 @@ __global__ void work_kernel(int k, int64_t G, const int64_t* __restrict__ gp,
 // plan: workspace layout
 // ---------------------------------------------------------------------------------------
 struct Plan {
-  int k, d, ds, n_cta;
+  int k, d, n_cta;
   int64_t G, E, R;
   size_t fixed, per_cta;
 };
 
-int pick_ds(int64_t G, int d, int n_cta) {
-  for (int ds : {32, 16, 8, 4, 2, 1}) {
-    if (ds > d || d % ds) continue;
-    if ((size_t)n_cta * (size_t)G * ds * sizeof(float) <= DHN_SLAB_BUDGET) return ds;
-  }
-  return 1;
-}
-
 struct Bufs {
   int32_t* gor; int32_t* nbr; float* F[4]; uint32_t* key; int32_t* order; int* counter;
-  void* sort_ws; char* cta;
+  uint32_t* wout; void* sort_ws; char* cta;
+  uint64_t* hkey; int32_t* nbrh; int32_t* sgh;   // k = 4: hash-ordered adjacency lists
 };
 
 Bufs carve(const Plan& P, void* base, size_t* used = nullptr) {
@@ -330,7 +647,11 @@ Bufs carve(const Plan& P, void* base, size_t* used = nullptr) {
   b.key = c.take<uint32_t>(P.G);
   b.order = c.take<int32_t>(P.G);
   b.counter = c.take<int>(64);
-  b.sort_ws = c.take<char>(radix_sort_workspace_bytes(P.G));
+  b.wout = c.take<uint32_t>(P.G);
+  b.hkey = P.k == 4 ? c.take<uint64_t>(P.E) : nullptr;
+  b.nbrh = P.k == 4 ? c.take<int32_t>(P.E) : nullptr;
+  b.sgh = P.k == 4 ? c.take<int32_t>(P.E) : nullptr;
+  b.sort_ws = c.take<char>(radix_sort_workspace_bytes(P.k == 4 ? std::max(P.G, P.E) : P.G));
   b.cta = c.take<char>(0);
   if (used) *used = c.used;
   return b;
@@ -341,9 +662,10 @@ Plan make_plan(const rnn_join_index* adj, int k, int d) {
   P.k = k; P.d = d;
   P.G = adj->n_groups; P.E = adj->n_join_rows; P.R = adj->n_src_rows;
   P.n_cta = (int)std::min<int64_t>((int64_t)num_sms() * DHN_CTAS_PER_SM, std::max<int64_t>(P.G, 1));
-  P.ds = k == 4 ? pick_ds(P.G, d, P.n_cta) : 0;
+  // k = 3: per-CTA global mark array for roots whose in-degree exceeds the smem hash set;
+  // k = 4: per-CTA value slab of the S1 hash table (H4_CAP x 32 floats, zero between roots)
   P.per_cta = k == 3 ? ((size_t)P.G * sizeof(int32_t) + 255) & ~size_t(255)
-            : k == 4 ? ((size_t)P.G * P.ds * sizeof(float) + 255) & ~size_t(255) : 0;
+            : k == 4 ? (size_t)H4_CAP * 32 * sizeof(float) : 0;
   carve(P, nullptr, &P.fixed);
   P.fixed = (P.fixed + 255) & ~size_t(255);
   return P;
@@ -362,6 +684,8 @@ rnn_status check_adj(const rnn_join_index* adj, int k, int d) {
               "DHN needs the transposed CSR (index built without RNN_IDX_NO_TRANSPOSE)");
   RNN_REQUIRE(adj->n_groups <= INT32_MAX && adj->n_src_rows < INT32_MAX, RNN_ERR_UNSUPPORTED,
               "DHN group / row ids are int32");
+  RNN_REQUIRE(k != 4 || adj->n_groups == 0 || (adj->pos_group && adj->src_seg),
+              RNN_ERR_INVALID_ARGUMENT, "DHN k = 4 needs pos_group and src_seg in the index");
   return RNN_OK;
 }
 
@@ -397,22 +721,19 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
   if (P.k == 3) {
     a.mark = reinterpret_cast<int*>(b.cta);
     const int dpl = (P.d + 31) / 32;
-    switch (dpl) {
-      case 1: dhn3_kernel<1><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      case 2: dhn3_kernel<2><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      case 3: dhn3_kernel<3><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      default: dhn3_kernel<4><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-    }
+    const size_t smem = 2 * H3_CAP * sizeof(int) + (size_t)DHN_WARPS * dpl * 32 * sizeof(float);
+    auto kern = dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2> : dpl == 3 ? dhn3_kernel<3>
+                                                                                  : dhn3_kernel<4>;
+    RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
   } else {
+    a.wout = b.wout; a.nbrh = b.nbrh; a.sgh = b.sgh;
     a.slab = reinterpret_cast<float*>(b.cta);
-    switch (P.ds) {
-      case 32: dhn4_kernel<32><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      case 16: dhn4_kernel<16><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      case 8: dhn4_kernel<8><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      case 4: dhn4_kernel<4><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      case 2: dhn4_kernel<2><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-      default: dhn4_kernel<1><<<P.n_cta, DHN_THREADS, 0, st>>>(a); break;
-    }
+    const size_t smem = 2 * H4_CAP * sizeof(int) + (size_t)DHN_WARPS * 32 * sizeof(float) +
+                        2 * H4_DEG_CAP * sizeof(int) + H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
+    RNN_CUDA(cudaFuncSetAttribute(dhn4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
+    dhn4_kernel<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
   }
   RNN_LAUNCH_CHECK();
   return RNN_OK;
@@ -430,9 +751,21 @@ rnn_status prepare(const Plan& P, const Bufs& b, const rnn_join_index* adj, cuda
   if (P.k >= 3) {
     work_kernel<<<(unsigned)ceil_div(P.G, 8), 256, 0, st>>>(P.k, P.G, adj->group_ptr, b.nbr,
                                                             adj->src_ptr, adj->src_group,
-                                                            adj->group_dst_row, b.key, b.order);
+                                                            adj->group_dst_row, b.key, b.order,
+                                                            b.wout);
     RNN_LAUNCH_CHECK();
     RNN_TRY(radix_sort_u32(b.key, b.order, P.G, 24, b.sort_ws, st));
+  }
+  if (P.k == 4 && P.E > 0) {
+    // every out-list (group segment) and in-list (row segment) sorted by hash partition
+    auto bitlen = [](int64_t x) { int b = 1; while ((int64_t(1) << b) <= x) ++b; return b; };
+    const unsigned g = (unsigned)ceil_div(P.E, 256);
+    h4_keys_kernel<<<g, 256, 0, st>>>(adj->pos_group, b.nbr, P.E, b.hkey, b.nbrh);
+    RNN_LAUNCH_CHECK();
+    RNN_TRY(radix_sort_u64(b.hkey, b.nbrh, P.E, H4_HBITS + bitlen(P.G), b.sort_ws, st));
+    h4_keys_kernel<<<g, 256, 0, st>>>(adj->src_seg, adj->src_group, P.E, b.hkey, b.sgh);
+    RNN_LAUNCH_CHECK();
+    RNN_TRY(radix_sort_u64(b.hkey, b.sgh, P.E, H4_HBITS + bitlen(P.R), b.sort_ws, st));
   }
   return RNN_OK;
 }
@@ -556,4 +889,14 @@ extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rn
     RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[j], ld_df, 1, launch++, st));
   }
   return RNN_OK;
+}
+
+extern "C" int rnn_internal_dhn_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, rnn::g_dhn4_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
+    return 1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(rnn::g_dhn4_stats, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
 }
