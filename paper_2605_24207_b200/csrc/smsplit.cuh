@@ -51,8 +51,8 @@ __device__ __noinline__ void st_zero_range(const Pol& pol, int64_t g0, int64_t g
   for (int64_t g = g0; g < g1; ++g) pol.zero(g);
 }
 
-template <class Pol, int U>
-__global__ void __launch_bounds__(256) st_kernel(Pol pol, RSCtx cx) {
+template <class Pol, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) st_kernel(Pol pol, RSCtx cx) {
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (item >= cx.n_work) return;
   const int lane = lane_id();
@@ -113,11 +113,11 @@ __global__ void __launch_bounds__(256) st_kernel(Pol pol, RSCtx cx) {
     st_zero_range(pol, cx.E > 0 ? cx.seg[cx.E - 1] + 1 : 0, cx.n_seg);
 }
 
-template <class Pol, int U>
+template <class Pol, int U, int MINB = 1>
 rnn_status launch_st(const Pol& pol, RSCtx cx, cudaStream_t st) {
   if (cx.n_work <= 0) return RNN_OK;
   RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * cx.n_work, st));
-  st_kernel<Pol, U><<<(unsigned)ceil_div(cx.n_work, 8), 256, 0, st>>>(pol, cx);
+  st_kernel<Pol, U, MINB><<<(unsigned)ceil_div(cx.n_work, 8), 256, 0, st>>>(pol, cx);
   RNN_LAUNCH_CHECK();
   return RNN_OK;
 }
