@@ -36,8 +36,8 @@
  * - Keys are signed int64 (any value).  Row ids are int32 (relations < 2^31 rows); join-row
  *   counts and CSR pointers are int64.
  * - Determinism: identical inputs give bit-identical outputs (no floating-point atomics on
- *   any path; every reduction has a fixed order) -- except the k = 4 DHN aggregate (A6),
- *   whose slab scatter uses fp32 atomics (rounding order only).
+ *   any path; every reduction has a fixed order) -- except the k = 3 / 4 DHN aggregates
+ *   (A6), whose hash-table accumulation uses fp32 atomics (rounding order only).
  */
 #ifndef RNN_H
 #define RNN_H
@@ -247,10 +247,14 @@ rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, co
  * Closed walks are rotation invariant, so the backward is the same kernel with rotated
  * operands (d f_j(x) = the walk aggregate rooted at x of (f_{j+1}, ..., g, ..., f_{j-1}),
  * g = f0 (.) dOut), and d f0 = dOut (.) sum_walks prod f_i.
- * Work: k = 3 enumerates sum_v deg(v)^2 candidate wedges against a per-root mark array;
- * k = 4 is factorised through the middle vertex: S3(w) = sum_{w->p->n} f3(p) is scattered
- * into a per-CTA dense slab, then every 2-path n->v->w reads it.  k = 4 uses fp32 atomics
- * into the slab, so its rounding order (only) is not deterministic. */
+ * Work: k = 3 probes the sum_v deg(v)^2 candidate wedges n -> v -> w against a shared-memory
+ * hash set of the root's in-neighbours (a per-CTA mark array for in-degrees > 6144).
+ * k = 4 is factorised through the middle vertex w: S1(w) = sum_{n->v->w} f1(v) accumulates
+ * in a hash table of the root's 2-hop keys (shared memory; values in an L2-resident per-CTA
+ * slab), then every in-wedge w -> p -> n adds f3(p) (.) f2(w) (.) S1(w).  Roots with more
+ * than 8192 possible 2-hop keys run in hash partitions of w (adjacency lists pre-sorted by
+ * the hash, per-neighbour cursors).  k = 3 and k = 4 accumulate with fp32 atomics (shared
+ * memory / L2), so their rounding order (only) is not deterministic. */
 rnn_status rnn_dhn_workspace_size(const rnn_join_index* adj, int32_t k, int32_t d,
                                   size_t* bytes);   /* host-only, no device work */
 rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,

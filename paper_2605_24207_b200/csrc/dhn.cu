@@ -8,16 +8,14 @@
 //    int32 group ids: nbr[p] = group of the neighbour at join position p (-1 if it has no
 //    out-edges and so cannot continue a walk), in-neighbours of group n = src_group[] over
 //    the transposed CSR of n's row;
-//  * one CTA per root, roots taken heaviest-first from an atomic counter (persistent grid);
-//  * C3: the root's in-neighbours are counted into a per-CTA mark array (multiplicity =
-//    number of closing Edge rows), then the CTA's warps walk the wedges n->v->w with lanes
-//    over w and ballot the marked ones; the hits gather f1(v) (.) f2(w) with lane = channel;
-//  * C4: factorised through the middle vertex w: S3(w) = sum_{w->p->n} f3(p) is scattered
-//    (fp32 red) into a per-CTA dense slab indexed by group, then every 2-path n->v->w reads
-//    it: C4(n) = f0(n) (.) sum_{n->v->w} f1(v) (.) f2(w) (.) S3(w).  The slab holds a DS-wide
-//    channel slice (DS chosen so the slabs of all resident CTAs fit the workspace budget);
-//    the walk is repeated per slice, and the touched slab entries are re-zeroed by walking
-//    the same lists again (no full clears);
+//  * one CTA (32 warps) per root, roots taken heaviest-first from an atomic counter;
+//  * C3: the root's in-neighbours go into a shared-memory hash set (count = multiplicity of
+//    the closing Edge rows), then the warps walk the wedges n->v->w with lanes over w and
+//    probe the set; the hits gather f1(v) (.) f2(w) with lane = channel;
+//  * C4: factorised through the middle vertex w (see dhn4_kernel): S1(w) accumulates over
+//    out-wedges in a shared-memory hash of 2-hop keys with compact ids (values: a dense,
+//    L2-resident per-CTA slab), the in-wedges w->p->n then add f3(p) (.) f2(w) (.) S1(w);
+//    big roots run in hash partitions of w over hash-sorted adjacency lists;
 //  * the backward is the same kernels with rotated operands (rnn.h).
 #include <algorithm>
 

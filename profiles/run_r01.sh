@@ -33,7 +33,7 @@ if [[ $what == ncu || $what == all ]]; then
   mkdir -p /tmp/ncu
   # full capture of the dominant kernels (fwd / bwd gathers, softmax walker, DHN walk, GEMM)
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:'lean_kernel|tc_gemm' -s 12 -c 4 -o /tmp/ncu/prof_arxiv -f \
+    -k regex:'lean_kernel|tc_gemm|tc_projt|splitk' -s 12 -c 6 -o /tmp/ncu/prof_arxiv -f \
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_full_arxiv.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on \
     -k regex:'st_kernel|seg_kernel' -s 8 -c 3 -o /tmp/ncu/prof_mag -f \
@@ -42,7 +42,7 @@ if [[ $what == ncu || $what == all ]]; then
     -k regex:'lean_kernel|rowsplit' -s 8 -c 4 -o /tmp/ncu/prof_hyper -f \
     python bench.py --config hyper --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_full_hyper.log 2>&1
   timeout 900 ncu --set full --clock-control none --import-source on \
-    -k regex:'dhn' -s 6 -c 4 -o /tmp/ncu/prof_dhn -f \
+    -k regex:'dhn[234]_kernel' -s 3 -c 3 -o /tmp/ncu/prof_dhn -f \
     python bench.py --config dhn --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/ncu_full_dhn.log 2>&1
   for c in arxiv mag hyper dhn; do
     if [[ -f /tmp/ncu/prof_$c.ncu-rep ]]; then
