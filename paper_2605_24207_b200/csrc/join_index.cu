@@ -479,7 +479,14 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
   P.n_e = n_edge_rows; P.n_s = src_key ? n_src : 0; P.n_t = dst_key ? n_dst : 0;
   P.has_s = src_key != nullptr; P.has_t = dst_key != nullptr;
   P.cap_s = pow2_at_least(2 * P.n_s + 2); P.cap_t = pow2_at_least(2 * P.n_t + 2);
-  P.C = rows_per_item > 0 ? rows_per_item : 128;
+  // default work-item size: 128 rows, smaller for small relations so that the schedule
+  // still gives every SM several warps of work (Cora: 13k join rows -> 16-row items)
+  if (rows_per_item > 0) {
+    P.C = rows_per_item;
+  } else {
+    const int64_t per_warp = n_edge_rows / ((int64_t)num_sms() * 32);
+    P.C = per_warp >= 128 ? 128 : per_warp <= 16 ? 16 : (per_warp + 15) / 16 * 16;
+  }
   P.transpose = P.has_s && !(flags & RNN_IDX_NO_TRANSPOSE);
   P.by_key = by_key;
   if (by_key)

@@ -570,6 +570,19 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
 // ------------------------------------------------------------------------------------------
 constexpr int PX_STAGES = 6;
 
+// per-role wait cycles of tc_projt_kernel (lane 0 of warps 0, 1, 2, 6), read by the internal
+// hook rnn_internal_proj_stats: [0] producer waits for a free slot, [1] MMA waits for W in
+// TMEM, [2] MMA waits for a free accumulator, [3] MMA waits for a converted stage,
+// [4] converter waits for a landed stage, [5] epilogue waits for an accumulator;
+// [8..11] total cycles of the producer, MMA, converter, epilogue lanes
+__device__ unsigned long long g_proj_stats[16];
+#define PT_WAIT(slot, stmt)                                      \
+  do {                                                           \
+    const long long t0_ = clock64();                             \
+    stmt;                                                        \
+    if (lane == 0) pt_w[slot] += (unsigned long long)(clock64() - t0_); \
+  } while (0)
+
 struct ProjTParams {
   int64_t M;            // rows of X / Y
   int N, K;             // out features, reduction length (K <= 128)
@@ -601,7 +614,8 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
 
 template <bool SPLIT3>
 __global__ void __launch_bounds__(PT_THREADS, 1)
-    tc_projt_kernel(const __grid_constant__ CUtensorMap tx, ProjTParams p) {
+    tc_projt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ty,
+                    ProjTParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -617,6 +631,8 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long pt_t0 = clock64();
+  unsigned long long pt_w[6] = {0, 0, 0, 0, 0, 0};
   const int nt = blockIdx.x % p.n_tiles_n;
   const int n0 = nt * 128;
   const int64_t mt0 = blockIdx.x / p.n_tiles_n;
@@ -657,7 +673,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         for (int kb = 0; kb < p.nkb; ++kb, ++it) {
           const int s = (int)(it % p.stages);
           const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-          if (it >= p.stages) mbar_wait(&x_empty[s], ph ^ 1);
+          if (it >= p.stages) PT_WAIT(0, mbar_wait(&x_empty[s], ph ^ 1));
           mbar_expect_tx(&x_full[s], X_BYTES);
           tma_load_2d(&tx, smem + s * X_STAGE, &x_full[s], kb * BK, (int)(mt * BM));
         }
@@ -666,19 +682,19 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
   } else if (warp == 1) {
     // A = W block from TMEM (M = 128 features), B = X tile (N = 128 rows, K-major)
     const uint32_t idesc = make_idesc(BM, false, false);
-    mbar_wait(w_ready, 0);
+    PT_WAIT(1, mbar_wait(w_ready, 0));
     tc_fence_after();
     int64_t it = 0;
     int j = 0;
     for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
       const int buf = j & 1;
-      if (j >= 2) mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+      if (j >= 2) PT_WAIT(2, mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1));
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(buf * 128);
       for (int kb = 0; kb < p.nkb; ++kb, ++it) {
         const int s = (int)(it % p.stages);
         const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-        mbar_wait(SPLIT3 ? &x_conv[s] : &x_full[s], ph);
+        PT_WAIT(3, mbar_wait(SPLIT3 ? &x_conv[s] : &x_full[s], ph));
         tc_fence_after();
         if (lane == 0) {
           const uint32_t xs = smem_u32(smem + s * X_STAGE);
@@ -708,7 +724,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         for (int kb = 0; kb < p.nkb; ++kb, ++it) {
           const int s = (int)(it % p.stages);
           const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-          mbar_wait(&x_full[s], ph);
+          PT_WAIT(4, mbar_wait(&x_full[s], ph));
           uint8_t* x = smem + s * X_STAGE;
           lo_tile(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(x + X_BYTES),
                   X_BYTES / 16, t);
@@ -725,29 +741,48 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     // probe_tf32.py; lo = w - trunc(w)); padding features / k columns are zero.  32 x 32
     // blocks are read coalesced (lane = k) and transposed through shared memory so that
     // thread l ends up holding feature row f's k values for tcgen05.st (lane = feature).
-    float* tp = reinterpret_cast<float*>(smem + p.stages * X_STAGE + 1024) + quad * 32 * 33;
+    float* tp = reinterpret_cast<float*>(smem + p.stages * X_STAGE + 1024) + quad * 32 * 65;
     const int kpad = p.nkb * BK;
     const int fbase = n0 + quad * 32;
-    for (int k0 = 0; k0 < kpad; k0 += 32) {
-      const int k = k0 + lane;
-      float v[32];
+    const bool vec = (p.K % 4 == 0) && (p.ldw % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(p.W) & 15u) == 0);
+    // 64-k halves of the warp's 32 feature rows: 16 float4 loads per thread in flight
+    // (lanes 0-15 row 2rr, lanes 16-31 row 2rr+1), transposed through a [32][65] tile
+    for (int k0 = 0; k0 < kpad; k0 += 64) {
+      float4 v[16];
 #pragma unroll
-      for (int r = 0; r < 32; ++r)
-        v[r] = (fbase + r < p.N && k < p.K) ? __ldg(p.W + (int64_t)(fbase + r) * p.ldw + k) : 0.f;
+      for (int rr = 0; rr < 16; ++rr) {
+        const int row = fbase + 2 * rr + (lane >> 4);
+        const int k = k0 + 4 * (lane & 15);
+        v[rr] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (row < p.N) {
+          const float* src = p.W + (int64_t)row * p.ldw + k;
+          if (vec) {
+            if (k < p.K) v[rr] = __ldg(reinterpret_cast<const float4*>(src));
+          } else {
+            if (k < p.K) v[rr].x = __ldg(src);
+            if (k + 1 < p.K) v[rr].y = __ldg(src + 1);
+            if (k + 2 < p.K) v[rr].z = __ldg(src + 2);
+            if (k + 3 < p.K) v[rr].w = __ldg(src + 3);
+          }
+        }
+      }
 #pragma unroll
-      for (int r = 0; r < 32; ++r) tp[r * 33 + lane] = v[r];
+      for (int rr = 0; rr < 16; ++rr) {
+        float* t = tp + (2 * rr + (lane >> 4)) * 65 + 4 * (lane & 15);
+        t[0] = v[rr].x; t[1] = v[rr].y; t[2] = v[rr].z; t[3] = v[rr].w;
+      }
       __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
+      for (int h = 0; h < 64 && k0 + h < kpad; h += 16) {
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float w = tp[lane * 33 + h * 16 + q];
+          const float w = tp[lane * 65 + h + q];
           hi[q] = __float_as_uint(w);
           lo[q] = __float_as_uint(w - __uint_as_float(__float_as_uint(w) & 0xFFFFE000u));
         }
-        tc_st16(lane_base + W_HI + (uint32_t)(k0 + 16 * h), hi);
-        if (SPLIT3) tc_st16(lane_base + W_LO + (uint32_t)(k0 + 16 * h), lo);
+        tc_st16(lane_base + W_HI + (uint32_t)(k0 + h), hi);
+        if (SPLIT3) tc_st16(lane_base + W_LO + (uint32_t)(k0 + h), lo);
       }
       __syncwarp();
     }
@@ -755,27 +790,50 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     tc_fence_before();
     mbar_arrive(w_ready);
     // ---- epilogue ----
+    // output staging (2 x 4 KB per warp) aliases the W transpose tiles, which are done
+    float* stage_out = reinterpret_cast<float*>(smem + p.stages * X_STAGE + 1024) + quad * 2 * 32 * 32;
     const float bf = (p.bias && f < p.N) ? __ldg(p.bias + f) : 0.f;
     int j = 0;
     for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
       const int buf = j & 1;
-      mbar_wait(&acc_full[buf], (j >> 1) & 1);
+      PT_WAIT(5, mbar_wait(&acc_full[buf], (j >> 1) & 1));
       tc_fence_after();
       const int64_t r0 = mt * BM;
-      for (int c0 = 0; c0 < BM; c0 += 16) {
-        uint32_t r[16];
-        tc_ld16(lane_base + (uint32_t)(buf * 128 + c0), r);
-        if (f < p.N) {
+      // 32-row chunks: TMEM -> registers (+bias) -> a [32 rows x 32 features] smem tile
+      // (thread = feature, so each row of the tile is one conflict-free 128-byte store) ->
+      // one TMA bulk tensor store; two tiles per warp alternate (wait_group.read 1)
+      for (int c0 = 0; c0 < BM; c0 += 32) {
+        uint32_t r[32];
+        tc_ld16(lane_base + (uint32_t)(buf * 128 + c0), *reinterpret_cast<uint32_t(*)[16]>(r));
+        tc_ld16(lane_base + (uint32_t)(buf * 128 + c0 + 16),
+                *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+        const int sb = (c0 >> 5) & 1;
+        float* st = stage_out + sb * 32 * 32;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int64_t row = r0 + c0 + q;
-            if (row < p.M) __stcs(p.out + row * p.ldo + f, __uint_as_float(r[q]) + bf);
-          }
+        for (int q = 0; q < 32; ++q) st[q * 32 + lane] = __uint_as_float(r[q]) + bf;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0 && r0 + c0 < p.M && n0 + quad * 32 < p.N) {
+          asm volatile(
+              "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                  reinterpret_cast<uint64_t>(&ty)),
+              "r"(n0 + quad * 32), "r"((int)(r0 + c0)), "r"(smem_u32(st))
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
       }
       tc_fence_before();
       mbar_arrive(&acc_empty[buf]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 6)) {
+    const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : 3;
+    atomicAdd(&g_proj_stats[8 + role], (unsigned long long)(clock64() - pt_t0));
+    for (int i = 0; i < 6; ++i)
+      if (pt_w[i]) atomicAdd(&g_proj_stats[i], pt_w[i]);
   }
   tc_fence_before();
   __syncthreads();
@@ -877,7 +935,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D fp32 tensor [rows, inner] with row stride ld (elements); box {box_inner, box_rows}
 rnn_status make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t rows, int64_t ld,
-                    uint32_t box_inner, uint32_t box_rows, bool mn_major = false) {
+                    uint32_t box_inner, uint32_t box_rows, bool mn_major = false,
+                    bool swizzle = true) {
   auto fn = encode_fn();
   RNN_REQUIRE(fn, RNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   RNN_REQUIRE(aligned16(base) && (ld * 4) % 16 == 0, RNN_ERR_INVALID_ARGUMENT,
@@ -888,7 +947,8 @@ rnn_status make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t ro
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  !swizzle ? CU_TENSOR_MAP_SWIZZLE_NONE
+                  : mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   RNN_REQUIRE(r == CUDA_SUCCESS, RNN_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return RNN_OK;
@@ -952,19 +1012,21 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
     q.n_tiles_n = (int)ceil_div(N, 128);
     q.n_tiles_m = ceil_div(M, BM);
     const size_t x_stage = (size_t)BM * BK * 4 * (s3 ? 2 : 1);
-    const size_t tscratch = 4 * 32 * 33 * sizeof(float) + 1024;   // W transpose tiles
+    // W transpose tiles (4 x 32 x 33 floats), later the output staging (4 warps x 2 x 4 KB)
+    const size_t tscratch = 4 * 2 * 32 * 32 * sizeof(float) + 1024;
     const size_t budget = 227 * 1024 - 1024 - 256 - tscratch;
     q.stages = (int)std::min<size_t>(PX_STAGES, budget / x_stage);
     q.W = B; q.ldw = ldb; q.out = Y; q.ldo = ldy; q.bias = bias;
-    CUtensorMap tx;
+    CUtensorMap tx, ty;
     RNN_TRY(make_map(&tx, A, Kred, M, lda, BK, BM));
+    RNN_TRY(make_map(&ty, Y, N, M, ldy, 32, 32, false, /*swizzle=*/false));
     const int64_t per_n =
         std::max<int64_t>(1, std::min<int64_t>(num_sms() / q.n_tiles_n, q.n_tiles_m));
     const unsigned grid = (unsigned)(per_n * q.n_tiles_n);
     const size_t smem = q.stages * x_stage + 1024 + tscratch;
     auto kern = s3 ? tc_projt_kernel<true> : tc_projt_kernel<false>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, PT_THREADS, smem, st>>>(tx, q);
+    kern<<<grid, PT_THREADS, smem, st>>>(tx, ty, q);
     RNN_LAUNCH_CHECK();
     return RNN_OK;
   }
@@ -1147,4 +1209,14 @@ extern "C" rnn_status rnn_internal_gemm(int a_mn, int b_mn, const float* A, int6
   if (a_mn) return gemm<true, false>(ta, tb, p, 1, pr, st);
   if (b_mn) return gemm<false, true>(ta, tb, p, 1, pr, st);
   return gemm<false, false>(ta, tb, p, 1, pr, st);
+}
+
+extern "C" int rnn_internal_proj_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, rnn::g_proj_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
+    return 1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(rnn::g_proj_stats, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
 }
