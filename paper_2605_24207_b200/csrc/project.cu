@@ -29,7 +29,7 @@ namespace {
 constexpr int BM = 128;   // UMMA_M (cta_group::1): accumulator row i <-> TMEM lane i
 constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row
 constexpr int THREADS = 192;
-constexpr int MAX_STAGES = 4;
+constexpr int MAX_STAGES = 8;
 
 struct GemmParams {
   int64_t M;        // output rows
@@ -160,7 +160,7 @@ __device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n1
   }
 }
 
-template <bool A_MN, bool B_MN, bool SPLIT3>
+template <bool A_MN, bool B_MN, bool SPLIT3, int KB = BK>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    GemmParams p) {
@@ -168,8 +168,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // 1024-byte align the carve (swizzle atoms)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const uint32_t A_BYTES = BM * BK * 4;
-  const uint32_t B_BYTES = (uint32_t)p.BN * BK * 4;
+  // KB = reduction elements per stage: 32 (K-major, one 128-byte swizzle row) or 16 (MN-major
+  // operands: half-size stages, twice as many in flight)
+  const uint32_t A_BYTES = BM * KB * 4;
+  const uint32_t B_BYTES = (uint32_t)p.BN * KB * 4;
   const uint32_t STAGE = (A_BYTES + B_BYTES) * (SPLIT3 ? 2u : 1u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE);
   uint64_t* empty = full + MAX_STAGES;
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int n0 = blockIdx.y * p.BN;
   const int64_t kbeg = (int64_t)blockIdx.z * p.k_split;
   const int64_t kend = kbeg + p.k_split < p.Kred ? kbeg + p.k_split : p.Kred;
-  const int nkb = (int)((kend - kbeg + BK - 1) / BK);
+  const int nkb = (int)((kend - kbeg + KB - 1) / KB);
 
   if (warp == 1) {
     if (lane == 0) {
@@ -222,19 +224,19 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t ph = (kb / p.stages) & 1;
         if (kb >= p.stages) mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        const int k = (int)(kbeg + (int64_t)kb * BK);
+        const int k = (int)(kbeg + (int64_t)kb * KB);
         if (!A_MN) {
           tma_load_2d(&ta, a_hi(s), &full[s], k, (int)m0);
         } else {
 #pragma unroll
           for (int j = 0; j < BM / 32; ++j)
-            tma_load_2d(&ta, a_hi(s) + j * 4096, &full[s], (int)m0 + 32 * j, k);
+            tma_load_2d(&ta, a_hi(s) + j * (KB * 128), &full[s], (int)m0 + 32 * j, k);
         }
         if (!B_MN) {
           tma_load_2d(&tb, b_hi(s), &full[s], k, n0);
         } else {
           for (int j = 0; j < p.BN / 32; ++j)
-            tma_load_2d(&tb, b_hi(s) + j * 4096, &full[s], n0 + 32 * j, k);
+            tma_load_2d(&tb, b_hi(s) + j * (KB * 128), &full[s], n0 + 32 * j, k);
         }
       }
     }
@@ -248,13 +250,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc_fence_after();
       if (lane == 0) {
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          const uint64_t ad = make_desc(smem_u32(a_hi(s)), A_MN, kk, 4096);
-          const uint64_t bd = make_desc(smem_u32(b_hi(s)), B_MN, kk, 4096);
+        for (int kk = 0; kk < KB / 8; ++kk) {
+          const uint64_t ad = make_desc(smem_u32(a_hi(s)), A_MN, kk, KB * 128);
+          const uint64_t bd = make_desc(smem_u32(b_hi(s)), B_MN, kk, KB * 128);
           tc_mma_tf32(tmem, ad, bd, idesc, (kb | kk) != 0);
           if (SPLIT3) {
-            const uint64_t al = make_desc(smem_u32(a_lo(s)), A_MN, kk, 4096);
-            const uint64_t bl = make_desc(smem_u32(b_lo(s)), B_MN, kk, 4096);
+            const uint64_t al = make_desc(smem_u32(a_lo(s)), A_MN, kk, KB * 128);
+            const uint64_t bl = make_desc(smem_u32(b_lo(s)), B_MN, kk, KB * 128);
             tc_mma_tf32(tmem, ad, bl, idesc, 1u);
             tc_mma_tf32(tmem, al, bd, idesc, 1u);
           }
@@ -273,26 +275,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
         mbar_wait(&full[s], ph);
-        float4* ah = reinterpret_cast<float4*>(a_hi(s));
-        float4* al = reinterpret_cast<float4*>(a_lo(s));
-        for (uint32_t i = et; i < A_BYTES / 16; i += 128) {
-          float4 x = ah[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
-          ah[i] = h; al[i] = l;
-        }
-        float4* bh = reinterpret_cast<float4*>(b_hi(s));
-        float4* bl = reinterpret_cast<float4*>(b_lo(s));
-        for (uint32_t i = et; i < B_BYTES / 16; i += 128) {
-          float4 x = bh[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u); l.x = x.x - h.x;
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u); l.y = x.y - h.y;
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u); l.z = x.z - h.z;
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u); l.w = x.w - h.w;
-          bh[i] = h; bl[i] = l;
-        }
+        // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
+        lo_tile(reinterpret_cast<const float4*>(a_hi(s)), reinterpret_cast<float4*>(a_lo(s)),
+                A_BYTES / 16, et);
+        lo_tile(reinterpret_cast<const float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)),
+                B_BYTES / 16, et);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[s]);
       }
@@ -807,6 +794,10 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         tc_ld16(lane_base + (uint32_t)(buf * 128 + c0), *reinterpret_cast<uint32_t(*)[16]>(r));
         tc_ld16(lane_base + (uint32_t)(buf * 128 + c0 + 16),
                 *reinterpret_cast<uint32_t(*)[16]>(r + 16));
+        // every staged chunk is committed as one bulk group, so "at most one group pending"
+        // below means the previous user of this buffer has finished reading it; chunks
+        // entirely outside Y are neither staged nor stored
+        if (!(r0 + c0 < p.M && n0 + quad * 32 < p.N)) continue;
         const int sb = (c0 >> 5) & 1;
         float* st = stage_out + sb * 32 * 32;
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
@@ -815,7 +806,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         for (int q = 0; q < 32; ++q) st[q * 32 + lane] = __uint_as_float(r[q]) + bf;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0 && r0 + c0 < p.M && n0 + quad * 32 < p.N) {
+        if (lane == 0) {
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                   reinterpret_cast<uint64_t>(&ty)),
@@ -963,17 +954,18 @@ uint32_t pow2_cols(int bn) {
 template <bool A_MN, bool B_MN, bool SPLIT3>
 rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int splits,
                        cudaStream_t st) {
-  const uint32_t stage = (uint32_t)(BM * BK * 4 + p.BN * BK * 4) * (SPLIT3 ? 2u : 1u);
-  const int64_t nkb_max = ceil_div(p.k_split, BK);
+  constexpr int KB = (A_MN && B_MN) ? 16 : BK;
+  const uint32_t stage = (uint32_t)(BM * KB * 4 + p.BN * KB * 4) * (SPLIT3 ? 2u : 1u);
+  const int64_t nkb_max = ceil_div(p.k_split, KB);
   int stages = (int)((200 * 1024) / stage);
-  if (!SPLIT3 && stages > 3 && stage * 3 <= 100 * 1024) stages = 3;  // 2 CTAs / SM
+  if (!SPLIT3 && stages > 3 && stage * 3 <= 100 * 1024 && !(A_MN && B_MN)) stages = 3;  // 2 CTAs / SM
   if (stages > MAX_STAGES) stages = MAX_STAGES;
   if (stages > nkb_max) stages = (int)nkb_max;
   if (stages < 1) stages = 1;
   p.stages = stages;
   p.tmem_cols = pow2_cols(p.BN);
   const size_t smem = (size_t)stages * stage + 1024 + 8 * (3 * MAX_STAGES + 2) + 64;
-  auto kern = tc_gemm_kernel<A_MN, B_MN, SPLIT3>;
+  auto kern = tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB>;
   RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)ceil_div(p.M, BM), (unsigned)ceil_div(p.N, p.BN), (unsigned)splits);
   kern<<<grid, THREADS, smem, st>>>(ta, tb, p);
@@ -1158,8 +1150,8 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
     const int splits = (int)ceil_div(M, p.k_split);
     p.mode = 1; p.partial = w.part; p.ldp = K; p.part_stride = (int64_t)N * K;
     CUtensorMap ta, tb;
-    RNN_TRY(make_map(&ta, dY, N, M, lddy, 32, BK, true));
-    RNN_TRY(make_map(&tb, X, K, M, ldx, 32, BK, true));
+    RNN_TRY(make_map(&ta, dY, N, M, lddy, 32, 16, true));
+    RNN_TRY(make_map(&tb, X, K, M, ldx, 32, 16, true));
     RNN_TRY((gemm<true, true>(ta, tb, p, splits, prec, st)));
     // partial tiles and dW are contiguous [N, K]
     const int64_t nk = (int64_t)N * K;
@@ -1199,9 +1191,10 @@ extern "C" rnn_status rnn_internal_gemm(int a_mn, int b_mn, const float* A, int6
   p.Kred = Kred; p.k_split = ceil_div(Kred, BK) * BK;
   p.out = Cout; p.ldo = ldc; p.mode = 0;
   CUtensorMap ta, tb;
-  if (a_mn) RNN_TRY(make_map(&ta, A, M, Kred, lda, 32, BK, true));
+  const uint32_t kb_rows = (a_mn && b_mn) ? 16 : BK;   // launch_gemm's stage depth (KB)
+  if (a_mn) RNN_TRY(make_map(&ta, A, M, Kred, lda, 32, kb_rows, true));
   else RNN_TRY(make_map(&ta, A, Kred, M, lda, BK, BM));
-  if (b_mn) RNN_TRY(make_map(&tb, B, N, Kred, ldb, 32, BK, true));
+  if (b_mn) RNN_TRY(make_map(&tb, B, N, Kred, ldb, 32, kb_rows, true));
   else RNN_TRY(make_map(&tb, B, Kred, N, ldb, BK, (uint32_t)p.BN));
   const rnn_precision pr = (rnn_precision)prec;
   cudaStream_t st = as_stream(stream);
