@@ -175,12 +175,15 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     graph = make_graph(args.config, args.seed)
-    sharded = world > 1 and args.config in ("arxiv", "cora")
+    sharded = world > 1 and args.config in ("arxiv", "cora", "hyper")
     if sharded:
         # multi-GPU: the join relation hash-partitioned by group key, NCCL all-gather of the
-        # source embeddings / reduce-scatter of their gradients per layer
-        from paper_2605_24207_b200.shard import ShardedGCNProgram
-        prog = ShardedGCNProgram(graph, prec=args.prec)
+        # source embeddings / reduce-scatter of their gradients per hop
+        from paper_2605_24207_b200.shard import ShardedGCNProgram, ShardedHypergraphProgram
+        if args.config == "hyper":
+            prog = ShardedHypergraphProgram(graph, prec=args.prec)
+        else:
+            prog = ShardedGCNProgram(graph, prec=args.prec)
         r = torch.tensor([prog.join_rows_per_step], dtype=torch.float64, device=dev)
         dist.all_reduce(r)
         rows = int(r.item())              # all ranks' join rows = the whole job
@@ -306,7 +309,7 @@ def run_ours(args):
                        "projection_precision": args.prec, "l2": "flushed between timed steps",
                        "step_launch": "one CUDA graph replay" if graphed else "eager launches",
                        "parallelism": (f"hash-partition by group key x{world} (NCCL all-gather / "
-                                       f"reduce-scatter per layer)" if sharded else
+                                       f"reduce-scatter per layer or hop)" if sharded else
                                        f"replica x{world}" if world > 1 else "single")},
             "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }

@@ -246,9 +246,10 @@ class RnnBackend:
         k = torch.as_tensor(np.asarray(keys, np.int64), device=self.dev)
         return self.rnn.hash_partition(k, P, seed).cpu().numpy()
 
-    def build_index(self, e_src, e_dst, s_keys, t_keys):
+    def build_index(self, e_src, e_dst, s_keys, t_keys, dense=False):
         cu = lambda a: torch.as_tensor(np.asarray(a, np.int64), device=self.dev)
-        return self.rnn.build_join_index(cu(e_src), cu(e_dst), cu(s_keys), cu(t_keys))
+        return self.rnn.build_join_index(cu(e_src), cu(e_dst), cu(s_keys), cu(t_keys),
+                                         dense_groups=dense)
 
     def n_groups(self, idx):
         return idx.n_groups
@@ -270,6 +271,20 @@ class RnnBackend:
                                                    edge_mode=self.rnn.BY_POSITION)
         return q
 
+    def _query_agg(self, idx, Z, agg):
+        key = (id(idx), Z.data_ptr(), agg)
+        q = self._q.get(key)
+        if q is None:
+            q = self._q[key] = self.rnn.make_query("src", agg, src=Z)
+        return q
+
+    def lja_fwd_agg(self, idx, Z, agg, out):
+        self.rnn.join_aggregate_fwd(idx, self._query_agg(idx, Z, agg), out=out, ws=self.ws)
+
+    def lja_bwd_src_agg(self, idx, Z, agg, d_out, d_src):
+        from .programs import _lja_src_grad
+        _lja_src_grad(idx, self._query_agg(idx, Z, agg), d_out, d_src, self.ws)
+
     def project(self, X, W, out):
         self.rnn.project(X, W, out=out, prec=self.prec)
 
@@ -283,3 +298,163 @@ class RnnBackend:
     def project_bwd(self, X, W, dY, dX, dW):
         self.rnn.project_bwd(X, W, dY, want_dx=True, prec=self.prec, ws=self.ws_p, dx_out=dX,
                              dw_out=dW)
+
+
+def block_layout(keys, owner, P):
+    """Rank-major padded layout of one relation over P ranks: rank r's block holds its owned
+    keys ascending, padded to n_pad = max_r |owned_r| with unique sentinel keys below every
+    real key (they match no join row).  Returns (owned keys per rank, n_pad, s_keys [P*n_pad])."""
+    keys = np.asarray(keys, np.int64)
+    owner = np.asarray(owner, np.int64)
+    owned = [np.sort(keys[owner == r]) for r in range(P)]
+    n_pad = int(max(1, max(len(k) for k in owned))) if len(keys) else 1
+    lo = int(keys.min()) if len(keys) else 0
+    if lo - P * n_pad - 1 < np.iinfo(np.int64).min + 1:
+        raise ValueError("keys too close to INT64_MIN for sentinel padding")
+    s = np.empty(P * n_pad, np.int64)
+    for r in range(P):
+        blk = s[r * n_pad:(r + 1) * n_pad]
+        c = len(owned[r])
+        blk[:c] = owned[r]
+        blk[c:] = lo - 1 - (r * n_pad + np.arange(n_pad - c))
+    return owned, n_pad, s
+
+
+def _owner_of(rel_keys, owner, query):
+    """Owning rank of each query key (-1 if the key is not in the relation: dangling)."""
+    rel_keys = np.asarray(rel_keys, np.int64)
+    o = np.argsort(rel_keys, kind="stable")
+    ks = rel_keys[o]
+    q = np.asarray(query, np.int64)
+    if len(ks) == 0:
+        return np.full(len(q), -1, np.int64)
+    j = np.clip(np.searchsorted(ks, q), 0, len(ks) - 1)
+    return np.where(ks[j] == q, np.asarray(owner, np.int64)[o[j]], -1)
+
+
+class ShardedHypergraphProgram:
+    """Two-hop hypergraph layer (config 4; O8) over P ranks, one exchange per hop:
+
+        Z_own   = X_own Theta^T                                    (owned nodes)
+        Z_all   = all_gather(Z_own)
+        Eh_own  = LJA_sum(Inc rows of owned hyperedges, Z_all)      hop 1, group by hyperedge
+        Eh_all  = all_gather(Eh_own)
+        Xo_own  = LJA_mean(Inc rows of owned nodes, Eh_all)         hop 2, group by node
+      backward: hop 2 source grads over all hyperedges -> reduce_scatter -> hop 1 source grads
+      over all nodes -> reduce_scatter -> projection backward, all_reduce(dTheta).
+
+    Both hops use dense groups over the rank's owned keys (key order), so a hop's output block
+    is exactly the next hop's all-gather block; nodes without incidences output 0 (MEAN of an
+    empty multiset, reading #4's dense mode)."""
+
+    def __init__(self, hg: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32"):
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        be = self.be = backend if backend is not None else RnnBackend(prec=prec)
+        P, r = self.P, self.rank
+        nk = np.asarray(hg["nodes"]["key"], np.int64)
+        hk = np.asarray(hg["hyperedges"]["key"], np.int64)
+        iv = np.asarray(hg["inc"]["node"], np.int64)
+        ih = np.asarray(hg["inc"]["hyper"], np.int64)
+        ov = be.hash_partition(nk, P, seed)
+        oe = be.hash_partition(hk, P, seed)
+        v_owned, self.nv_pad, v_s = block_layout(nk, ov, P)
+        e_owned, self.ne_pad, e_s = block_layout(hk, oe, P)
+        self.my_v, self.my_e = v_owned[r], e_owned[r]
+        self.nv, self.ne = len(self.my_v), len(self.my_e)
+        m1 = _owner_of(hk, oe, ih) == r          # hop 1: incidences of owned hyperedges
+        m2 = _owner_of(nk, ov, iv) == r          # hop 2: incidences of owned nodes
+        self.idx1 = be.build_index(iv[m1], ih[m1], v_s, self.my_e, dense=True)
+        self.idx2 = be.build_index(ih[m2], iv[m2], e_s, self.my_v, dense=True)
+        d = int(np.asarray(hg["nodes"]["x"]).shape[1])
+        self.d = d
+        order = np.argsort(nk, kind="stable")
+        self.my_rows = order[np.searchsorted(nk[order], self.my_v)]
+        x = np.zeros((self.nv_pad, d), np.float32)
+        x[: self.nv] = np.asarray(hg["nodes"]["x"], np.float32)[self.my_rows]
+        self.X = be.tensor(x)
+        self.theta = be.tensor(np.asarray(hg["theta"], np.float32))
+        self.Z = be.zeros(self.nv_pad, d)
+        self.Zall = be.zeros(P * self.nv_pad, d)
+        self.Eh = be.zeros(self.ne_pad, d)
+        self.Ehall = be.zeros(P * self.ne_pad, d)
+        self.Xo = be.zeros(self.nv_pad, d)
+        self.dEhall = be.zeros(P * self.ne_pad, d)
+        self.dEh = be.zeros(self.ne_pad, d)
+        self.dZall = be.zeros(P * self.nv_pad, d)
+        self.dZ = be.zeros(self.nv_pad, d)
+        self.dX = be.zeros(self.nv_pad, d)
+        self.dTheta = be.zeros(d, d)
+        # upstream gradient: the single-process program's d_out row of each node group (groups
+        # = nodes with >= 1 incidence, ascending key); nodes without incidences get 0
+        present = np.unique(iv[np.isin(iv, nk) & np.isin(ih, hk)])
+        g_pos = np.searchsorted(present, self.my_v)
+        has = (g_pos < len(present)) & (present[np.minimum(g_pos, max(len(present) - 1, 0))] == self.my_v) \
+            if len(present) else np.zeros(self.nv, bool)
+        dout = np.zeros((self.nv_pad, d), np.float32)
+        dout[: self.nv][has] = np.asarray(hg["d_out"], np.float32)[g_pos[has], :d]
+        self.d_out = be.tensor(dout)
+        self.timers = None
+
+    @property
+    def join_rows_per_step(self):
+        return self.be.n_join_rows(self.idx1) + self.be.n_join_rows(self.idx2)
+
+    def roof_model(self):
+        from .programs import _sum_bwd_bytes, _sum_bytes
+        i1, i2, d = self.idx1, self.idx2, self.d
+        return {"lja_fwd": {"bound": "hbm", "amount": (_sum_bytes(i1, d) + _sum_bytes(i2, d, mean=True)) / 2},
+                "lja_bwd": {"bound": "hbm", "amount": (_sum_bwd_bytes(i1, d) + _sum_bwd_bytes(i2, d, mean=True)) / 2}}
+
+    def host_io(self):
+        return [self.X, self.d_out], [self.dTheta]
+
+    def _t(self, name):
+        if self.timers is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.timers.setdefault(name, []).append(e)
+
+    def forward(self):
+        be, g = self.be, self.group
+        self._t("proj_fwd")
+        be.project(self.X, self.theta, self.Z)
+        self._t("proj_fwd_end")
+        all_gather_rows(self.Zall, self.Z, g)
+        self._t("lja_fwd")
+        be.lja_fwd_agg(self.idx1, self.Zall, "sum", self.Eh[: self.ne])
+        self._t("lja_fwd_end")
+        all_gather_rows(self.Ehall, self.Eh, g)
+        self._t("lja_fwd")
+        be.lja_fwd_agg(self.idx2, self.Ehall, "mean", self.Xo[: self.nv])
+        self._t("lja_fwd_end")
+        return self.Xo
+
+    def backward(self):
+        be, g = self.be, self.group
+        self._t("lja_bwd")
+        be.lja_bwd_src_agg(self.idx2, self.Ehall, "mean", self.d_out, self.dEhall)
+        self._t("lja_bwd_end")
+        reduce_scatter_rows(self.dEh, self.dEhall, g)
+        self._t("lja_bwd")
+        be.lja_bwd_src_agg(self.idx1, self.Zall, "sum", self.dEh, self.dZall)
+        self._t("lja_bwd_end")
+        reduce_scatter_rows(self.dZ, self.dZall, g)
+        self._t("proj_bwd")
+        be.project_bwd(self.X, self.theta, self.dZ, self.dX, self.dTheta)
+        self._t("proj_bwd_end")
+        if self.P > 1:
+            dist.all_reduce(self.dTheta, group=g)
+        return self.dTheta, self.dX
+
+    def step(self):
+        self.forward()
+        return self.backward()
+
+    def owned_output(self):
+        return self.be.numpy(self.Xo)[: self.nv]
+
+    def owned_dx(self):
+        return self.be.numpy(self.dX)[: self.nv]

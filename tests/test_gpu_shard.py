@@ -67,3 +67,53 @@ def test_sharded_world_2(which):
         mp.spawn(_worker, args=(2, _free_port(), d, which), nprocs=2, join=True)
         res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
     check(res, graph_with_weights() if which == "small" else arxiv_small())
+
+
+def _run_hyper():
+    from paper_2605_24207_b200.shard import ShardedHypergraphProgram
+    from tests.test_shard_hyper_cpu import small_hypergraph
+    import synth
+    hg = synth.hypergraph_like(5, n_nodes=20000, n_hyper=4000, n_inc=100000, d=128)
+    prog = ShardedHypergraphProgram(hg)
+    prog.step()
+    torch.cuda.synchronize()
+    return hg, {"keys": prog.my_v, "rows": prog.my_rows, "out": prog.owned_output(),
+                "dx": prog.owned_dx(), "dtheta": prog.dTheta.cpu().numpy()}
+
+
+def _worker_hyper(rank, world, port, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        np.savez(os.path.join(path, f"r{rank}.npz"), **_run_hyper()[1])
+    finally:
+        dist.destroy_process_group()
+
+
+def check_hyper(res, hg):
+    from tests.test_shard_hyper_cpu import reference
+    ref, gk = reference(hg)
+    keys = np.concatenate([r["keys"] for r in res])
+    out = np.concatenate([r["out"] for r in res])
+    pos = np.searchsorted(gk, keys)
+    has = (pos < len(gk)) & (gk[np.minimum(pos, len(gk) - 1)] == keys)
+    assert_close(out[has], ref["Xo"][pos[has]], FP32_TOL, "out")
+    assert np.all(out[~has] == 0)
+    rows = np.concatenate([r["rows"] for r in res])
+    assert_close(np.concatenate([r["dx"] for r in res]), ref["dX"][rows], FP32_TOL, "dX")
+    for r in res:
+        assert_close(r["dtheta"], ref["dTheta"], FP32_TOL, "dTheta")
+
+
+def test_sharded_hyper_world_1():
+    hg, r = _run_hyper()
+    check_hyper([r], hg)
+
+
+def test_sharded_hyper_world_2():
+    import synth
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_hyper, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    check_hyper(res, synth.hypergraph_like(5, n_nodes=20000, n_hyper=4000, n_inc=100000, d=128))
