@@ -175,13 +175,16 @@ def run_ours(args):
     dev = torch.device("cuda", local)
 
     graph = make_graph(args.config, args.seed)
-    sharded = world > 1 and args.config in ("arxiv", "cora", "hyper")
+    sharded = world > 1 and args.config in ("arxiv", "cora", "hyper", "mag")
     if sharded:
         # multi-GPU: the join relation hash-partitioned by group key, NCCL all-gather of the
         # source embeddings / reduce-scatter of their gradients per hop
-        from paper_2605_24207_b200.shard import ShardedGCNProgram, ShardedHypergraphProgram
+        from paper_2605_24207_b200.shard import (ShardedGCNProgram, ShardedHGTProgram,
+                                                   ShardedHypergraphProgram)
         if args.config == "hyper":
             prog = ShardedHypergraphProgram(graph, prec=args.prec)
+        elif args.config == "mag":
+            prog = ShardedHGTProgram(graph, prec=args.prec)
         else:
             prog = ShardedGCNProgram(graph, prec=args.prec)
         r = torch.tensor([prog.join_rows_per_step], dtype=torch.float64, device=dev)

@@ -250,6 +250,39 @@ def _lja_src_grad(idx, q, d_out, d_src, ws):
     return d_src
 
 
+def hgt_parameters(mag: dict, seed=7):
+    """Weights and upstream gradient of the HGT layer (host, numpy), shared by HGTProgram and
+    the sharded program: per node type the stacked projection W [nb * d, d] whose column
+    blocks are (K'_phi, M'_phi) for every relation phi leaving the type and Q for every
+    relation entering it (Q shared by the relations into a type; K' carries
+    mu / sqrt(d / h), reading 12); d_out [n_t, d] per target type in T-key order."""
+    d, h = mag["d"], mag["heads"]
+    rng = np.random.default_rng(seed)
+    types = list(mag["n"].keys())
+    blocks = {t: [] for t in types}
+    for name, r in mag["rels"].items():
+        blocks[r["src_type"]] += [("k", name), ("m", name)]
+        blocks[r["dst_type"]] += [("q", name)]
+    blocks = {t: b for t, b in blocks.items() if b}
+    scale = 1.0 / np.sqrt(d / h)
+    wq = {t: rng.standard_normal((d, d)) / np.sqrt(d) for t in types}
+    W = {}
+    for t, b in blocks.items():
+        ws = []
+        for kind, name in b:
+            w = rng.standard_normal((d, d)) / np.sqrt(d)
+            if kind == "k":
+                w = w * scale            # mu / sqrt(d/h) folded into K'
+            if kind == "q":
+                w = wq[t]                # Q shared by every relation into t
+            ws.append(w)
+        W[t] = np.concatenate(ws, 0).astype(np.float32)
+    col = {(kind, name): (t, i) for t, b in blocks.items() for i, (kind, name) in enumerate(b)}
+    targets = sorted({r["dst_type"] for r in mag["rels"].values()})
+    d_out = {t: rng.standard_normal((mag["n"][t], d)).astype(np.float32) for t in targets}
+    return {"blocks": blocks, "W": W, "col": col, "targets": targets, "d_out": d_out}
+
+
 class HGTProgram(_Program):
     """One HGT attention layer over a heterogeneous schema (config 3; Fig. 4, PAPER.md:905-936,
     appendix :1343-1409; SURVEY sec 8c reading 3/12).
@@ -269,42 +302,25 @@ class HGTProgram(_Program):
         self.prec = prec
         self.d, self.h = mag["d"], mag["heads"]
         d = self.d
-        rng = np.random.default_rng(seed)
         types = list(mag["n"].keys())
         self.keys = {t: torch.as_tensor(mag["key"][t]).to(dev) for t in types}
         self.H = {t: _dev_f32(mag["h"][t], dev) for t in types}
         self.n = dict(mag["n"])
         rels = mag["rels"]
-        # column blocks of each type's stacked projection
-        blocks = {t: [] for t in types}
-        for name, r in rels.items():
-            blocks[r["src_type"]] += [("k", name), ("m", name)]
-            blocks[r["dst_type"]] += [("q", name)]
-        self.blocks = {t: b for t, b in blocks.items() if b}
-        scale = 1.0 / np.sqrt(d / self.h)
+        par = hgt_parameters(mag, seed)
+        self.blocks, self.col, self.targets = par["blocks"], par["col"], par["targets"]
         self.W, self.Y, self.dY, self.dW, self.dH = {}, {}, {}, {}, {}
-        wq = {t: rng.standard_normal((d, d)) / np.sqrt(d) for t in types}
         for t, b in self.blocks.items():
-            ws = []
-            for kind, name in b:
-                w = rng.standard_normal((d, d)) / np.sqrt(d)
-                if kind == "k":
-                    w = w * scale            # mu / sqrt(d/h) folded into K'
-                if kind == "q":
-                    w = wq[t]                # Q shared by every relation into t
-                ws.append(w)
-            self.W[t] = _dev_f32(np.concatenate(ws, 0).astype(np.float32), dev)
+            self.W[t] = _dev_f32(par["W"][t], dev)
             nb = len(b)
             self.Y[t] = _empty(self.n[t], nb * d, dev)
             self.dY[t] = _empty(self.n[t], nb * d, dev)
             self.dW[t] = torch.empty(nb * d, d, dtype=torch.float32, device=dev)
             self.dH[t] = _empty(self.n[t], d, dev)
-        self.col = {(kind, name): (t, i) for t, b in self.blocks.items() for i, (kind, name) in enumerate(b)}
         self.idx, self.q, self.O, self.lse, self.dO = {}, {}, {}, {}, {}
         self.targets = sorted({r["dst_type"] for r in rels.values()})
         self.Ht = {t: _empty(self.n[t], d, dev) for t in self.targets}
-        self.d_out = {t: _dev_f32(rng.standard_normal((self.n[t], d)).astype(np.float32), dev)
-                      for t in self.targets}
+        self.d_out = {t: _dev_f32(par["d_out"][t], dev) for t in self.targets}
         for name, r in rels.items():
             ts, tt = r["src_type"], r["dst_type"]
             self.idx[name] = rnn.build_join_index(

@@ -285,6 +285,30 @@ class RnnBackend:
         from .programs import _lja_src_grad
         _lja_src_grad(idx, self._query_agg(idx, Z, agg), d_out, d_src, self.ws)
 
+    def n_src_rows(self, idx):
+        return idx.n_src_rows
+
+    def fill_zero(self, t):
+        t.zero_()
+
+    def accumulate(self, out, x, beta):
+        self.rnn.accumulate(out, x, beta=beta)
+
+    def lja_sm_fwd(self, idx, M, K, Q, heads, out, lse):
+        q = self.rnn.make_query("src", "softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
+        self.rnn.join_aggregate_fwd(idx, q, out=out, lse=lse, ws=self.ws)
+
+    def lja_sm_bwd(self, idx, M, K, Q, heads, out, lse, d_out, dM, dK, dQ):
+        import ctypes as C
+        rnn = self.rnn
+        q = rnn.make_query("src", "softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
+        _, bb = rnn.lja_workspace_size(idx, q)
+        w = self.ws.get(bb)
+        rnn._check(rnn.lib().rnn_join_aggregate_bwd(
+            C.byref(idx.c), C.byref(q), rnn._ptr(out), out.stride(0), rnn._ptr(lse),
+            rnn._ptr(d_out), d_out.stride(0), rnn._ptr(dM), rnn._ptr(dK), None, rnn._ptr(dQ),
+            rnn._ptr(w), w.numel(), rnn._stream()))
+
     def project(self, X, W, out):
         self.rnn.project(X, W, out=out, prec=self.prec)
 
@@ -458,3 +482,155 @@ class ShardedHypergraphProgram:
 
     def owned_dx(self):
         return self.be.numpy(self.dX)[: self.nv]
+
+
+class ShardedHGTProgram:
+    """One HGT layer (config 3) over P ranks.  Every node type is hash-partitioned by key;
+    each relation's join rows live on the owner of their TARGET key (the GROUP BY key), with
+    dense groups over the rank's owned target keys.  Per step:
+
+        Y_own[t]  = H_own[t] W[t]^T                 stacked K', M', Q blocks, owned rows
+        Y_all[s]  = all_gather(Y_own[s])            for every source type s
+        O_phi     = softmax-LJA(K' = Y_all[s][k], M' = Y_all[s][m], Q = Y_own[t][q])
+        Ht[t]     = sum_phi O_phi                    (rnn_accumulate)
+      backward: per phi dK', dM' over all source rows into dY_all[s] (disjoint column blocks)
+      and dQ into dY_own[t]; reduce_scatter(dY_all[s]) added to dY_own[s]; projection
+      backward on owned rows; all_reduce(dW[t])."""
+
+    def __init__(self, mag: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32",
+                 param_seed=7):
+        from .programs import hgt_parameters
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        be = self.be = backend if backend is not None else RnnBackend(prec=prec)
+        P, r = self.P, self.rank
+        self.d, self.h = d, h = mag["d"], mag["heads"]
+        par = hgt_parameters(mag, param_seed)
+        self.blocks, self.col, self.targets = par["blocks"], par["col"], par["targets"]
+        self.rels = mag["rels"]
+        types = list(self.blocks)
+        self.owner, self.n_pad, self.s_keys, self.my_keys, self.my_rows = {}, {}, {}, {}, {}
+        for t in types:
+            k = np.asarray(mag["key"][t], np.int64)
+            o = be.hash_partition(k, P, seed)
+            owned, self.n_pad[t], self.s_keys[t] = block_layout(k, o, P)
+            self.owner[t] = o
+            self.my_keys[t] = owned[r]
+            order = np.argsort(k, kind="stable")
+            self.my_rows[t] = order[np.searchsorted(k[order], owned[r])]
+        self.n_own = {t: len(self.my_keys[t]) for t in types}
+        self.sources = sorted({x["src_type"] for x in self.rels.values()})
+        self.H, self.W, self.Y, self.dY, self.dW, self.dH = {}, {}, {}, {}, {}, {}
+        self.Yall, self.dYall, self.R = {}, {}, {}
+        for t in types:
+            nb = len(self.blocks[t])
+            x = np.zeros((self.n_pad[t], d), np.float32)
+            x[: self.n_own[t]] = np.asarray(mag["h"][t], np.float32)[self.my_rows[t]]
+            self.H[t] = be.tensor(x)
+            self.W[t] = be.tensor(par["W"][t])
+            self.Y[t] = be.zeros(self.n_pad[t], nb * d)
+            self.dY[t] = be.zeros(self.n_pad[t], nb * d)
+            self.dW[t] = be.zeros(nb * d, d)
+            self.dH[t] = be.zeros(self.n_pad[t], d)
+            if t in self.sources:
+                self.Yall[t] = be.zeros(P * self.n_pad[t], nb * d)
+                self.dYall[t] = be.zeros(P * self.n_pad[t], nb * d)
+                self.R[t] = be.zeros(self.n_pad[t], nb * d)
+        self.idx, self.O, self.lse = {}, {}, {}
+        for name, x in self.rels.items():
+            ts, tt = x["src_type"], x["dst_type"]
+            mine = _owner_of(mag["key"][tt], self.owner[tt], x["dst"]) == r
+            self.idx[name] = be.build_index(np.asarray(x["src"])[mine], np.asarray(x["dst"])[mine],
+                                            self.s_keys[ts], self.my_keys[tt], dense=True)
+            self.O[name] = be.zeros(self.n_pad[tt], d)
+            self.lse[name] = be.zeros(self.n_pad[tt], h)
+        self.Ht = {t: be.zeros(self.n_pad[t], d) for t in self.targets}
+        self.d_out = {}
+        for t in self.targets:
+            full = np.asarray(par["d_out"][t], np.float32)       # T-key order of all keys
+            ks = np.sort(np.asarray(mag["key"][t], np.int64))
+            dout = np.zeros((self.n_pad[t], d), np.float32)
+            dout[: self.n_own[t]] = full[np.searchsorted(ks, self.my_keys[t])]
+            self.d_out[t] = be.tensor(dout)
+        self.timers = None
+
+    def _blk(self, buf, t, kind, name):
+        i = self.col[(kind, name)][1]
+        return buf[t][:, i * self.d:(i + 1) * self.d]
+
+    @property
+    def join_rows_per_step(self):
+        return sum(self.be.n_join_rows(i) for i in self.idx.values())
+
+    def roof_model(self):
+        d, h = self.d, self.h
+        f, b = [], []
+        for ix in self.idx.values():
+            nj, ng, ns = self.be.n_join_rows(ix), self.be.n_groups(ix), self.be.n_src_rows(ix)
+            f.append(nj * (4 + 8 * d) + ng * (8 * d + 4 * h + 8))
+            b.append(nj * ((4 + 8 * d + 8 * h) + (8 + 8 * h + 8 * d)) + ng * (16 * d + 4 * h + 8)
+                     + ns * (8 * d + 8))
+        return {"lja_fwd": {"bound": "hbm", "amount": float(np.mean(f))},
+                "lja_bwd": {"bound": "hbm", "amount": float(np.mean(b))}}
+
+    def host_io(self):
+        return list(self.H.values()) + list(self.d_out.values()), list(self.dW.values())
+
+    def _t(self, name):
+        if self.timers is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.timers.setdefault(name, []).append(e)
+
+    def forward(self):
+        be, g = self.be, self.group
+        self._t("proj_fwd")
+        for t in self.blocks:
+            be.project(self.H[t], self.W[t], self.Y[t])
+        self._t("proj_fwd_end")
+        for s in self.sources:
+            all_gather_rows(self.Yall[s], self.Y[s], g)
+        first = {t: True for t in self.targets}
+        for name, x in self.rels.items():
+            ts, tt = x["src_type"], x["dst_type"]
+            n = self.n_own[tt]
+            self._t("lja_fwd")
+            be.lja_sm_fwd(self.idx[name], self._blk(self.Yall, ts, "m", name),
+                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", name),
+                          self.h, self.O[name][:n], self.lse[name][:n])
+            self._t("lja_fwd_end")
+            be.accumulate(self.Ht[tt][:n], self.O[name][:n], 0.0 if first[tt] else 1.0)
+            first[tt] = False
+        return self.Ht
+
+    def backward(self):
+        be, g = self.be, self.group
+        for t in self.blocks:
+            be.fill_zero(self.dY[t])
+        for name, x in self.rels.items():
+            ts, tt = x["src_type"], x["dst_type"]
+            n = self.n_own[tt]
+            self._t("lja_bwd")
+            be.lja_sm_bwd(self.idx[name], self._blk(self.Yall, ts, "m", name),
+                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", name),
+                          self.h, self.O[name][:n], self.lse[name][:n], self.d_out[tt][:n],
+                          self._blk(self.dYall, ts, "m", name), self._blk(self.dYall, ts, "k", name),
+                          self._blk(self.dY, tt, "q", name)[:n])
+            self._t("lja_bwd_end")
+        for s in self.sources:
+            reduce_scatter_rows(self.R[s], self.dYall[s], g)
+            be.accumulate(self.dY[s], self.R[s], 1.0)
+        self._t("proj_bwd")
+        for t in self.blocks:
+            be.project_bwd(self.H[t], self.W[t], self.dY[t], self.dH[t], self.dW[t])
+        self._t("proj_bwd_end")
+        if self.P > 1:
+            for t in self.blocks:
+                dist.all_reduce(self.dW[t], group=g)
+        return self.dW, self.dH
+
+    def step(self):
+        self.forward()
+        return self.backward()

@@ -117,3 +117,45 @@ def test_sharded_hyper_world_2():
         mp.spawn(_worker_hyper, args=(2, _free_port(), d), nprocs=2, join=True)
         res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
     check_hyper(res, synth.hypergraph_like(5, n_nodes=20000, n_hyper=4000, n_inc=100000, d=128))
+
+
+def _mag_gpu():
+    import synth
+    m = synth.mag_like(9, scale=0.003, d=128, heads=8)
+    m.pop("rng", None)
+    return m
+
+
+def _run_hgt():
+    from paper_2605_24207_b200.shard import ShardedHGTProgram
+    from tests.test_shard_hgt_cpu import _run
+    from paper_2605_24207_b200.shard import RnnBackend
+    r = _run(_mag_gpu(), RnnBackend())
+    torch.cuda.synchronize()
+    return r
+
+
+def _worker_hgt(rank, world, port, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        np.savez(os.path.join(path, f"r{rank}.npz"), **_run_hgt())
+    finally:
+        dist.destroy_process_group()
+
+
+def _check_hgt(res):
+    from tests.test_shard_hgt_cpu import check
+    check(res, _mag_gpu(), close=lambda a, b, what: assert_close(a, b, FP32_TOL, what))
+
+
+def test_sharded_hgt_world_1():
+    _check_hgt([_run_hgt()])
+
+
+def test_sharded_hgt_world_2():
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_hgt, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    _check_hgt(res)
