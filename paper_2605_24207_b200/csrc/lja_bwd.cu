@@ -718,14 +718,13 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
     s.dk = d_src_key; s.ld_dk = q->src_key.ld;
     s.heads = q->heads; s.scale = q->scale;
     if (sm_rowsplit_ok(idx, q, qi.D) && idx->src_seg) {
-      SmBwd1GPol p1;
+      SmBwd1Pol p1;
       p1.a = sm_rows(idx, q);
       p1.out = out; p1.ld_out = ld_out; p1.lse = lse; p1.dO = d_out; p1.ld_do = ld_dout;
       p1.AD = Lw.AD; p1.dq = d_dst; p1.ld_dq = q->dst.ld;
       RSCtx c1{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
                idx->n_work, Lw.part_fwd, qi.pstride, Lw.cnt_fwd, 1};
-      if (sm_nocache()) RNN_TRY((launch_st<SmBwd1Pol, 2, 3>(p1, c1, st)));
-      else RNN_TRY(launch_stg_bwd1(p1, c1, st));
+      RNN_TRY((launch_st<SmBwd1Pol, 2, 3>(p1, c1, st)));
       if (d_src || d_src_key) {
         SmBwd2Pol p2;
         p2.a = p1.a;

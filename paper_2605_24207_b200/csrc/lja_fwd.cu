@@ -474,13 +474,12 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
     return launch_rs_mode<4>(a, rx, st);
   }
   if (q->agg == RNN_AGG_SOFTMAX && sm_rowsplit_ok(idx, q, qi.D)) {
-    SmFwdGPol pol;
+    SmFwdPol pol;
     pol.a = sm_rows(idx, q);
     pol.out = out; pol.ld_out = ld_out; pol.beta = beta; pol.lse = lse;
     RSCtx rx{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
              idx->n_work, cx.partial, cx.pstride, cx.counter, 1};
-    if (sm_nocache()) return launch_st<SmFwdPol, 4, 3>(pol, rx, st);
-    return launch_stg_fwd(pol, rx, st);
+    return launch_st<SmFwdPol, 4, 3>(pol, rx, st);
   }
   if (q->agg == RNN_AGG_SOFTMAX) {
     switch (qi.D / 4) {

@@ -859,7 +859,16 @@ __global__ void splitk_final(const float* __restrict__ tmp, int64_t groups, int6
   if (4 * i4 >= n) return;
   const float4* t = reinterpret_cast<const float4*>(tmp) + i4;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int64_t g = 0; g < groups; ++g) acc = f4_add(acc, __ldcs(t + g * (n / 4)));
+  // 8 loads in flight, additions still in group order
+  for (int64_t g = 0; g < groups; g += 8) {
+    float4 x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      x[u] = g + u < groups ? __ldcs(t + (g + u) * (n / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (g + u < groups) acc = f4_add(acc, x[u]);
+  }
   reinterpret_cast<float4*>(out)[i4] = acc;
 }
 __global__ void splitk_reduce1(const float* __restrict__ part, int64_t splits, int64_t stride,
@@ -957,7 +966,8 @@ rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams 
   constexpr int KB = (A_MN && B_MN) ? 16 : BK;
   const uint32_t stage = (uint32_t)(BM * KB * 4 + p.BN * KB * 4) * (SPLIT3 ? 2u : 1u);
   const int64_t nkb_max = ceil_div(p.k_split, KB);
-  int stages = (int)((200 * 1024) / stage);
+  static const int budget_kb = getenv("RNN_GEMM_SMEM_KB") ? atoi(getenv("RNN_GEMM_SMEM_KB")) : 200;
+  int stages = (int)((budget_kb * 1024) / stage);
   if (!SPLIT3 && stages > 3 && stage * 3 <= 100 * 1024 && !(A_MN && B_MN)) stages = 3;  // 2 CTAs / SM
   if (stages > MAX_STAGES) stages = MAX_STAGES;
   if (stages > nkb_max) stages = (int)nkb_max;

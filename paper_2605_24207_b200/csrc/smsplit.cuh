@@ -123,139 +123,6 @@ rnn_status launch_st(const Pol& pol, RSCtx cx, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Group-cached walker (group-major passes whose rows also read a per-SEGMENT operand, e.g. the
-// query row Q[t] and dO[t] of the group): the segment-side values are loaded once per segment
-// and kept in registers instead of once per row.  A batch of at most U rows spans at most two
-// segments (it is cut after the second segment end), so besides the cached segment `gc` at
-// most one more segment's values `gb` are in flight; each row picks its segment's values by
-// a select.  Extra Pol interface:
-//   struct G;  void gload(G&, const Meta&) const;  void gprep(G&) const  (warp-converged)
-//   G pick(bool first, const G& a, const G& b) const;
-//   void load(Row&, const Meta&, bool ok) const;  void prep(Row&, const G&) const;
-//   void row(State&, const Row&, const G&, int64_t pos) const;
-// ------------------------------------------------------------------------------------------
-template <class Pol, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) stg_kernel(Pol pol, RSCtx cx) {
-  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (item >= cx.n_work) return;
-  const int lane = lane_id();
-  const int64_t b = cx.work_ptr[item], e = cx.work_ptr[item + 1];
-  bool head_piece = b > 0 && cx.seg[b - 1] == cx.seg[b];
-  typename Pol::State st;
-  pol.init(st);
-  typename Pol::G gc, gb;
-  int gc_id = -1;
-  bool pending = false;
-  int g_tail = -1;
-  for (int64_t r0 = b; r0 < e; r0 += 32) {
-    const int P = (int)((e - r0) < 32 ? (e - r0) : 32);
-    typename Pol::Meta m{};
-    int gl = -1;
-    bool endf = false;
-    if (lane < P) {
-      const int64_t r = r0 + lane;
-      gl = cx.seg[r];
-      m = pol.meta(r, gl);
-      endf = r + 1 >= cx.E || cx.seg[r + 1] != gl;
-    }
-    if (cx.zero_empty) {
-      const int gprev = lane < P ? (r0 + lane > 0 ? cx.seg[r0 + lane - 1] : -1) : 0;
-      unsigned gaps = __ballot_sync(FULL, lane < P && gl > gprev + 1);
-      while (gaps) {
-        const int j = __ffs(gaps) - 1;
-        gaps &= gaps - 1;
-        st_zero_range(pol, __shfl_sync(FULL, gprev, j) + 1, __shfl_sync(FULL, gl, j));
-      }
-    }
-    const unsigned ends = __ballot_sync(FULL, endf);
-    for (int j0 = 0; j0 < P;) {
-      const unsigned eb = ends >> j0;  // bit u: row j0 + u closes its segment
-      int len = P - j0 < U ? P - j0 : U;
-      const int fe = eb ? __ffs(eb) - 1 : 31;
-      const unsigned eb2 = eb & (eb - 1);
-      if (eb2 && __ffs(eb2) < len) len = __ffs(eb2);  // cut after the second segment end
-      const bool cross = fe + 1 < len;                // rows fe+1 .. len-1: next segment
-      const int jn = cross ? j0 + fe + 1 : j0;
-      const int g0 = __shfl_sync(FULL, gl, j0), g1 = __shfl_sync(FULL, gl, jn);
-      const typename Pol::Meta m0 = pol.shfl(m, j0), m1 = pol.shfl(m, jn);
-      const bool need0 = g0 != gc_id;
-      if (need0) pol.gload(gc, m0);
-      if (cross) pol.gload(gb, m1);
-      typename Pol::Row rw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) pol.load(rw[u], pol.shfl(m, (j0 + u) & 31), u < len);
-      if (need0) {
-        pol.gprep(gc);
-        gc_id = g0;
-      }
-      if (cross) pol.gprep(gb);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (u < len) pol.prep(rw[u], pol.pick(u <= fe, gc, gb));
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u < len) {
-          pol.row(st, rw[u], pol.pick(u <= fe, gc, gb), r0 + j0 + u);
-          pending = true;
-          if ((eb >> u) & 1u) {
-            const int g = u <= fe ? g0 : g1;
-            if (head_piece) st_piece(pol, cx, item, g, st);
-            else pol.finish(st, g);
-            head_piece = false;
-            pending = false;
-            pol.init(st);
-          }
-        }
-      }
-      if (cross) {
-        gc = gb;
-        gc_id = g1;
-      }
-      j0 += len;
-    }
-    g_tail = __shfl_sync(FULL, gl, P - 1);
-  }
-  if (pending) st_piece(pol, cx, item, g_tail, st);
-  if (cx.zero_empty && item == cx.n_work - 1)
-    st_zero_range(pol, cx.E > 0 ? cx.seg[cx.E - 1] + 1 : 0, cx.n_seg);
-}
-
-template <class Pol, int U, int MINB = 1>
-rnn_status launch_stg(const Pol& pol, RSCtx cx, cudaStream_t st) {
-  if (cx.n_work <= 0) return RNN_OK;
-  RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * cx.n_work, st));
-  stg_kernel<Pol, U, MINB><<<(unsigned)ceil_div(cx.n_work, 8), 256, 0, st>>>(pol, cx);
-  RNN_LAUNCH_CHECK();
-  return RNN_OK;
-}
-
-// (U rows in flight, min CTAs per SM) of the group-cached walkers; RNN_SM_VAR="fU,fB,bU,bB"
-// picks another instantiated variant (measurement only)
-struct SmVar { int fu, fb, bu, bb; };
-inline SmVar sm_var() {
-  static SmVar v = [] {
-    SmVar r{6, 2, 4, 2};
-    if (const char* e = getenv("RNN_SM_VAR")) sscanf(e, "%d,%d,%d,%d", &r.fu, &r.fb, &r.bu, &r.bb);
-    return r;
-  }();
-  return v;
-}
-// A/B switch for measurement: RNN_SM_NOCACHE=1 selects the per-row-load walkers
-inline bool sm_nocache() {
-  static const int v = getenv("RNN_SM_NOCACHE") ? 1 : 0;
-  return v != 0;
-}
-
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float4 f4_sel(bool c, const float4& a, const float4& b) {
-  return make_float4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
-}
-
-// ------------------------------------------------------------------------------------------
 // softmax-weighted aggregate over 128-float rows (lane = float4 column, LH lanes per head)
 // ------------------------------------------------------------------------------------------
 constexpr float SM_LOG2E = 1.4426950408889634f;
@@ -434,79 +301,6 @@ struct SmBwd1Pol {
   }
 };
 
-// forward on the group-cached walker: Q[t] is loaded once per group, rows gather K', M' only
-struct SmFwdGPol : SmFwdPol {
-  struct Row { float4 k, v; float sc; };
-  struct G { float4 q; };
-  __device__ __forceinline__ void gload(G& g, const Meta& m) const {
-    g.q = ld_f4(a.q + (int64_t)m.t * a.ld_q + 4 * lane_id());
-  }
-  __device__ __forceinline__ void gprep(G&) const {}
-  __device__ __forceinline__ G pick(bool first, const G& x, const G& y) const {
-    return G{f4_sel(first, x.q, y.q)};
-  }
-  __device__ __forceinline__ void load(Row& w, const Meta& m, bool) const {
-    const int k = lane_id();
-    w.k = ld_f4(a.key + (int64_t)m.s * a.ld_key + 4 * k);
-    w.v = ld_f4(a.val + (int64_t)m.s * a.ld_val + 4 * k);
-  }
-  __device__ __forceinline__ void prep(Row& w, const G& g) const {
-    w.sc = sm_head_sum(f4_dot(w.k, g.q), a.LH) * (a.scale * SM_LOG2E);
-  }
-  __device__ __forceinline__ void row(State& s, const Row& w, const G&, int64_t) const {
-    const float d = w.sc - s.m;
-    const bool up = d > 0.f;
-    const float x = ex2_approx(-fabsf(d));
-    const float cs = up ? x : 1.f, p = up ? 1.f : x;
-    s.l = fmaf(s.l, cs, p);
-    s.acc = f4_fma(p, w.v, f4_scale(cs, s.acc));
-    s.m = up ? w.sc : s.m;
-  }
-};
-
-// backward pass 1 on the group-cached walker: Q[t], dO[g], lse[g] and D = <dO, O> per head are
-// loaded / computed once per group; rows gather K', M' only
-struct SmBwd1GPol : SmBwd1Pol {
-  struct Row { float4 k, v; float sc, da; };
-  struct G { float4 q, dO, o; float lse2, D; };
-  __device__ __forceinline__ void gload(G& g, const Meta& m) const {
-    const int k = lane_id();
-    g.q = ld_f4(a.q + (int64_t)m.t * a.ld_q + 4 * k);
-    g.dO = ld_f4(dO + (int64_t)m.g * ld_do + 4 * k);
-    g.o = ld_f4(out + (int64_t)m.g * ld_out + 4 * k);
-    g.lse2 = __ldg(lse + (int64_t)m.g * a.heads + k / a.LH) * SM_LOG2E;
-  }
-  __device__ __forceinline__ void gprep(G& g) const { g.D = sm_head_sum(f4_dot(g.dO, g.o), a.LH); }
-  __device__ __forceinline__ G pick(bool first, const G& x, const G& y) const {
-    G r;
-    r.q = f4_sel(first, x.q, y.q);
-    r.dO = f4_sel(first, x.dO, y.dO);
-    r.lse2 = first ? x.lse2 : y.lse2;
-    r.D = first ? x.D : y.D;
-    return r;
-  }
-  __device__ __forceinline__ void load(Row& w, const Meta& m, bool) const {
-    const int k = lane_id();
-    w.k = ld_f4(a.key + (int64_t)m.s * a.ld_key + 4 * k);
-    w.v = ld_f4(a.val + (int64_t)m.s * a.ld_val + 4 * k);
-  }
-  __device__ __forceinline__ void prep(Row& w, const G& g) const {
-    w.sc = sm_head_sum(f4_dot(w.k, g.q), a.LH);
-    w.da = sm_head_sum(f4_dot(g.dO, w.v), a.LH);
-  }
-  __device__ __forceinline__ void row(State& s, const Row& w, const G& g, int64_t p) const {
-    const int k = lane_id();
-    const float pa = ex2_approx(w.sc * (a.scale * SM_LOG2E) - g.lse2);
-    const float de = pa * (w.da - g.D);
-    s.dq = f4_fma(de, w.k, s.dq);
-    if (k % a.LH == 0) {
-      float* ad = AD + p * 2 * a.heads + k / a.LH;
-      ad[0] = pa;
-      ad[a.heads] = de;
-    }
-  }
-};
-
 // backward pass 2 (source-major): dM'[s] = sum_r a_r dO[g_r];  dK'[s] = scale sum_r de_r Q[t_r]
 struct SmBwd2Pol {
   SmRows a;
@@ -561,22 +355,4 @@ struct SmBwd2Pol {
   }
 };
 
-}  // namespace rnn
-
-namespace rnn {
-template <class Pol>
-rnn_status launch_stg_fwd(const Pol& pol, RSCtx cx, cudaStream_t st) {
-  const SmVar v = sm_var();
-  if (v.fu == 4 && v.fb == 3) return launch_stg<Pol, 4, 3>(pol, cx, st);
-  if (v.fu == 4 && v.fb == 2) return launch_stg<Pol, 4, 2>(pol, cx, st);
-  if (v.fu == 8 && v.fb == 2) return launch_stg<Pol, 8, 2>(pol, cx, st);
-  return launch_stg<Pol, 6, 2>(pol, cx, st);
-}
-template <class Pol>
-rnn_status launch_stg_bwd1(const Pol& pol, RSCtx cx, cudaStream_t st) {
-  const SmVar v = sm_var();
-  if (v.bu == 2 && v.bb == 3) return launch_stg<Pol, 2, 3>(pol, cx, st);
-  if (v.bu == 3 && v.bb == 2) return launch_stg<Pol, 3, 2>(pol, cx, st);
-  return launch_stg<Pol, 4, 2>(pol, cx, st);
-}
 }  // namespace rnn

@@ -178,6 +178,33 @@ def test_softmax_attention_parity(R, ora, heads, D):
         assert_close(np_(g[k]), gr[k], FP32_TOL, f"d_{k}")
 
 
+@pytest.mark.parametrize("n_t,n_e,rpi", [(3000, 4000, 32), (900, 5000, 64), (2500, 2600, 0)])
+def test_softmax_small_groups(R, ora, n_t, n_e, rpi):
+    """Many groups of 1-3 rows next to a split hub: the group-cached walkers see batches that
+    cross one or two group ends, groups that start mid-batch and pieces of the hub."""
+    rng = np.random.default_rng(n_t + n_e)
+    D, heads = 128, 8
+    db = make_case(rng, n_s=500, n_t=n_t, n_e=n_e)
+    gi = R.build_join_index(cu(db["e_src"]), cu(db["e_dst"]), cu(db["s_key"]), cu(db["t_key"]),
+                            rows_per_item=rpi)
+    oi = ora.build_join_index(db["e_src"], db["e_dst"], db["s_key"], db["t_key"])
+    K = (rng.standard_normal((500, D)) * 0.5).astype(np.float32)
+    M = rng.standard_normal((500, D)).astype(np.float32)
+    Q = (rng.standard_normal((n_t, D)) * 0.5).astype(np.float32)
+    scale = 1.0 / np.sqrt(D / heads)
+    q = R.make_query("src", "softmax", src=padded(M), src_key=padded(K), dst=padded(Q), heads=heads,
+                     scale=scale)
+    out, lse = R.join_aggregate_fwd(gi, q)
+    ref, rlse = ora.lja_fwd(oi, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=scale)
+    assert_close(np_(out), ref, FP32_TOL, "out")
+    assert_close(np_(lse)[: oi["n_groups"]], rlse, FP32_TOL, "lse")
+    dO = rng.standard_normal(ref.shape).astype(np.float32)
+    g = R.join_aggregate_bwd(gi, q, padded(dO), out=out, lse=lse)
+    gr = ora.lja_bwd(oi, dO, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=scale)
+    for k in ("src", "src_key", "dst"):
+        assert_close(np_(g[k]), gr[k], FP32_TOL, f"d_{k}")
+
+
 def test_softmax_dense_groups_beta(R, ora):
     """Row-split softmax (D = 128) over a dense-group index: T keys with no join row give
     out 0 / lse -inf / dQ 0; beta = 1 adds onto an existing union (A7); hub pieces merge."""
