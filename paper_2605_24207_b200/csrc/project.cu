@@ -43,6 +43,7 @@ struct GemmParams {
   int mode;         // 0: out = acc + bias ; 1: partial[z] = acc
   float* partial; int64_t ldp; int64_t part_stride;
   uint32_t tmem_cols;
+  int a3d, b3d;     // MN-major operand loaded as ONE 3D box {32, KB, MN/32} per stage
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -77,6 +78,14 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, void* dst, u
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
       "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, void* dst, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
@@ -148,17 +157,32 @@ __device__ __forceinline__ uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
 
 // lo = x - trunc_tf32(x) only: the tcgen05 tf32 MMA truncates its fp32 inputs itself, so the
 // raw tile is its own hi part
-__device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n16, int t) {
-  for (uint32_t i = t; i < n16; i += 128) {
-    const float4 v = x[i];
-    float4 l;
-    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-    lo[i] = l;
-  }
+__device__ __forceinline__ float4 lo_part(float4 v) {
+  float4 l;
+  l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+  l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+  l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+  l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+  return l;
 }
+// 128 threads; 8 shared-memory loads in flight per thread (the converter was latency-bound)
+__device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n16, int t) {
+  uint32_t i = t;
+  for (; i + 7 * 128 < n16; i += 8 * 128) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = x[i + u * 128];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) lo[i + u * 128] = lo_part(v[u]);
+  }
+  for (; i < n16; i += 128) lo[i] = lo_part(x[i]);
+}
+
+// per-role wait cycles of tc_gemm_kernel (internal hook rnn_internal_gemm_stats): [0] producer
+// waits for a free slot, [1] MMA waits for a ready stage, [2] converter waits for a landed
+// stage, [3] TMA latency (issue -> landed, summed over stages, converter / MMA side),
+// [4] stages counted for [3]; [8..10] total cycles of producer, MMA, converter lanes
+__device__ unsigned long long g_gemm_stats[16];
 
 template <bool A_MN, bool B_MN, bool SPLIT3, int KB = BK>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -180,6 +204,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long gs_t0 = clock64();
+  unsigned long long gs_w[5] = {0, 0, 0, 0, 0};
+  __shared__ long long gs_issue[MAX_STAGES];
   const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int n0 = blockIdx.y * p.BN;
   const int64_t kbeg = (int64_t)blockIdx.z * p.k_split;
@@ -222,11 +249,20 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
-        if (kb >= p.stages) mbar_wait(&empty[s], ph ^ 1);
+        if (kb >= p.stages) {
+          const long long t0 = clock64();
+          mbar_wait(&empty[s], ph ^ 1);
+          gs_w[0] += clock64() - t0;
+        }
+        gs_issue[s] = clock64();
         mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
         const int k = (int)(kbeg + (int64_t)kb * KB);
+        // MN-major operands: 32-wide MN chunks every KB * 128 bytes, either one 3D box
+        // {32, KB, chunks} (a single TMA op) or one 2D box per chunk
         if (!A_MN) {
           tma_load_2d(&ta, a_hi(s), &full[s], k, (int)m0);
+        } else if (p.a3d) {
+          tma_load_3d(&ta, a_hi(s), &full[s], 0, k, (int)(m0 / 32));
         } else {
 #pragma unroll
           for (int j = 0; j < BM / 32; ++j)
@@ -234,11 +270,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (!B_MN) {
           tma_load_2d(&tb, b_hi(s), &full[s], k, n0);
+        } else if (p.b3d) {
+          tma_load_3d(&tb, b_hi(s), &full[s], 0, k, n0 / 32);
         } else {
           for (int j = 0; j < p.BN / 32; ++j)
             tma_load_2d(&tb, b_hi(s) + j * (KB * 128), &full[s], n0 + 32 * j, k);
         }
       }
+      atomicAdd(&g_gemm_stats[8], (unsigned long long)(clock64() - gs_t0));
+      atomicAdd(&g_gemm_stats[0], gs_w[0]);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -246,7 +286,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % p.stages;
       const uint32_t ph = (kb / p.stages) & 1;
-      mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+      {
+        const long long t0 = clock64();
+        mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+        const long long t1 = clock64();
+        gs_w[1] += t1 - t0;
+        if (!SPLIT3) { gs_w[3] += t1 - *(volatile long long*)&gs_issue[s]; gs_w[4] += 1; }
+      }
       tc_fence_after();
       if (lane == 0) {
 #pragma unroll
@@ -267,6 +313,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (lane == 0) tc_commit(acc_full);
     __syncwarp();
+    if (lane == 0) {
+      atomicAdd(&g_gemm_stats[9], (unsigned long long)(clock64() - gs_t0));
+      atomicAdd(&g_gemm_stats[1], gs_w[1]);
+      if (!SPLIT3) { atomicAdd(&g_gemm_stats[3], gs_w[3]); atomicAdd(&g_gemm_stats[4], gs_w[4]); }
+    }
   } else {
     // ---------------- converters (3xTF32) + epilogue: warps 2..5 ----------------
     const int et = threadIdx.x - 64;  // 0..127
@@ -274,7 +325,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
-        mbar_wait(&full[s], ph);
+        {
+          const long long t0 = clock64();
+          mbar_wait(&full[s], ph);
+          const long long t1 = clock64();
+          gs_w[2] += t1 - t0;
+          gs_w[3] += t1 - *(volatile long long*)&gs_issue[s];
+          gs_w[4] += 1;
+        }
         // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
         lo_tile(reinterpret_cast<const float4*>(a_hi(s)), reinterpret_cast<float4*>(a_lo(s)),
                 A_BYTES / 16, et);
@@ -283,6 +341,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[s]);
       }
+    }
+    if (lane == 0 && warp == 2) {
+      atomicAdd(&g_gemm_stats[10], (unsigned long long)(clock64() - gs_t0));
+      for (int i = 2; i < 5; ++i) atomicAdd(&g_gemm_stats[i], gs_w[i]);
     }
     mbar_wait(acc_full, 0);
     tc_fence_after();
@@ -954,6 +1016,28 @@ rnn_status make_map(CUtensorMap* m, const float* base, int64_t inner, int64_t ro
   return RNN_OK;
 }
 
+// MN-major operand [rows, mn] (row stride ld) viewed as 3D {32, rows, ceil(mn / 32)} so that one
+// box {32, box_rows, chunks} lands as `chunks` 32-wide MN chunks every box_rows * 128 bytes.
+// Only when the padded width fits the row stride (the last chunk's tail then reads inside the
+// row; those elements only feed accumulator rows / columns >= mn, which are never stored).
+bool map3_ok(const float* base, int64_t mn, int64_t ld) {
+  return ld >= (mn + 31) / 32 * 32 && aligned16(base) && (ld * 4) % 16 == 0 && !getenv("RNN_NO_TMA3D");
+}
+rnn_status make_map3(CUtensorMap* m, const float* base, int64_t mn, int64_t rows, int64_t ld,
+                     uint32_t box_rows, uint32_t chunks) {
+  auto fn = encode_fn();
+  RNN_REQUIRE(fn, RNN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {32, (cuuint64_t)(rows > 0 ? rows : 1), (cuuint64_t)((mn + 31) / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)(ld * 4), 128};
+  cuuint32_t box[3] = {32, box_rows, chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  RNN_REQUIRE(r == CUDA_SUCCESS, RNN_ERR_CUDA, "cuTensorMapEncodeTiled (3D) failed (%d)", (int)r);
+  return RNN_OK;
+}
+
 uint32_t pow2_cols(int bn) {
   uint32_t c = 32;
   while ((int)c < bn) c <<= 1;
@@ -1160,8 +1244,12 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
     const int splits = (int)ceil_div(M, p.k_split);
     p.mode = 1; p.partial = w.part; p.ldp = K; p.part_stride = (int64_t)N * K;
     CUtensorMap ta, tb;
-    RNN_TRY(make_map(&ta, dY, N, M, lddy, 32, 16, true));
-    RNN_TRY(make_map(&tb, X, K, M, ldx, 32, 16, true));
+    p.a3d = map3_ok(dY, N, lddy);
+    p.b3d = map3_ok(X, K, ldx);
+    if (p.a3d) RNN_TRY(make_map3(&ta, dY, N, M, lddy, 16, BM / 32));
+    else RNN_TRY(make_map(&ta, dY, N, M, lddy, 32, 16, true));
+    if (p.b3d) RNN_TRY(make_map3(&tb, X, K, M, ldx, 16, (uint32_t)(p.BN / 32)));
+    else RNN_TRY(make_map(&tb, X, K, M, ldx, 32, 16, true));
     RNN_TRY((gemm<true, true>(ta, tb, p, splits, prec, st)));
     // partial tiles and dW are contiguous [N, K]
     const int64_t nk = (int64_t)N * K;
@@ -1220,6 +1308,16 @@ extern "C" int rnn_internal_proj_stats(unsigned long long* out, int reset) {
   if (reset) {
     unsigned long long z[16] = {0};
     if (cudaMemcpyToSymbol(rnn::g_proj_stats, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+
+extern "C" int rnn_internal_gemm_stats(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, rnn::g_gemm_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
+    return 1;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    if (cudaMemcpyToSymbol(rnn::g_gemm_stats, z, sizeof(z)) != cudaSuccess) return 1;
   }
   return 0;
 }
