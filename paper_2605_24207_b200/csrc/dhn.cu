@@ -312,6 +312,63 @@ __device__ __forceinline__ void h4_chunk(int* keys, int* ids, int* n_ids, float*
   }
 }
 
+// V4 variant of h4_chunk: lane = (hit slot sub = lane / 8, channel quad cq = lane % 8), so
+// one instruction moves FOUR hits' 32-channel rows -- OUT: one red.global.add.v4.f32 per lane
+// (4x fewer L2 reduction requests than one 4-byte red per lane per hit); IN: float4 loads of
+// S1(w) and f2(w).  fv4 / t4: channels 4 cq .. 4 cq + 3 of this 32-channel block.
+__device__ __forceinline__ int h4_take4(unsigned& bal, int sub) {
+  int mine = -1;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int q = bal ? __ffs(bal) - 1 : -1;
+    if (q >= 0) bal &= bal - 1;
+    if (k == sub) mine = q;
+  }
+  return mine;
+}
+template <bool OUT>
+__device__ __forceinline__ void h4_chunk4(int* keys, int* ids, int* n_ids, float* S, int32_t w,
+                                          bool in, float4 fv4, float4& t4, int lane,
+                                          const float* F2q, int d) {
+  const int sub = lane >> 3, cq = lane & 7;
+  if (OUT) {
+    const int sl = (in && w >= 0) ? h4_insert(keys, ids, n_ids, w) : -1;
+    unsigned bal = __ballot_sync(FULL, sl >= 0);
+    while (bal) {
+      const int mine = h4_take4(bal, sub);
+      const int slq = __shfl_sync(FULL, sl, mine < 0 ? 0 : mine);
+      if (mine >= 0)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(S + slq * 32 + 4 * cq),
+                     "f"(fv4.x), "f"(fv4.y), "f"(fv4.z), "f"(fv4.w)
+                     : "memory");
+    }
+  } else {
+    int sl = (in && w >= 0) ? hs_find(keys, H4_CAP - 1, w) : -1;
+    if (sl >= 0) sl = ids[sl];
+    unsigned bal = __ballot_sync(FULL, sl >= 0);
+    while (bal) {   // G(w) = f2(w) (.) S1(w) formed on the fly, 8 hits in flight (2 per slot)
+      float4 x[2], y[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int mine = h4_take4(bal, sub);
+        const int slq = __shfl_sync(FULL, sl, mine < 0 ? 0 : mine);
+        const int wq = __shfl_sync(FULL, w, mine < 0 ? 0 : mine);
+        x[u] = mine >= 0 ? __ldcg(reinterpret_cast<const float4*>(S + slq * 32 + 4 * cq))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        y[u] = mine >= 0 ? __ldg(reinterpret_cast<const float4*>(F2q + (int64_t)wq * d))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        t4.x = fmaf(x[u].x, y[u].x, t4.x);
+        t4.y = fmaf(x[u].y, y[u].y, t4.y);
+        t4.z = fmaf(x[u].z, y[u].z, t4.z);
+        t4.w = fmaf(x[u].w, y[u].w, t4.w);
+      }
+    }
+  }
+}
+
 struct H4Root {
   int64_t n, ib, pb;
   int deg;               // neighbours on this side
@@ -325,8 +382,8 @@ struct H4Root {
 // serves neighbours (one per warp, or 32 per step in chunked mode) and walks their runs of
 // this partition; runs longer than H4_LONG are queued.  Phase B: every queued run is split
 // over all warps.  Returns this thread's contribution to the root's accumulator (IN).
-template <bool OUT>
-__device__ float h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids, int* n_ids,
+template <bool OUT, bool V4>
+__device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids, int* n_ids,
                           float* S, int* cur, int* q_i, int64_t* q_b, int64_t* q_e, int* q_n,
                           int* grab, int c, bool cok) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -334,7 +391,20 @@ __device__ float h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids
   const float* Fv = OUT ? a.F1 : a.F3;
   const int d = a.d;
   const float* F2c = a.F2 + (cok ? c : 0);   // f2 column of this lane (rows gathered by w)
+  // V4: this lane's channel quad c0 + 4 (lane % 8) .. + 3
+  const int cq4 = (c - lane) + 4 * (lane & 7);
+  const bool cok4 = cq4 < d;
+  const float* F2q = a.F2 + (cok4 ? cq4 : 0);
   float acc = 0.f;
+  float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto ld_fv4 = [&](int32_t u) {
+    return cok4 ? __ldg(reinterpret_cast<const float4*>(Fv + (int64_t)u * d + cq4))
+                : make_float4(0.f, 0.f, 0.f, 0.f);
+  };
+  auto fma4 = [](float4& acc_, const float4& f, const float4& t_) {
+    acc_.x = fmaf(f.x, t_.x, acc_.x); acc_.y = fmaf(f.y, t_.y, acc_.y);
+    acc_.z = fmaf(f.z, t_.z, acc_.z); acc_.w = fmaf(f.w, t_.w, acc_.w);
+  };
   // phase A: warps grab neighbours dynamically (chunked mode: 32 at a time, lanes in parallel)
   const int step = R.chunked ? 32 : 1;
   for (;;) {
@@ -384,19 +454,25 @@ __device__ float h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids
           continue;
         }
       }
-      const float fv = cok ? Fv[(int64_t)uj * d + c] : 0.f;
-      float t = 0.f;
+      float fv = 0.f, t = 0.f;
+      float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4;
+      if (V4) fv4 = ld_fv4(uj);
+      else fv = cok ? Fv[(int64_t)uj * d + c] : 0.f;
       int64_t t0 = bj;
       for (;;) {
         const int64_t tt = t0 + lane;
         const int32_t w = tt < ej ? L[tt] : -1;
         const bool in = tt < ej && (h4_top(w) >> R.sh) == R.part;
         const unsigned im = __ballot_sync(FULL, in);
-        h4_chunk<OUT>(keys, ids, n_ids, S, w, in, fv, t, lane, F2c, d);
+        if (V4) h4_chunk4<OUT>(keys, ids, n_ids, S, w, in, fv4, t4, lane, F2q, d);
+        else h4_chunk<OUT>(keys, ids, n_ids, S, w, in, fv, t, lane, F2c, d);
         t0 += __popc(im);
         if (im != FULL) break;
       }
-      if (!OUT) acc += fv * t;
+      if (!OUT) {
+        if (V4) fma4(acc4, fv4, t4);
+        else acc += fv * t;
+      }
       if (R.cur_ok && lane == 0) cur[ij] = (int)(t0 - sj);
     }
   }
@@ -410,6 +486,7 @@ __device__ float h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids
     int64_t k_end = 0;    // first global chunk id after item k
     int64_t k_beg = 0;
     float fv = 0.f, t = 0.f;
+    float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4;
     int32_t uk = -1;
     for (;;) {
       int g = 0;
@@ -418,29 +495,37 @@ __device__ float h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids
       // advance to the item holding chunk g (grabs are increasing per warp)
       bool done = false;
       while (g >= k_end) {
-        if (uk >= 0 && !OUT) acc += fv * t;
+        if (uk >= 0 && !OUT) {
+          if (V4) fma4(acc4, fv4, t4);
+          else acc += fv * t;
+        }
         t = 0.f;
+        t4 = make_float4(0.f, 0.f, 0.f, 0.f);
         uk = -1;
         if (k >= nq) { done = true; break; }
         k_beg = k_end;
         k_end += (q_e[k] - q_b[k] + 31) / 32;
         uk = q_i[k];
-        fv = cok ? Fv[(int64_t)uk * d + c] : 0.f;
+        if (V4) fv4 = ld_fv4(uk);
+        else fv = cok ? Fv[(int64_t)uk * d + c] : 0.f;
         ++k;
       }
       if (done) break;
       const int64_t qb = q_b[k - 1], qe = q_e[k - 1];
       const int64_t tt = qb + (g - k_beg) * 32 + lane;
       const int32_t w = tt < qe ? L[tt] : -1;
-      h4_chunk<OUT>(keys, ids, n_ids, S, w, tt < qe, fv, t, lane, F2c, d);
+      if (V4) h4_chunk4<OUT>(keys, ids, n_ids, S, w, tt < qe, fv4, t4, lane, F2q, d);
+      else h4_chunk<OUT>(keys, ids, n_ids, S, w, tt < qe, fv, t, lane, F2c, d);
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) { *q_n = 0; *grab = 0; }
   __syncthreads();
-  return acc;
+  if (!V4) acc4.x = acc;
+  return acc4;
 }
 
+template <bool V4>
 __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
   extern __shared__ int h4[];
   int* keys = h4;
@@ -477,7 +562,7 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
     for (int c0 = 0; c0 < d; c0 += 32) {
       const int c = c0 + lane;
       const bool cok = c < d;
-      float acc = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (cur_ok) {
         for (int i = threadIdx.x; i < deg_out; i += DHN_THREADS) cur_out[i] = 0;
         for (int i = threadIdx.x; i < deg_in; i += DHN_THREADS) cur_in[i] = 0;
@@ -492,11 +577,15 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
         }
         // (1) S1(w) += f1(v) over out-wedges n -> v -> w of this partition
         R.deg = deg_out;
-        h4_sweep<true>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c, cok);
+        h4_sweep<true, V4>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c, cok);
         H4_T(1);
         // (3) acc += f3(p) (.) G(w) over in-wedges w -> p -> n of this partition
         R.deg = deg_in;
-        acc += h4_sweep<false>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b, q_e, &q_n, &grab, c, cok);
+        {
+          const float4 r4 = h4_sweep<false, V4>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b, q_e,
+                                                &q_n, &grab, c, cok);
+          acc.x += r4.x; acc.y += r4.y; acc.z += r4.z; acc.w += r4.w;
+        }
         H4_T(3);
         // (4) clear the table for the next partition / root
         for (int i = threadIdx.x; i < n_ids * 8; i += DHN_THREADS)   // dense prefix, float4
@@ -507,7 +596,18 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
         __syncthreads();
         H4_T(4);
       }
-      s_red[warp * 32 + lane] = acc;
+      if (V4) {
+        // sum the four hit slots (lanes cq, cq + 8, cq + 16, cq + 24), then lane cq < 8 holds
+        // channels 4 cq .. 4 cq + 3
+#pragma unroll
+        for (int m = 8; m < 32; m <<= 1) {
+          acc.x += __shfl_xor_sync(FULL, acc.x, m); acc.y += __shfl_xor_sync(FULL, acc.y, m);
+          acc.z += __shfl_xor_sync(FULL, acc.z, m); acc.w += __shfl_xor_sync(FULL, acc.w, m);
+        }
+        if (lane < 8) *reinterpret_cast<float4*>(&s_red[warp * 32 + 4 * lane]) = acc;
+      } else {
+        s_red[warp * 32 + lane] = acc.x;
+      }
       __syncthreads();
       if (warp == 0) {
         float s = 0.f;
@@ -729,9 +829,13 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     a.slab = reinterpret_cast<float*>(b.cta);
     const size_t smem = 2 * H4_CAP * sizeof(int) + (size_t)DHN_WARPS * 32 * sizeof(float) +
                         2 * H4_DEG_CAP * sizeof(int) + H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
-    RNN_CUDA(cudaFuncSetAttribute(dhn4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    dhn4_kernel<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
+    // four hits per instruction (float4 per lane) when rows are whole float4s
+    static const bool scalar = getenv("RNN_DHN_SCALAR") != nullptr;
+    const bool v4 = !scalar && P.d % 4 == 0 && aligned16(a.F1) && aligned16(a.F2) &&
+                    aligned16(a.F3) && aligned16(a.slab);
+    auto kern = v4 ? dhn4_kernel<true> : dhn4_kernel<false>;
+    RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
   }
   RNN_LAUNCH_CHECK();
   return RNN_OK;
