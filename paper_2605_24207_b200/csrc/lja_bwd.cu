@@ -724,7 +724,7 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
       p1.AD = Lw.AD; p1.dq = d_dst; p1.ld_dq = q->dst.ld;
       RSCtx c1{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
                idx->n_work, Lw.part_fwd, qi.pstride, Lw.cnt_fwd, 1};
-      RNN_TRY((launch_st<SmBwd1Pol, 2, 3>(p1, c1, st)));
+      RNN_TRY(launch_st_var(p1, c1, st, 1));
       if (d_src || d_src_key) {
         SmBwd2Pol p2;
         p2.a = p1.a;
@@ -732,7 +732,7 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
         p2.dv = d_src; p2.ld_dv = q->src.ld; p2.dk = d_src_key; p2.ld_dk = q->src_key.ld;
         RSCtx c2{idx->src_seg, idx->src_ptr, idx->n_src_rows, idx->n_join_rows,
                  idx->src_work_ptr, idx->n_src_work, Lw.part_src, 2 * ld4, Lw.cnt_src, 1};
-        RNN_TRY((launch_st<SmBwd2Pol, 4, 3>(p2, c2, st)));
+        RNN_TRY(launch_st_var(p2, c2, st, 2));
       }
       return RNN_OK;
     }

@@ -479,7 +479,7 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
     pol.out = out; pol.ld_out = ld_out; pol.beta = beta; pol.lse = lse;
     RSCtx rx{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
              idx->n_work, cx.partial, cx.pstride, cx.counter, 1};
-    return launch_st<SmFwdPol, 4, 3>(pol, rx, st);
+    return launch_st_var(pol, rx, st, 0);
   }
   if (q->agg == RNN_AGG_SOFTMAX) {
     switch (qi.D / 4) {

@@ -122,6 +122,30 @@ rnn_status launch_st(const Pol& pol, RSCtx cx, cudaStream_t st) {
   return RNN_OK;
 }
 
+// (rows in flight U, min CTAs per SM) of the three softmax walkers; RNN_ST_VAR="fU,fB,aU,aB,bU,bB"
+// selects another instantiated variant (measurement only)
+struct StVar { int u[3], b[3]; };
+inline StVar st_var() {
+  static StVar v = [] {
+    StVar r{{4, 1, 2}, {3, 4, 4}};   // measured best on MAG (profiles/r01/st_var)
+    if (const char* e = getenv("RNN_ST_VAR"))
+      sscanf(e, "%d,%d,%d,%d,%d,%d", &r.u[0], &r.b[0], &r.u[1], &r.b[1], &r.u[2], &r.b[2]);
+    return r;
+  }();
+  return v;
+}
+template <class Pol>
+rnn_status launch_st_var(const Pol& pol, RSCtx cx, cudaStream_t st, int which) {
+  const StVar v = st_var();
+  const int U = v.u[which], B = v.b[which];
+  if (U == 2 && B == 3) return launch_st<Pol, 2, 3>(pol, cx, st);
+  if (U == 6 && B == 2) return launch_st<Pol, 6, 2>(pol, cx, st);
+  if (U == 1 && B == 4) return launch_st<Pol, 1, 4>(pol, cx, st);
+  if (U == 2 && B == 4) return launch_st<Pol, 2, 4>(pol, cx, st);
+  if (U == 3 && B == 4) return launch_st<Pol, 3, 4>(pol, cx, st);
+  return launch_st<Pol, 4, 3>(pol, cx, st);
+}
+
 // ------------------------------------------------------------------------------------------
 // softmax-weighted aggregate over 128-float rows (lane = float4 column, LH lanes per head)
 // ------------------------------------------------------------------------------------------
