@@ -240,8 +240,8 @@ __device__ __noinline__ void lean_zero(const LeanOut& o, int64_t g0, int64_t g1)
   for (int64_t g = g0; g < g1; ++g) lean_store<VEC>(o, g, z);
 }
 
-template <class MP, int VEC, int U>
-__global__ void __launch_bounds__(256) lean_kernel(MP mp, RSCtx cx, LeanOut o) {
+template <class MP, int VEC, int U, int MINB = 0>
+__global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOut o) {
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (item >= cx.n_work) return;
   const int lane = lane_id();
@@ -311,12 +311,32 @@ __global__ void __launch_bounds__(256) lean_kernel(MP mp, RSCtx cx, LeanOut o) {
   if (cx.zero_empty && item == cx.n_work - 1) lean_zero<VEC>(o, cx.seg[cx.E - 1] + 1, cx.n_seg);
 }
 
+// (rows in flight, min CTAs per SM) of the VEC = 1 lean kernel; RNN_LEAN_VAR="U,B" selects
+// another instantiated variant (measurement only)
+inline void lean_var(int* u, int* b) {
+  static int v[2] = {4, 4};   // measured best on arxiv and hyper (profiles/r01/lean_var)
+  static bool init = false;
+  if (!init) {
+    if (const char* e = getenv("RNN_LEAN_VAR")) sscanf(e, "%d,%d", &v[0], &v[1]);
+    init = true;
+  }
+  *u = v[0];
+  *b = v[1];
+}
+
 template <class MP, int VEC>
 rnn_status launch_lean(const MP& mp, RSCtx cx, const LeanOut& o, cudaStream_t st) {
   if (cx.n_work <= 0) return RNN_OK;
   constexpr int U = VEC == 1 ? 8 : (VEC == 2 ? 4 : 2);
   RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * cx.n_work, st));
-  lean_kernel<MP, VEC, U><<<(unsigned)ceil_div(cx.n_work, 8), 256, 0, st>>>(mp, cx, o);
+  const unsigned grid = (unsigned)ceil_div(cx.n_work, 8);
+  int vu = U, vb = 1;
+  if (VEC == 1) lean_var(&vu, &vb);
+  if (VEC == 1 && vu == 8 && vb == 4) lean_kernel<MP, VEC, 8, 4><<<grid, 256, 0, st>>>(mp, cx, o);
+  else if (VEC == 1 && vu == 4 && vb == 4) lean_kernel<MP, VEC, 4, 4><<<grid, 256, 0, st>>>(mp, cx, o);
+  else if (VEC == 1 && vu == 8 && vb == 3) lean_kernel<MP, VEC, 8, 3><<<grid, 256, 0, st>>>(mp, cx, o);
+  else if (VEC == 1 && vu == 4 && vb == 6) lean_kernel<MP, VEC, 4, 6><<<grid, 256, 0, st>>>(mp, cx, o);
+  else lean_kernel<MP, VEC, U><<<grid, 256, 0, st>>>(mp, cx, o);
   RNN_LAUNCH_CHECK();
   return RNN_OK;
 }
