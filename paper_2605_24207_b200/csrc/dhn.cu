@@ -231,9 +231,25 @@ __device__ unsigned long long g_dhn4_stats[16];
     }                                                                               \
   } while (0)
 
-constexpr int H4_CAP = 16384;                // key slots in shared memory (64 KB)
-constexpr int H4_PART = 8192;                // target distinct w per partition (load <= 0.5)
-constexpr int H4_DEG_CAP = 8192;             // neighbours with smem cursors (per side)
+// C4 CTA shape (compile-time; -D overrides for measurement builds)
+#ifndef H4_THREADS_CFG
+#define H4_THREADS_CFG 1024
+#endif
+#ifndef H4_CTAS_CFG
+#define H4_CTAS_CFG 1
+#endif
+#ifndef H4_CAP_CFG
+#define H4_CAP_CFG 16384
+#endif
+#ifndef H4_DEG_CAP_CFG
+#define H4_DEG_CAP_CFG 8192
+#endif
+constexpr int H4_THREADS = H4_THREADS_CFG;   // threads per C4 CTA (one root at a time)
+constexpr int H4_WARPS = H4_THREADS / 32;
+constexpr int H4_CTAS = H4_CTAS_CFG;         // C4 CTAs per SM
+constexpr int H4_CAP = H4_CAP_CFG;           // key slots in shared memory
+constexpr int H4_PART = H4_CAP / 2;          // target distinct w per partition (load <= 0.5)
+constexpr int H4_DEG_CAP = H4_DEG_CAP_CFG;   // neighbours with smem cursors (per side)
 constexpr int H4_HBITS = 16;                 // hash bits the lists are sorted by
 
 __device__ __forceinline__ uint32_t h4_top(int32_t w) {   // sort key / partition source
@@ -526,13 +542,13 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
 }
 
 template <bool V4>
-__global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
+__global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
   extern __shared__ int h4[];
   int* keys = h4;
   int* ids = h4 + H4_CAP;                                  // compact id of each slot
   float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;  // [H4_CAP][32] by compact id
-  float* s_red = reinterpret_cast<float*>(ids + H4_CAP);   // [DHN_WARPS][32]
-  int* cur_out = reinterpret_cast<int*>(s_red + DHN_WARPS * 32);   // [H4_DEG_CAP]
+  float* s_red = reinterpret_cast<float*>(ids + H4_CAP);   // [H4_WARPS][32]
+  int* cur_out = reinterpret_cast<int*>(s_red + H4_WARPS * 32);   // [H4_DEG_CAP]
   int* cur_in = cur_out + H4_DEG_CAP;                               // [H4_DEG_CAP]
   int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
   int64_t* q_e = q_b + H4_LONG_MAX;
@@ -540,7 +556,7 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
   __shared__ int s_root, q_n, n_ids, grab;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = a.d;
-  for (int i = threadIdx.x; i < H4_CAP; i += DHN_THREADS) { keys[i] = -1; ids[i] = -1; }
+  for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
   if (threadIdx.x == 0) { q_n = 0; n_ids = 0; grab = 0; }
   long long t_last = clock64();
   for (;;) {
@@ -564,8 +580,8 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
       const bool cok = c < d;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       if (cur_ok) {
-        for (int i = threadIdx.x; i < deg_out; i += DHN_THREADS) cur_out[i] = 0;
-        for (int i = threadIdx.x; i < deg_in; i += DHN_THREADS) cur_in[i] = 0;
+        for (int i = threadIdx.x; i < deg_out; i += H4_THREADS) cur_out[i] = 0;
+        for (int i = threadIdx.x; i < deg_in; i += H4_THREADS) cur_in[i] = 0;
       }
       __syncthreads();
       H4_T(0);
@@ -588,9 +604,9 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
         }
         H4_T(3);
         // (4) clear the table for the next partition / root
-        for (int i = threadIdx.x; i < n_ids * 8; i += DHN_THREADS)   // dense prefix, float4
+        for (int i = threadIdx.x; i < n_ids * 8; i += H4_THREADS)   // dense prefix, float4
           __stcg(reinterpret_cast<float4*>(S) + i, make_float4(0.f, 0.f, 0.f, 0.f));
-        for (int i = threadIdx.x; i < H4_CAP; i += DHN_THREADS) { keys[i] = -1; ids[i] = -1; }
+        for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
         __syncthreads();
         if (threadIdx.x == 0) n_ids = 0;
         __syncthreads();
@@ -611,7 +627,7 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn4_kernel(DhnArgs a) {
       __syncthreads();
       if (warp == 0) {
         float s = 0.f;
-        for (int w = 0; w < DHN_WARPS; ++w) s += s_red[w * 32 + lane];
+        for (int w = 0; w < H4_WARPS; ++w) s += s_red[w * 32 + lane];
         if (cok) dhn_store(a, n, c, s);
       }
       __syncthreads();
@@ -759,7 +775,8 @@ Plan make_plan(const rnn_join_index* adj, int k, int d) {
   Plan P;
   P.k = k; P.d = d;
   P.G = adj->n_groups; P.E = adj->n_join_rows; P.R = adj->n_src_rows;
-  P.n_cta = (int)std::min<int64_t>((int64_t)num_sms() * DHN_CTAS_PER_SM, std::max<int64_t>(P.G, 1));
+  P.n_cta = (int)std::min<int64_t>((int64_t)num_sms() * (k == 4 ? H4_CTAS : DHN_CTAS_PER_SM),
+                                    std::max<int64_t>(P.G, 1));
   // k = 3: per-CTA global mark array for roots whose in-degree exceeds the smem hash set;
   // k = 4: per-CTA value slab of the S1 hash table (H4_CAP x 32 floats, zero between roots)
   P.per_cta = k == 3 ? ((size_t)P.G * sizeof(int32_t) + 255) & ~size_t(255)
@@ -823,11 +840,11 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     auto kern = dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2> : dpl == 3 ? dhn3_kernel<3>
                                                                                   : dhn3_kernel<4>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
+    kern<<<P.n_cta, H4_THREADS, smem, st>>>(a);
   } else {
     a.wout = b.wout; a.nbrh = b.nbrh; a.sgh = b.sgh;
     a.slab = reinterpret_cast<float*>(b.cta);
-    const size_t smem = 2 * H4_CAP * sizeof(int) + (size_t)DHN_WARPS * 32 * sizeof(float) +
+    const size_t smem = 2 * H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                         2 * H4_DEG_CAP * sizeof(int) + H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
     // four hits per instruction (float4 per lane) when rows are whole float4s
     static const bool scalar = getenv("RNN_DHN_SCALAR") != nullptr;
@@ -835,7 +852,7 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
                     aligned16(a.F3) && aligned16(a.slab);
     auto kern = v4 ? dhn4_kernel<true> : dhn4_kernel<false>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
+    kern<<<P.n_cta, H4_THREADS, smem, st>>>(a);
   }
   RNN_LAUNCH_CHECK();
   return RNN_OK;

@@ -28,7 +28,8 @@ namespace {
 
 constexpr int BM = 128;   // UMMA_M (cta_group::1): accumulator row i <-> TMEM lane i
 constexpr int BK = 32;    // fp32 elements per 128-byte swizzle row
-constexpr int THREADS = 192;
+constexpr int THREADS = 320;    // tile GEMM: producer, MMA, 8 converter warps (2-9; 2-5 epilogue)
+constexpr int CONV_THREADS = 256;
 constexpr int MAX_STAGES = 8;
 
 struct GemmParams {
@@ -165,17 +166,18 @@ __device__ __forceinline__ float4 lo_part(float4 v) {
   l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
   return l;
 }
-// 128 threads; 8 shared-memory loads in flight per thread (the converter was latency-bound)
+// NT threads; 8 shared-memory loads in flight per thread (the converter was latency-bound)
+template <int NT = 128>
 __device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n16, int t) {
   uint32_t i = t;
-  for (; i + 7 * 128 < n16; i += 8 * 128) {
+  for (; i + 7 * NT < n16; i += 8 * NT) {
     float4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = x[i + u * 128];
+    for (int u = 0; u < 8; ++u) v[u] = x[i + u * NT];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) lo[i + u * 128] = lo_part(v[u]);
+    for (int u = 0; u < 8; ++u) lo[i + u * NT] = lo_part(v[u]);
   }
-  for (; i < n16; i += 128) lo[i] = lo_part(x[i]);
+  for (; i < n16; i += NT) lo[i] = lo_part(x[i]);
 }
 
 // per-role wait cycles of tc_gemm_kernel (internal hook rnn_internal_gemm_stats): [0] producer
@@ -218,7 +220,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int s = 0; s < MAX_STAGES; ++s) {
         mbar_init(&full[s], 1);
         mbar_init(&empty[s], 1);
-        mbar_init(&conv[s], 128);
+        mbar_init(&conv[s], CONV_THREADS);
       }
       mbar_init(acc_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -319,8 +321,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (!SPLIT3) { atomicAdd(&g_gemm_stats[3], gs_w[3]); atomicAdd(&g_gemm_stats[4], gs_w[4]); }
     }
   } else {
-    // ---------------- converters (3xTF32) + epilogue: warps 2..5 ----------------
-    const int et = threadIdx.x - 64;  // 0..127
+    // ---------------- converters (3xTF32): warps 2..9; epilogue: warps 2..5 ----------------
+    const int et = threadIdx.x - 64;  // 0..255
     if (SPLIT3) {
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % p.stages;
@@ -334,10 +336,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           gs_w[4] += 1;
         }
         // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
-        lo_tile(reinterpret_cast<const float4*>(a_hi(s)), reinterpret_cast<float4*>(a_lo(s)),
-                A_BYTES / 16, et);
-        lo_tile(reinterpret_cast<const float4*>(b_hi(s)), reinterpret_cast<float4*>(b_lo(s)),
-                B_BYTES / 16, et);
+        lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(a_hi(s)),
+                              reinterpret_cast<float4*>(a_lo(s)), A_BYTES / 16, et);
+        lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(b_hi(s)),
+                              reinterpret_cast<float4*>(b_lo(s)), B_BYTES / 16, et);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[s]);
       }
@@ -346,12 +348,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       atomicAdd(&g_gemm_stats[10], (unsigned long long)(clock64() - gs_t0));
       for (int i = 2; i < 5; ++i) atomicAdd(&g_gemm_stats[i], gs_w[i]);
     }
-    mbar_wait(acc_full, 0);
+    if (warp < 6) mbar_wait(acc_full, 0);   // warps 6-9 only convert
     tc_fence_after();
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) belong to this warp
     const int64_t row = m0 + quad * 32 + lane;
     const bool row_ok = row < p.M;
-    for (int c0 = 0; c0 < p.BN; c0 += 16) {
+    for (int c0 = 0; c0 < (warp < 6 ? p.BN : 0); c0 += 16) {
       uint32_t r[16];
       tc_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, r);
       if (!row_ok) continue;
@@ -1177,16 +1179,24 @@ extern "C" rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t 
 
 namespace {
 struct BwdWs {
-  float* Wt; float* part; float* part2; float* cpart;
+  float* Wt; float* dWt; float* part; float* part2; float* cpart;
   size_t bytes;
   int splits; int64_t chunks;
 };
+// dW for a wide dY (N > 128) and K <= 128 is computed transposed, dW^T = X^T dY: one 128-row
+// MMA tile over k and N = 256 columns of n per MMA, so X is re-read ceil(N / 256) times instead
+// of ceil(N / 128) and the shared-memory reads per loaded byte drop (the 3xTF32 tile GEMM is
+// bound by shared-memory traffic); the ordered reduce writes dW^T, a small transpose gives dW.
+inline bool dw_swapped(int K, int N) { return N > 128 && K <= 128 && !getenv("RNN_NO_DWT"); }
+
 BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
   BwdWs w{};
   Carve c(base);
   const int64_t ldt = (N + 3) / 4 * 4;
   w.Wt = c.take<float>((size_t)K * ldt);
-  const int64_t tiles = ceil_div(N, BM) * ceil_div(K, 256);
+  w.dWt = c.take<float>((size_t)K * N);
+  const int64_t tiles = dw_swapped(K, N) ? ceil_div(K, BM) * ceil_div(N, 256)
+                                         : ceil_div(N, BM) * ceil_div(K, 256);
   int64_t splits = ceil_div(M, 8 * BK);
   const int64_t cap = (148 + tiles - 1) / tiles;   // about one wave of CTAs
   if (splits > cap) splits = cap;
@@ -1235,6 +1245,36 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
   // dW = dY^T X : both operands MN-major, split over M, ordered reduction
   if (M == 0) {
     RNN_CUDA(cudaMemsetAsync(dW, 0, sizeof(float) * (size_t)N * K, st));
+  } else if (dw_swapped(K, N)) {
+    // dW^T [K, N] = X^T dY: A = X (MN-major, M = k), B = dY (MN-major, N = n, 256 per tile)
+    GemmParams p{};
+    p.M = K; p.N = N;
+    p.BN = N <= 256 ? (int)((N + 31) / 32 * 32) : 256;
+    p.Kred = M;
+    p.k_split = ceil_div(ceil_div(M, w.splits), BK) * BK;
+    const int splits = (int)ceil_div(M, p.k_split);
+    p.mode = 1; p.partial = w.part; p.ldp = N; p.part_stride = (int64_t)N * K;
+    CUtensorMap ta, tb;
+    p.a3d = map3_ok(X, K, ldx);
+    p.b3d = map3_ok(dY, N, lddy);
+    if (p.a3d) RNN_TRY(make_map3(&ta, X, K, M, ldx, 16, BM / 32));
+    else RNN_TRY(make_map(&ta, X, K, M, ldx, 32, 16, true));
+    if (p.b3d) RNN_TRY(make_map3(&tb, dY, N, M, lddy, 16, (uint32_t)(p.BN / 32)));
+    else RNN_TRY(make_map(&tb, dY, N, M, lddy, 32, 16, true));
+    RNN_TRY((gemm<true, true>(ta, tb, p, splits, prec, st)));
+    const int64_t nk = (int64_t)N * K;
+    if (nk % 4 == 0) {
+      const int64_t groups = ceil_div(splits, 8);
+      splitk_stage<<<dim3((unsigned)ceil_div(nk / 4, 128), (unsigned)groups), 128, 0, st>>>(
+          w.part, splits, p.part_stride, nk, w.part2);
+      splitk_final<<<(unsigned)ceil_div(nk / 4, 128), 128, 0, st>>>(w.part2, groups, nk, w.dWt);
+    } else
+      splitk_reduce1<<<(unsigned)ceil_div(nk, 128), 128, 0, st>>>(w.part, splits, p.part_stride,
+                                                                  nk, w.dWt);
+    RNN_LAUNCH_CHECK();
+    // dW [N, K] = (dW^T [K, N])^T
+    transpose_kernel<<<(unsigned)ceil_div(nk, 256), 256, 0, st>>>(w.dWt, K, N, N, dW, K);
+    RNN_LAUNCH_CHECK();
   } else {
     GemmParams p{};
     p.M = N; p.N = K;

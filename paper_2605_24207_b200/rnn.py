@@ -13,7 +13,9 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librnn.so")
+# RNN_LIB: an alternative in-tree build of the same library (measurement variants built by
+# profiles/build_variant.py); default the package's librnn.so
+LIB_PATH = os.environ.get("RNN_LIB") or os.path.join(_HERE, "librnn.so")
 
 # enums (include/rnn.h)
 RNN_OK = 0
