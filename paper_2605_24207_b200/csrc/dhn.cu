@@ -840,7 +840,7 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     auto kern = dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2> : dpl == 3 ? dhn3_kernel<3>
                                                                                   : dhn3_kernel<4>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<P.n_cta, H4_THREADS, smem, st>>>(a);
+    kern<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
   } else {
     a.wout = b.wout; a.nbrh = b.nbrh; a.sgh = b.sgh;
     a.slab = reinterpret_cast<float*>(b.cta);
