@@ -265,6 +265,21 @@ rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rnn_operand* 
                        const float* d_out, int64_t ld_dout, float* const* d_f, int64_t ld_df,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Saved walk sum (reverse-mode reuse of the forward): rnn_dhn_fwd_save also writes
+ * walk_sum [n_groups, ld_ws] (group order) = sum over closed walks of prod_{i>=1} f_i, i.e.
+ * C_k before the root factor f0; rnn_dhn_bwd_saved then forms d f0 = dOut (.) walk_sum
+ * elementwise instead of a k-th walk launch (d f0 is linear in the walk sum, PAPER.md:943-946;
+ * the other d f_j are computed as in rnn_dhn_bwd).  Same arguments, layouts and errors as
+ * rnn_dhn_fwd / rnn_dhn_bwd; walk_sum is caller-owned device memory, NULL is an error when
+ * n_groups > 0, ld_ws >= d. */
+rnn_status rnn_dhn_fwd_save(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                            float* out, int64_t ld_out, float* walk_sum, int64_t ld_ws,
+                            void* workspace, size_t workspace_bytes, void* stream);
+rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                             const float* d_out, int64_t ld_dout, const float* walk_sum,
+                             int64_t ld_ws, float* const* d_f, int64_t ld_df, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 /* ===================================================================================== */
 /* Program helpers                                                                       */
 /* ===================================================================================== */

@@ -53,9 +53,12 @@ struct DhnArgs {
   const int32_t* nbrh;    // k=4: nbr[] with every group's list sorted by hash partition
   const int32_t* sgh;     // k=4: src_group[] with every row's list sorted likewise
   int64_t cta_stride;     // elements between consecutive CTAs' mark
+  float* sum_out;         // optional: the walk sum before the root multiplier [G, ld_sum]
+  int64_t ld_sum;
 };
 
 __device__ __forceinline__ void dhn_store(const DhnArgs& a, int64_t n, int c, float v) {
+  if (a.sum_out) a.sum_out[n * a.ld_sum + c] = v;
   if (a.rm) {
     const int64_t rr = a.rm_by_group ? n : (int64_t)a.row_of[n];
     v *= a.rm[rr * a.ld_rm + c];
@@ -821,8 +824,10 @@ rnn_status check_ops(const rnn_operand* f, int k, int d, int64_t R) {
 // one walk-aggregate launch (k >= 3) with operands W[0..k-2] in group order
 rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const float* const* W,
                 const float* rm, int64_t ld_rm, int rm_by_group, float* out, int64_t ld_out,
-                int out_by_row, int launch_id, cudaStream_t st) {
+                int out_by_row, int launch_id, cudaStream_t st, float* sum_out = nullptr,
+                int64_t ld_sum = 0) {
   DhnArgs a{};
+  a.sum_out = sum_out; a.ld_sum = ld_sum;
   a.G = P.G; a.d = P.d;
   a.gp = adj->group_ptr; a.nbr = b.nbr; a.sp = adj->src_ptr; a.sg = adj->src_group;
   a.row_of = adj->group_dst_row;
@@ -924,15 +929,66 @@ extern "C" rnn_status rnn_dhn_workspace_size(const rnn_join_index* adj, int32_t 
   return RNN_OK;
 }
 
+// d f0 (row of n) = dOut(n) (.) S(n), S = the forward's walk sum (group order)
+static __global__ void dhn_df0_kernel(int64_t G, int d, const int32_t* __restrict__ row_of,
+                               const float* __restrict__ dout, int64_t ld_dout,
+                               const float* __restrict__ S, int64_t ld_s, float* __restrict__ df0,
+                               int64_t ld_df) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= G * d) return;
+  const int64_t n = i / d;
+  const int c = (int)(i % d);
+  df0[(int64_t)row_of[n] * ld_df + c] = dout[n * ld_dout + c] * S[n * ld_s + c];
+}
+
+static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,
+                        int64_t ld_out, float* walk_sum, int64_t ld_ws, void* workspace,
+                        size_t workspace_bytes, void* stream);
+static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                        const float* d_out, int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
+                        float* const* d_f, int64_t ld_df, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
 extern "C" rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                                   float* out, int64_t ld_out, void* workspace,
                                   size_t workspace_bytes, void* stream) {
   clear_error();
+  return dhn_fwd_impl(adj, k, f, out, ld_out, nullptr, 0, workspace, workspace_bytes, stream);
+}
+
+extern "C" rnn_status rnn_dhn_fwd_save(const rnn_join_index* adj, int32_t k,
+                                       const rnn_operand* f, float* out, int64_t ld_out,
+                                       float* walk_sum, int64_t ld_ws, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(walk_sum || !adj || adj->n_groups == 0, RNN_ERR_INVALID_ARGUMENT,
+              "walk_sum is NULL");
+  return dhn_fwd_impl(adj, k, f, out, ld_out, walk_sum, ld_ws, workspace, workspace_bytes,
+                      stream);
+}
+
+extern "C" rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k,
+                                        const rnn_operand* f, const float* d_out,
+                                        int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
+                                        float* const* d_f, int64_t ld_df, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(walk_sum || !adj || adj->n_groups == 0, RNN_ERR_INVALID_ARGUMENT,
+              "walk_sum is NULL");
+  return dhn_bwd_impl(adj, k, f, d_out, ld_dout, walk_sum, ld_ws, d_f, ld_df, workspace,
+                      workspace_bytes, stream);
+}
+
+static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,
+                        int64_t ld_out, float* walk_sum, int64_t ld_ws, void* workspace,
+                        size_t workspace_bytes, void* stream) {
   RNN_TRY(check_adj(adj, k, f ? f[1].dim : 0));
   const int d = f[1].dim;
   RNN_TRY(check_ops(f, k, d, adj->n_src_rows));
   RNN_REQUIRE(out || adj->n_groups == 0, RNN_ERR_INVALID_ARGUMENT, "out is NULL");
   RNN_REQUIRE(ld_out >= d, RNN_ERR_SHAPE_MISMATCH, "ld_out %lld < d %d", (long long)ld_out, d);
+  RNN_REQUIRE(!walk_sum || ld_ws >= d, RNN_ERR_SHAPE_MISMATCH, "ld_ws %lld < d %d",
+              (long long)ld_ws, d);
   Plan P = make_plan(adj, k, d);
   RNN_TRY(ws_check(P, workspace, workspace_bytes, &P.n_cta));
   if (P.G == 0) return RNN_OK;
@@ -943,6 +999,7 @@ extern "C" rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rn
     DhnArgs a{};
     a.G = P.G; a.d = d; a.gp = adj->group_ptr; a.row_of = adj->group_dst_row;
     a.rm = f[0].data; a.ld_rm = f[0].ld; a.rm_by_group = 0; a.out = out; a.ld_out = ld_out;
+    a.sum_out = walk_sum; a.ld_sum = ld_ws;
     dhn2_kernel<<<(unsigned)ceil_div(P.G, 8), 256, 0, st>>>(a, adj->src_row, f[1].data, f[1].ld);
     RNN_LAUNCH_CHECK();
     return RNN_OK;
@@ -950,7 +1007,7 @@ extern "C" rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rn
   for (int i = 1; i < k; ++i)
     RNN_TRY(to_group(P, adj, f[i].data, f[i].ld, nullptr, 0, b.F[i - 1], st));
   const float* W[3] = {b.F[0], b.F[1], b.F[2]};
-  return walk(P, b, adj, W, f[0].data, f[0].ld, 0, out, ld_out, 0, 0, st);
+  return walk(P, b, adj, W, f[0].data, f[0].ld, 0, out, ld_out, 0, 0, st, walk_sum, ld_ws);
 }
 
 extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
@@ -958,12 +1015,21 @@ extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rn
                                   int64_t ld_df, void* workspace, size_t workspace_bytes,
                                   void* stream) {
   clear_error();
+  return dhn_bwd_impl(adj, k, f, d_out, ld_dout, nullptr, 0, d_f, ld_df, workspace,
+                      workspace_bytes, stream);
+}
+
+static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                        const float* d_out, int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
+                        float* const* d_f, int64_t ld_df, void* workspace, size_t workspace_bytes,
+                        void* stream) {
   RNN_TRY(check_adj(adj, k, f ? f[1].dim : 0));
   const int d = f[1].dim;
   RNN_TRY(check_ops(f, k, d, adj->n_src_rows));
   RNN_REQUIRE(d_f, RNN_ERR_INVALID_ARGUMENT, "d_f is NULL");
   RNN_REQUIRE(d_out || adj->n_groups == 0, RNN_ERR_INVALID_ARGUMENT, "d_out is NULL");
   RNN_REQUIRE(ld_dout >= d && ld_df >= d, RNN_ERR_SHAPE_MISMATCH, "ld < d");
+  RNN_REQUIRE(!walk_sum || ld_ws >= d, RNN_ERR_SHAPE_MISMATCH, "ld_ws < d");
   Plan P = make_plan(adj, k, d);
   RNN_TRY(ws_check(P, workspace, workspace_bytes, &P.n_cta));
   cudaStream_t st = as_stream(stream);
@@ -976,8 +1042,15 @@ extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rn
   // g = f0 (.) dOut in group order (slot k-1)
   float* g = b.F[k - 1];
   RNN_TRY(to_group(P, adj, f[0].data, f[0].ld, d_out, ld_dout, g, st));
+  if (d_f[0] && walk_sum) {   // d f0 = dOut (.) the forward's walk sum: no walk needed
+    const int64_t n = P.G * d;
+    dhn_df0_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(P.G, d, adj->group_dst_row, d_out,
+                                                               ld_dout, walk_sum, ld_ws, d_f[0],
+                                                               ld_df);
+    RNN_LAUNCH_CHECK();
+  }
   if (k == 2) {
-    if (d_f[0]) {   // d f0(n) = dOut(n) (.) sum f1
+    if (d_f[0] && !walk_sum) {   // d f0(n) = dOut(n) (.) sum f1
       DhnArgs a{};
       a.G = P.G; a.d = d; a.gp = adj->group_ptr; a.row_of = adj->group_dst_row;
       a.rm = d_out; a.ld_rm = ld_dout; a.rm_by_group = 1; a.out = d_f[0]; a.ld_out = ld_df;
@@ -997,7 +1070,7 @@ extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rn
   // operand sequence around the cycle: position 0 = g, positions 1..k-1 = f_i
   const float* cyc[4] = {g, b.F[0], b.F[1], b.F[2]};
   int launch = 0;
-  if (d_f[0]) {
+  if (d_f[0] && !walk_sum) {
     const float* W[3] = {cyc[1], cyc[2], cyc[3]};
     RNN_TRY(walk(P, b, adj, W, d_out, ld_dout, 1, d_f[0], ld_df, 1, launch++, st));
   }

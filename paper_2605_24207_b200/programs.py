@@ -437,6 +437,9 @@ class DHNProgram(_Program):
         G = self.idx.n_groups
         self.out = _empty(G, len(self.ks) * d, dev)
         self.d_out = _dev_f32(rng.standard_normal((G, len(self.ks) * d)).astype(np.float32), dev)
+        # each pattern's walk sum before the root factor, saved by the forward so the backward
+        # forms d f0 = dOut (.) sum without a walk (rnn_dhn_fwd_save / rnn_dhn_bwd_saved)
+        self.walk_sum = {k: _empty(G, d, dev) for k in self.ks}
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
         self.pos0 = {}
@@ -480,9 +483,11 @@ class DHNProgram(_Program):
             walks3 = self._walks(3)
             self._flops = {"dhn2_fwd": E * d, "dhn3_fwd": 2 * d * walks3,
                            "dhn4_fwd": d * (3 * two_paths + E)}
-            self._flops["dhn2_bwd"] = 2 * self._flops["dhn2_fwd"]
-            self._flops["dhn3_bwd"] = 3 * self._flops["dhn3_fwd"]
-            self._flops["dhn4_bwd"] = 4 * self._flops["dhn4_fwd"]
+            # backward: one walk per rotated operand f1 .. f_{k-1}; d f0 = dOut (.) the saved
+            # walk sum (elementwise, not counted)
+            self._flops["dhn2_bwd"] = self._flops["dhn2_fwd"]
+            self._flops["dhn3_bwd"] = 2 * self._flops["dhn3_fwd"]
+            self._flops["dhn4_bwd"] = 3 * self._flops["dhn4_fwd"]
         return {k: {"bound": "alu", "amount": v} for k, v in self._flops.items()
                 if int(k[3]) in self.ks}
 
@@ -498,7 +503,7 @@ class DHNProgram(_Program):
         for j, k in enumerate(self.ks):
             self._t(f"dhn{k}_fwd")
             rnn.dhn_fwd(self.idx, k, self._f(k, self.Y), out=self.out[:, j * self.d:(j + 1) * self.d],
-                        ws=self.ws)
+                        ws=self.ws, walk_sum=self.walk_sum[k])
             self._t(f"dhn{k}_fwd_end")
         return self.out
 
@@ -506,7 +511,7 @@ class DHNProgram(_Program):
         for j, k in enumerate(self.ks):
             self._t(f"dhn{k}_bwd")
             rnn.dhn_bwd(self.idx, k, self._f(k, self.Y), self.d_out[:, j * self.d:(j + 1) * self.d],
-                        d_f=self._f(k, self.dY), ws=self.ws)
+                        d_f=self._f(k, self.dY), ws=self.ws, walk_sum=self.walk_sum[k])
             self._t(f"dhn{k}_bwd_end")
         self._t("proj_bwd")
         rnn.project_bwd(self.H, self.W, self.dY, want_dx=True, prec=self.prec, ws=self.ws_p,

@@ -90,11 +90,16 @@ def lib():
         L.rnn_accumulate.restype = C.c_int
         L.rnn_dhn_workspace_size.argtypes = [C.POINTER(JoinIndexC), i32, i32, C.POINTER(sz)]
         L.rnn_dhn_fwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64, vp, sz, vp]
+        L.rnn_dhn_fwd_save.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
+                                       vp, i64, vp, sz, vp]
+        L.rnn_dhn_bwd_saved.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
+                                        vp, i64, C.POINTER(vp), i64, vp, sz, vp]
         L.rnn_dhn_bwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
                                   C.POINTER(vp), i64, vp, sz, vp]
         L.rnn_gcn_norm_src_deg.argtypes = [C.POINTER(JoinIndexC), vp, vp, vp]
         L.rnn_group_sizes.argtypes = [C.POINTER(JoinIndexC), vp, vp]
-        for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd", "rnn_gcn_norm_src_deg",
+        for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd", "rnn_dhn_fwd_save",
+                  "rnn_dhn_bwd_saved", "rnn_gcn_norm_src_deg",
                   "rnn_group_sizes"):
             getattr(L, f).restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
@@ -421,9 +426,10 @@ def _dhn_ops(f):
     return ops
 
 
-def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None):
+def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None, walk_sum=None):
     """C_k per root (group order) of the closed-walk rule; f = [f0 (or None), f1, ..., f_{k-1}]
-    by node row (rnn_dhn_fwd)."""
+    by node row (rnn_dhn_fwd).  walk_sum [n_groups, >= d]: also save the walk sum before the
+    root factor for dhn_bwd (rnn_dhn_fwd_save)."""
     assert len(f) == k
     dev = adj.group_ptr.device
     d = f[1].shape[1]
@@ -431,13 +437,20 @@ def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None):
         out = torch.empty(max(adj.n_groups, 1), (d + 3) // 4 * 4, dtype=torch.float32, device=dev)[:adj.n_groups, :d]
     nb = dhn_workspace_size(adj, k, d)
     w = ws.get(nb) if ws is not None else _ws(nb, dev)
+    if walk_sum is not None:
+        _check(lib().rnn_dhn_fwd_save(C.byref(adj.c), k, _dhn_ops(f), _ptr(out), out.stride(0),
+                                      _ptr(walk_sum), walk_sum.stride(0), _ptr(w), w.numel(),
+                                      _stream(stream)))
+        return out
     _check(lib().rnn_dhn_fwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(out), out.stride(0), _ptr(w),
                              w.numel(), _stream(stream)))
     return out
 
 
-def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=None):
-    """[d f0, ..., d f_{k-1}] by node row (rnn_dhn_bwd); want[i] False -> None."""
+def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=None,
+            walk_sum=None):
+    """[d f0, ..., d f_{k-1}] by node row (rnn_dhn_bwd); want[i] False -> None.  walk_sum: the
+    forward's saved walk sum (d f0 without a walk launch, rnn_dhn_bwd_saved)."""
     dev = adj.group_ptr.device
     d = f[1].shape[1]
     n = adj.n_src_rows
@@ -452,6 +465,11 @@ def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=No
     ptrs = (C.c_void_p * k)(*[None if t is None else t.data_ptr() for t in d_f])
     nb = dhn_workspace_size(adj, k, d)
     w = ws.get(nb) if ws is not None else _ws(nb, dev)
+    if walk_sum is not None:
+        _check(lib().rnn_dhn_bwd_saved(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out),
+                                       d_out.stride(0), _ptr(walk_sum), walk_sum.stride(0), ptrs,
+                                       ld, _ptr(w), w.numel(), _stream(stream)))
+        return d_f
     _check(lib().rnn_dhn_bwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out), d_out.stride(0), ptrs,
                              ld, _ptr(w), w.numel(), _stream(stream)))
     return d_f

@@ -79,6 +79,16 @@ def run_case(rnn, keys, e_n, e_v, k, d, seed, dense=False, f0_none=False, bwd=Tr
     ref_g = oracle.dhn_bwd(k, oi, keys, f, d_out[rows])
     for i in range(k):
         assert_close(np_(grads[i]), ref_g[i], FP32_TOL, f"C{k} d f{i}")
+    # saved walk sum (rnn_dhn_fwd_save / rnn_dhn_bwd_saved): the sum is C_k with f0 = 1, and
+    # d f0 = dOut (.) sum replaces the f0 walk
+    ws = torch.full((max(gi.n_groups, 1), d + 5), float("nan"), device="cuda")[: gi.n_groups, :d]
+    out2 = np_(rnn.dhn_fwd(gi, k, fg, walk_sum=ws))
+    assert_close(out2[rows], ref, FP32_TOL, f"C{k} fwd (save)")
+    ones = [np.ones((n, d), np.float32)] + f[1:]
+    assert_close(np_(ws)[rows], oracle.dhn_fwd(k, oi, keys, ones), FP32_TOL, f"C{k} walk sum")
+    grads2 = rnn.dhn_bwd(gi, k, fg, cu(d_out), walk_sum=ws)
+    for i in range(k):
+        assert_close(np_(grads2[i]), ref_g[i], FP32_TOL, f"C{k} d f{i} (saved)")
 
 
 @pytest.mark.parametrize("k", [2, 3, 4])
