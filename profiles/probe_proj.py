@@ -13,7 +13,7 @@ from paper_2605_24207_b200 import rnn  # noqa: E402
 L = rnn.lib()
 names = ["producer waits slot", "MMA waits W", "MMA waits accum", "MMA waits stage",
          "converter waits stage", "epilogue waits accum"]
-for (M, K, N) in [(169343, 128, 128), (1000000, 128, 128), (1134649, 128, 512)]:
+for (M, K, N) in [(169343, 128, 128), (1000000, 128, 128), (1134649, 128, 512), (736389, 128, 768)]:
     X = torch.randn(M, K, device="cuda"); W = torch.randn(N, K, device="cuda")
     Y = torch.empty(M, N, device="cuda")
     for prec in ("3xtf32", "tf32"):
