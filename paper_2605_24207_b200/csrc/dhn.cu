@@ -55,6 +55,8 @@ struct DhnArgs {
   int64_t cta_stride;     // elements between consecutive CTAs' mark
   float* sum_out;         // optional: the walk sum before the root multiplier [G, ld_sum]
   int64_t ld_sum;
+  const float* F2b;       // k=4, optional second middle operand (symmetric Edge, see walk2)
+  float* out_b;           // its result (same layout as out, no root multiplier)
 };
 
 __device__ __forceinline__ void dhn_store(const DhnArgs& a, int64_t n, int c, float v) {
@@ -345,10 +347,11 @@ __device__ __forceinline__ int h4_take4(unsigned& bal, int sub) {
   }
   return mine;
 }
-template <bool OUT>
+template <bool OUT, bool DUAL = false>
 __device__ __forceinline__ void h4_chunk4(int* keys, int* ids, int* n_ids, float* S, int32_t w,
                                           bool in, float4 fv4, float4& t4, int lane,
-                                          const float* F2q, int d) {
+                                          const float* F2q, int d, float4* t4b = nullptr,
+                                          const float* F2bq = nullptr) {
   const int sub = lane >> 3, cq = lane & 7;
   if (OUT) {
     const int sl = (in && w >= 0) ? h4_insert(keys, ids, n_ids, w) : -1;
@@ -366,7 +369,7 @@ __device__ __forceinline__ void h4_chunk4(int* keys, int* ids, int* n_ids, float
     if (sl >= 0) sl = ids[sl];
     unsigned bal = __ballot_sync(FULL, sl >= 0);
     while (bal) {   // G(w) = f2(w) (.) S1(w) formed on the fly, 8 hits in flight (2 per slot)
-      float4 x[2], y[2];
+      float4 x[2], y[2], yb[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int mine = h4_take4(bal, sub);
@@ -376,6 +379,9 @@ __device__ __forceinline__ void h4_chunk4(int* keys, int* ids, int* n_ids, float
                          : make_float4(0.f, 0.f, 0.f, 0.f);
         y[u] = mine >= 0 ? __ldg(reinterpret_cast<const float4*>(F2q + (int64_t)wq * d))
                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (DUAL)
+          yb[u] = mine >= 0 ? __ldg(reinterpret_cast<const float4*>(F2bq + (int64_t)wq * d))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -383,6 +389,12 @@ __device__ __forceinline__ void h4_chunk4(int* keys, int* ids, int* n_ids, float
         t4.y = fmaf(x[u].y, y[u].y, t4.y);
         t4.z = fmaf(x[u].z, y[u].z, t4.z);
         t4.w = fmaf(x[u].w, y[u].w, t4.w);
+        if (DUAL) {
+          t4b->x = fmaf(x[u].x, yb[u].x, t4b->x);
+          t4b->y = fmaf(x[u].y, yb[u].y, t4b->y);
+          t4b->z = fmaf(x[u].z, yb[u].z, t4b->z);
+          t4b->w = fmaf(x[u].w, yb[u].w, t4b->w);
+        }
       }
     }
   }
@@ -401,10 +413,10 @@ struct H4Root {
 // serves neighbours (one per warp, or 32 per step in chunked mode) and walks their runs of
 // this partition; runs longer than H4_LONG are queued.  Phase B: every queued run is split
 // over all warps.  Returns this thread's contribution to the root's accumulator (IN).
-template <bool OUT, bool V4>
+template <bool OUT, bool V4, bool DUAL = false>
 __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids, int* n_ids,
                           float* S, int* cur, int* q_i, int64_t* q_b, int64_t* q_e, int* q_n,
-                          int* grab, int c, bool cok) {
+                          int* grab, int c, bool cok, float4* acc_b = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* L = OUT ? a.nbrh : a.sgh;
   const float* Fv = OUT ? a.F1 : a.F3;
@@ -414,6 +426,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
   const int cq4 = (c - lane) + 4 * (lane & 7);
   const bool cok4 = cq4 < d;
   const float* F2q = a.F2 + (cok4 ? cq4 : 0);
+  const float* F2bq = DUAL ? a.F2b + (cok4 ? cq4 : 0) : nullptr;   // second middle operand
   float acc = 0.f;
   float4 acc4 = make_float4(0.f, 0.f, 0.f, 0.f);
   auto ld_fv4 = [&](int32_t u) {
@@ -474,7 +487,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         }
       }
       float fv = 0.f, t = 0.f;
-      float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4;
+      float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4, t4b = fv4;
       if (V4) fv4 = ld_fv4(uj);
       else fv = cok ? Fv[(int64_t)uj * d + c] : 0.f;
       int64_t t0 = bj;
@@ -483,7 +496,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         const int32_t w = tt < ej ? L[tt] : -1;
         const bool in = tt < ej && (h4_top(w) >> R.sh) == R.part;
         const unsigned im = __ballot_sync(FULL, in);
-        if (V4) h4_chunk4<OUT>(keys, ids, n_ids, S, w, in, fv4, t4, lane, F2q, d);
+        if (V4) h4_chunk4<OUT, DUAL>(keys, ids, n_ids, S, w, in, fv4, t4, lane, F2q, d, &t4b, F2bq);
         else h4_chunk<OUT>(keys, ids, n_ids, S, w, in, fv, t, lane, F2c, d);
         t0 += __popc(im);
         if (im != FULL) break;
@@ -491,6 +504,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
       if (!OUT) {
         if (V4) fma4(acc4, fv4, t4);
         else acc += fv * t;
+        if (DUAL) fma4(*acc_b, fv4, t4b);
       }
       if (R.cur_ok && lane == 0) cur[ij] = (int)(t0 - sj);
     }
@@ -505,7 +519,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
     int64_t k_end = 0;    // first global chunk id after item k
     int64_t k_beg = 0;
     float fv = 0.f, t = 0.f;
-    float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4;
+    float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4, t4b = fv4;
     int32_t uk = -1;
     for (;;) {
       int g = 0;
@@ -517,9 +531,11 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         if (uk >= 0 && !OUT) {
           if (V4) fma4(acc4, fv4, t4);
           else acc += fv * t;
+          if (DUAL) fma4(*acc_b, fv4, t4b);
         }
         t = 0.f;
         t4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        t4b = t4;
         uk = -1;
         if (k >= nq) { done = true; break; }
         k_beg = k_end;
@@ -533,7 +549,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
       const int64_t qb = q_b[k - 1], qe = q_e[k - 1];
       const int64_t tt = qb + (g - k_beg) * 32 + lane;
       const int32_t w = tt < qe ? L[tt] : -1;
-      if (V4) h4_chunk4<OUT>(keys, ids, n_ids, S, w, tt < qe, fv4, t4, lane, F2q, d);
+      if (V4) h4_chunk4<OUT, DUAL>(keys, ids, n_ids, S, w, tt < qe, fv4, t4, lane, F2q, d, &t4b, F2bq);
       else h4_chunk<OUT>(keys, ids, n_ids, S, w, tt < qe, fv, t, lane, F2c, d);
     }
   }
@@ -544,7 +560,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
   return acc4;
 }
 
-template <bool V4>
+template <bool V4, bool DUAL = false>
 __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
   extern __shared__ int h4[];
   int* keys = h4;
@@ -581,7 +597,7 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
     for (int c0 = 0; c0 < d; c0 += 32) {
       const int c = c0 + lane;
       const bool cok = c < d;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), acc_b = acc;
       if (cur_ok) {
         for (int i = threadIdx.x; i < deg_out; i += H4_THREADS) cur_out[i] = 0;
         for (int i = threadIdx.x; i < deg_in; i += H4_THREADS) cur_in[i] = 0;
@@ -601,8 +617,8 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
         // (3) acc += f3(p) (.) G(w) over in-wedges w -> p -> n of this partition
         R.deg = deg_in;
         {
-          const float4 r4 = h4_sweep<false, V4>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b, q_e,
-                                                &q_n, &grab, c, cok);
+          const float4 r4 = h4_sweep<false, V4, DUAL>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b,
+                                                      q_e, &q_n, &grab, c, cok, &acc_b);
           acc.x += r4.x; acc.y += r4.y; acc.z += r4.z; acc.w += r4.w;
         }
         H4_T(3);
@@ -634,6 +650,22 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
         if (cok) dhn_store(a, n, c, s);
       }
       __syncthreads();
+      if (DUAL) {   // the second middle operand's result (V4 layout, no root multiplier)
+#pragma unroll
+        for (int m = 8; m < 32; m <<= 1) {
+          acc_b.x += __shfl_xor_sync(FULL, acc_b.x, m); acc_b.y += __shfl_xor_sync(FULL, acc_b.y, m);
+          acc_b.z += __shfl_xor_sync(FULL, acc_b.z, m); acc_b.w += __shfl_xor_sync(FULL, acc_b.w, m);
+        }
+        if (lane < 8) *reinterpret_cast<float4*>(&s_red[warp * 32 + 4 * lane]) = acc_b;
+        __syncthreads();
+        if (warp == 0) {
+          float s = 0.f;
+          for (int w = 0; w < H4_WARPS; ++w) s += s_red[w * 32 + lane];
+          const int64_t orow = a.out_by_row ? (int64_t)a.row_of[n] : n;
+          if (cok) a.out_b[orow * a.ld_out + c] = s;
+        }
+        __syncthreads();
+      }
       H4_T(5);
     }
   }
@@ -825,9 +857,10 @@ rnn_status check_ops(const rnn_operand* f, int k, int d, int64_t R) {
 rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const float* const* W,
                 const float* rm, int64_t ld_rm, int rm_by_group, float* out, int64_t ld_out,
                 int out_by_row, int launch_id, cudaStream_t st, float* sum_out = nullptr,
-                int64_t ld_sum = 0) {
+                int64_t ld_sum = 0, const float* F2b = nullptr, float* out_b = nullptr) {
   DhnArgs a{};
   a.sum_out = sum_out; a.ld_sum = ld_sum;
+  a.F2b = F2b; a.out_b = out_b;
   a.G = P.G; a.d = P.d;
   a.gp = adj->group_ptr; a.nbr = b.nbr; a.sp = adj->src_ptr; a.sg = adj->src_group;
   a.row_of = adj->group_dst_row;
@@ -855,7 +888,9 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     static const bool scalar = getenv("RNN_DHN_SCALAR") != nullptr;
     const bool v4 = !scalar && P.d % 4 == 0 && aligned16(a.F1) && aligned16(a.F2) &&
                     aligned16(a.F3) && aligned16(a.slab);
-    auto kern = v4 ? dhn4_kernel<true> : dhn4_kernel<false>;
+    RNN_REQUIRE(!F2b || (v4 && aligned16(F2b)), RNN_ERR_UNSUPPORTED,
+                "dual-middle C4 walk needs the float4 path");
+    auto kern = F2b ? dhn4_kernel<true, true> : v4 ? dhn4_kernel<true> : dhn4_kernel<false>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<P.n_cta, H4_THREADS, smem, st>>>(a);
   }
@@ -947,7 +982,7 @@ static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
 static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                         const float* d_out, int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
                         float* const* d_f, int64_t ld_df, void* workspace, size_t workspace_bytes,
-                        void* stream);
+                        void* stream, uint32_t flags = 0);
 
 extern "C" rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                                   float* out, int64_t ld_out, void* workspace,
@@ -970,13 +1005,15 @@ extern "C" rnn_status rnn_dhn_fwd_save(const rnn_join_index* adj, int32_t k,
 extern "C" rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k,
                                         const rnn_operand* f, const float* d_out,
                                         int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
-                                        float* const* d_f, int64_t ld_df, void* workspace,
-                                        size_t workspace_bytes, void* stream) {
+                                        float* const* d_f, int64_t ld_df, uint32_t flags,
+                                        void* workspace, size_t workspace_bytes, void* stream) {
   clear_error();
   RNN_REQUIRE(walk_sum || !adj || adj->n_groups == 0, RNN_ERR_INVALID_ARGUMENT,
               "walk_sum is NULL");
+  RNN_REQUIRE((flags & ~(uint32_t)RNN_DHN_SYMMETRIC_EDGE) == 0, RNN_ERR_INVALID_ARGUMENT,
+              "unknown DHN flags 0x%x", flags);
   return dhn_bwd_impl(adj, k, f, d_out, ld_dout, walk_sum, ld_ws, d_f, ld_df, workspace,
-                      workspace_bytes, stream);
+                      workspace_bytes, stream, flags);
 }
 
 static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,
@@ -1022,7 +1059,7 @@ extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rn
 static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                         const float* d_out, int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
                         float* const* d_f, int64_t ld_df, void* workspace, size_t workspace_bytes,
-                        void* stream) {
+                        void* stream, uint32_t flags) {
   RNN_TRY(check_adj(adj, k, f ? f[1].dim : 0));
   const int d = f[1].dim;
   RNN_TRY(check_ops(f, k, d, adj->n_src_rows));
@@ -1074,8 +1111,19 @@ static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
     const float* W[3] = {cyc[1], cyc[2], cyc[3]};
     RNN_TRY(walk(P, b, adj, W, d_out, ld_dout, 1, d_f[0], ld_df, 1, launch++, st));
   }
+  // symmetric Edge, k = 4: the d f1 walk (f2, f3, g) and the d f3 walk (g, f1, f2) -- reversed,
+  // (f2, f1, g) -- share both partial sums S_f2 and S_g and differ only in the middle operand,
+  // so one walk with two middle operands yields both
+  bool done3 = false;
+  if ((flags & RNN_DHN_SYMMETRIC_EDGE) && k == 4 && d_f[1] && d_f[3] && d % 4 == 0 &&
+      !getenv("RNN_DHN_SCALAR") && !getenv("RNN_DHN_NO_DUAL")) {
+    const float* W[3] = {cyc[2], cyc[3], cyc[0]};
+    RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[1], ld_df, 1, launch++, st, nullptr, 0, cyc[1],
+                 d_f[3]));
+    done3 = true;
+  }
   for (int j = 1; j < k; ++j) {
-    if (!d_f[j]) continue;
+    if (!d_f[j] || (done3 && (j == 1 || j == 3))) continue;
     const float* W[3] = {nullptr, nullptr, nullptr};
     for (int i = 1; i < k; ++i) W[i - 1] = cyc[(j + i) % k];
     RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[j], ld_df, 1, launch++, st));

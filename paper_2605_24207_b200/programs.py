@@ -440,6 +440,14 @@ class DHNProgram(_Program):
         # each pattern's walk sum before the root factor, saved by the forward so the backward
         # forms d f0 = dOut (.) sum without a walk (rnn_dhn_fwd_save / rnn_dhn_bwd_saved)
         self.walk_sum = {k: _empty(G, d, dev) for k in self.ks}
+        # RNN_DHN_SYMMETRIC_EDGE: verified once at setup (Edge equals its reverse as a multiset)
+        ks = torch.sort(keys).values
+        es = torch.searchsorted(ks, torch.as_tensor(g["edges"]["src"]).to(dev))
+        ed = torch.searchsorted(ks, torch.as_tensor(g["edges"]["dst"]).to(dev))
+        nn_ = max(len(ks), 1)
+        self.symmetric = bool(torch.equal(torch.sort(es * nn_ + ed).values,
+                                          torch.sort(ed * nn_ + es).values))
+        del es, ed
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
         self.pos0 = {}
@@ -487,7 +495,10 @@ class DHNProgram(_Program):
             # walk sum (elementwise, not counted)
             self._flops["dhn2_bwd"] = self._flops["dhn2_fwd"]
             self._flops["dhn3_bwd"] = 2 * self._flops["dhn3_fwd"]
-            self._flops["dhn4_bwd"] = 3 * self._flops["dhn4_fwd"]
+            # (symmetric Edge: d f1 and d f3 share one walk with two middle operands, which
+            # adds 2d per in-wedge to that walk)
+            self._flops["dhn4_bwd"] = (2 * self._flops["dhn4_fwd"] + 2 * d * two_paths
+                                       if self.symmetric else 3 * self._flops["dhn4_fwd"])
         return {k: {"bound": "alu", "amount": v} for k, v in self._flops.items()
                 if int(k[3]) in self.ks}
 
@@ -511,7 +522,8 @@ class DHNProgram(_Program):
         for j, k in enumerate(self.ks):
             self._t(f"dhn{k}_bwd")
             rnn.dhn_bwd(self.idx, k, self._f(k, self.Y), self.d_out[:, j * self.d:(j + 1) * self.d],
-                        d_f=self._f(k, self.dY), ws=self.ws, walk_sum=self.walk_sum[k])
+                        d_f=self._f(k, self.dY), ws=self.ws, walk_sum=self.walk_sum[k],
+                        symmetric=self.symmetric)
             self._t(f"dhn{k}_bwd_end")
         self._t("proj_bwd")
         rnn.project_bwd(self.H, self.W, self.dY, want_dx=True, prec=self.prec, ws=self.ws_p,

@@ -93,7 +93,7 @@ def lib():
         L.rnn_dhn_fwd_save.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
                                        vp, i64, vp, sz, vp]
         L.rnn_dhn_bwd_saved.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
-                                        vp, i64, C.POINTER(vp), i64, vp, sz, vp]
+                                        vp, i64, C.POINTER(vp), i64, C.c_uint32, vp, sz, vp]
         L.rnn_dhn_bwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
                                   C.POINTER(vp), i64, vp, sz, vp]
         L.rnn_gcn_norm_src_deg.argtypes = [C.POINTER(JoinIndexC), vp, vp, vp]
@@ -447,8 +447,11 @@ def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None, walk_sum=None)
     return out
 
 
+DHN_SYMMETRIC_EDGE = 1
+
+
 def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=None,
-            walk_sum=None):
+            walk_sum=None, symmetric=False):
     """[d f0, ..., d f_{k-1}] by node row (rnn_dhn_bwd); want[i] False -> None.  walk_sum: the
     forward's saved walk sum (d f0 without a walk launch, rnn_dhn_bwd_saved)."""
     dev = adj.group_ptr.device
@@ -468,7 +471,8 @@ def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=No
     if walk_sum is not None:
         _check(lib().rnn_dhn_bwd_saved(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out),
                                        d_out.stride(0), _ptr(walk_sum), walk_sum.stride(0), ptrs,
-                                       ld, _ptr(w), w.numel(), _stream(stream)))
+                                       ld, DHN_SYMMETRIC_EDGE if symmetric else 0, _ptr(w),
+                                       w.numel(), _stream(stream)))
         return d_f
     _check(lib().rnn_dhn_bwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out), d_out.stride(0), ptrs,
                              ld, _ptr(w), w.numel(), _stream(stream)))

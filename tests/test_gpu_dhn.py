@@ -89,6 +89,18 @@ def run_case(rnn, keys, e_n, e_v, k, d, seed, dense=False, f0_none=False, bwd=Tr
     grads2 = rnn.dhn_bwd(gi, k, fg, cu(d_out), walk_sum=ws)
     for i in range(k):
         assert_close(np_(grads2[i]), ref_g[i], FP32_TOL, f"C{k} d f{i} (saved)")
+    if symmetric(e_n, e_v):   # RNN_DHN_SYMMETRIC_EDGE: d f1 | d f3 from one C4 walk
+        grads3 = rnn.dhn_bwd(gi, k, fg, cu(d_out), walk_sum=ws, symmetric=True)
+        for i in range(k):
+            assert_close(np_(grads3[i]), ref_g[i], FP32_TOL, f"C{k} d f{i} (saved, symmetric)")
+
+
+def symmetric(e_n, e_v):
+    """Edge equals its reverse as a multiset."""
+    a = np.stack([np.asarray(e_n), np.asarray(e_v)], 1)
+    rec = [("x", a.dtype), ("y", a.dtype)]
+    return np.array_equal(np.sort(np.ascontiguousarray(a).view(rec), axis=0),
+                          np.sort(np.ascontiguousarray(a[:, ::-1]).view(rec), axis=0))
 
 
 @pytest.mark.parametrize("k", [2, 3, 4])
@@ -96,6 +108,14 @@ def run_case(rnn, keys, e_n, e_v, k, d, seed, dense=False, f0_none=False, bwd=Tr
 def test_random_graph(rnn, k, directed):
     keys, e_n, e_v = random_graph(10 + k, 300, 2400, directed)
     run_case(rnn, keys, e_n, e_v, k, 32, seed=k)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_random_graph_symmetric(rnn, k):
+    """Undirected without duplicates: the symmetric-Edge backward path runs (checked inside)."""
+    keys, e_n, e_v = random_graph(30 + k, 300, 2400, directed=False, dup=0)
+    assert symmetric(e_n, e_v)
+    run_case(rnn, keys, e_n, e_v, k, 32, seed=k + 5)
 
 
 @pytest.mark.parametrize("k", [3, 4])
