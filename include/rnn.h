@@ -279,7 +279,9 @@ rnn_status rnn_dhn_fwd_save(const rnn_join_index* adj, int32_t k, const rnn_oper
  * symmetric ((n, v) and (v, n) occur with equal multiplicity, e.g. an undirected graph stored
  * in both directions, reading 10).  Closed walks then reverse, so for k = 4 the
  * d f1 and d f3 walks share both partial sums and run as ONE walk with two middle operands
- * (d f1 | d f3).  Results are undefined if the assertion is false.  Unknown bits: error. */
+ * (d f1 | d f3), and for k = 3 the d f1 and d f2 walks share the probe work and run as one
+ * walk with two first-hop operands.  Results are undefined if the assertion is false.
+ * Unknown bits: error. */
 #define RNN_DHN_SYMMETRIC_EDGE 1u
 rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                              const float* d_out, int64_t ld_dout, const float* walk_sum,

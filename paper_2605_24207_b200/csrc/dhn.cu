@@ -55,7 +55,8 @@ struct DhnArgs {
   int64_t cta_stride;     // elements between consecutive CTAs' mark
   float* sum_out;         // optional: the walk sum before the root multiplier [G, ld_sum]
   int64_t ld_sum;
-  const float* F2b;       // k=4, optional second middle operand (symmetric Edge, see walk2)
+  const float* F2b;       // k=4, optional second middle operand (symmetric Edge)
+  const float* F1b;       // k=3, optional second first-hop operand (symmetric Edge)
   float* out_b;           // its result (same layout as out, no root multiplier)
 };
 
@@ -114,7 +115,7 @@ __device__ __forceinline__ int hs_find(const int* keys, int cap_mask, int w) {
 constexpr int H3_CAP = 8192;                 // slots (keys + counts: 64 KB)
 constexpr int H3_MAX_INDEG = 6144;           // load factor <= 0.75
 
-template <int DPL>
+template <int DPL, bool DUAL = false>
 __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
   extern __shared__ int h3[];
   int* keys = h3;
@@ -138,18 +139,19 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) atomicAdd(&mark[a.sg[q]], 1);
     }
     __syncthreads();
-    float acc[DPL];
+    float acc[DPL], acc_b[DPL];
 #pragma unroll
-    for (int j = 0; j < DPL; ++j) acc[j] = 0.f;
+    for (int j = 0; j < DPL; ++j) acc[j] = acc_b[j] = 0.f;
     const int64_t pe = a.gp[n + 1];
     for (int64_t pos = a.gp[n] + warp; pos < pe; pos += DHN_WARPS) {
       const int32_t v = a.nbr[pos];
       if (v < 0) continue;
-      float f1v[DPL];
+      float f1v[DPL], f1bv[DPL];
 #pragma unroll
       for (int j = 0; j < DPL; ++j) {
         const int c = lane + 32 * j;
         f1v[j] = c < d ? a.F1[(int64_t)v * d + c] : 0.f;
+        f1bv[j] = DUAL && c < d ? a.F1b[(int64_t)v * d + c] : 0.f;
       }
       const int64_t we = a.gp[v + 1];
       for (int64_t i0 = a.gp[v]; i0 < we; i0 += 32) {
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
 #pragma unroll
               for (int h = 0; h < 4; ++h) t += (float)mm[h] * x[h];
               acc[j] += f1v[j] * t;
+              if (DUAL) acc_b[j] += f1bv[j] * t;
             }
           }
         }
@@ -202,6 +205,18 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
       float s = 0.f;
       for (int w = 0; w < DHN_WARPS; ++w) s += s_acc[w * DPL * 32 + c];
       dhn_store(a, n, c, s);
+    }
+    if (DUAL) {   // the second first-hop operand's result (no root multiplier)
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < DPL; ++j) s_acc[warp * DPL * 32 + lane + 32 * j] = acc_b[j];
+      __syncthreads();
+      const int64_t orow = a.out_by_row ? (int64_t)a.row_of[n] : n;
+      for (int c = threadIdx.x; c < d; c += DHN_THREADS) {
+        float s = 0.f;
+        for (int w = 0; w < DHN_WARPS; ++w) s += s_acc[w * DPL * 32 + c];
+        a.out_b[orow * a.ld_out + c] = s;
+      }
     }
     if (hashed) {
       for (int i = threadIdx.x; i < H3_CAP; i += DHN_THREADS) { keys[i] = -1; cnt[i] = 0; }
@@ -857,10 +872,14 @@ rnn_status check_ops(const rnn_operand* f, int k, int d, int64_t R) {
 rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const float* const* W,
                 const float* rm, int64_t ld_rm, int rm_by_group, float* out, int64_t ld_out,
                 int out_by_row, int launch_id, cudaStream_t st, float* sum_out = nullptr,
-                int64_t ld_sum = 0, const float* F2b = nullptr, float* out_b = nullptr) {
+                int64_t ld_sum = 0, const float* Fb = nullptr, float* out_b = nullptr) {
+  // Fb (symmetric Edge): k = 3 second first-hop operand, k = 4 second middle operand
   DhnArgs a{};
   a.sum_out = sum_out; a.ld_sum = ld_sum;
-  a.F2b = F2b; a.out_b = out_b;
+  a.F2b = P.k == 4 ? Fb : nullptr;
+  a.F1b = P.k == 3 ? Fb : nullptr;
+  a.out_b = out_b;
+  const float* F2b = a.F2b;
   a.G = P.G; a.d = P.d;
   a.gp = adj->group_ptr; a.nbr = b.nbr; a.sp = adj->src_ptr; a.sg = adj->src_group;
   a.row_of = adj->group_dst_row;
@@ -875,8 +894,10 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     a.mark = reinterpret_cast<int*>(b.cta);
     const int dpl = (P.d + 31) / 32;
     const size_t smem = 2 * H3_CAP * sizeof(int) + (size_t)DHN_WARPS * dpl * 32 * sizeof(float);
-    auto kern = dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2> : dpl == 3 ? dhn3_kernel<3>
-                                                                                  : dhn3_kernel<4>;
+    auto kern = a.F1b ? (dpl == 1 ? dhn3_kernel<1, true> : dpl == 2 ? dhn3_kernel<2, true>
+                         : dpl == 3 ? dhn3_kernel<3, true> : dhn3_kernel<4, true>)
+                      : (dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2>
+                         : dpl == 3 ? dhn3_kernel<3> : dhn3_kernel<4>);
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<P.n_cta, DHN_THREADS, smem, st>>>(a);
   } else {
@@ -1114,16 +1135,24 @@ static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
   // symmetric Edge, k = 4: the d f1 walk (f2, f3, g) and the d f3 walk (g, f1, f2) -- reversed,
   // (f2, f1, g) -- share both partial sums S_f2 and S_g and differ only in the middle operand,
   // so one walk with two middle operands yields both
-  bool done3 = false;
-  if ((flags & RNN_DHN_SYMMETRIC_EDGE) && k == 4 && d_f[1] && d_f[3] && d % 4 == 0 &&
-      !getenv("RNN_DHN_SCALAR") && !getenv("RNN_DHN_NO_DUAL")) {
+  // k = 3 likewise: the d f1 walk (f2, g) and the d f2 walk (g, f1) -- reversed, (f1, g) --
+  // share the probe and the g gathers; one walk with two first-hop operands yields both
+  bool dual = false;
+  const bool sym = (flags & RNN_DHN_SYMMETRIC_EDGE) && !getenv("RNN_DHN_NO_DUAL");
+  if (sym && k == 4 && d_f[1] && d_f[3] && d % 4 == 0 && !getenv("RNN_DHN_SCALAR")) {
     const float* W[3] = {cyc[2], cyc[3], cyc[0]};
     RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[1], ld_df, 1, launch++, st, nullptr, 0, cyc[1],
                  d_f[3]));
-    done3 = true;
+    dual = true;
+  }
+  if (sym && k == 3 && d_f[1] && d_f[2]) {
+    const float* W[3] = {cyc[2], cyc[0], nullptr};
+    RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[1], ld_df, 1, launch++, st, nullptr, 0, cyc[1],
+                 d_f[2]));
+    dual = true;
   }
   for (int j = 1; j < k; ++j) {
-    if (!d_f[j] || (done3 && (j == 1 || j == 3))) continue;
+    if (!d_f[j] || (dual && (k == 3 || j == 1 || j == 3))) continue;
     const float* W[3] = {nullptr, nullptr, nullptr};
     for (int i = 1; i < k; ++i) W[i - 1] = cyc[(j + i) % k];
     RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[j], ld_df, 1, launch++, st));

@@ -494,7 +494,7 @@ class DHNProgram(_Program):
             # backward: one walk per rotated operand f1 .. f_{k-1}; d f0 = dOut (.) the saved
             # walk sum (elementwise, not counted)
             self._flops["dhn2_bwd"] = self._flops["dhn2_fwd"]
-            self._flops["dhn3_bwd"] = 2 * self._flops["dhn3_fwd"]
+            self._flops["dhn3_bwd"] = (1.5 if self.symmetric else 2) * self._flops["dhn3_fwd"]
             # (symmetric Edge: d f1 and d f3 share one walk with two middle operands, which
             # adds 2d per in-wedge to that walk)
             self._flops["dhn4_bwd"] = (2 * self._flops["dhn4_fwd"] + 2 * d * two_paths
