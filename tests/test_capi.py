@@ -57,3 +57,16 @@ def test_host_side_checks_without_gpu(lib):
     assert lib.rnn_project(C.c_void_p(16), 10, 10, 10, C.c_void_p(16), 9000, 10, None,
                            C.c_void_p(16), 9000, 0, None) == 5
     assert lib.rnn_hash_partition(None, 10, 0, 0, None, None) == 1
+
+
+def test_dhn_saved_entry_points_host_checks(lib):
+    """rnn_dhn_fwd_save / rnn_dhn_bwd_saved reject a missing walk sum and unknown flags before
+    any device work (an empty index has no groups, so no pointer is dereferenced)."""
+    from paper_2605_24207_b200 import rnn
+    idx = rnn.JoinIndexC()          # zeroed: n_groups = 0
+    ops = (rnn.OperandC * 4)()
+    # unknown flag bit
+    st = lib.rnn_dhn_bwd_saved(C.byref(idx), 4, ops, None, 32, C.c_void_p(16), 32, None, 32,
+                               C.c_uint32(2), None, 0, None)
+    assert st == 1 and b"flags" in lib.rnn_last_error()
+    assert lib.rnn_dhn_bwd_saved.argtypes is not None
