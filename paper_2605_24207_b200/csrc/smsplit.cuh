@@ -143,6 +143,8 @@ rnn_status launch_st_var(const Pol& pol, RSCtx cx, cudaStream_t st, int which) {
   if (U == 1 && B == 4) return launch_st<Pol, 1, 4>(pol, cx, st);
   if (U == 2 && B == 4) return launch_st<Pol, 2, 4>(pol, cx, st);
   if (U == 3 && B == 4) return launch_st<Pol, 3, 4>(pol, cx, st);
+  if (U == 1 && B == 5) return launch_st<Pol, 1, 5>(pol, cx, st);
+  if (U == 2 && B == 5) return launch_st<Pol, 2, 5>(pol, cx, st);
   return launch_st<Pol, 4, 3>(pol, cx, st);
 }
 
