@@ -717,6 +717,32 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
     s.dv = d_src; s.ld_dv = q->src.ld;
     s.dk = d_src_key; s.ld_dk = q->src_key.ld;
     s.heads = q->heads; s.scale = q->scale;
+    static const bool two_pass = getenv("RNN_SM_TWOPASS") != nullptr;
+    if (sm_rowsplit_ok(idx, q, qi.D) && idx->src_seg && !two_pass) {
+      // source-major backward: D, pass A (dM', dK', DE), pass B (dQ)
+      const SmRows rows = sm_rows(idx, q);
+      float* Dg = Lw.Ubuf;     // [G, h] <= [G, ld4]
+      float* DE = Lw.AD;       // [E', h] <= [E', 2h]
+      sm_d_kernel<<<(unsigned)ceil_div(idx->n_groups, 8), 256, 0, st>>>(
+          d_out, ld_dout, out, ld_out, idx->n_groups, q->heads, rows.LH, Dg);
+      RNN_LAUNCH_CHECK();
+      SmBwdAPol pa;
+      pa.a = rows;
+      pa.dO = d_out; pa.ld_do = ld_dout; pa.lse = lse; pa.Dg = Dg; pa.DE = DE;
+      pa.dv = d_src; pa.ld_dv = q->src.ld; pa.dk = d_src_key; pa.ld_dk = q->src_key.ld;
+      RSCtx c2{idx->src_seg, idx->src_ptr, idx->n_src_rows, idx->n_join_rows,
+               idx->src_work_ptr, idx->n_src_work, Lw.part_src, 2 * ld4, Lw.cnt_src, 1};
+      RNN_TRY(launch_st_var(pa, c2, st, 1));
+      if (d_dst) {
+        SmBwdBPol pb;
+        pb.a = rows;
+        pb.DE = DE; pb.dq = d_dst; pb.ld_dq = q->dst.ld;
+        RSCtx c1{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
+                 idx->n_work, Lw.part_fwd, qi.pstride, Lw.cnt_fwd, 1};
+        RNN_TRY(launch_st_var(pb, c1, st, 2));
+      }
+      return RNN_OK;
+    }
     if (sm_rowsplit_ok(idx, q, qi.D) && idx->src_seg) {
       SmBwd1Pol p1;
       p1.a = sm_rows(idx, q);

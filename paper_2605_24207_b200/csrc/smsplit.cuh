@@ -381,4 +381,128 @@ struct SmBwd2Pol {
   }
 };
 
+
+// ------------------------------------------------------------------------------------------
+// Source-major softmax backward (default): the probabilities are recomputed where the source
+// rows are resident, so M' is never gathered again and no (a, de) pair makes a round trip.
+//   D[g, h]  = <dO[g], O[g]> per head                          (sm_d_kernel, warp per group)
+//   pass A (source-major, segment = source s; K'[s], M'[s] stay in L1 across the segment):
+//     a = exp(<K'[s], Q[t]> - lse[g]),  de = a (<dO[g], M'[s]> - D[g])
+//     dM'[s] = sum a dO[g],  dK'[s] = scale sum de Q[t],  DE[p] = de   (p = group-major pos)
+//   pass B (group-major): dQ[t] = scale sum_p DE[p] K'[s_p]
+// Per join row: pass A gathers Q[t] and dO[g] (8d bytes) + 8h, writes 4h; pass B gathers K'
+// (4d) + 4h -- against 16d + 16h for the two-pass (a, de) scheme above.
+// ------------------------------------------------------------------------------------------
+static __global__ void sm_d_kernel(const float* __restrict__ dO, int64_t ld_do, const float* __restrict__ O,
+                            int64_t ld_o, int64_t G, int heads, int LH, float* __restrict__ D) {
+  const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (g >= G) return;
+  const int k = lane_id();
+  const float x = sm_head_sum(f4_dot(ld_f4(dO + g * ld_do + 4 * k), ld_f4(O + g * ld_o + 4 * k)), LH);
+  if (k % LH == 0) D[g * heads + k / LH] = x;
+}
+
+struct SmBwdAPol {
+  SmRows a;
+  const float* dO; int64_t ld_do;
+  const float* lse;
+  const float* Dg;                 // [G, h]
+  float* DE;                       // [E', h] by group-major position
+  float* dv; int64_t ld_dv;        // nullable
+  float* dk; int64_t ld_dk;        // nullable
+  struct Meta { int g, t, p, s; };
+  struct Row { float4 k, v, q, dO; float lse2, D, sc, da; int p; };
+  struct State { float4 dv, dk; };
+
+  __device__ __forceinline__ Meta meta(int64_t r, int seg) const {
+    const int g = a.src_group[r];
+    return Meta{g, a.q_by_group ? g : a.dst_row[g], a.src_pos[r], seg};
+  }
+  __device__ __forceinline__ Meta shfl(const Meta& m, int j) const {
+    return Meta{__shfl_sync(FULL, m.g, j), __shfl_sync(FULL, m.t, j), __shfl_sync(FULL, m.p, j),
+                __shfl_sync(FULL, m.s, j)};
+  }
+  __device__ __forceinline__ void load(Row& w, const Meta& m, bool) const {
+    const int k = lane_id();
+    w.k = ld_f4(a.key + (int64_t)m.s * a.ld_key + 4 * k);
+    w.v = ld_f4(a.val + (int64_t)m.s * a.ld_val + 4 * k);
+    w.q = ld_f4(a.q + (int64_t)m.t * a.ld_q + 4 * k);
+    w.dO = ld_f4(dO + (int64_t)m.g * ld_do + 4 * k);
+    const int64_t gh = (int64_t)m.g * a.heads + k / a.LH;
+    w.lse2 = __ldg(lse + gh) * SM_LOG2E;
+    w.D = __ldg(Dg + gh);
+    w.p = m.p;
+  }
+  __device__ __forceinline__ void prep(Row& w) const {
+    w.sc = sm_head_sum(f4_dot(w.k, w.q), a.LH);
+    w.da = sm_head_sum(f4_dot(w.dO, w.v), a.LH);
+  }
+  __device__ __forceinline__ void init(State& s) const { s.dv = f4_zero(); s.dk = f4_zero(); }
+  __device__ __forceinline__ void row(State& s, const Row& w, int64_t) const {
+    const int k = lane_id();
+    const float pa = exp2f(w.sc * (a.scale * SM_LOG2E) - w.lse2);
+    const float de = pa * (w.da - w.D);
+    s.dv = f4_fma(pa, w.dO, s.dv);
+    s.dk = f4_fma(de, w.q, s.dk);
+    if (k % a.LH == 0) DE[(int64_t)w.p * a.heads + k / a.LH] = de;
+  }
+  __device__ __forceinline__ void finish(const State& s, int64_t src) const {
+    const int k = lane_id();
+    if (dv) st_f4(dv + src * ld_dv + 4 * k, s.dv);
+    if (dk) st_f4(dk + src * ld_dk + 4 * k, f4_scale(a.scale, s.dk));
+  }
+  __device__ __forceinline__ void zero(int64_t src) const {
+    State s;
+    init(s);
+    finish(s, src);
+  }
+  __device__ __forceinline__ void save(const State& s, float* dst) const {
+    const int k = lane_id();
+    __stcg(reinterpret_cast<float4*>(dst + 4 * k), s.dv);
+    __stcg(reinterpret_cast<float4*>(dst + 128 + 4 * k), s.dk);
+  }
+  __device__ __forceinline__ void merge(State& s, const float* src) const {
+    const int k = lane_id();
+    s.dv = f4_add(s.dv, ld_f4_cg(src + 4 * k));
+    s.dk = f4_add(s.dk, ld_f4_cg(src + 128 + 4 * k));
+  }
+};
+
+struct SmBwdBPol {
+  SmRows a;
+  const float* DE;                 // [E', h]
+  float* dq; int64_t ld_dq;
+  struct Meta { int s; };
+  struct Row { float4 k; float de; };
+  struct State { float4 dq; };
+  __device__ __forceinline__ Meta meta(int64_t r, int) const { return Meta{a.src_row[r]}; }
+  __device__ __forceinline__ Meta shfl(const Meta& m, int j) const {
+    return Meta{__shfl_sync(FULL, m.s, j)};
+  }
+  __device__ __forceinline__ void load(Row& w, const Meta& m, bool) const {
+    const int k = lane_id();
+    w.k = ld_f4(a.key + (int64_t)m.s * a.ld_key + 4 * k);
+  }
+  __device__ __forceinline__ void prep(Row&) const {}
+  __device__ __forceinline__ void init(State& s) const { s.dq = f4_zero(); }
+  __device__ __forceinline__ void row(State& s, const Row& w, int64_t p) const {
+    const float de = __ldg(DE + p * a.heads + lane_id() / a.LH);
+    s.dq = f4_fma(de, w.k, s.dq);
+  }
+  __device__ __forceinline__ int64_t qrow(int64_t g) const {
+    return a.q_by_group ? g : (int64_t)a.dst_row[g];
+  }
+  __device__ __forceinline__ void finish(const State& s, int64_t g) const {
+    st_f4(dq + qrow(g) * ld_dq + 4 * lane_id(), f4_scale(a.scale, s.dq));
+  }
+  __device__ __forceinline__ void zero(int64_t g) const {
+    st_f4(dq + qrow(g) * ld_dq + 4 * lane_id(), f4_zero());
+  }
+  __device__ __forceinline__ void save(const State& s, float* dst) const {
+    __stcg(reinterpret_cast<float4*>(dst + 4 * lane_id()), s.dq);
+  }
+  __device__ __forceinline__ void merge(State& s, const float* src) const {
+    s.dq = f4_add(s.dq, ld_f4_cg(src + 4 * lane_id()));
+  }
+};
 }  // namespace rnn

@@ -345,18 +345,19 @@ class HGTProgram(_Program):
         return sum(ix.n_join_rows for ix in self.idx.values())
 
     def lja_bytes(self):
-        """Softmax LJA gather model (h heads).  fwd, per join row: src id 4 +
-        K' and M' rows 8d; per group: Q row 4d, out 4d, lse 4h, pointer 8.  bwd pass 1
-        (group-major), per join row: src id 4 + K', M' rows 8d + (a, de) written 8h; per group:
-        Q, O, dO rows 12d + lse 4h + dQ written 4d + pointer 8.  bwd pass 2 (source-major), per
-        join row: group id + position 8 + (a, de) read 8h + dO[g] and Q[t] rows 8d; per source
-        row: dK', dM' written 8d + pointer 8."""
+        """Softmax LJA gather model (h heads), for the algorithm the library
+        runs.  fwd, per join row: src id 4 + K' and M' rows 8d; per group: Q row 4d, out 4d,
+        lse 4h, pointer 8.  bwd (source-major): D = <dO, O> per group reads
+        8d and writes 4h; pass A per join row: group id + position 8 + Q[t] and dO[g] rows 8d +
+        lse and D 8h + DE written 4h, per source row: K', M' read 8d + dK', dM' written 8d +
+        pointer 8; pass B per join row: src id 4 + K' row 4d + DE 4h, per group dQ written 4d +
+        pointer 8.  (The two-pass (a, de) scheme, RNN_SM_TWOPASS, moved 16d + 16h per row.)"""
         d, h = self.d, self.h
         f, b = [], []
         for ix in self.idx.values():
             f.append(ix.n_join_rows * (4 + 8 * d) + ix.n_groups * (8 * d + 4 * h + 8))
-            b.append(ix.n_join_rows * ((4 + 8 * d + 8 * h) + (8 + 8 * h + 8 * d)) +
-                     ix.n_groups * (16 * d + 4 * h + 8) + ix.n_src_rows * (8 * d + 8))
+            b.append(ix.n_join_rows * ((8 + 8 * d + 12 * h) + (4 + 4 * d + 4 * h)) +
+                     ix.n_groups * (8 * d + 4 * h + 4 * d + 8) + ix.n_src_rows * (16 * d + 8))
         return {"lja_fwd": float(np.mean(f)), "lja_bwd": float(np.mean(b))}
 
     def host_io(self):

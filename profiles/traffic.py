@@ -46,12 +46,18 @@ def main(src, dst):
                         "dram__bytes_read.sum + dram__bytes_write.sum per launch, mean"}
         if cfg == "mag":
             f = [b for n, b in cap if "SmFwdPol" in n]
+            t["lja_fwd"] = mean(f)
+            dk = [b for n, b in cap if "sm_d_kernel" in n]
+            ba = [b for n, b in cap if "SmBwdAPol" in n]
+            bb = [b for n, b in cap if "SmBwdBPol" in n]
             b1 = [b for n, b in cap if "SmBwd1Pol" in n]
             b2 = [b for n, b in cap if "SmBwd2Pol" in n]
-            t["lja_fwd"] = mean(f)
-            if b1 and len(b1) == len(b2):
+            if ba and len(ba) == len(bb) == len(dk):      # source-major backward (default)
+                t["lja_bwd"] = mean([x + y + z for x, y, z in zip(dk, ba, bb)])
+                t["_source"] += "; lja_bwd = D kernel + pass A + pass B of one relation"
+            elif b1 and len(b1) == len(b2):                # two-pass (a, de) backward
                 t["lja_bwd"] = mean([x + y for x, y in zip(b1, b2)])
-            t["_source"] += "; lja_bwd = pass 1 + pass 2 of one relation"
+                t["_source"] += "; lja_bwd = pass 1 + pass 2 of one relation"
         else:
             t["lja_fwd"] = mean([b for n, b in cap if "LeanFwdMeta" in n])
             t["lja_bwd"] = mean([b for n, b in cap if "LeanBwdMeta" in n])
