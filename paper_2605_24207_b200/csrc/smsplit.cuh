@@ -127,7 +127,7 @@ rnn_status launch_st(const Pol& pol, RSCtx cx, cudaStream_t st) {
 struct StVar { int u[3], b[3]; };
 inline StVar st_var() {
   static StVar v = [] {
-    StVar r{{4, 1, 2}, {3, 4, 4}};   // measured best on MAG (profiles/r01/st_var)
+    StVar r{{4, 1, 4}, {3, 4, 4}};   // measured best on MAG (profiles/r01/st_var, sm_src)
     if (const char* e = getenv("RNN_ST_VAR"))
       sscanf(e, "%d,%d,%d,%d,%d,%d", &r.u[0], &r.b[0], &r.u[1], &r.b[1], &r.u[2], &r.b[2]);
     return r;
@@ -143,8 +143,8 @@ rnn_status launch_st_var(const Pol& pol, RSCtx cx, cudaStream_t st, int which) {
   if (U == 1 && B == 4) return launch_st<Pol, 1, 4>(pol, cx, st);
   if (U == 2 && B == 4) return launch_st<Pol, 2, 4>(pol, cx, st);
   if (U == 3 && B == 4) return launch_st<Pol, 3, 4>(pol, cx, st);
-  if (U == 1 && B == 5) return launch_st<Pol, 1, 5>(pol, cx, st);
-  if (U == 2 && B == 5) return launch_st<Pol, 2, 5>(pol, cx, st);
+  if (U == 4 && B == 4) return launch_st<Pol, 4, 4>(pol, cx, st);
+  if (U == 8 && B == 4) return launch_st<Pol, 8, 4>(pol, cx, st);
   return launch_st<Pol, 4, 3>(pol, cx, st);
 }
 
