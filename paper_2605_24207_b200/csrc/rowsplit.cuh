@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
 // (rows in flight, min CTAs per SM) of the VEC = 1 lean kernel; RNN_LEAN_VAR="U,B" selects
 // another instantiated variant (measurement only)
 inline void lean_var(int* u, int* b) {
-  static int v[2] = {4, 4};   // measured best on arxiv and hyper (profiles/r01/lean_var)
+  static int v[2] = {6, 4};   // measured best on arxiv and hyper (profiles/r01/lean_var)
   static bool init = false;
   if (!init) {
     if (const char* e = getenv("RNN_LEAN_VAR")) sscanf(e, "%d,%d", &v[0], &v[1]);
@@ -336,6 +336,9 @@ rnn_status launch_lean(const MP& mp, RSCtx cx, const LeanOut& o, cudaStream_t st
   else if (VEC == 1 && vu == 4 && vb == 4) lean_kernel<MP, VEC, 4, 4><<<grid, 256, 0, st>>>(mp, cx, o);
   else if (VEC == 1 && vu == 8 && vb == 3) lean_kernel<MP, VEC, 8, 3><<<grid, 256, 0, st>>>(mp, cx, o);
   else if (VEC == 1 && vu == 4 && vb == 6) lean_kernel<MP, VEC, 4, 6><<<grid, 256, 0, st>>>(mp, cx, o);
+  else if (VEC == 1 && vu == 4 && vb == 5) lean_kernel<MP, VEC, 4, 5><<<grid, 256, 0, st>>>(mp, cx, o);
+  else if (VEC == 1 && vu == 2 && vb == 6) lean_kernel<MP, VEC, 2, 6><<<grid, 256, 0, st>>>(mp, cx, o);
+  else if (VEC == 1 && vu == 6 && vb == 4) lean_kernel<MP, VEC, 6, 4><<<grid, 256, 0, st>>>(mp, cx, o);
   else lean_kernel<MP, VEC, U><<<grid, 256, 0, st>>>(mp, cx, o);
   RNN_LAUNCH_CHECK();
   return RNN_OK;
