@@ -169,9 +169,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RNN_BENCH_DIST_BACKEND=gloo: exercise the N > 1 path with several ranks sharing the
+    # visible GPUs (LOCAL_RANK mod device count; smoke-testing on a 1-GPU box only -- NCCL over
+    # NVLink with one GPU per rank is the measured configuration)
+    backend = os.environ.get("RNN_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     graph = make_graph(args.config, args.seed)
