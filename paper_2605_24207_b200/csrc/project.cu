@@ -46,6 +46,7 @@ struct GemmParams {
   uint32_t tmem_cols;
   int a3d, b3d;     // MN-major operand loaded as ONE 3D box {32, KB, MN/32} per stage
   int smem_kb;      // shared-memory budget of the stage ring (0: default 200 KB, 1 CTA / SM)
+  int b_lo_row;     // K-major B with its 3xTF32 lo part precomputed b_lo_row rows below (0: none)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -258,7 +259,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           gs_w[0] += clock64() - t0;
         }
         gs_issue[s] = clock64();
-        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+        const bool blo = SPLIT3 && !B_MN && p.b_lo_row > 0;
+        mbar_expect_tx(&full[s], A_BYTES + B_BYTES * (blo ? 2u : 1u));
         const int k = (int)(kbeg + (int64_t)kb * KB);
         // MN-major operands: 32-wide MN chunks every KB * 128 bytes, either one 3D box
         // {32, KB, chunks} (a single TMA op) or one 2D box per chunk
@@ -273,6 +275,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (!B_MN) {
           tma_load_2d(&tb, b_hi(s), &full[s], k, n0);
+          if (blo) tma_load_2d(&tb, b_lo(s), &full[s], k, n0 + p.b_lo_row);
         } else if (p.b3d) {
           tma_load_3d(&tb, b_hi(s), &full[s], 0, k, n0 / 32);
         } else {
@@ -339,8 +342,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
         lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(a_hi(s)),
                               reinterpret_cast<float4*>(a_lo(s)), A_BYTES / 16, et);
-        lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(b_hi(s)),
-                              reinterpret_cast<float4*>(b_lo(s)), B_BYTES / 16, et);
+        if (B_MN || p.b_lo_row == 0)   // else B's lo part was precomputed and loaded by TMA
+          lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(b_hi(s)),
+                                reinterpret_cast<float4*>(b_lo(s)), B_BYTES / 16, et);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[s]);
       }
@@ -974,6 +978,16 @@ __global__ void colsum_final(const float* __restrict__ part, int64_t chunks, int
   out[c] = s;
 }
 
+// Wt[k, n] = W[n, k] (hi, rows 0..K-1) and Wt[K + k, n] = lo part (3xTF32 B operand)
+__global__ void transpose_hilo_kernel(const float* __restrict__ W, int N, int K, int64_t ldw,
+                                      float* __restrict__ Wt, int64_t ldt) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)N * K) return;
+  const int n = (int)(i / K), k = (int)(i % K);
+  const float x = W[(int64_t)n * ldw + k];
+  Wt[(int64_t)k * ldt + n] = x;
+  Wt[(int64_t)(K + k) * ldt + n] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
 __global__ void transpose_kernel(const float* __restrict__ W, int N, int K, int64_t ldw,
                                  float* __restrict__ Wt, int64_t ldt) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1083,9 +1097,10 @@ __global__ void bias_fill(float* Y, int64_t M, int N, int64_t ldy, const float* 
 }
 
 // Y[M, N] = A[M, Kred] B[N, Kred]^T (+bias), both K-major
+// b_has_lo: rows N .. 2N-1 of B hold lo = B - trunc_tf32(B) (precomputed by the caller)
 rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const float* B, int N,
                    int64_t ldb, const float* bias, float* Y, int64_t ldy, rnn_precision prec,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool b_has_lo = false) {
   if (M == 0 || N == 0) return RNN_OK;
   if (Kred == 0) {
     bias_fill<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(Y, M, N, ldy, bias);
@@ -1154,9 +1169,11 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
   p.BN = N <= 256 ? (int)((N + 15) / 16 * 16) : 256;
   p.Kred = Kred; p.k_split = ceil_div(Kred, BK) * BK;
   p.out = Y; p.ldo = ldy; p.bias = bias; p.mode = 0;
+  const bool blo = b_has_lo && prec == RNN_PREC_3XTF32 && !getenv("RNN_NO_BLO");
+  p.b_lo_row = blo ? N : 0;
   CUtensorMap ta, tb;
   RNN_TRY(make_map(&ta, A, Kred, M, lda, BK, BM));
-  RNN_TRY(make_map(&tb, B, Kred, N, ldb, BK, (uint32_t)p.BN));
+  RNN_TRY(make_map(&tb, B, Kred, blo ? 2 * (int64_t)N : N, ldb, BK, (uint32_t)p.BN));
   return gemm<false, false>(ta, tb, p, 1, prec, st);
 }
 
@@ -1194,7 +1211,7 @@ BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
   BwdWs w{};
   Carve c(base);
   const int64_t ldt = (N + 3) / 4 * 4;
-  w.Wt = c.take<float>((size_t)K * ldt);
+  w.Wt = c.take<float>((size_t)2 * K * ldt);   // W^T hi (rows 0..K-1) and lo (rows K..2K-1)
   w.dWt = c.take<float>((size_t)K * N);
   const int64_t tiles = dw_swapped(K, N) ? ceil_div(K, BM) * ceil_div(N, 256)
                                          : ceil_div(N, BM) * ceil_div(K, 256);
@@ -1238,10 +1255,10 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
   const int64_t ldt = (N + 3) / 4 * 4;
   // dX = dY W : K-major A = dY [M, N], K-major B = W^T [K, N]
   if (dX) {
-    transpose_kernel<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, st>>>(W, N, K, ldw, w.Wt,
+    transpose_hilo_kernel<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, st>>>(W, N, K, ldw, w.Wt,
                                                                              ldt);
     RNN_LAUNCH_CHECK();
-    RNN_TRY(gemm_kk(dY, M, N, lddy, w.Wt, K, ldt, nullptr, dX, lddx, prec, st));
+    RNN_TRY(gemm_kk(dY, M, N, lddy, w.Wt, K, ldt, nullptr, dX, lddx, prec, st, true));
   }
   // dW = dY^T X : both operands MN-major, split over M, ordered reduction
   if (M == 0) {
