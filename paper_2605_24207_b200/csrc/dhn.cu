@@ -286,7 +286,10 @@ __device__ __forceinline__ int64_t h4_lower(const int32_t* L, int64_t b, int64_t
   return b;
 }
 
-constexpr int H4_LONG = 96;                 // runs longer than this are split over all warps
+#ifndef H4_LONG_CFG
+#define H4_LONG_CFG 96
+#endif
+constexpr int H4_LONG = H4_LONG_CFG;        // runs longer than this are split over all warps
 constexpr int H4_LONG_MAX = 512;             // long runs queued per sweep (overflow: inline)
 
 // One 32-entry chunk of a run: OUT inserts w and adds f1(v) to S1(w) (one 128-byte red per
