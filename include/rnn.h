@@ -36,8 +36,9 @@
  * - Keys are signed int64 (any value).  Row ids are int32 (relations < 2^31 rows); join-row
  *   counts and CSR pointers are int64.
  * - Determinism: identical inputs give bit-identical outputs (no floating-point atomics on
- *   any path; every reduction has a fixed order) -- except the k = 3 / 4 DHN aggregates
- *   (A6), whose hash-table accumulation uses fp32 atomics (rounding order only).
+ *   any path; every reduction has a fixed order) -- except the k = 4 DHN aggregates (A6),
+ *   whose hash-table accumulation uses fp32 atomics (rounding order only); the exact
+ *   integer walk counts (rnn_dhn_count) are deterministic.
  */
 #ifndef RNN_H
 #define RNN_H
@@ -287,6 +288,19 @@ rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k, const rnn_ope
                              const float* d_out, int64_t ld_dout, const float* walk_sum,
                              int64_t ld_ws, float* const* d_f, int64_t ld_df, uint32_t flags,
                              void* workspace, size_t workspace_bytes, void* stream);
+
+/* Exact closed-walk (homomorphism) counts: counts[g] = number of closed k-walks rooted at
+ * group g's node, with Edge multiplicity -- C_k(n) of the rule above with every operand 1,
+ * i.e. (A^k)_nn of the Edge relation's (multi)adjacency matrix (Eq. 3 :1500
+ * with mu = 1; k = 2: the out-degree, the single Edge atom of the C2 rule :1509).  Integer
+ * arithmetic throughout (int64 totals, uint64 partial counts), so the result is exact and
+ * deterministic -- unlike rnn_dhn_fwd, whose fp32 atomics are exact only below 2^24 and in
+ * any rounding order.  adj: as for rnn_dhn_fwd.  counts [n_groups] int64 (device, group
+ * order), overwritten.  workspace: rnn_dhn_count_workspace_size (host-only query).
+ * k outside 2..4: RNN_ERR_UNSUPPORTED. */
+rnn_status rnn_dhn_count_workspace_size(const rnn_join_index* adj, int32_t k, size_t* bytes);
+rnn_status rnn_dhn_count(const rnn_join_index* adj, int32_t k, int64_t* counts, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* ===================================================================================== */
 /* Program helpers                                                                       */

@@ -10,6 +10,15 @@
 
 #include "../../include/rnn.h"
 
+// Measurement probes (clock64 phase timers, event counters read through the
+// rnn_internal_*_stats hooks) are compiled in only for measurement builds (-DRNN_PROBES);
+// the production library carries none of them.
+#ifdef RNN_PROBES
+#define RNN_PROBE(...) __VA_ARGS__
+#else
+#define RNN_PROBE(...)
+#endif
+
 namespace rnn {
 
 // --------------------------------------------------------------------------------------

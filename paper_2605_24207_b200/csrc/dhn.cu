@@ -78,6 +78,15 @@ __device__ __forceinline__ int64_t dhn_next_root(const DhnArgs& a, int* s_root) 
   return i < a.G ? (int64_t)a.order[i] : -1;
 }
 
+// Path counters of the walk kernels (which code paths a launch took), read by the internal
+// hook rnn_internal_dhn_stats so the tests can prove the big-root paths ran:
+//   [0] C3 roots, [1] C3 roots on the global mark array (in-degree > H3_MAX_INDEG),
+//   [2] C4 roots, [3] C4 (root, partition) passes, [4] of them in chunked mode,
+//   [5] C4 long runs queued for phase B, [6] long runs past the queue (walked inline),
+//   [7] C4 roots with hash partitions (P > 1).
+// Counted per CTA (registers / shared memory) and added once per CTA at exit.
+__device__ unsigned long long g_dhn_paths[16];
+
 // -------------------------------------------------------------------------------------
 // shared-memory open-addressing hash sets keyed by group id (linear probing, key -1 = empty)
 // -------------------------------------------------------------------------------------
@@ -126,12 +135,15 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
   int* mark = a.mark + (int64_t)blockIdx.x * a.cta_stride;
   const int d = a.d;
   for (int i = threadIdx.x; i < H3_CAP; i += DHN_THREADS) { keys[i] = -1; cnt[i] = 0; }
+  unsigned long long c_roots = 0, c_mark = 0;   // path counters (thread 0)
   for (;;) {
     const int64_t n = dhn_next_root(a, &s_root);
     if (n < 0) break;
     const int32_t r = a.row_of[n];
     const int64_t ib = a.sp[r], ie = a.sp[r + 1];
     const bool hashed = ie - ib <= H3_MAX_INDEG;
+    ++c_roots;
+    c_mark += !hashed;
     if (hashed) {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS)
         atomicAdd(&cnt[hs_insert(keys, H3_CAP - 1, a.sg[q])], 1);
@@ -224,6 +236,10 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) mark[a.sg[q]] = 0;
     }
   }
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_dhn_paths[0], c_roots);
+    atomicAdd(&g_dhn_paths[1], c_mark);
+  }
 }
 
 // -------------------------------------------------------------------------------------
@@ -238,18 +254,23 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
 // starts where partition k-1 ended: per-neighbour cursors in shared memory make each pass
 // touch only its own entries (no re-scan), lanes test 32 neighbours' cursors at a time.
 // -------------------------------------------------------------------------------------
-// phase timing of dhn4_kernel (thread 0's clock between barriers), read by the internal hook
-// rnn_internal_dhn_stats: [0] root setup, [1] out sweep, [2] finalize, [3] in sweep,
-// [4] clear, [5] reduce/store, [6] partitions, [7] roots, [8] chunked partitions
-__device__ unsigned long long g_dhn4_stats[16];
+// measurement builds only (-DRNN_PROBES): thread 0's clock between the C4 phases
+// [0] root setup, [1] out sweep, [3] in sweep, [4] clear, [5] reduce/store
+__device__ unsigned long long g_dhn4_clock[16];
+#ifdef RNN_PROBES
 #define H4_T(slot)                                                                  \
   do {                                                                              \
     if (threadIdx.x == 0) {                                                         \
       const long long t_ = clock64();                                               \
-      atomicAdd(&g_dhn4_stats[slot], (unsigned long long)(t_ - t_last));            \
+      atomicAdd(&g_dhn4_clock[slot], (unsigned long long)(t_ - t_last));            \
       t_last = t_;                                                                  \
     }                                                                               \
   } while (0)
+#else
+#define H4_T(slot) \
+  do {             \
+  } while (0)
+#endif
 
 // C4 CTA shape (compile-time; -D overrides for measurement builds)
 #ifndef H4_THREADS_CFG
@@ -434,7 +455,7 @@ struct H4Root {
 template <bool OUT, bool V4, bool DUAL = false>
 __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids, int* n_ids,
                           float* S, int* cur, int* q_i, int64_t* q_b, int64_t* q_e, int* q_n,
-                          int* grab, int c, bool cok, float4* acc_b = nullptr) {
+                          int* grab, int c, bool cok, int* s_cnt, float4* acc_b = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int32_t* L = OUT ? a.nbrh : a.sgh;
   const float* Fv = OUT ? a.F1 : a.F3;
@@ -499,10 +520,11 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         if (lane == 0) slot = atomicAdd(q_n, 1);
         slot = __shfl_sync(FULL, slot, 0);
         if (slot < H4_LONG_MAX) {
-          if (lane == 0) { q_i[slot] = uj; q_b[slot] = bj; q_e[slot] = re; }
+          if (lane == 0) { q_i[slot] = uj; q_b[slot] = bj; q_e[slot] = re; atomicAdd(&s_cnt[0], 1); }
           if (R.cur_ok && lane == 0) cur[ij] = (int)(re - sj);
           continue;
         }
+        if (lane == 0) atomicAdd(&s_cnt[1], 1);   // queue full: walk this long run inline
       }
       float fv = 0.f, t = 0.f;
       float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4, t4b = fv4;
@@ -591,15 +613,17 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
   int64_t* q_e = q_b + H4_LONG_MAX;
   int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
   __shared__ int s_root, q_n, n_ids, grab;
+  __shared__ int s_cnt[2];   // long runs queued / walked inline (queue full)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = a.d;
   for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
-  if (threadIdx.x == 0) { q_n = 0; n_ids = 0; grab = 0; }
-  long long t_last = clock64();
+  if (threadIdx.x == 0) { q_n = 0; n_ids = 0; grab = 0; s_cnt[0] = 0; s_cnt[1] = 0; }
+  RNN_PROBE(long long t_last = clock64();)
+  unsigned long long c_roots = 0, c_parts = 0, c_chunked = 0, c_multi = 0;   // thread 0
   for (;;) {
     const int64_t n = dhn_next_root(a, &s_root);
     if (n < 0) break;
-    if (threadIdx.x == 0) atomicAdd(&g_dhn4_stats[7], 1ull);
+    ++c_roots;
     const int32_t r = a.row_of[n];
     const int64_t ib = a.sp[r], ie = a.sp[r + 1];
     const int64_t pb = a.gp[n], pe = a.gp[n + 1];
@@ -612,6 +636,7 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
     // lanes test 32 neighbours per step only when a neighbour's list has under one entry
     // per partition on average (hubs); otherwise one neighbour per warp
     R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
+    c_multi += R.P > 1;
     for (int c0 = 0; c0 < d; c0 += 32) {
       const int c = c0 + lane;
       const bool cok = c < d;
@@ -624,19 +649,18 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
       H4_T(0);
       for (uint32_t part = 0; part < R.P; ++part) {
         R.part = part;
-        if (threadIdx.x == 0) {
-          atomicAdd(&g_dhn4_stats[6], 1ull);
-          if (R.chunked) atomicAdd(&g_dhn4_stats[8], 1ull);
-        }
+        ++c_parts;
+        c_chunked += R.chunked;
         // (1) S1(w) += f1(v) over out-wedges n -> v -> w of this partition
         R.deg = deg_out;
-        h4_sweep<true, V4>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c, cok);
+        h4_sweep<true, V4>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c, cok,
+                           s_cnt);
         H4_T(1);
         // (3) acc += f3(p) (.) G(w) over in-wedges w -> p -> n of this partition
         R.deg = deg_in;
         {
           const float4 r4 = h4_sweep<false, V4, DUAL>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b,
-                                                      q_e, &q_n, &grab, c, cok, &acc_b);
+                                                      q_e, &q_n, &grab, c, cok, s_cnt, &acc_b);
           acc.x += r4.x; acc.y += r4.y; acc.z += r4.z; acc.w += r4.w;
         }
         H4_T(3);
@@ -686,6 +710,14 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
       }
       H4_T(5);
     }
+  }
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_dhn_paths[2], c_roots);
+    atomicAdd(&g_dhn_paths[3], c_parts);
+    atomicAdd(&g_dhn_paths[4], c_chunked);
+    atomicAdd(&g_dhn_paths[5], (unsigned long long)s_cnt[0]);
+    atomicAdd(&g_dhn_paths[6], (unsigned long long)s_cnt[1]);
+    atomicAdd(&g_dhn_paths[7], c_multi);
   }
 }
 
@@ -788,6 +820,134 @@ __global__ void work_kernel(int k, int64_t G, const int64_t* __restrict__ gp,
     key[n] = cap - (uint32_t)(w < (int64_t)cap ? w : cap);
     order[n] = (int32_t)n;
   }
+}
+
+// -------------------------------------------------------------------------------------
+// Exact closed-walk counts (rnn_dhn_count): C_k(n) with every operand 1, in int64.
+// The float kernels above accumulate with fp32 atomics (exact only below 2^24 and in any
+// rounding order); this integer path is the homomorphism count itself (PAPER.md:1481,
+// Eq. 3 :1500 with mu = 1): (A^k)_nn for k = 3, 4.  One CTA per root (heaviest first), a
+// shared-memory hash of group id -> uint64 count, and P = 2^b passes over hash partitions
+// of the keyed vertex when the root could name more keys than the table holds:
+//   k = 3: key = in-neighbour w of n (count = closing Edge rows w -> n); every out-wedge
+//          n -> v -> w of the pass adds count(w);
+//   k = 4: key = middle vertex w, count = S1(n, w) = #(n -> v -> w); every in-wedge
+//          w -> p -> n of the pass adds S1(n, w)   (= sum_w S1(n, w) S3(n, w)).
+// -------------------------------------------------------------------------------------
+constexpr int HC_THREADS = 512;
+constexpr int HC_CAP = 8192;      // slots: int32 key + uint64 count = 96 KB
+constexpr int HC_PART = HC_CAP / 2;
+
+struct CountArgs {
+  int k;
+  int64_t G;
+  const int64_t* gp; const int32_t* nbr; const int64_t* sp; const int32_t* sg;
+  const int32_t* row_of; const int32_t* order; int* counter; const uint32_t* wout;
+  int64_t* out;
+};
+
+__device__ __forceinline__ uint32_t hc_part(int32_t w, int bits) {
+  return bits ? dhn_hash((uint32_t)w ^ 0x2545F491u) >> (32 - bits) : 0u;
+}
+
+// count one occurrence of key w.  The table never fills: a pass holds at most
+// max(bound, 2 * HC_PART / 2^bits ...) keys -- cap >= 2 (bound / P + 1) -- so a failed insert
+// (slot -1) cannot happen; it is still guarded (no out-of-range shared store).
+__device__ __forceinline__ void hc_add(unsigned long long* cnt, int* keys, int mask, int32_t w) {
+  const int sl = hs_insert(keys, mask, w);
+  if (sl >= 0) atomicAdd(&cnt[sl], 1ull);
+}
+
+__global__ void __launch_bounds__(HC_THREADS) dhn_count_kernel(CountArgs a) {
+  extern __shared__ unsigned long long hc_raw[];
+  unsigned long long* cnt = hc_raw;                       // [HC_CAP]
+  int* keys = reinterpret_cast<int*>(cnt + HC_CAP);        // [HC_CAP]
+  __shared__ int s_root;
+  __shared__ long long s_tot[HC_THREADS / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = HC_THREADS / 32;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_root = atomicAdd(a.counter, 1);
+    __syncthreads();
+    if (s_root >= a.G) break;
+    const int64_t n = a.order[s_root];
+    const int32_t r = a.row_of[n];
+    const int64_t pb = a.gp[n], pe = a.gp[n + 1], ib = a.sp[r], ie = a.sp[r + 1];
+    // bound on the distinct keys of the table: k = 3 the in-degree, k = 4 the out-wedges
+    int64_t bound = a.k == 3 ? ie - ib : (int64_t)a.wout[n];
+    if (bound > a.G) bound = a.G;
+    int bits = 0;
+    while (((int64_t)HC_PART << bits) < bound) ++bits;
+    int cap = 32;
+    while (cap < HC_CAP && (int64_t)cap < 2 * ((bound >> bits) + 1)) cap <<= 1;
+    const int mask = cap - 1;
+    long long tot = 0;
+    for (uint32_t part = 0; part < (1u << bits); ++part) {
+      for (int i = threadIdx.x; i < cap; i += HC_THREADS) { keys[i] = -1; cnt[i] = 0; }
+      __syncthreads();
+      if (a.k == 3) {
+        // keys: in-neighbours of this partition, with multiplicity
+        for (int64_t q = ib + threadIdx.x; q < ie; q += HC_THREADS) {
+          const int32_t w = a.sg[q];
+          if (hc_part(w, bits) == part) hc_add(cnt, keys, mask, w);
+        }
+      } else {
+        // S1(n, w): out-wedges n -> v -> w (w must have out-edges to continue the walk)
+        for (int64_t pos = pb + warp; pos < pe; pos += NW) {
+          const int32_t v = a.nbr[pos];
+          if (v < 0) continue;
+          for (int64_t i = a.gp[v] + lane; i < a.gp[v + 1]; i += 32) {
+            const int32_t w = a.nbr[i];
+            if (w >= 0 && hc_part(w, bits) == part) hc_add(cnt, keys, mask, w);
+          }
+        }
+      }
+      __syncthreads();
+      if (a.k == 3) {
+        // out-wedges n -> v -> w closing on a keyed in-neighbour w
+        for (int64_t pos = pb + warp; pos < pe; pos += NW) {
+          const int32_t v = a.nbr[pos];
+          if (v < 0) continue;
+          for (int64_t i = a.gp[v] + lane; i < a.gp[v + 1]; i += 32) {
+            const int32_t w = a.nbr[i];
+            if (w >= 0 && hc_part(w, bits) == part) {
+              const int sl = hs_find(keys, mask, w);
+              if (sl >= 0) tot += (long long)cnt[sl];
+            }
+          }
+        }
+      } else {
+        // in-wedges w -> p -> n: p = in-neighbour of n, w = in-neighbour of p
+        for (int64_t q = ib + warp; q < ie; q += NW) {
+          const int32_t pg = a.sg[q];
+          const int32_t rp = a.row_of[pg];
+          for (int64_t i = a.sp[rp] + lane; i < a.sp[rp + 1]; i += 32) {
+            const int32_t w = a.sg[i];
+            if (hc_part(w, bits) == part) {
+              const int sl = hs_find(keys, mask, w);
+              if (sl >= 0) tot += (long long)cnt[sl];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+    if (lane == 0) s_tot[warp] = tot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t = 0;
+      for (int w = 0; w < NW; ++w) t += s_tot[w];
+      a.out[n] = t;
+    }
+  }
+}
+
+__global__ void dhn_count2_kernel(int64_t G, const int64_t* __restrict__ gp, int64_t* __restrict__ out) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < G) out[g] = gp[g + 1] - gp[g];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1163,12 +1323,84 @@ static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
   return RNN_OK;
 }
 
-extern "C" int rnn_internal_dhn_stats(unsigned long long* out, int reset) {
-  if (cudaMemcpyFromSymbol(out, rnn::g_dhn4_stats, sizeof(unsigned long long) * 16) != cudaSuccess)
-    return 1;
+// ---- exact counts ----
+namespace {
+struct CountBufs {
+  int32_t* gor; int32_t* nbr; uint32_t* key; int32_t* order; int* counter; uint32_t* wout;
+  void* sort_ws;
+};
+CountBufs carve_count(const rnn_join_index* adj, void* base, size_t* used) {
+  Carve c(base);
+  CountBufs b;
+  const int64_t G = adj->n_groups, E = adj->n_join_rows, R = adj->n_src_rows;
+  b.gor = c.take<int32_t>(R);
+  b.nbr = c.take<int32_t>(E);
+  b.key = c.take<uint32_t>(G);
+  b.order = c.take<int32_t>(G);
+  b.counter = c.take<int>(64);
+  b.wout = c.take<uint32_t>(G);
+  b.sort_ws = c.take<char>(radix_sort_workspace_bytes(G));
+  if (used) *used = (c.used + 255) & ~size_t(255);
+  return b;
+}
+}  // namespace
+
+extern "C" rnn_status rnn_dhn_count_workspace_size(const rnn_join_index* adj, int32_t k,
+                                                   size_t* bytes) {
+  clear_error();
+  RNN_TRY(check_adj(adj, k, 1));
+  RNN_REQUIRE(bytes, RNN_ERR_INVALID_ARGUMENT, "bytes is NULL");
+  carve_count(adj, nullptr, bytes);
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_dhn_count(const rnn_join_index* adj, int32_t k, int64_t* counts,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_TRY(check_adj(adj, k, 1));
+  const int64_t G = adj->n_groups;
+  RNN_REQUIRE(counts || G == 0, RNN_ERR_INVALID_ARGUMENT, "counts is NULL");
+  size_t need = 0;
+  CountBufs b = carve_count(adj, workspace, &need);
+  RNN_REQUIRE(workspace && workspace_bytes >= need, RNN_ERR_WORKSPACE_TOO_SMALL,
+              "DHN count workspace needs %zu bytes (rnn_dhn_count_workspace_size)", need);
+  if (G == 0) return RNN_OK;
+  cudaStream_t st = as_stream(stream);
+  if (k == 2) {
+    dhn_count2_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(G, adj->group_ptr, counts);
+    RNN_LAUNCH_CHECK();
+    return RNN_OK;
+  }
+  const int64_t E = adj->n_join_rows, R = adj->n_src_rows;
+  RNN_CUDA(cudaMemsetAsync(b.gor, 0xff, sizeof(int32_t) * std::max<int64_t>(R, 1), st));
+  RNN_CUDA(cudaMemsetAsync(b.counter, 0, sizeof(int) * 64, st));
+  grp_of_row_kernel<<<(unsigned)ceil_div(G, 256), 256, 0, st>>>(adj->group_dst_row, G, b.gor);
+  if (E > 0) nbr_kernel<<<(unsigned)ceil_div(E, 256), 256, 0, st>>>(adj->src_row, E, b.gor, b.nbr);
+  // heaviest roots first; k = 4 also yields the out-wedge bound wout
+  work_kernel<<<(unsigned)ceil_div(G, 8), 256, 0, st>>>(4, G, adj->group_ptr, b.nbr, adj->src_ptr,
+                                                        adj->src_group, adj->group_dst_row, b.key,
+                                                        b.order, b.wout);
+  RNN_LAUNCH_CHECK();
+  RNN_TRY(radix_sort_u32(b.key, b.order, G, 24, b.sort_ws, st));
+  CountArgs a{k, G, adj->group_ptr, b.nbr, adj->src_ptr, adj->src_group, adj->group_dst_row,
+              b.order, b.counter, b.wout, counts};
+  const size_t smem = (size_t)HC_CAP * (sizeof(unsigned long long) + sizeof(int));
+  RNN_CUDA(cudaFuncSetAttribute(dhn_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
+  const int n_cta = (int)std::min<int64_t>((int64_t)num_sms() * 2, G);
+  dhn_count_kernel<<<n_cta, HC_THREADS, smem, st>>>(a);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+// internal hook (not part of rnn.h): which = 0 -> the path counters g_dhn_paths,
+// 1 -> the C4 phase clocks (measurement builds only; zeros otherwise).  SYNC.
+extern "C" int rnn_internal_dhn_stats(unsigned long long* out, int reset, int which) {
+  const void* sym = which ? (const void*)&rnn::g_dhn4_clock : (const void*)&rnn::g_dhn_paths;
+  if (cudaMemcpyFromSymbol(out, sym, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
   if (reset) {
     unsigned long long z[16] = {0};
-    if (cudaMemcpyToSymbol(rnn::g_dhn4_stats, z, sizeof(z)) != cudaSuccess) return 1;
+    if (cudaMemcpyToSymbol(sym, z, sizeof(z)) != cudaSuccess) return 1;
   }
   return 0;
 }

@@ -701,6 +701,13 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
   if (d_dst && q->dst.mode == RNN_BY_ROW && idx->n_groups < idx->n_dst_rows)
     RNN_TRY(zero2d(d_dst, q->dst.ld, q->dst.dim, idx->n_dst_rows));
   if (idx->n_groups == 0) return RNN_OK;
+  if (idx->n_join_rows == 0) {
+    // dense groups over an empty join: every group-side gradient is 0 (no work items run)
+    if (d_dst)
+      RNN_TRY(zero2d(d_dst, q->dst.ld, q->dst.dim,
+                     q->dst.mode == RNN_BY_ROW ? idx->n_dst_rows : idx->n_groups));
+    return RNN_OK;
+  }
   LjaArgs a = make_args(idx, q, nullptr, 0, 0.f, nullptr, qi.D);
   const int64_t ld4 = (qi.D + 3) / 4 * 4;
 

@@ -401,6 +401,12 @@ __global__ void __launch_bounds__(256) fwd_concat_kernel(LjaArgs a, int64_t n_gr
   }
 }
 
+// lse of groups with no join row (dense index, E' = 0): log-sum-exp of {} = -inf
+__global__ void fill_neg_inf_kernel(float* __restrict__ p, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) p[i] = -INFINITY;
+}
+
 template <template <class> class Pol, class L>
 rnn_status launch_pol(Pol<L> pol, const SegCtx& cx, cudaStream_t st) {
   if (cx.n_work <= 0) return RNN_OK;
@@ -447,6 +453,19 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
   RNN_REQUIRE(beta == 0.f || q->agg != RNN_AGG_MEAN, RNN_ERR_UNSUPPORTED,
               "beta = 1 with MEAN is not decomposable (PAPER.md:340)");
   if (idx->n_groups == 0) return RNN_OK;
+  if (idx->n_join_rows == 0 && !qi.concat) {
+    // every group is empty (dense index over an empty join): the aggregate of {} is 0, so
+    // out = beta * out + 0, and lse = -inf -- no work items exist for the walkers to do this
+    if (beta == 0.f)
+      RNN_CUDA(cudaMemset2DAsync(out, sizeof(float) * ld_out, 0, sizeof(float) * qi.D,
+                                 idx->n_groups, st));
+    if (q->agg == RNN_AGG_SOFTMAX && lse) {
+      const int64_t n = idx->n_groups * q->heads;
+      fill_neg_inf_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(lse, n);
+      RNN_LAUNCH_CHECK();
+    }
+    return RNN_OK;
+  }
   LjaArgs a = make_args(idx, q, out, ld_out, beta, lse, qi.D);
   if (qi.concat) {
     fwd_concat_kernel<<<(unsigned)ceil_div(idx->n_groups, 8), 256, 0, st>>>(a, idx->n_groups);

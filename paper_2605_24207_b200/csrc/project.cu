@@ -208,9 +208,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long gs_t0 = clock64();
-  unsigned long long gs_w[5] = {0, 0, 0, 0, 0};
-  __shared__ long long gs_issue[MAX_STAGES];
+  RNN_PROBE(const long long gs_t0 = clock64(); unsigned long long gs_w[5] = {0, 0, 0, 0, 0};
+            __shared__ long long gs_issue[MAX_STAGES];)
   const int64_t m0 = (int64_t)blockIdx.x * BM;
   const int n0 = blockIdx.y * p.BN;
   const int64_t kbeg = (int64_t)blockIdx.z * p.k_split;
@@ -254,11 +253,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
         if (kb >= p.stages) {
-          const long long t0 = clock64();
+          RNN_PROBE(const long long t0 = clock64();)
           mbar_wait(&empty[s], ph ^ 1);
-          gs_w[0] += clock64() - t0;
+          RNN_PROBE(gs_w[0] += clock64() - t0;)
         }
-        gs_issue[s] = clock64();
+        RNN_PROBE(gs_issue[s] = clock64();)
         const bool blo = SPLIT3 && !B_MN && p.b_lo_row > 0;
         mbar_expect_tx(&full[s], A_BYTES + B_BYTES * (blo ? 2u : 1u));
         const int k = (int)(kbeg + (int64_t)kb * KB);
@@ -283,8 +282,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             tma_load_2d(&tb, b_hi(s) + j * (KB * 128), &full[s], n0 + 32 * j, k);
         }
       }
-      atomicAdd(&g_gemm_stats[8], (unsigned long long)(clock64() - gs_t0));
-      atomicAdd(&g_gemm_stats[0], gs_w[0]);
+      RNN_PROBE(atomicAdd(&g_gemm_stats[8], (unsigned long long)(clock64() - gs_t0));
+                atomicAdd(&g_gemm_stats[0], gs_w[0]);)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
@@ -293,11 +292,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = kb % p.stages;
       const uint32_t ph = (kb / p.stages) & 1;
       {
-        const long long t0 = clock64();
+        RNN_PROBE(const long long t0 = clock64();)
         mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
-        const long long t1 = clock64();
-        gs_w[1] += t1 - t0;
-        if (!SPLIT3) { gs_w[3] += t1 - *(volatile long long*)&gs_issue[s]; gs_w[4] += 1; }
+        RNN_PROBE(const long long t1 = clock64(); gs_w[1] += t1 - t0;
+                  if (!SPLIT3) { gs_w[3] += t1 - *(volatile long long*)&gs_issue[s]; gs_w[4] += 1; })
       }
       tc_fence_after();
       if (lane == 0) {
@@ -319,11 +317,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if (lane == 0) tc_commit(acc_full);
     __syncwarp();
-    if (lane == 0) {
+    RNN_PROBE(if (lane == 0) {
       atomicAdd(&g_gemm_stats[9], (unsigned long long)(clock64() - gs_t0));
       atomicAdd(&g_gemm_stats[1], gs_w[1]);
       if (!SPLIT3) { atomicAdd(&g_gemm_stats[3], gs_w[3]); atomicAdd(&g_gemm_stats[4], gs_w[4]); }
-    }
+    })
   } else {
     // ---------------- converters (3xTF32): warps 2..9; epilogue: warps 2..5 ----------------
     const int et = threadIdx.x - 64;  // 0..255
@@ -332,12 +330,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
         {
-          const long long t0 = clock64();
+          RNN_PROBE(const long long t0 = clock64();)
           mbar_wait(&full[s], ph);
-          const long long t1 = clock64();
-          gs_w[2] += t1 - t0;
-          gs_w[3] += t1 - *(volatile long long*)&gs_issue[s];
-          gs_w[4] += 1;
+          RNN_PROBE(const long long t1 = clock64(); gs_w[2] += t1 - t0;
+                    gs_w[3] += t1 - *(volatile long long*)&gs_issue[s]; gs_w[4] += 1;)
         }
         // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
         lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(a_hi(s)),
@@ -349,10 +345,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_arrive(&conv[s]);
       }
     }
-    if (lane == 0 && warp == 2) {
+    RNN_PROBE(if (lane == 0 && warp == 2) {
       atomicAdd(&g_gemm_stats[10], (unsigned long long)(clock64() - gs_t0));
       for (int i = 2; i < 5; ++i) atomicAdd(&g_gemm_stats[i], gs_w[i]);
-    }
+    })
     if (warp < 6) mbar_wait(acc_full, 0);   // warps 6-9 only convert
     tc_fence_after();
     const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) belong to this warp
@@ -632,12 +628,19 @@ constexpr int PX_STAGES = 6;
 // [4] converter waits for a landed stage, [5] epilogue waits for an accumulator;
 // [8..11] total cycles of the producer, MMA, converter, epilogue lanes
 __device__ unsigned long long g_proj_stats[16];
+#ifdef RNN_PROBES
 #define PT_WAIT(slot, stmt)                                      \
   do {                                                           \
     const long long t0_ = clock64();                             \
     stmt;                                                        \
     if (lane == 0) pt_w[slot] += (unsigned long long)(clock64() - t0_); \
   } while (0)
+#else
+#define PT_WAIT(slot, stmt) \
+  do {                      \
+    stmt;                   \
+  } while (0)
+#endif
 
 struct ProjTParams {
   int64_t M;            // rows of X / Y
@@ -687,8 +690,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long pt_t0 = clock64();
-  unsigned long long pt_w[6] = {0, 0, 0, 0, 0, 0};
+  RNN_PROBE(const long long pt_t0 = clock64(); unsigned long long pt_w[6] = {0, 0, 0, 0, 0, 0};)
   const int nt = blockIdx.x % p.n_tiles_n;
   const int n0 = nt * 128;
   const int64_t mt0 = blockIdx.x / p.n_tiles_n;
@@ -889,12 +891,12 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
-  if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 6)) {
+  RNN_PROBE(if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 6)) {
     const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : 3;
     atomicAdd(&g_proj_stats[8 + role], (unsigned long long)(clock64() - pt_t0));
     for (int i = 0; i < 6; ++i)
       if (pt_w[i]) atomicAdd(&g_proj_stats[i], pt_w[i]);
-  }
+  })
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

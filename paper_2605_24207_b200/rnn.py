@@ -96,10 +96,14 @@ def lib():
                                         vp, i64, C.POINTER(vp), i64, C.c_uint32, vp, sz, vp]
         L.rnn_dhn_bwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
                                   C.POINTER(vp), i64, vp, sz, vp]
+        L.rnn_dhn_count_workspace_size.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(sz)]
+        L.rnn_dhn_count.argtypes = [C.POINTER(JoinIndexC), i32, vp, vp, sz, vp]
+        L.rnn_internal_dhn_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]
         L.rnn_gcn_norm_src_deg.argtypes = [C.POINTER(JoinIndexC), vp, vp, vp]
         L.rnn_group_sizes.argtypes = [C.POINTER(JoinIndexC), vp, vp]
         for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd", "rnn_dhn_fwd_save",
-                  "rnn_dhn_bwd_saved", "rnn_gcn_norm_src_deg",
+                  "rnn_dhn_bwd_saved", "rnn_gcn_norm_src_deg", "rnn_dhn_count_workspace_size",
+                  "rnn_dhn_count", "rnn_internal_dhn_stats",
                   "rnn_group_sizes"):
             getattr(L, f).restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
@@ -477,3 +481,29 @@ def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=No
     _check(lib().rnn_dhn_bwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out), d_out.stride(0), ptrs,
                              ld, _ptr(w), w.numel(), _stream(stream)))
     return d_f
+
+
+def dhn_count(adj: JoinIndex, k, out=None, stream=None):
+    """Exact closed-walk counts C_k(n) (all operands 1) per root in group order, int64
+    (rnn_dhn_count): (A^k)_nn of the Edge relation, with multiplicity."""
+    dev = adj.group_ptr.device
+    if out is None:
+        out = torch.empty(max(adj.n_groups, 1), dtype=torch.int64, device=dev)[:adj.n_groups]
+    b = C.c_size_t(0)
+    _check(lib().rnn_dhn_count_workspace_size(C.byref(adj.c), k, C.byref(b)))
+    w = _ws(b.value, dev)
+    _check(lib().rnn_dhn_count(C.byref(adj.c), k, _ptr(out), _ptr(w), w.numel(), _stream(stream)))
+    return out
+
+
+DHN_PATHS = ("c3_roots", "c3_mark_roots", "c4_roots", "c4_passes", "c4_chunked_passes",
+             "c4_long_runs", "c4_long_overflow", "c4_partitioned_roots")
+
+
+def dhn_path_counters(reset=False):
+    """Internal: which code paths the DHN walk kernels took since the last reset (SYNC)."""
+    torch.cuda.synchronize()
+    buf = (C.c_ulonglong * 16)()
+    if lib().rnn_internal_dhn_stats(buf, 1 if reset else 0, 0) != 0:
+        raise RuntimeError("rnn_internal_dhn_stats failed")
+    return dict(zip(DHN_PATHS, [int(x) for x in buf[:len(DHN_PATHS)]]))

@@ -20,12 +20,12 @@ f = prog._f(4, prog.Y)
 rnn.project(prog.H, prog.W, out=prog.Y)
 rnn.dhn_fwd(prog.idx, 4, f, out=prog.out[:, :prog.d], ws=prog.ws)
 torch.cuda.synchronize()
-L.rnn_internal_dhn_stats(st, 1)
+L.rnn_internal_dhn_stats(st, 1, 1)
 t = time.time()
 rnn.dhn_fwd(prog.idx, 4, f, out=prog.out[:, :prog.d], ws=prog.ws)
 torch.cuda.synchronize()
 el = time.time() - t
-L.rnn_internal_dhn_stats(st, 0)
+L.rnn_internal_dhn_stats(st, 0, 1)
 names = ["root setup", "out sweep", "finalize G", "in sweep", "clear", "reduce/store"]
 tot = sum(st[i] for i in range(6))
 print(f"scale {scale}: dhn4 fwd {el * 1e3:.1f} ms wall; roots {st[7]}, partitions {st[6]}, chunked {st[8]}")

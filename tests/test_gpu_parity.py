@@ -351,3 +351,35 @@ def test_projection_repeat_bitwise(R, M, K, N):
         assert torch.equal(R.project(Xd, Wd), Y0)
         dX, dW, _ = R.project_bwd(Xd, Wd, dYd)
         assert torch.equal(dX, dX0) and torch.equal(dW, dW0)
+
+
+@pytest.mark.parametrize("agg", ["sum", "softmax"])
+def test_empty_join_dense_groups(R, agg):
+    """Dense-group index over an empty join (no S key matches): every T row is a group with no
+    rows, so out = 0 (beta = 0; beta = 1 leaves out unchanged), lse = -inf and every gradient
+    is 0 -- even though there are no work items (rnn.h contract)."""
+    gi = R.build_join_index(cu(np.array([5, 6, 5])), cu(np.array([7, 8, 8])), cu(np.array([1, 2])),
+                            cu(np.array([7, 8, 9])), dense_groups=True)
+    assert gi.n_join_rows == 0 and gi.n_groups == 3
+    D, h = (8, 1) if agg == "sum" else (128, 8)
+    src = padded(np.ones((2, D), np.float32))
+    if agg == "sum":
+        q = R.make_query("mul", "sum", src=src, dst=padded(np.ones((3, D), np.float32)))
+    else:
+        q = R.make_query("src", "softmax", src=src, src_key=src, dst=padded(np.ones((3, D), np.float32)),
+                         heads=h, scale=0.25)
+    out = padded(np.full((3, D), np.nan, np.float32))
+    lse = torch.full((3, h), 7.0, device="cuda") if agg == "softmax" else None
+    R.join_aggregate_fwd(gi, q, out=out, lse=lse)
+    assert torch.count_nonzero(out) == 0
+    if lse is not None:
+        assert bool(torch.all(torch.isneginf(lse)))
+    base = padded(np.full((3, D), 2.0, np.float32))
+    R.join_aggregate_fwd(gi, q, out=base, lse=lse, beta=1.0)
+    assert bool(torch.all(base == 2.0))
+    dO = padded(np.ones((3, D), np.float32))
+    kw = {"out": out, "lse": lse} if agg == "softmax" else {}
+    g = R.join_aggregate_bwd(gi, q, dO, **kw)
+    for k in ("src", "src_key", "dst"):
+        if g.get(k) is not None:
+            assert torch.count_nonzero(g[k]) == 0, k
