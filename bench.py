@@ -39,18 +39,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="arxiv", choices=["arxiv", "cora", "hyper", "mag", "dhn"])
-    ap.add_argument("--dhn-scale", type=float, default=0.1,
+    ap.add_argument("--config", default="mag", choices=["arxiv", "cora", "hyper", "mag", "dhn"],
+                    help="workload (default: MAG-shaped HGT, the largest single-GPU config)")
+    ap.add_argument("--dhn-scale", type=float, default=1.0,
                     help="fraction of the ogbn-products-shaped graph for --config dhn")
     ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32"])
-    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--seeds", default=None,
+                    help="comma-separated input seeds (default 42..46, PAPER.md:851; dhn: 42)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="launch the step kernel by kernel instead of replaying its CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-launches", action="store_true",
                     help="count kernel launches with torch.profiler (untimed pass)")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.seeds is None:
+        a.seeds = "42" if a.config == "dhn" else "42,43,44,45,46"
+    return a
 
 
 def make_graph(cfg, seed, sample=False):
@@ -70,7 +75,7 @@ def make_graph(cfg, seed, sample=False):
     return synth.cora_like(seed)
 
 
-DHN_SCALE = [0.1]
+DHN_SCALE = [1.0]
 
 
 def make_program(cfg, data, dev, prec):
@@ -162,10 +167,9 @@ def peaks():
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
-def run_ours(args):
+def _dist_setup():
     import torch
     import torch.distributed as dist
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -178,39 +182,51 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group(backend)
-    dev = torch.device("cuda", local)
+    return world, rank, local, torch.device("cuda", local)
 
-    graph = make_graph(args.config, args.seed)
-    sharded = world > 1 and args.config in ("arxiv", "cora", "hyper", "mag")
+
+def _build(args, seed, world, dev):
+    """(program, job join rows per step, sharded?) for one seed's synthetic input."""
+    import torch
+    import torch.distributed as dist
+    graph = make_graph(args.config, seed)
+    sharded = world > 1 and args.config in SHARDED
     if sharded:
         # multi-GPU: the join relation hash-partitioned by group key, NCCL all-gather of the
         # source embeddings / reduce-scatter of their gradients per hop (DESIGN.md "Multi-GPU")
-        from paper_2605_24207_b200.shard import (ShardedGCNProgram, ShardedHGTProgram,
-                                                   ShardedHypergraphProgram)
-        if args.config == "hyper":
-            prog = ShardedHypergraphProgram(graph, prec=args.prec)
-        elif args.config == "mag":
-            prog = ShardedHGTProgram(graph, prec=args.prec)
-        else:
-            prog = ShardedGCNProgram(graph, prec=args.prec)
+        from paper_2605_24207_b200 import shard
+        prog = SHARDED[args.config](shard)(graph, prec=args.prec)
         r = torch.tensor([prog.join_rows_per_step], dtype=torch.float64, device=dev)
         dist.all_reduce(r)
         rows = int(r.item())              # all ranks' join rows = the whole job
     else:
         # other configs at N > 1: independent replicas (DESIGN.md "Multi-GPU")
         prog = make_program(args.config, graph, dev, args.prec)
-        rows = None
+        rows = world * prog.join_rows_per_step
     del graph
-    if rows is None:
-        rows = prog.join_rows_per_step
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    return prog, rows, sharded
+
+
+SHARDED = {
+    "arxiv": lambda m: m.ShardedGCNProgram, "cora": lambda m: m.ShardedGCNProgram,
+    "hyper": lambda m: m.ShardedHypergraphProgram, "mag": lambda m: m.ShardedHGTProgram,
+    "dhn": lambda m: m.ShardedDHNProgram,
+}
+
+
+def _time_steps(prog, args, world, dev, graphed, flush):
+    """W untimed warm-up steps, then K timed steps (barrier + synchronize on both sides; L2
+    flushed between steps outside the events).  Returns (per-step ms, {kernel: [launch ms]},
+    replay function)."""
+    import torch
+    import torch.distributed as dist
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
-    graphed = not sharded and not args.eager
+    cs = None
     if graphed:
         # the step as ONE CUDA graph (programs.CapturedStep): event record nodes around the
         # step and around every kernel the program brackets give device times per replay
@@ -222,10 +238,6 @@ def run_ours(args):
     for _ in range(args.warmup):
         run_step()
     barrier()
-
-    # ---- timed region ----
-    sampler = ClockSampler(local)
-    sampler.start()
     step_ms, launches_ms = [], {}
     if graphed:
         barrier()
@@ -258,20 +270,83 @@ def run_ours(args):
         for k, a in timers.items():
             if not k.endswith("_end"):
                 launches_ms[k] = [x.elapsed_time(y) for x, y in zip(a, timers.get(k + "_end", []))]
-    clocks = sampler.finish()
-    t_step = float(np.mean(step_ms))
+    return step_ms, launches_ms, (cs.replay if cs is not None else None)
+
+
+def _index_build_ms(prog, world):
+    """One-time join-index build (A1, content caching -- excluded from the metric): the
+    program's build_indices() again after warm-up, wall clock with a synchronize on both
+    sides (its size-query phase is a host sync), max over ranks."""
+    import torch
+    if not hasattr(prog, "build_indices"):
+        return float("nan")
+    # the captured step graph and the queries hold the current index / weight pointers: build
+    # a second copy, time it, then restore the program's own attributes
+    saved = {k: (dict(v) if isinstance(v, dict) else v) for k, v in vars(prog).items()}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prog.build_indices()
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) * 1e3
+    prog.__dict__.update(saved)
+    return t
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local, dev = _dist_setup()
+    seeds = [int(x) for x in str(args.seeds).split(",") if x != ""]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    sampler = ClockSampler(local)
+    per_seed, launches_ms = [], {}
+    first = None
+    for si, seed in enumerate(seeds):
+        prog, rows, sharded = _build(args, seed, world, dev)
+        graphed = not args.eager and (not sharded or args.config != "dhn")
+        if si == 0:
+            sampler.start()                   # clocks sampled during the timed regions
+        step_ms, lm, replay = _time_steps(prog, args, world, dev, graphed, flush)
+        t_seed = float(np.mean(step_ms))
+        if world > 1:
+            t = torch.tensor([t_seed], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_seed = float(t.item())
+        per_seed.append({"seed": seed, "ms_per_step": t_seed, "value": rows / (t_seed * 1e-3),
+                         "join_rows_per_step": rows})
+        for k, v in lm.items():
+            launches_ms.setdefault(k, []).extend(v)
+        if si == 0:
+            clocks = sampler.finish()
+            first = {"prog": prog, "rows": rows, "sharded": sharded, "graphed": graphed,
+                     "replay": replay}
+            first["index_ms"] = _index_build_ms(prog, world)
+            first["model"] = prog.roof_model()
+            first["launches"] = count_launches(prog)
+            if not args.no_e2e:
+                first["e2e"] = run_e2e(prog, args, world, dev, rows, replay)
+            first["meta"] = {k: getattr(prog, k) for k in ("L", "dims") if hasattr(prog, k)}
+            first["prog"] = None
+        del prog, replay
+        torch.cuda.empty_cache()
+    vals = np.array([r["value"] for r in per_seed])
+    msl = np.array([r["ms_per_step"] for r in per_seed])
+    value = float(np.median(vals))
+    t_step = float(np.median(msl))
+    rows, sharded = first["rows"], first["sharded"]
     if world > 1:
-        t = torch.tensor([t_step], device=dev)
+        t = torch.tensor([first["index_ms"]], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_step = float(t.item())
-    value = (rows if sharded else world * rows) / (t_step * 1e-3)
+        first["index_ms"] = float(t.item())
 
     def kernel_ms(name):
         v = launches_ms.get(name)
         return float(np.mean(v)) if v else None
 
-    model = prog.roof_model()
-    per = {k: kernel_ms(k) for k in ["proj_fwd", "proj_bwd"] + list(model)}
+    model = first["model"]
+    per = {k: kernel_ms(k) for k in ["proj_fwd", "proj_bwd", "allgather", "reduce_scatter"] + list(model)}
+    n_steps = args.steps * len(seeds)
 
     # ---- roofline of the dominant hot-path kernel (the fused LJA; see DESIGN.md) ----
     peak, peak_src = peaks()
@@ -287,45 +362,75 @@ def run_ours(args):
         unit, pk, pk_src = "TFLOP/s", FP32_ALU_TFLOPS, FP32_ALU_SRC
     roof = {"kernel": dom, "bound": spec["bound"], "achieved": round(achieved, 3), "peak": pk,
             "peak_source": pk_src, "unit": unit, "frac": round(achieved / pk, 4),
+            "model": "gather (SURVEY sec 8d: every gathered row counted per join row)"
+            if spec["bound"] == "hbm" else "factorised flop count (DESIGN.md sec 6)",
             "algorithmic_per_launch": int(spec["amount"]), "avg_launch_ms": round(ms, 5),
-            "traffic": None,
-            "kernel_ms": {k: (round(v, 5) if v else None) for k, v in per.items()}}
+            "traffic": None}
+    if spec.get("compulsory"):
+        c = spec["compulsory"] / (ms * 1e-3) / 1e9
+        roof["compulsory_per_launch"] = int(spec["compulsory"])
+        roof["frac_compulsory"] = round(c / pk, 4)
     tr = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tr):
         with open(tr) as f:
             roof["traffic"] = json.load(f).get(dom)
-
-    launches = None
-    if args.profile_launches or True:
-        launches = count_launches(prog)
-
-    # ---- end to end through the C-ABI with host buffers ----
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(prog, args, world, dev, rows if sharded else world * rows,
-                      cs.replay if graphed else None)
-
+        if roof["traffic"] and spec["bound"] == "hbm":
+            # ncu DRAM bytes (one --set full capture, per launch) over the live launch time
+            roof["frac_dram"] = round(roof["traffic"] / (ms * 1e-3) / 1e9 / pk, 4)
+    # every bracketed kernel's mean launch time and its launches per step
+    roof["kernel_ms"] = {k: (round(v, 5) if v else None) for k, v in per.items()}
+    roof["launches_per_step"] = {k: len(v) // max(n_steps, 1) for k, v in launches_ms.items()}
+    lja_ms = sum((per[k] or 0.0) * roof["launches_per_step"].get(k, 0) for k in model)
     result = None
     if rank == 0:
+        cfg = {"workload": workload(args), "config": args.config,
+               "join_rows_per_step": rows, **first["meta"],
+               "projection_precision": args.prec, "l2": "flushed between timed steps",
+               "step_launch": "one CUDA graph replay" if first["graphed"] else "eager launches",
+               "seeds": seeds,
+               "parallelism": (f"hash-partition by group key x{world} ({SHARD_DESC[args.config]})"
+                               if sharded else f"replica x{world}" if world > 1 else "single")}
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded; shapes of BASELINE.json configs, see DESIGN.md)",
-            "config": {"workload": WORKLOAD[args.config], "config": args.config,
-                       "join_rows_per_step": rows,
-                       **({"layers": prog.L, "dims": prog.dims} if hasattr(prog, "dims") else {}),
-                       "projection_precision": args.prec, "l2": "flushed between timed steps",
-                       "step_launch": "one CUDA graph replay" if graphed else "eager launches",
-                       "parallelism": (f"hash-partition by group key x{world} (NCCL all-gather / "
-                                       f"reduce-scatter per layer or hop)" if sharded else
-                                       f"replica x{world}" if world > 1 else "single")},
-            "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "config": cfg,
+            "seed_stats": {"statistic": f"median over seeds {seeds} of the per-seed mean of "
+                                        f"{args.steps} timed steps",
+                           "value_median": value, "value_std": float(np.std(vals)),
+                           "ms_median": t_step, "ms_std": float(np.std(msl)), "per_seed": per_seed},
+            "lja_only": {"value": rows / (lja_ms * 1e-3) if lja_ms else None, "unit": UNIT,
+                         "lja_ms_per_step": lja_ms,
+                         "what": "join rows / summed LJA kernel time of a step (first seed's "
+                                 "kernels bracketed by CUDA events)"},
+            "index_build_ms": round(first["index_ms"], 3),
+            "roofline": roof, "e2e": first.get("e2e"), "gpu_launches": first["launches"],
+            "clocks": clocks,
         }
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+SHARD_DESC = {
+    "arxiv": "NCCL all-gather / reduce-scatter of the layer's source rows per layer",
+    "cora": "NCCL all-gather / reduce-scatter of the layer's source rows per layer",
+    "hyper": "NCCL all-gather / reduce-scatter per hop",
+    "mag": "NCCL all-gather of K'/M' per source type, reduce-scatter of dK'/dM'",
+    "dhn": "roots hash-partitioned, adjacency replicated, NCCL all-gather of f per layer and "
+           "reduce-scatter of d f",
+}
+
+
+def workload(args):
+    w = WORKLOAD[args.config]
+    if args.config == "dhn":
+        n = max(64, int(2_449_029 * args.dhn_scale))
+        m = 2 * max(64, int(61_859_140 * args.dhn_scale))
+        w += f" at scale {args.dhn_scale:g} ({n:,} nodes, {m:,} Edge tuples)"
+    return w
 
 
 def count_launches(prog):
@@ -378,98 +483,126 @@ def run_e2e(prog, args, world, dev, job_rows, replay=None):
 # ------------------------------------------------------------------------------------------
 # the oracle (CPU, fp64): cpu_baseline and the --impl reference arm
 # ------------------------------------------------------------------------------------------
-def oracle_timing(args, steps=1):
-    """The oracle (fp64, single-threaded C) on a bounded sample of the same workload (~10-30 s
-    of CPU on the GPU box): arxiv -- the first of the three layers, fwd + bwd incl. its
-    projections; hyper / mag -- the whole step on a same-structure instance scaled down
-    (make_graph sample=True).  Rows/s = the sample's join rows / t."""
+def oracle_sample(cfg, seed):
+    """The bounded sample of a config's step the oracle (fp64, single-threaded C, as it
+    stands) is timed on (~5-30 s of one core): returns (run, join rows, description).
+    arxiv -- the first of the three layers (fwd + bwd incl. projections); cora -- both
+    layers; hyper / mag -- the whole step on a 1/20-scale instance of the same generator;
+    dhn -- the whole layer on a 1/10,000-scale products-shaped graph (the oracle enumerates
+    closed walks, so the full graph is out of reach)."""
     import oracle
     from oracle import programs as op
     oracle.build()
-    if args.config in ("hyper", "mag"):
-        return _oracle_sampled(args, steps, oracle, op)
-    if args.config == "dhn":
-        return _oracle_dhn(args, steps, oracle, op)
-    graph = make_graph(args.config, args.seed)
-    L = len(graph["W"])
-    if args.config == "arxiv":
-        sample_layers = 1
-    else:
-        sample_layers = L
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        op.gcn_step(graph, layers=sample_layers)
-        times.append(time.perf_counter() - t0)
-    o = oracle.build_join_index(graph["edges"]["src"], graph["edges"]["dst"],
-                                graph["nodes"]["key"], graph["nodes"]["key"])
-    rows = o["n_join_rows"] * sample_layers
-    t = float(np.median(times))
-    return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{args.config}: first {sample_layers} of {L} layers (fwd+bwd incl. "
-                      f"projections, {rows} join rows), {steps} run(s), fp64 single-threaded C, "
-                      f"median {t:.2f} s"}, t, rows
-
-
-def _oracle_sampled(args, steps, oracle, op):
-    data = make_graph(args.config, args.seed, sample=True)
-    times = []
-    if args.config == "hyper":
+    if cfg == "hyper":
+        data = make_graph(cfg, seed, sample=True)
         o1 = oracle.build_join_index(data["inc"]["node"], data["inc"]["hyper"],
                                      data["nodes"]["key"], data["hyperedges"]["key"])
         rows = 2 * o1["n_join_rows"]
         what = (f"whole step on a 1/20-scale hypergraph ({len(data['nodes']['key'])} nodes, "
                 f"{len(data['inc']['node'])} incidences)")
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            op.hypergraph_step(data)
-            times.append(time.perf_counter() - t0)
-    else:
+        return (lambda: op.hypergraph_step(data)), rows, what
+    if cfg == "mag":
+        data = make_graph(cfg, seed, sample=True)
         rng = np.random.default_rng(1)
         d, h = data["d"], data["heads"]
         rows = sum(len(r["src"]) for r in data["rels"].values())
-        what = f"whole HGT layer on a 1/20-scale ogbn-mag-shaped schema ({rows} edges)"
         Ws = {k: rng.standard_normal((d, d)) / np.sqrt(d) for k in ("k", "m", "q")}
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            for r in data["rels"].values():
+        dO = {name: rng.standard_normal((data["n"][r["dst_type"]], d)) for name, r in data["rels"].items()}
+
+        def run():
+            for name, r in data["rels"].items():
                 ts, tt = r["src_type"], r["dst_type"]
                 op.hgt_relation(data["h"][ts], data["h"][tt], Ws["k"], Ws["m"], Ws["q"],
-                                data["key"][ts], data["key"][tt], r["src"], r["dst"], h,
-                                rng.standard_normal((data["n"][tt], d)))
-            times.append(time.perf_counter() - t0)
-    t = float(np.median(times))
-    return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{args.config}: {what}, {steps} run(s), fp64 single-threaded C, "
-                      f"median {t:.2f} s"}, t, rows
+                                data["key"][ts], data["key"][tt], r["src"], r["dst"], h, dO[name])
+        return run, rows, f"whole HGT layer on a 1/20-scale ogbn-mag-shaped schema ({rows} edges)"
+    if cfg == "dhn":
+        g = make_graph("dhn", seed, sample=True)
+        keys = g["nodes"]["key"]
+        n, d = g["nodes"]["x"].shape
+        rng = np.random.default_rng(11)
+        W = rng.standard_normal((9 * d, d)) / np.sqrt(d)
+        dO = rng.standard_normal((n, 3 * d))
+        oi = oracle.build_join_index(g["edges"]["src"], g["edges"]["dst"], keys, keys,
+                                     within_by_src_key=True)
+        ones = [np.ones((n, 1))]
+        rows = int(oi["n_join_rows"]) + sum(int(round(oracle.dhn_fwd(k, oi, keys, ones * k).sum()))
+                                            for k in (3, 4))
+        return (lambda: op.dhn_step(g, W, dO)), rows, (
+            f"whole layer (C2/C3/C4 fwd+bwd, projections) on a {n}-node products-shaped graph "
+            f"({len(g['edges']['src'])} Edge rows, {rows} homomorphisms)")
+    graph = make_graph(cfg, seed)
+    L = len(graph["W"])
+    layers = 1 if cfg == "arxiv" else L
+    o = oracle.build_join_index(graph["edges"]["src"], graph["edges"]["dst"],
+                                graph["nodes"]["key"], graph["nodes"]["key"])
+    rows = o["n_join_rows"] * layers
+    return (lambda: op.gcn_step(graph, layers=layers)), rows, (
+        f"first {layers} of {L} layers (fwd+bwd incl. projections, {rows} join rows)")
 
 
-def _oracle_dhn(args, steps, oracle, op):
-    """DHN layer (C2, C3, C4 fwd + bwd incl. the nine projections) on a 1/10000-scale
-    products-shaped graph: the oracle enumerates closed walks with nested loops, so the full
-    graph (tr(A^4) ~ 1e11 walks) is out of reach; rows = Edge rows + closed 3- and 4-walks,
-    the same unit as the GPU arm."""
-    g = make_graph("dhn", args.seed, sample=True)
-    keys = g["nodes"]["key"]
-    n, d = g["nodes"]["x"].shape
-    rng = np.random.default_rng(11)
-    W = rng.standard_normal((9 * d, d)) / np.sqrt(d)
-    dO = rng.standard_normal((n, 3 * d))
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        op.dhn_step(g, W, dO)
-        times.append(time.perf_counter() - t0)
-    oi = oracle.build_join_index(g["edges"]["src"], g["edges"]["dst"], keys, keys,
-                                 within_by_src_key=True)
-    ones = [np.ones((n, 1))]
-    rows = int(oi["n_join_rows"]) + sum(int(round(oracle.dhn_fwd(k, oi, keys, ones * k).sum()))
-                                        for k in (3, 4))
-    t = float(np.median(times))
-    return {"value": rows / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"dhn: whole layer (C2/C3/C4 fwd+bwd, projections) on a {n}-node "
-                      f"products-shaped graph ({len(g['edges']['src'])} Edge rows, {rows} "
-                      f"homomorphisms), {steps} run(s), fp64 single-threaded C, median {t:.2f} s"}, t, rows
+def _oracle_worker(cfg, seed, reps, barrier, out):
+    import time as _t
+    run, rows, what = oracle_sample(cfg, seed)
+    barrier.wait()
+    t0 = _t.time()
+    for _ in range(reps):
+        run()
+    out.put((t0, _t.time(), rows, what))
+
+
+def host_info():
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        info["lscpu"] = {k.strip(): v.strip() for k, v in (
+            l.split(":", 1) for l in subprocess.run(["lscpu"], capture_output=True, text=True,
+                                                     timeout=10).stdout.splitlines() if ":" in l)
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core",
+                             "NUMA node(s)", "L3 cache")}
+    except Exception:
+        pass
+    return info
+
+
+def oracle_timing(args, procs=None, reps=1):
+    """The oracle timed on the host's cores: `procs` concurrent processes (default: every
+    core), each running the bounded sample `reps` times; value = procs x reps x rows / wall
+    (first start to last end).  The single-core figure is one process alone.  Returns
+    (cpu_baseline dict, wall seconds of the all-core run, rows per sample)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")        # fresh interpreters: no CUDA state in the workers
+    seed = int(str(args.seeds).split(",")[0])
+
+    def run(p):
+        barrier, q = ctx.Barrier(p), ctx.Queue()
+        ws = [ctx.Process(target=_oracle_worker, args=(args.config, seed, reps, barrier, q))
+              for _ in range(p)]
+        for w in ws:
+            w.start()
+        res = [q.get() for _ in ws]
+        for w in ws:
+            w.join()
+        wall = max(r[1] for r in res) - min(r[0] for r in res)
+        return wall, res[0][2], res[0][3]
+
+    P = procs or os.cpu_count() or 1
+    t1, rows, what = run(1)
+    tP, _, _ = run(P) if P > 1 else (t1, rows, what)
+    single = rows * reps / t1
+    value = P * rows * reps / tP
+    return {"value": value, "unit": UNIT, "cores": P, "kind": "oracle",
+            "sample": f"{args.config}: {what}; {P} concurrent processes (one per host core), "
+                      f"each running the sample {reps}x; value = {P} x rows / wall "
+                      f"({tP:.2f} s); fp64 single-threaded C per process",
+            "single_core": {"value": single, "cores": 1, "seconds": t1 / reps},
+            "host": host_info()}, tP, rows
 
 
 def run_reference(args):
@@ -477,12 +610,12 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if world > 1 and rank != 0:
         return None
-    steps = max(1, min(args.steps, 2))
-    cb, t, rows = oracle_timing(args, steps)
+    reps = max(1, min(args.steps, 2))
+    cb, t, rows = oracle_timing(args, reps=reps)
     return {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": 0, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "steps": reps, "warmup": 0, "ms_per_step": t * 1e3 / reps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD[args.config], "config": args.config,
+            "config": {"workload": workload(args), "config": args.config,
                        "join_rows_per_step": rows},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -497,7 +630,7 @@ def main():
     else:
         res = run_ours(args)
         if res is not None and not args.no_cpu_baseline:
-            res["cpu_baseline"] = oracle_timing(args, 1)[0]
+            res["cpu_baseline"] = oracle_timing(args)[0]
     if res is not None:
         print(json.dumps(res), flush=True)
 

@@ -181,7 +181,8 @@ rnn_status rnn_join_aggregate_fwd(const rnn_join_index* idx, const rnn_lifted_qu
 /* ===================================================================================== */
 /* A5. Backward                                                                          */
 /* ===================================================================================== */
-/* Gradients are WRITTEN (not accumulated) into dense full-relation buffers with ld = dim:
+/* Gradients are WRITTEN (not accumulated) into dense full-relation buffers laid out like
+ * their operand (same leading dimension: d_src uses src.ld, d_dst uses dst.ld, ...):
  *   d_src[n_src_rows, src.dim], d_src_key[n_src_rows, src_key.dim],
  *   d_edge[(n_edge_rows or E' for RNN_BY_POSITION), edge.dim],
  *   d_dst[(n_dst_rows or G), dst.dim].  Any may be NULL (not computed).  Rows never
@@ -289,6 +290,26 @@ rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k, const rnn_ope
                              int64_t ld_ws, float* const* d_f, int64_t ld_df, uint32_t flags,
                              void* workspace, size_t workspace_bytes, void* stream);
 
+/* Root subsets (multi-GPU: roots hash-partitioned over ranks, the adjacency replicated,
+ * SURVEY sec 8e): the same operations restricted to the roots listed in roots[n_roots]
+ * (group ids of adj, device memory; ids outside [0, n_groups) and repeats are ignored).
+ * Forward: out (and walk_sum, nullable here) rows of listed roots are written, other rows
+ * are left untouched.  Backward: d f_j(x) is the walk aggregate ROOTED AT x with rotated
+ * operands, so the listed roots x get their complete gradient rows (every other row of d_f
+ * is 0, as are rows on no walk); g = f0 (.) d_out must be valid for EVERY root (d_out rows
+ * of all groups, e.g. all-gathered), and d f0 = d_out (.) walk_sum is written for every
+ * group when walk_sum is given.  k = 2 ignores the subset (every root; it is one gather).
+ * Otherwise the arguments, layouts and errors of rnn_dhn_fwd_save / rnn_dhn_bwd_saved. */
+rnn_status rnn_dhn_fwd_roots(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                             const int32_t* roots, int64_t n_roots, float* out, int64_t ld_out,
+                             float* walk_sum, int64_t ld_ws, void* workspace,
+                             size_t workspace_bytes, void* stream);
+rnn_status rnn_dhn_bwd_roots(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
+                             const int32_t* roots, int64_t n_roots, const float* d_out,
+                             int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
+                             float* const* d_f, int64_t ld_df, uint32_t flags, void* workspace,
+                             size_t workspace_bytes, void* stream);
+
 /* Exact closed-walk (homomorphism) counts: counts[g] = number of closed k-walks rooted at
  * group g's node, with Edge multiplicity -- C_k(n) of the rule above with every operand 1,
  * i.e. (A^k)_nn of the Edge relation's (multi)adjacency matrix (Eq. 3 :1500
@@ -325,6 +346,12 @@ rnn_status rnn_group_sizes(const rnn_join_index* idx, int32_t* size, void* strea
  * y[r, c] = beta * y[r, c] + x[r, c] for r < rows, c < cols (fp32, row-major, any ld). */
 rnn_status rnn_accumulate(float* y, int64_t ldy, const float* x, int64_t ldx, int64_t rows,
                           int32_t cols, float beta, void* stream);
+
+/* Row gather (multi-GPU plumbing: permuting gathered rows into group order, packing /
+ * unpacking exchanged rows): y[i, c] = x[idx[i], c] for i < n, c < cols, and 0 where
+ * idx[i] < 0 (fp32, row-major, any ld; idx int32, device).  Indices are not range-checked. */
+rnn_status rnn_gather_rows(float* y, int64_t ldy, const float* x, int64_t ldx, const int32_t* idx,
+                           int64_t n, int32_t cols, void* stream);
 
 /* Multi-GPU ownership of group keys: owner[i] = splitmix64(keys[i] ^ seed) mod P. */
 rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed,

@@ -45,8 +45,9 @@ struct DhnArgs {
   float* out;
   int64_t ld_out;
   int out_by_row;         // write out[row_of[n]] instead of out[n]
-  const int32_t* order;   // roots, heaviest first
+  const int32_t* order;   // roots, heaviest first (active roots first)
   int* counter;
+  const int* n_active;    // number of active roots at the head of order[] (device)
   int* mark;              // k=3: per-CTA [G] int32
   const uint32_t* wout;   // k=4: out-wedges per root (bound on distinct 2-hop w)
   float* slab;            // k=4: per-CTA S1 values [H4_CAP][32]
@@ -75,7 +76,7 @@ __device__ __forceinline__ int64_t dhn_next_root(const DhnArgs& a, int* s_root) 
   if (threadIdx.x == 0) *s_root = atomicAdd(a.counter, 1);
   __syncthreads();
   const int i = *s_root;
-  return i < a.G ? (int64_t)a.order[i] : -1;
+  return i < *a.n_active ? (int64_t)a.order[i] : -1;
 }
 
 // Path counters of the walk kernels (which code paths a launch took), read by the internal
@@ -950,6 +951,23 @@ __global__ void dhn_count2_kernel(int64_t G, const int64_t* __restrict__ gp, int
   if (g < G) out[g] = gp[g + 1] - gp[g];
 }
 
+// active roots: every key gets bit 24 (sorted after all real keys); listed roots clear it
+// and count themselves once (duplicates and out-of-range ids are ignored)
+__global__ void root_exclude_kernel(uint32_t* __restrict__ key, int64_t G) {
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g < G) key[g] |= 1u << 24;
+}
+__global__ void root_include_kernel(const int32_t* __restrict__ roots, int64_t n, int64_t G,
+                                    uint32_t* __restrict__ key, int* __restrict__ n_active) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int32_t g = roots[i];
+  if (g < 0 || g >= G) return;
+  const uint32_t old = atomicAnd(&key[g], ~(1u << 24));
+  if (old & (1u << 24)) atomicAdd(n_active, 1);
+}
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
 // ---------------------------------------------------------------------------------------
 // plan: workspace layout
 // ---------------------------------------------------------------------------------------
@@ -957,7 +975,10 @@ struct Plan {
   int k, d, n_cta;
   int64_t G, E, R;
   size_t fixed, per_cta;
+  const int32_t* roots = nullptr;   // active root subset (group ids); NULL = every group
+  int64_t n_roots = 0;
 };
+constexpr int ACTIVE_SLOT = 63;     // counter[63]: number of active roots (device)
 
 struct Bufs {
   int32_t* gor; int32_t* nbr; float* F[4]; uint32_t* key; int32_t* order; int* counter;
@@ -1050,6 +1071,7 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
   a.rm = rm; a.ld_rm = ld_rm; a.rm_by_group = rm_by_group;
   a.out = out; a.ld_out = ld_out; a.out_by_row = out_by_row;
   a.order = b.order; a.counter = b.counter + launch_id;
+  a.n_active = b.counter + ACTIVE_SLOT;
   a.cta_stride = (int64_t)(P.per_cta / (P.k == 3 ? sizeof(int32_t) : sizeof(float)));
   // the kernels leave their per-CTA scratch zeroed, so only the first launch clears it
   if (launch_id == 0) RNN_CUDA(cudaMemsetAsync(b.cta, 0, P.per_cta * P.n_cta, st));
@@ -1097,7 +1119,18 @@ rnn_status prepare(const Plan& P, const Bufs& b, const rnn_join_index* adj, cuda
                                                             adj->group_dst_row, b.key, b.order,
                                                             b.wout);
     RNN_LAUNCH_CHECK();
-    RNN_TRY(radix_sort_u32(b.key, b.order, P.G, 24, b.sort_ws, st));
+    int* n_active = b.counter + ACTIVE_SLOT;
+    if (P.roots) {
+      root_exclude_kernel<<<(unsigned)ceil_div(P.G, 256), 256, 0, st>>>(b.key, P.G);
+      if (P.n_roots > 0)
+        root_include_kernel<<<(unsigned)ceil_div(P.n_roots, 256), 256, 0, st>>>(
+            P.roots, P.n_roots, P.G, b.key, n_active);
+      RNN_LAUNCH_CHECK();
+    } else {
+      set_int_kernel<<<1, 1, 0, st>>>(n_active, (int)P.G);
+      RNN_LAUNCH_CHECK();
+    }
+    RNN_TRY(radix_sort_u32(b.key, b.order, P.G, P.roots ? 25 : 24, b.sort_ws, st));
   }
   if (P.k == 4 && P.E > 0) {
     // every out-list (group segment) and in-list (row segment) sorted by hash partition
@@ -1160,13 +1193,28 @@ static __global__ void dhn_df0_kernel(int64_t G, int d, const int32_t* __restric
   df0[(int64_t)row_of[n] * ld_df + c] = dout[n * ld_dout + c] * S[n * ld_s + c];
 }
 
+static __global__ void dhn_df0_roots_kernel(const int32_t* __restrict__ roots, int64_t n_roots,
+                                            int64_t G, int d, const int32_t* __restrict__ row_of,
+                                            const float* __restrict__ dout, int64_t ld_dout,
+                                            const float* __restrict__ S, int64_t ld_s,
+                                            float* __restrict__ df0, int64_t ld_df) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_roots * d) return;
+  const int64_t n = roots[i / d];
+  const int c = (int)(i % d);
+  if (n < 0 || n >= G) return;
+  df0[(int64_t)row_of[n] * ld_df + c] = dout[n * ld_dout + c] * S[n * ld_s + c];
+}
+
 static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,
                         int64_t ld_out, float* walk_sum, int64_t ld_ws, void* workspace,
-                        size_t workspace_bytes, void* stream);
+                        size_t workspace_bytes, void* stream, const int32_t* roots = nullptr,
+                        int64_t n_roots = 0);
 static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                         const float* d_out, int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
                         float* const* d_f, int64_t ld_df, void* workspace, size_t workspace_bytes,
-                        void* stream, uint32_t flags = 0);
+                        void* stream, uint32_t flags = 0, const int32_t* roots = nullptr,
+                        int64_t n_roots = 0);
 
 extern "C" rnn_status rnn_dhn_fwd(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                                   float* out, int64_t ld_out, void* workspace,
@@ -1202,7 +1250,8 @@ extern "C" rnn_status rnn_dhn_bwd_saved(const rnn_join_index* adj, int32_t k,
 
 static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f, float* out,
                         int64_t ld_out, float* walk_sum, int64_t ld_ws, void* workspace,
-                        size_t workspace_bytes, void* stream) {
+                        size_t workspace_bytes, void* stream, const int32_t* roots,
+                        int64_t n_roots) {
   RNN_TRY(check_adj(adj, k, f ? f[1].dim : 0));
   const int d = f[1].dim;
   RNN_TRY(check_ops(f, k, d, adj->n_src_rows));
@@ -1210,7 +1259,11 @@ static rnn_status dhn_fwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
   RNN_REQUIRE(ld_out >= d, RNN_ERR_SHAPE_MISMATCH, "ld_out %lld < d %d", (long long)ld_out, d);
   RNN_REQUIRE(!walk_sum || ld_ws >= d, RNN_ERR_SHAPE_MISMATCH, "ld_ws %lld < d %d",
               (long long)ld_ws, d);
+  RNN_REQUIRE(n_roots >= 0 && (n_roots == 0 || roots), RNN_ERR_INVALID_ARGUMENT,
+              "roots NULL with n_roots %lld", (long long)n_roots);
   Plan P = make_plan(adj, k, d);
+  P.roots = roots;
+  P.n_roots = n_roots;
   RNN_TRY(ws_check(P, workspace, workspace_bytes, &P.n_cta));
   if (P.G == 0) return RNN_OK;
   cudaStream_t st = as_stream(stream);
@@ -1243,7 +1296,7 @@ extern "C" rnn_status rnn_dhn_bwd(const rnn_join_index* adj, int32_t k, const rn
 static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_operand* f,
                         const float* d_out, int64_t ld_dout, const float* walk_sum, int64_t ld_ws,
                         float* const* d_f, int64_t ld_df, void* workspace, size_t workspace_bytes,
-                        void* stream, uint32_t flags) {
+                        void* stream, uint32_t flags, const int32_t* roots, int64_t n_roots) {
   RNN_TRY(check_adj(adj, k, f ? f[1].dim : 0));
   const int d = f[1].dim;
   RNN_TRY(check_ops(f, k, d, adj->n_src_rows));
@@ -1251,7 +1304,11 @@ static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
   RNN_REQUIRE(d_out || adj->n_groups == 0, RNN_ERR_INVALID_ARGUMENT, "d_out is NULL");
   RNN_REQUIRE(ld_dout >= d && ld_df >= d, RNN_ERR_SHAPE_MISMATCH, "ld < d");
   RNN_REQUIRE(!walk_sum || ld_ws >= d, RNN_ERR_SHAPE_MISMATCH, "ld_ws < d");
+  RNN_REQUIRE(n_roots >= 0 && (n_roots == 0 || roots), RNN_ERR_INVALID_ARGUMENT,
+              "roots NULL with n_roots %lld", (long long)n_roots);
   Plan P = make_plan(adj, k, d);
+  P.roots = roots;
+  P.n_roots = n_roots;
   RNN_TRY(ws_check(P, workspace, workspace_bytes, &P.n_cta));
   cudaStream_t st = as_stream(stream);
   for (int i = 0; i < k; ++i)
@@ -1264,10 +1321,19 @@ static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
   float* g = b.F[k - 1];
   RNN_TRY(to_group(P, adj, f[0].data, f[0].ld, d_out, ld_dout, g, st));
   if (d_f[0] && walk_sum) {   // d f0 = dOut (.) the forward's walk sum: no walk needed
-    const int64_t n = P.G * d;
-    dhn_df0_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(P.G, d, adj->group_dst_row, d_out,
-                                                               ld_dout, walk_sum, ld_ws, d_f[0],
-                                                               ld_df);
+    if (P.roots && k > 2) {    // listed roots only (the walk sum exists for those)
+      if (P.n_roots > 0) {
+        const int64_t n = P.n_roots * d;
+        dhn_df0_roots_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(
+            P.roots, P.n_roots, P.G, d, adj->group_dst_row, d_out, ld_dout, walk_sum, ld_ws,
+            d_f[0], ld_df);
+      }
+    } else {
+      const int64_t n = P.G * d;
+      dhn_df0_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(P.G, d, adj->group_dst_row,
+                                                                 d_out, ld_dout, walk_sum, ld_ws,
+                                                                 d_f[0], ld_df);
+    }
     RNN_LAUNCH_CHECK();
   }
   if (k == 2) {
@@ -1321,6 +1387,33 @@ static rnn_status dhn_bwd_impl(const rnn_join_index* adj, int32_t k, const rnn_o
     RNN_TRY(walk(P, b, adj, W, nullptr, 0, 0, d_f[j], ld_df, 1, launch++, st));
   }
   return RNN_OK;
+}
+
+extern "C" rnn_status rnn_dhn_fwd_roots(const rnn_join_index* adj, int32_t k,
+                                        const rnn_operand* f, const int32_t* roots,
+                                        int64_t n_roots, float* out, int64_t ld_out,
+                                        float* walk_sum, int64_t ld_ws, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(roots || n_roots == 0, RNN_ERR_INVALID_ARGUMENT, "roots is NULL");
+  static const int32_t none = 0;
+  return dhn_fwd_impl(adj, k, f, out, ld_out, walk_sum, ld_ws, workspace, workspace_bytes,
+                      stream, roots ? roots : &none, n_roots);
+}
+
+extern "C" rnn_status rnn_dhn_bwd_roots(const rnn_join_index* adj, int32_t k,
+                                        const rnn_operand* f, const int32_t* roots,
+                                        int64_t n_roots, const float* d_out, int64_t ld_dout,
+                                        const float* walk_sum, int64_t ld_ws, float* const* d_f,
+                                        int64_t ld_df, uint32_t flags, void* workspace,
+                                        size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(roots || n_roots == 0, RNN_ERR_INVALID_ARGUMENT, "roots is NULL");
+  RNN_REQUIRE((flags & ~(uint32_t)RNN_DHN_SYMMETRIC_EDGE) == 0, RNN_ERR_INVALID_ARGUMENT,
+              "unknown DHN flags 0x%x", flags);
+  static const int32_t none = 0;
+  return dhn_bwd_impl(adj, k, f, d_out, ld_dout, walk_sum, ld_ws, d_f, ld_df, workspace,
+                      workspace_bytes, stream, flags, roots ? roots : &none, n_roots);
 }
 
 // ---- exact counts ----

@@ -58,8 +58,15 @@ class _Program:
         return self.backward()
 
     def roof_model(self):
-        """{kernel timer name: {"bound": "hbm", "amount": algorithmic bytes per launch}}"""
-        return {k: {"bound": "hbm", "amount": v} for k, v in self.lja_bytes().items()}
+        """{kernel timer name: {"bound": "hbm", "amount": algorithmic bytes per launch,
+        "compulsory": compulsory bytes per launch}}"""
+        comp = self.compulsory_bytes() if hasattr(self, "compulsory_bytes") else {}
+        return {k: {"bound": "hbm", "amount": v, "compulsory": comp.get(k)}
+                for k, v in self.lja_bytes().items()}
+
+    def build_indices(self):
+        """(Re)build every join index of the program (A1; content caching: done once)."""
+        raise NotImplementedError
 
 
 def _sum_bytes(idx, d, weighted=False, mean=False):
@@ -78,6 +85,31 @@ def _sum_bwd_bytes(idx, d, weighted=False, mean=False):
         idx.n_src_rows * (4 * d + 8)
 
 
+def _n_referenced(idx):
+    """U = distinct source rows the join rows reference (cached on the index object)."""
+    u = getattr(idx, "_n_ref", None)
+    if u is None:
+        u = int((idx.src_ptr[1:] > idx.src_ptr[:-1]).sum().item()) if idx.n_join_rows else 0
+        idx._n_ref = u
+    return u
+
+
+def _comp_fwd(idx, d, weighted=False):
+    """Compulsory bytes of one SUM/MEAN forward launch: every index entry,
+    every REFERENCED input row and every output row crosses HBM once -- src_row (4) and the
+    weight (4) per join row, the CSR pointers, U source rows and G output rows of 4d."""
+    return idx.n_join_rows * (4 + (4 if weighted else 0)) + 8 * (idx.n_groups + 1) + \
+        4 * d * (_n_referenced(idx) + idx.n_groups)
+
+
+def _comp_bwd(idx, d, weighted=False):
+    """... of one backward launch over the transposed CSR: src_pos + group id (8) and the
+    weight (4) per join row, the source CSR pointers, G upstream rows read and every source
+    gradient row written (4d each)."""
+    return idx.n_join_rows * (8 + (4 if weighted else 0)) + 8 * (idx.n_src_rows + 1) + \
+        4 * d * (idx.n_groups + idx.n_src_rows)
+
+
 class GCNProgram(_Program):
     """L-layer GCN as lifted queries; step() = forward + backward of every layer."""
 
@@ -88,16 +120,10 @@ class GCNProgram(_Program):
         nodes, edges = graph["nodes"], graph["edges"]
         self.dims = list(graph["dims"])
         self.L = len(self.dims) - 1
-        key = torch.as_tensor(nodes["key"]).to(dev)
-        e_src = torch.as_tensor(edges["src"]).to(dev)
-        e_dst = torch.as_tensor(edges["dst"]).to(dev)
-        # A1 (content caching): index 1 joins AEdge with the node relation in storage order
-        self.idx1 = rnn.build_join_index(e_src, e_dst, key, key, rows_per_item=rows_per_item)
-        self.w1 = rnn.gcn_norm(self.idx1)
-        if self.L > 1:
-            gk = self.idx1.group_key.clone()
-            self.idx2 = rnn.build_join_index(e_src, e_dst, gk, gk, rows_per_item=rows_per_item)
-            self.w2 = rnn.gcn_norm(self.idx2)
+        self._key = torch.as_tensor(nodes["key"]).to(dev)
+        self._e = (torch.as_tensor(edges["src"]).to(dev), torch.as_tensor(edges["dst"]).to(dev))
+        self._rpi = rows_per_item
+        self.build_indices()
         self.n_nodes = len(nodes["key"])
         self.G = self.idx1.n_groups
         self.X0 = _dev_f32(nodes["x"], dev)
@@ -117,16 +143,36 @@ class GCNProgram(_Program):
             self.q.append((idx, rnn.make_query("src", "sum", src=self.Z[l], edge=w,
                                                edge_mode=rnn.BY_POSITION)))
 
+    def build_indices(self):
+        """A1 (content caching, built once): index 1 joins AEdge with the node relation in
+        storage order, index 2 with the key-ordered layer output; plus the GCN weights."""
+        e_src, e_dst = self._e
+        self.idx1 = rnn.build_join_index(e_src, e_dst, self._key, self._key, rows_per_item=self._rpi)
+        self.w1 = rnn.gcn_norm(self.idx1)
+        if self.L > 1:
+            gk = self.idx1.group_key.clone()
+            self.idx2 = rnn.build_join_index(e_src, e_dst, gk, gk, rows_per_item=self._rpi)
+            self.w2 = rnn.gcn_norm(self.idx2)
+
     @property
     def join_rows_per_step(self):
         return self.idx1.n_join_rows + (self.L - 1) * (self.idx2.n_join_rows if self.L > 1 else 0)
 
+    def _layer_idx(self):
+        return [self.idx1] + [self.idx2] * (self.L - 1)
+
     def lja_bytes(self):
         """Average algorithmic bytes per LJA launch {kernel: bytes} (fwd, bwd over layers)."""
-        ix = [self.idx1] + [self.idx2] * (self.L - 1)
+        ix = self._layer_idx()
         d = self.dims[1:]
         return {"lja_fwd": float(np.mean([_sum_bytes(i, dd, True) for i, dd in zip(ix, d)])),
                 "lja_bwd": float(np.mean([_sum_bwd_bytes(i, dd, True) for i, dd in zip(ix, d)]))}
+
+    def compulsory_bytes(self):
+        ix = self._layer_idx()
+        d = self.dims[1:]
+        return {"lja_fwd": float(np.mean([_comp_fwd(i, dd, True) for i, dd in zip(ix, d)])),
+                "lja_bwd": float(np.mean([_comp_bwd(i, dd, True) for i, dd in zip(ix, d)]))}
 
     def host_io(self):
         """(inputs, outputs) a user's step moves across PCIe: features + upstream gradient in,
@@ -179,13 +225,10 @@ class HypergraphProgram(_Program):
     def __init__(self, hg: dict, device="cuda", prec="3xtf32", rows_per_item=0):
         dev = self.device = torch.device(device)
         self.prec = prec
-        nk = torch.as_tensor(hg["nodes"]["key"]).to(dev)
-        hk = torch.as_tensor(hg["hyperedges"]["key"]).to(dev)
-        iv = torch.as_tensor(hg["inc"]["node"]).to(dev)
-        ih = torch.as_tensor(hg["inc"]["hyper"]).to(dev)
-        self.idx1 = rnn.build_join_index(iv, ih, nk, hk, rows_per_item=rows_per_item)
-        self.idx2 = rnn.build_join_index(ih, iv, self.idx1.group_key.clone(), nk,
-                                         rows_per_item=rows_per_item)
+        self._in = tuple(torch.as_tensor(a).to(dev) for a in (
+            hg["nodes"]["key"], hg["hyperedges"]["key"], hg["inc"]["node"], hg["inc"]["hyper"]))
+        self._rpi = rows_per_item
+        self.build_indices()
         d = hg["nodes"]["x"].shape[1]
         self.d = d
         self.X = _dev_f32(hg["nodes"]["x"], dev)
@@ -204,6 +247,12 @@ class HypergraphProgram(_Program):
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
 
+    def build_indices(self):
+        nk, hk, iv, ih = self._in
+        self.idx1 = rnn.build_join_index(iv, ih, nk, hk, rows_per_item=self._rpi)
+        self.idx2 = rnn.build_join_index(ih, iv, self.idx1.group_key.clone(), nk,
+                                         rows_per_item=self._rpi)
+
     @property
     def join_rows_per_step(self):
         return self.idx1.n_join_rows + self.idx2.n_join_rows
@@ -212,6 +261,11 @@ class HypergraphProgram(_Program):
         d = self.d
         return {"lja_fwd": (_sum_bytes(self.idx1, d) + _sum_bytes(self.idx2, d, mean=True)) / 2,
                 "lja_bwd": (_sum_bwd_bytes(self.idx1, d) + _sum_bwd_bytes(self.idx2, d, mean=True)) / 2}
+
+    def compulsory_bytes(self):
+        d = self.d
+        return {"lja_fwd": (_comp_fwd(self.idx1, d) + _comp_fwd(self.idx2, d)) / 2,
+                "lja_bwd": (_comp_bwd(self.idx1, d) + _comp_bwd(self.idx2, d)) / 2}
 
     def host_io(self):
         return [self.X, self.d_out], [self.dTheta]
@@ -253,16 +307,18 @@ def _lja_src_grad(idx, q, d_out, d_src, ws):
 def hgt_parameters(mag: dict, seed=7):
     """Weights and upstream gradient of the HGT layer (host, numpy), shared by HGTProgram and
     the sharded program: per node type the stacked projection W [nb * d, d] whose column
-    blocks are (K'_phi, M'_phi) for every relation phi leaving the type and Q for every
-    relation entering it (Q shared by the relations into a type; K' carries
-    mu / sqrt(d / h), reading 12); d_out [n_t, d] per target type in T-key order."""
+    blocks are (K'_phi, M'_phi) for every relation phi leaving the type and ONE query block
+    ("q", type) for the relations entering it (QLin<L, tau_t> is per target type, PAPER.md
+    Fig. 4, so every relation into t reads the same Q and dQ is the sum over them; K'
+    carries mu / sqrt(d / h), reading 12); d_out [n_t, d] per target type in T-key order."""
     d, h = mag["d"], mag["heads"]
     rng = np.random.default_rng(seed)
     types = list(mag["n"].keys())
     blocks = {t: [] for t in types}
     for name, r in mag["rels"].items():
         blocks[r["src_type"]] += [("k", name), ("m", name)]
-        blocks[r["dst_type"]] += [("q", name)]
+        if ("q", r["dst_type"]) not in blocks[r["dst_type"]]:
+            blocks[r["dst_type"]] += [("q", r["dst_type"])]
     blocks = {t: b for t, b in blocks.items() if b}
     scale = 1.0 / np.sqrt(d / h)
     wq = {t: rng.standard_normal((d, d)) / np.sqrt(d) for t in types}
@@ -274,7 +330,7 @@ def hgt_parameters(mag: dict, seed=7):
             if kind == "k":
                 w = w * scale            # mu / sqrt(d/h) folded into K'
             if kind == "q":
-                w = wq[t]                # Q shared by every relation into t
+                w = wq[t]                # the target type's query map
             ws.append(w)
         W[t] = np.concatenate(ws, 0).astype(np.float32)
     col = {(kind, name): (t, i) for t, b in blocks.items() for i, (kind, name) in enumerate(b)}
@@ -321,17 +377,25 @@ class HGTProgram(_Program):
         self.targets = sorted({r["dst_type"] for r in rels.values()})
         self.Ht = {t: _empty(self.n[t], d, dev) for t in self.targets}
         self.d_out = {t: _dev_f32(par["d_out"][t], dev) for t in self.targets}
+        self._rel_keys = {name: (torch.as_tensor(r["src"]).to(dev), torch.as_tensor(r["dst"]).to(dev))
+                          for name, r in rels.items()}
+        self._rpi = rows_per_item
+        self.rels = rels
+        self.build_indices()
         for name, r in rels.items():
             ts, tt = r["src_type"], r["dst_type"]
-            self.idx[name] = rnn.build_join_index(
-                torch.as_tensor(r["src"]).to(dev), torch.as_tensor(r["dst"]).to(dev),
-                self.keys[ts], self.keys[tt], dense_groups=True, rows_per_item=rows_per_item)
             self.q[name] = rnn.make_query("src", "softmax", src=self._blk("m", name),
-                                          src_key=self._blk("k", name), dst=self._blk("q", name),
+                                          src_key=self._blk("k", name), dst=self._blk("q", tt),
                                           heads=self.h, scale=1.0)
             self.O[name] = _empty(self.n[tt], d, dev)
             self.lse[name] = torch.empty(max(self.n[tt], 1), self.h, dtype=torch.float32, device=dev)
-        self.rels = rels
+        # dQ of the second and later relations into a target type: written here, then added
+        # onto the type's query-gradient block (the shared Q's gradient is the sum over phi).
+        # A gradient buffer takes its operand's leading dimension (rnn.h), so the scratch is a
+        # d-column view of a buffer as wide as the stacked Y[t] (only its d columns are touched).
+        self.dQ_tmp = {t: torch.empty(max(self.n[t], 1), self.Y[t].stride(0), dtype=torch.float32,
+                                      device=dev)[: self.n[t], :d]
+                       for t in self.targets if sum(r["dst_type"] == t for r in rels.values()) > 1}
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
 
@@ -340,9 +404,33 @@ class HGTProgram(_Program):
         buf = self.dY[t] if grad else self.Y[t]
         return buf[:, i * self.d:(i + 1) * self.d]
 
+    def build_indices(self):
+        """One dense-group index per relation phi (A1, built once)."""
+        for name, r in self.rels.items():
+            e_src, e_dst = self._rel_keys[name]
+            self.idx[name] = rnn.build_join_index(
+                e_src, e_dst, self.keys[r["src_type"]], self.keys[r["dst_type"]],
+                dense_groups=True, rows_per_item=self._rpi)
+
     @property
     def join_rows_per_step(self):
         return sum(ix.n_join_rows for ix in self.idx.values())
+
+    def compulsory_bytes(self):
+        """Every index entry, referenced input row and output row once.  fwd: src_row (4) per
+        join row, CSR pointers, U referenced sources' K' and M' rows (8d), per group the Q
+        row, the output row and lse (8d + 4h).  bwd: src_row + src_group + src_pos (12) per
+        join row, both CSRs' pointers, K' and M' of the U sources (8d), per group Q, O and dO
+        (12d) and lse (4h) read and dQ written (4d), every source's dK' and dM' written (8d)."""
+        d, h = self.d, self.h
+        f, b = [], []
+        for ix in self.idx.values():
+            U = _n_referenced(ix)
+            G, E, ns = ix.n_groups, ix.n_join_rows, ix.n_src_rows
+            f.append(E * 4 + 8 * (G + 1) + 8 * d * U + G * (8 * d + 4 * h))
+            b.append(E * 12 + 8 * (G + 1) + 8 * (ns + 1) + 8 * d * U + G * (16 * d + 4 * h) +
+                     ns * 8 * d)
+        return {"lja_fwd": float(np.mean(f)), "lja_bwd": float(np.mean(b))}
 
     def lja_bytes(self):
         """Softmax LJA gather model (h heads), for the algorithm the library
@@ -381,24 +469,42 @@ class HGTProgram(_Program):
 
     def backward(self):
         import ctypes as C
+        first = {t: True for t in self.targets}
         for name, r in self.rels.items():
+            tt = r["dst_type"]
             idx, q = self.idx[name], self.q[name]
-            dO = self.d_out[r["dst_type"]]
+            dO = self.d_out[tt]
             _, bb = rnn.lja_workspace_size(idx, q)
             w = self.ws.get(bb)
-            dm, dk, dq = self._blk("m", name, True), self._blk("k", name, True), self._blk("q", name, True)
+            dm, dk = self._blk("m", name, True), self._blk("k", name, True)
+            dq = self._blk("q", tt, True) if first[tt] else self.dQ_tmp[tt]
             self._t("lja_bwd")
             rnn._check(rnn.lib().rnn_join_aggregate_bwd(
                 C.byref(idx.c), C.byref(q), rnn._ptr(self.O[name]), self.O[name].stride(0),
                 rnn._ptr(self.lse[name]), rnn._ptr(dO), dO.stride(0), rnn._ptr(dm), rnn._ptr(dk),
                 None, rnn._ptr(dq), rnn._ptr(w), w.numel(), rnn._stream()))
             self._t("lja_bwd_end")
+            if not first[tt]:
+                rnn.accumulate(self._blk("q", tt, True), dq, beta=1.0)
+            first[tt] = False
         self._t("proj_bwd")
         for t in self.blocks:
             rnn.project_bwd(self.H[t], self.W[t], self.dY[t], want_dx=True, prec=self.prec,
                             ws=self.ws_p, dx_out=self.dH[t], dw_out=self.dW[t])
         self._t("proj_bwd_end")
         return self.dW, self.dH
+
+
+def edge_is_symmetric(idx) -> bool:
+    """True iff the Edge join rows of a DHN adjacency index (root row, neighbour row) equal
+    their reverse as a multiset -- decided on the index itself, so Edge tuples dropped by the
+    join (absent keys) cannot make a non-symmetric relation look symmetric."""
+    if idx.n_join_rows == 0:
+        return True
+    r = idx.group_dst_row.long()[idx.pos_group.long()]
+    v = idx.src_row.long()
+    n = max(int(idx.n_src_rows), 1)
+    return bool(torch.equal(torch.sort(r * n + v).values, torch.sort(v * n + r).values))
 
 
 class DHNProgram(_Program):
@@ -419,11 +525,9 @@ class DHNProgram(_Program):
         dev = self.device = torch.device(device)
         self.prec = prec
         self.ks = tuple(ks)
-        keys = torch.as_tensor(g["nodes"]["key"]).to(dev)
-        # Edge(n, v): root n = dst column, neighbour v = src column
-        self.idx = rnn.build_join_index(torch.as_tensor(g["edges"]["src"]).to(dev),
-                                        torch.as_tensor(g["edges"]["dst"]).to(dev), keys, keys,
-                                        dense_groups=True)
+        self._in = tuple(torch.as_tensor(a).to(dev) for a in (
+            g["nodes"]["key"], g["edges"]["src"], g["edges"]["dst"]))
+        self.build_indices()
         self.n = len(g["nodes"]["key"])
         self.d = d = g["nodes"]["x"].shape[1]
         self.H = _dev_f32(g["nodes"]["x"], dev)
@@ -441,14 +545,9 @@ class DHNProgram(_Program):
         # each pattern's walk sum before the root factor, saved by the forward so the backward
         # forms d f0 = dOut (.) sum without a walk (rnn_dhn_fwd_save / rnn_dhn_bwd_saved)
         self.walk_sum = {k: _empty(G, d, dev) for k in self.ks}
-        # RNN_DHN_SYMMETRIC_EDGE: verified once at setup (Edge equals its reverse as a multiset)
-        ks = torch.sort(keys).values
-        es = torch.searchsorted(ks, torch.as_tensor(g["edges"]["src"]).to(dev))
-        ed = torch.searchsorted(ks, torch.as_tensor(g["edges"]["dst"]).to(dev))
-        nn_ = max(len(ks), 1)
-        self.symmetric = bool(torch.equal(torch.sort(es * nn_ + ed).values,
-                                          torch.sort(ed * nn_ + es).values))
-        del es, ed
+        # RNN_DHN_SYMMETRIC_EDGE: verified once at setup on the built index (the join rows
+        # that survived, as (root row, neighbour row) pairs, equal their reverse as a multiset)
+        self.symmetric = edge_is_symmetric(self.idx)
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
         self.pos0 = {}
@@ -457,6 +556,11 @@ class DHNProgram(_Program):
             self.pos0[k] = p
             p += k
         self._rows = None
+
+    def build_indices(self):
+        """Edge(n, v): root n = dst column, neighbour v = src column; dense groups."""
+        keys, e_src, e_dst = self._in
+        self.idx = rnn.build_join_index(e_src, e_dst, keys, keys, dense_groups=True)
 
     def _f(self, k, buf):
         p = self.pos0[k]
@@ -504,9 +608,8 @@ class DHNProgram(_Program):
                 if int(k[3]) in self.ks}
 
     def _walks(self, k):
-        ones = torch.ones(self.n, 1, dtype=torch.float32, device=self.device)
-        c = rnn.dhn_fwd(self.idx, k, [None] + [ones] * (k - 1), ws=self.ws)
-        return float(c.double().sum().item())
+        """Closed k-walks over all roots: the exact int64 homomorphism counts (rnn_dhn_count)."""
+        return int(rnn.dhn_count(self.idx, k).sum().item())
 
     def forward(self):
         self._t("proj_fwd")

@@ -88,6 +88,8 @@ def lib():
         L.rnn_hash_partition.argtypes = [vp, i64, i32, C.c_uint64, vp, vp]
         L.rnn_accumulate.argtypes = [vp, i64, vp, i64, i64, i32, C.c_float, vp]
         L.rnn_accumulate.restype = C.c_int
+        L.rnn_gather_rows.argtypes = [vp, i64, vp, i64, vp, i64, i32, vp]
+        L.rnn_gather_rows.restype = C.c_int
         L.rnn_dhn_workspace_size.argtypes = [C.POINTER(JoinIndexC), i32, i32, C.POINTER(sz)]
         L.rnn_dhn_fwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64, vp, sz, vp]
         L.rnn_dhn_fwd_save.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
@@ -96,6 +98,10 @@ def lib():
                                         vp, i64, C.POINTER(vp), i64, C.c_uint32, vp, sz, vp]
         L.rnn_dhn_bwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
                                   C.POINTER(vp), i64, vp, sz, vp]
+        L.rnn_dhn_fwd_roots.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
+                                        vp, i64, vp, i64, vp, sz, vp]
+        L.rnn_dhn_bwd_roots.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64,
+                                        vp, i64, vp, i64, C.POINTER(vp), i64, C.c_uint32, vp, sz, vp]
         L.rnn_dhn_count_workspace_size.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(sz)]
         L.rnn_dhn_count.argtypes = [C.POINTER(JoinIndexC), i32, vp, vp, sz, vp]
         L.rnn_internal_dhn_stats.argtypes = [C.POINTER(C.c_ulonglong), C.c_int, C.c_int]
@@ -103,7 +109,8 @@ def lib():
         L.rnn_group_sizes.argtypes = [C.POINTER(JoinIndexC), vp, vp]
         for f in ("rnn_dhn_workspace_size", "rnn_dhn_fwd", "rnn_dhn_bwd", "rnn_dhn_fwd_save",
                   "rnn_dhn_bwd_saved", "rnn_gcn_norm_src_deg", "rnn_dhn_count_workspace_size",
-                  "rnn_dhn_count", "rnn_internal_dhn_stats",
+                  "rnn_dhn_count", "rnn_internal_dhn_stats", "rnn_dhn_fwd_roots",
+                  "rnn_dhn_bwd_roots",
                   "rnn_group_sizes"):
             getattr(L, f).restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
@@ -416,6 +423,14 @@ def accumulate(y, x, beta=1.0, stream=None):
     return y
 
 
+def gather_rows(y, x, idx, stream=None):
+    """y[i] = x[idx[i]] (0 where idx[i] < 0), idx int32 on the device (rnn_gather_rows)."""
+    n, cols = y.shape
+    _check(lib().rnn_gather_rows(_ptr(y), y.stride(0), _ptr(x), x.stride(0), _ptr(idx), n, cols,
+                                 _stream(stream)))
+    return y
+
+
 # ------------------------------------------------------------------------------------------
 # A6 DHN closed-walk aggregates
 # ------------------------------------------------------------------------------------------
@@ -430,10 +445,11 @@ def _dhn_ops(f):
     return ops
 
 
-def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None, walk_sum=None):
+def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None, walk_sum=None, roots=None):
     """C_k per root (group order) of the closed-walk rule; f = [f0 (or None), f1, ..., f_{k-1}]
     by node row (rnn_dhn_fwd).  walk_sum [n_groups, >= d]: also save the walk sum before the
-    root factor for dhn_bwd (rnn_dhn_fwd_save)."""
+    root factor for dhn_bwd (rnn_dhn_fwd_save).  roots: int32 device tensor of group ids --
+    only those roots are computed (rnn_dhn_fwd_roots)."""
     assert len(f) == k
     dev = adj.group_ptr.device
     d = f[1].shape[1]
@@ -441,6 +457,12 @@ def dhn_fwd(adj: JoinIndex, k, f, out=None, ws=None, stream=None, walk_sum=None)
         out = torch.empty(max(adj.n_groups, 1), (d + 3) // 4 * 4, dtype=torch.float32, device=dev)[:adj.n_groups, :d]
     nb = dhn_workspace_size(adj, k, d)
     w = ws.get(nb) if ws is not None else _ws(nb, dev)
+    if roots is not None:
+        _check(lib().rnn_dhn_fwd_roots(C.byref(adj.c), k, _dhn_ops(f), _ptr(roots), roots.numel(),
+                                       _ptr(out), out.stride(0), _ptr(walk_sum),
+                                       0 if walk_sum is None else walk_sum.stride(0), _ptr(w),
+                                       w.numel(), _stream(stream)))
+        return out
     if walk_sum is not None:
         _check(lib().rnn_dhn_fwd_save(C.byref(adj.c), k, _dhn_ops(f), _ptr(out), out.stride(0),
                                       _ptr(walk_sum), walk_sum.stride(0), _ptr(w), w.numel(),
@@ -455,7 +477,7 @@ DHN_SYMMETRIC_EDGE = 1
 
 
 def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=None,
-            walk_sum=None, symmetric=False):
+            walk_sum=None, symmetric=False, roots=None):
     """[d f0, ..., d f_{k-1}] by node row (rnn_dhn_bwd); want[i] False -> None.  walk_sum: the
     forward's saved walk sum (d f0 without a walk launch, rnn_dhn_bwd_saved)."""
     dev = adj.group_ptr.device
@@ -472,6 +494,13 @@ def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=No
     ptrs = (C.c_void_p * k)(*[None if t is None else t.data_ptr() for t in d_f])
     nb = dhn_workspace_size(adj, k, d)
     w = ws.get(nb) if ws is not None else _ws(nb, dev)
+    if roots is not None:
+        _check(lib().rnn_dhn_bwd_roots(C.byref(adj.c), k, _dhn_ops(f), _ptr(roots), roots.numel(),
+                                       _ptr(d_out), d_out.stride(0), _ptr(walk_sum),
+                                       0 if walk_sum is None else walk_sum.stride(0), ptrs, ld,
+                                       DHN_SYMMETRIC_EDGE if symmetric else 0, _ptr(w), w.numel(),
+                                       _stream(stream)))
+        return d_f
     if walk_sum is not None:
         _check(lib().rnn_dhn_bwd_saved(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out),
                                        d_out.stride(0), _ptr(walk_sum), walk_sum.stride(0), ptrs,

@@ -117,7 +117,11 @@ class ShardedGCNProgram:
         keys = np.asarray(nodes["key"], np.int64)
         owner = be.hash_partition(keys, self.P, seed)
         plan = self.plan = ShardPlan(keys, edges["src"], edges["dst"], owner, self.P, self.rank)
+        # layer widths padded to a multiple of 4 (rnn_project / the LJA need ld % 4 == 0 and
+        # the collectives contiguous rows): W, features and d_out are zero-padded, so padded
+        # columns stay exactly 0 and the real columns are unchanged (Cora: 1,433 -> 16 -> 7)
         self.dims = list(graph["dims"])
+        dp = self.dims_pad = [(x + 3) // 4 * 4 for x in self.dims]
         self.L = len(self.dims) - 1
         n_pad, P = plan.n_pad, self.P
         self.n_own = int(plan.counts[self.rank])
@@ -130,21 +134,27 @@ class ShardedGCNProgram:
         all_gather_rows(all_deg, own_deg, group)
         self.w = be.gcn_norm_src_deg(self.idx, all_deg)
         # activations (rows >= n_own stay zero: padding of the gathered blocks)
-        x0 = np.zeros((n_pad, self.dims[0]), np.float32)
-        x0[: self.n_own] = np.asarray(nodes["x"], np.float32)[plan.my_rows]
-        self.H = [be.tensor(x0)] + [be.zeros(n_pad, self.dims[l + 1]) for l in range(self.L)]
-        self.W = [be.tensor(np.asarray(w, np.float32)) for w in graph["W"]]
-        self.Z = [be.zeros(n_pad, self.dims[l + 1]) for l in range(self.L)]
-        self.Zall = [be.zeros(P * n_pad, self.dims[l + 1]) for l in range(self.L)]
-        self.dZall = [be.zeros(P * n_pad, self.dims[l + 1]) for l in range(self.L)]
-        self.dZ = [be.zeros(n_pad, self.dims[l + 1]) for l in range(self.L)]
-        self.dH = [be.zeros(n_pad, self.dims[l]) for l in range(self.L)]
-        self.dW = [be.zeros(self.dims[l + 1], self.dims[l]) for l in range(self.L)]
+        x0 = np.zeros((n_pad, dp[0]), np.float32)
+        x0[: self.n_own, : self.dims[0]] = np.asarray(nodes["x"], np.float32)[plan.my_rows]
+        self.H = [be.tensor(x0)] + [be.zeros(n_pad, dp[l + 1]) for l in range(self.L)]
+        Wp = []
+        for l, w in enumerate(graph["W"]):
+            wp = np.zeros((dp[l + 1], dp[l]), np.float32)
+            wp[: self.dims[l + 1], : self.dims[l]] = np.asarray(w, np.float32)
+            Wp.append(be.tensor(wp))
+        self.W = Wp
+        self.Z = [be.zeros(n_pad, dp[l + 1]) for l in range(self.L)]
+        self.Zall = [be.zeros(P * n_pad, dp[l + 1]) for l in range(self.L)]
+        self.dZall = [be.zeros(P * n_pad, dp[l + 1]) for l in range(self.L)]
+        self.dZ = [be.zeros(n_pad, dp[l + 1]) for l in range(self.L)]
+        self.dH = [be.zeros(n_pad, dp[l]) for l in range(self.L)]
+        self._dW = [be.zeros(dp[l + 1], dp[l]) for l in range(self.L)]
+        self.dW = [w[: self.dims[l + 1], : self.dims[l]] for l, w in enumerate(self._dW)]
         # upstream gradient of the owned output rows (the oracle's d_out row of each group)
         G_all = np.sort(keys)
         rank_of = np.searchsorted(G_all, plan.my_keys)
-        d_out = np.zeros((n_pad, self.dims[-1]), np.float32)
-        d_out[: self.n_own] = np.asarray(graph["d_out"], np.float32)[rank_of, : self.dims[-1]]
+        d_out = np.zeros((n_pad, dp[-1]), np.float32)
+        d_out[: self.n_own, : self.dims[-1]] = np.asarray(graph["d_out"], np.float32)[rank_of, : self.dims[-1]]
         self.d_out = be.tensor(d_out)
         self.timers = None
 
@@ -155,12 +165,12 @@ class ShardedGCNProgram:
 
     def roof_model(self):
         from .programs import _sum_bwd_bytes, _sum_bytes
-        d = self.dims[1:]
+        d = self.dims_pad[1:]
         return {"lja_fwd": {"bound": "hbm", "amount": float(np.mean([_sum_bytes(self.idx, x, True) for x in d]))},
                 "lja_bwd": {"bound": "hbm", "amount": float(np.mean([_sum_bwd_bytes(self.idx, x, True) for x in d]))}}
 
     def host_io(self):
-        return [self.H[0], self.d_out], list(self.dW)
+        return [self.H[0], self.d_out], list(self._dW)
 
     def _t(self, name):
         if self.timers is None:
@@ -194,10 +204,10 @@ class ShardedGCNProgram:
             reduce_scatter_rows(self.dZ[l], self.dZall[l], g)
             self._t("reduce_scatter_end")
             self._t("proj_bwd")
-            be.project_bwd(self.H[l], self.W[l], self.dZ[l], self.dH[l], self.dW[l])
+            be.project_bwd(self.H[l], self.W[l], self.dZ[l], self.dH[l], self._dW[l])
             self._t("proj_bwd_end")
             if self.P > 1:
-                dist.all_reduce(self.dW[l], group=g)
+                dist.all_reduce(self._dW[l], group=g)
             dY = self.dH[l]
         return self.dW, self.dH[0]
 
@@ -207,10 +217,10 @@ class ShardedGCNProgram:
 
     # ---- gathering results for checks (host) ----
     def owned_output(self):
-        return self.be.numpy(self.H[-1])[: self.n_own]
+        return self.be.numpy(self.H[-1])[: self.n_own, : self.dims[-1]]
 
     def owned_dx(self):
-        return self.be.numpy(self.dH[0])[: self.n_own]
+        return self.be.numpy(self.dH[0])[: self.n_own, : self.dims[0]]
 
 
 class RnnBackend:
@@ -293,6 +303,43 @@ class RnnBackend:
 
     def accumulate(self, out, x, beta):
         self.rnn.accumulate(out, x, beta=beta)
+
+    # ---- DHN (A6) ----
+    def build_dhn_index(self, e_src, e_dst, s_keys):
+        """Replicated adjacency Edge(n, v) over the gathered node layout: S = T = s_keys
+        (rank-major blocks), dense groups in key order."""
+        cu = lambda a: torch.as_tensor(np.asarray(a, np.int64), device=self.dev)
+        k = cu(s_keys)
+        return self.rnn.build_join_index(cu(e_src), cu(e_dst), k, k, dense_groups=True)
+
+    def dhn_groups(self, idx):
+        """(group keys, T row of every group) on the host."""
+        return self.numpy(idx.group_key), self.numpy(idx.group_dst_row)
+
+    def dhn_symmetric(self, idx):
+        from .programs import edge_is_symmetric
+        return edge_is_symmetric(idx)
+
+    def index_i32(self, a):
+        return torch.as_tensor(np.asarray(a, np.int32), device=self.dev)
+
+    def gather_rows(self, out, x, idx):
+        self.rnn.gather_rows(out, x, idx)
+
+    def dhn_fwd(self, idx, k, f, roots, out, walk_sum):
+        self.rnn.dhn_fwd(idx, k, f, out=out, ws=self.ws, walk_sum=walk_sum, roots=roots)
+
+    def dhn_bwd(self, idx, k, f, roots, d_out, walk_sum, d_f, symmetric):
+        self.rnn.dhn_bwd(idx, k, f, d_out, d_f=d_f, ws=self.ws, walk_sum=walk_sum,
+                         symmetric=symmetric, roots=roots)
+
+    def dhn_rows(self, idx, roots, ks):
+        """Edge rows + exact closed-walk counts of the listed roots (rnn_dhn_count)."""
+        tot = 0
+        r = roots.long()
+        for k in ks:
+            tot += int(self.rnn.dhn_count(idx, k)[r].sum().item())
+        return tot
 
     def lja_sm_fwd(self, idx, M, K, Q, heads, out, lse):
         q = self.rnn.make_query("src", "softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
@@ -546,6 +593,9 @@ class ShardedHGTProgram:
             self.O[name] = be.zeros(self.n_pad[tt], d)
             self.lse[name] = be.zeros(self.n_pad[tt], h)
         self.Ht = {t: be.zeros(self.n_pad[t], d) for t in self.targets}
+        # per-relation dQ, summed into the target type's single query-gradient block (a
+        # gradient buffer takes its operand's ld -- here the stacked Y[t]'s -- rnn.h)
+        self.dQ = {t: be.zeros(self.n_pad[t], len(self.blocks[t]) * d)[:, :d] for t in self.targets}
         self.d_out = {}
         for t in self.targets:
             full = np.asarray(par["d_out"][t], np.float32)       # T-key order of all keys
@@ -598,7 +648,7 @@ class ShardedHGTProgram:
             n = self.n_own[tt]
             self._t("lja_fwd")
             be.lja_sm_fwd(self.idx[name], self._blk(self.Yall, ts, "m", name),
-                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", name),
+                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", tt),
                           self.h, self.O[name][:n], self.lse[name][:n])
             self._t("lja_fwd_end")
             be.accumulate(self.Ht[tt][:n], self.O[name][:n], 0.0 if first[tt] else 1.0)
@@ -614,11 +664,12 @@ class ShardedHGTProgram:
             n = self.n_own[tt]
             self._t("lja_bwd")
             be.lja_sm_bwd(self.idx[name], self._blk(self.Yall, ts, "m", name),
-                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", name),
+                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", tt),
                           self.h, self.O[name][:n], self.lse[name][:n], self.d_out[tt][:n],
                           self._blk(self.dYall, ts, "m", name), self._blk(self.dYall, ts, "k", name),
-                          self._blk(self.dY, tt, "q", name)[:n])
+                          self.dQ[tt][:n])
             self._t("lja_bwd_end")
+            be.accumulate(self._blk(self.dY, tt, "q", tt)[:n], self.dQ[tt][:n], 1.0)
         for s in self.sources:
             reduce_scatter_rows(self.R[s], self.dYall[s], g)
             be.accumulate(self.dY[s], self.R[s], 1.0)
@@ -634,3 +685,158 @@ class ShardedHGTProgram:
     def step(self):
         self.forward()
         return self.backward()
+
+
+class ShardedDHNProgram:
+    """One DHN layer (config 5) over P ranks (DHN bullet):
+    roots hash-partitioned by node key, the Edge adjacency replicated on every rank (built
+    once over the gathered node layout), the position features all-gathered once per layer.
+
+        Y_own   = H_own W^T                            (A2, the nine position maps)
+        Y_all   = all_gather(Y_own)                    (NCCL: f_{k,i} of every node)
+        C_k(n)  = closed-walk aggregate, n in owned roots        (rnn_dhn_fwd_roots)
+      backward: closed walks are rotation invariant, so d f_j(x) is the walk aggregate ROOTED
+      at x with rotated operands (g = f0 (.) dOut in the walk): each rank computes the
+      complete gradient rows of its OWN nodes from the all-gathered dOut -- no reduce-scatter
+        dOut_all = all_gather(dOut_own)                (3d per node)
+        d f_j(x), x owned                              (rnn_dhn_bwd_roots)
+        dH_own, dW = projection backward;  all_reduce(dW)
+    Owned rows sit at [rank * n_pad, rank * n_pad + n_own) of the gathered layout (ShardPlan),
+    so d f of owned nodes is a contiguous slice; outputs come back in owned-key order through
+    rnn_gather_rows (group order -> owned rows, dOut rows -> group order)."""
+
+    KS = (2, 3, 4)
+
+    def __init__(self, g: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32",
+                 param_seed=11, ks=KS):
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        be = self.be = backend if backend is not None else RnnBackend(prec=prec)
+        P, r = self.P, self.rank
+        self.ks = tuple(ks)
+        keys = np.asarray(g["nodes"]["key"], np.int64)
+        owner = be.hash_partition(keys, P, seed)
+        e_src, e_dst = np.asarray(g["edges"]["src"]), np.asarray(g["edges"]["dst"])
+        plan = self.plan = ShardPlan(keys, e_src, e_dst, owner, P, r)
+        self.n_pad, self.n_own = plan.n_pad, int(plan.counts[r])
+        self.d = d = g["nodes"]["x"].shape[1]
+        self.npos = sum(self.ks)
+        # replicated adjacency over ALL Edge rows, S = T = the gathered layout
+        self.idx = be.build_dhn_index(e_src, e_dst, plan.s_keys)
+        gkey, grow = be.dhn_groups(self.idx)
+        self.G = len(gkey)
+        self.symmetric = be.dhn_symmetric(self.idx)
+        # owned roots: groups whose key this rank owns (owned nodes without a group -- no
+        # out-edges -- aggregate to 0)
+        pos = np.searchsorted(gkey, plan.my_keys)
+        pos = np.clip(pos, 0, max(self.G - 1, 0))
+        has = (self.G > 0) & (gkey[pos] == plan.my_keys) if self.G else np.zeros(len(plan.my_keys), bool)
+        own_grp = np.where(has, pos, -1).astype(np.int32)
+        self.roots = be.index_i32(own_grp[own_grp >= 0])
+        og = np.full(self.n_pad, -1, np.int32)
+        og[: self.n_own] = own_grp
+        self.own_grp = be.index_i32(og)                   # owned row -> group (or -1)
+        self.row_of_grp = be.index_i32(grow)              # group -> gathered row
+        # parameters (DHNProgram's draws) and owned inputs
+        rng = np.random.default_rng(param_seed)
+        W = rng.standard_normal((self.npos * d, d)) / np.sqrt(d)
+        d_out_full = rng.standard_normal((len(keys), len(self.ks) * d)).astype(np.float32)
+        ks_sorted = np.sort(keys)
+        x = np.zeros((self.n_pad, d), np.float32)
+        x[: self.n_own] = np.asarray(g["nodes"]["x"], np.float32)[plan.my_rows]
+        dO = np.zeros((self.n_pad, len(self.ks) * d), np.float32)
+        dO[: self.n_own] = d_out_full[np.searchsorted(ks_sorted, plan.my_keys)]
+        self.H = be.tensor(x)
+        self.W = be.tensor(W.astype(np.float32))
+        self.d_out = be.tensor(dO)
+        nall = P * self.n_pad
+        self.Y = be.zeros(self.n_pad, self.npos * d)
+        self.Yall = be.zeros(nall, self.npos * d)
+        self.dYall = be.zeros(nall, self.npos * d)
+        self.out_grp = be.zeros(max(self.G, 1), len(self.ks) * d)[: self.G]
+        self.out = be.zeros(self.n_pad, len(self.ks) * d)
+        self.walk_sum = {k: be.zeros(max(self.G, 1), d)[: self.G] for k in self.ks}
+        self.dOall = be.zeros(nall, len(self.ks) * d)
+        self.dOgrp = be.zeros(max(self.G, 1), len(self.ks) * d)[: self.G]
+        self.dW = be.zeros(self.npos * d, d)
+        self.dH = be.zeros(self.n_pad, d)
+        self.pos0 = {}
+        p = 0
+        for k in self.ks:
+            self.pos0[k] = p
+            p += k
+        self.timers = None
+        self._rows = None
+
+    def _f(self, k, buf):
+        p, d = self.pos0[k], self.d
+        return [buf[:, (p + i) * d:(p + i + 1) * d] for i in range(k)]
+
+    @property
+    def join_rows_per_step(self):
+        """This rank's rows: Edge rows of its roots (C2) + closed 3- and 4-walks rooted at
+        them (exact counts over the replicated adjacency)."""
+        if self._rows is None:
+            self._rows = self.be.dhn_rows(self.idx, self.roots, self.ks)
+        return self._rows
+
+    def roof_model(self):
+        return {"dhn4_fwd": {"bound": "alu", "amount": float("nan")}}
+
+    def host_io(self):
+        return [self.H, self.d_out], [self.dW]
+
+    def _t(self, name):
+        if self.timers is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.timers.setdefault(name, []).append(e)
+
+    def forward(self):
+        be, g, d = self.be, self.group, self.d
+        self._t("proj_fwd")
+        be.project(self.H, self.W, self.Y)
+        self._t("proj_fwd_end")
+        self._t("allgather")
+        all_gather_rows(self.Yall, self.Y, g)
+        self._t("allgather_end")
+        for j, k in enumerate(self.ks):
+            self._t(f"dhn{k}_fwd")
+            be.dhn_fwd(self.idx, k, self._f(k, self.Yall), self.roots,
+                       self.out_grp[:, j * d:(j + 1) * d], self.walk_sum[k])
+            self._t(f"dhn{k}_fwd_end")
+        be.gather_rows(self.out, self.out_grp, self.own_grp)
+        return self.out
+
+    def backward(self):
+        be, g, d = self.be, self.group, self.d
+        self._t("allgather")
+        all_gather_rows(self.dOall, self.d_out, g)
+        self._t("allgather_end")
+        be.gather_rows(self.dOgrp, self.dOall, self.row_of_grp)
+        for j, k in enumerate(self.ks):
+            self._t(f"dhn{k}_bwd")
+            be.dhn_bwd(self.idx, k, self._f(k, self.Yall), self.roots,
+                       self.dOgrp[:, j * d:(j + 1) * d], self.walk_sum[k],
+                       self._f(k, self.dYall), self.symmetric)
+            self._t(f"dhn{k}_bwd_end")
+        lo = self.rank * self.n_pad
+        dY_own = self.dYall[lo:lo + self.n_pad]
+        self._t("proj_bwd")
+        be.project_bwd(self.H, self.W, dY_own, self.dH, self.dW)
+        self._t("proj_bwd_end")
+        if self.P > 1:
+            dist.all_reduce(self.dW, group=g)
+        return self.dW, self.dH
+
+    def step(self):
+        self.forward()
+        return self.backward()
+
+    def owned_output(self):
+        return self.be.numpy(self.out)[: self.n_own]
+
+    def owned_dx(self):
+        return self.be.numpy(self.dH)[: self.n_own]

@@ -27,8 +27,41 @@ def powerlaw_weights(rng, n, beta=BETA, cap_ratio=1000.0):
     return np.minimum(w, cap_ratio * w.mean())
 
 
+def _search_right(cdf, q):
+    """np.searchsorted(cdf, q, side="right") for a large batch of random queries, in
+    cache-friendly steps (identical result): a bucket table gives a lower bound of every
+    answer, then a few vectorised forward steps finish it (random probes of a multi-MB CDF
+    are ~20x slower than this)."""
+    n = len(cdf)
+    if n < 4096 or len(q) < 65536:
+        return np.searchsorted(cdf, q, side="right")
+    nb = 1 << max(10, int(np.ceil(np.log2(n))) + 1)
+    width = cdf[-1] / nb
+    # lower bound: entries <= bucket start (b - 1 guards the rounding of q / width)
+    table = np.searchsorted(cdf, np.arange(nb + 1) * width, side="right")
+    b = np.clip((q / width).astype(np.int64) - 1, 0, nb)
+    idx = table[b]
+    act = np.nonzero((idx < n) & (cdf[np.minimum(idx, n - 1)] <= q))[0]
+    while len(act):
+        idx[act] += 1
+        i = idx[act]
+        act = act[(i < n) & (cdf[np.minimum(i, n - 1)] <= q[act])]
+    return idx
+
+
+def _sorted_unique(x):
+    """np.unique(x) (sorted distinct values) via one in-place sort."""
+    x = np.sort(x)
+    if len(x) == 0:
+        return x
+    keep = np.empty(len(x), bool)
+    keep[0] = True
+    np.not_equal(x[1:], x[:-1], out=keep[1:])
+    return x[keep]
+
+
 def _draw(rng, cdf, k):
-    return np.searchsorted(cdf, rng.random(k) * cdf[-1], side="right").clip(0, len(cdf) - 1)
+    return _search_right(cdf, rng.random(k) * cdf[-1]).clip(0, len(cdf) - 1)
 
 
 def chung_lu(rng, w_s, w_t, m, same_set, undirected, block=None, mu_intra=0.0):
@@ -52,14 +85,14 @@ def chung_lu(rng, w_s, w_t, m, same_set, undirected, block=None, mu_intra=0.0):
             lo = np.where(b0 > 0, ct[np.maximum(b0 - 1, 0)], 0.0)
             hi = ct[b1 - 1]
             u = lo + rng.random(int(intra.sum())) * (hi - lo)
-            t[intra] = np.searchsorted(ct, u, side="right").clip(b0, b1 - 1)
+            t[intra] = _search_right(ct, u).clip(b0, b1 - 1)
         if same_set:
             keep = s != t
             s, t = s[keep], t[keep]
         if undirected:
             s, t = np.minimum(s, t), np.maximum(s, t)
         code = s.astype(np.int64) * n_t + t
-        have = np.unique(np.concatenate([have, code]))
+        have = _sorted_unique(np.concatenate([have, code]))
     pick = np.sort(rng.choice(len(have), size=m, replace=False))
     code = have[pick]
     return code // n_t, code % n_t

@@ -187,3 +187,57 @@ def test_dhn_program(rnn):
     cnt = sum(oracle.dhn_fwd(k, oi, g["nodes"]["key"], [np.ones((n, 1))] * k).sum() for k in (3, 4))
     ref_rows = oi["n_join_rows"] + int(cnt)
     assert abs(prog.join_rows_per_step - ref_rows) <= 1e-6 * ref_rows   # fp32 count sums
+
+
+def test_symmetry_decided_on_index(rnn):
+    """RNN_DHN_SYMMETRIC_EDGE is asserted only when the SURVIVING join rows are symmetric:
+    Edge tuples whose endpoint keys are absent are dropped by the join and must not make a
+    non-symmetric relation look symmetric."""
+    from paper_2605_24207_b200.programs import edge_is_symmetric
+    keys = np.array([1, 2, 3], np.int64)
+    # Edge(n, v) as (n, v): (1,2), (2,1), (1,3) survive; (3,99) dangles -> not symmetric
+    e_n, e_v = np.array([1, 2, 1, 3]), np.array([2, 1, 3, 99])
+    gi = rnn.build_join_index(cu(e_v), cu(e_n), cu(keys), cu(keys), dense_groups=True)
+    assert gi.n_join_rows == 3 and not edge_is_symmetric(gi)
+    # (1,2), (2,1) survive; the dangling pair (3,99), (99,3) is dropped -> symmetric
+    e_n, e_v = np.array([1, 2, 3, 99]), np.array([2, 1, 99, 3])
+    gi = rnn.build_join_index(cu(e_v), cu(e_n), cu(keys), cu(keys), dense_groups=True)
+    assert gi.n_join_rows == 2 and edge_is_symmetric(gi)
+    # multiplicity counts: (1,2) twice, (2,1) once -> not symmetric
+    e_n, e_v = np.array([1, 1, 2]), np.array([2, 2, 1])
+    gi = rnn.build_join_index(cu(e_v), cu(e_n), cu(keys), cu(keys), dense_groups=True)
+    assert not edge_is_symmetric(gi)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_root_subset(rnn, k):
+    """rnn_dhn_fwd_roots / rnn_dhn_bwd_roots: only the listed roots are computed (repeats and
+    out-of-range ids ignored; other output rows untouched); the backward gives the listed
+    roots' nodes their complete gradient rows (walks rooted there, operands rotated) and 0
+    elsewhere, from the FULL upstream gradient."""
+    keys, e_n, e_v = random_graph(60 + k, 300, 2400, directed=False)
+    gi, oi = build(rnn, keys, e_n, e_v)
+    n, d = len(keys), 16
+    f = feats(k, n, d, k)
+    fg = [cu(x) for x in f]
+    rng = np.random.default_rng(k)
+    sel = np.sort(rng.choice(gi.n_groups, 60, replace=False)).astype(np.int32)
+    roots = cu(np.concatenate([sel, sel[:5], [-3, gi.n_groups + 7]]).astype(np.int32))
+    out = torch.full((gi.n_groups, d), float("nan"), device="cuda")
+    ws = torch.full((gi.n_groups, d), float("nan"), device="cuda")
+    rnn.dhn_fwd(gi, k, fg, out=out, walk_sum=ws, roots=roots)
+    o = np_(out)
+    full = np_(rnn.dhn_fwd(gi, k, fg))
+    np.testing.assert_array_equal(o[sel], full[sel])
+    others = np.setdiff1d(np.arange(gi.n_groups), sel)
+    assert np.all(np.isnan(o[others]))
+    d_out = rng.standard_normal((gi.n_groups, d)).astype(np.float32)
+    grads = rnn.dhn_bwd(gi, k, fg, cu(d_out), walk_sum=ws, roots=roots)
+    rows = np.searchsorted(np_(gi.group_key), oi["group_key"])
+    ref = oracle.dhn_bwd(k, oi, keys, f, d_out[rows])
+    node_rows = np_(gi.group_dst_row)[sel]
+    other_rows = np.setdiff1d(np.arange(n), node_rows)
+    for i in range(k):
+        g = np_(grads[i])
+        assert_close(g[node_rows], ref[i][node_rows], FP32_TOL, f"d f{i} listed")
+        assert np.all(g[other_rows] == 0.0), i

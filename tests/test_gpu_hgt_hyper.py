@@ -45,7 +45,7 @@ def test_hgt_layer(P):
         W_s, W_t = np_(prog.W[ts]), np_(prog.W[tt])
         ik = prog.col[("k", name)][1]
         im = prog.col[("m", name)][1]
-        iq = prog.col[("q", name)][1]
+        iq = prog.col[("q", tt)][1]
         res = op.hgt_relation(mag["h"][ts], mag["h"][tt], W_s[ik * d:(ik + 1) * d],
                               W_s[im * d:(im + 1) * d], W_t[iq * d:(iq + 1) * d],
                               mag["key"][ts], mag["key"][tt], r["src"], r["dst"], prog.h,
@@ -59,7 +59,7 @@ def test_hgt_layer(P):
         Ht_ref[tt][rows] += res["out"]
         dY_ref[ts][:, ik * d:(ik + 1) * d] = res["dK"]
         dY_ref[ts][:, im * d:(im + 1) * d] = res["dM"]
-        dY_ref[tt][:, iq * d:(iq + 1) * d] = res["dQ"]      # d(Q) rows are T storage rows
+        dY_ref[tt][:, iq * d:(iq + 1) * d] += res["dQ"]     # shared Q: dQ summed over phi
     for t in prog.targets:                                   # Ht rows: dense, T-key order
         assert_close(np_(prog.Ht[t]), Ht_ref[t], FP32_TOL, f"Ht[{t}]")
     for t in prog.blocks:

@@ -159,3 +159,58 @@ def test_sharded_hgt_world_2():
         mp.spawn(_worker_hgt, args=(2, _free_port(), d), nprocs=2, join=True)
         res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
     _check_hgt(res)
+
+
+def test_sharded_cora_widths_world_1():
+    """Cora-shaped GCN (1,433 -> 16 -> 7) through the sharded program on the GPU: the
+    ld-padded buffers let rnn_project / the LJA run at width 7."""
+    import synth
+    g = synth.cora_like(42)
+    check([_run(g)], g)
+
+
+def _run_dhn():
+    from paper_2605_24207_b200.shard import ShardedDHNProgram
+    from tests.test_shard_dhn_cpu import graph
+    prog = ShardedDHNProgram(graph())
+    prog.step()
+    torch.cuda.synchronize()
+    return {"keys": prog.plan.my_keys, "rows": prog.plan.my_rows, "out": prog.owned_output(),
+            "dx": prog.owned_dx(), "dW": prog.dW.cpu().numpy(), "n_rows": prog.join_rows_per_step}
+
+
+def _worker_dhn(rank, world, port, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        np.savez(os.path.join(path, f"r{rank}.npz"), **_run_dhn())
+    finally:
+        dist.destroy_process_group()
+
+
+def _check_dhn(res):
+    from tests.test_shard_dhn_cpu import graph, reference
+    g = graph()
+    ref = reference(g)
+    keys = np.sort(np.asarray(g["nodes"]["key"]))
+    got = np.concatenate([r["keys"] for r in res])
+    assert sorted(got.tolist()) == keys.tolist()
+    assert_close(np.concatenate([r["out"] for r in res]), ref["out"][np.searchsorted(keys, got)],
+                 FP32_TOL, "out")
+    rows = np.concatenate([r["rows"] for r in res])
+    assert_close(np.concatenate([r["dx"] for r in res]), ref["dH"][rows], FP32_TOL, "dH")
+    for r in res:
+        assert_close(r["dW"], ref["dW"], FP32_TOL, "dW")
+
+
+def test_sharded_dhn_world_1():
+    """ShardedDHNProgram on librnn.so (rnn_dhn_fwd_roots / rnn_dhn_bwd_roots, rnn_gather_rows)."""
+    _check_dhn([_run_dhn()])
+
+
+def test_sharded_dhn_world_2():
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_dhn, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    _check_dhn(res)

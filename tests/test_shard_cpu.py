@@ -77,13 +77,15 @@ class OracleBackend:
         dW[:] = torch.from_numpy(b)
 
 
-def graph_with_weights():
-    g = synth.gcn_graph(7, n_nodes=400, n_edge_tuples=2400, d_in=12, undirected=True, cap_ratio=50.0)
+def graph_with_weights(dims=(12, 8, 4)):
+    """Small GCN; dims (13, 6, 7) gives Cora-like widths that are not multiples of 4."""
+    g = synth.gcn_graph(7, n_nodes=400, n_edge_tuples=2400, d_in=dims[0], undirected=True,
+                        cap_ratio=50.0)
     rng = np.random.default_rng(3)
-    g["dims"] = [12, 8, 4]
-    g["W"] = [rng.standard_normal((8, 12)).astype(np.float32) / 3,
-              rng.standard_normal((4, 8)).astype(np.float32) / 3]
-    g["d_out"] = rng.standard_normal((400, 4)).astype(np.float32)
+    g["dims"] = list(dims)
+    g["W"] = [(rng.standard_normal((dims[l + 1], dims[l])) / 3).astype(np.float32)
+              for l in range(len(dims) - 1)]
+    g["d_out"] = rng.standard_normal((400, dims[-1])).astype(np.float32)
     return g
 
 
@@ -93,11 +95,11 @@ def reference(g):
     return {"out_keys": np.sort(keys), "out": H[-1], "dW": dW, "dH0": dH0}
 
 
-def _worker(rank, world, port, path):
+def _worker(rank, world, port, path, dims=(12, 8, 4)):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        g = graph_with_weights()
+        g = graph_with_weights(dims)
         prog = ShardedGCNProgram(g, backend=OracleBackend())
         prog.step()
         np.savez(os.path.join(path, f"r{rank}.npz"), keys=prog.plan.my_keys, rows=prog.plan.my_rows,
@@ -156,4 +158,15 @@ def test_world_size_2_gloo():
         mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
         res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
     g = graph_with_weights()
+    check(res, reference(g), g)
+
+
+def test_world_size_2_gloo_ragged_widths():
+    """Layer widths 13 -> 6 -> 7 (Cora-like, not multiples of 4): the program pads them with
+    zeros for the ld % 4 == 0 kernels and collectives; the real columns are unchanged."""
+    dims = (13, 6, 7)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, dims), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    g = graph_with_weights(dims)
     check(res, reference(g), g)

@@ -62,7 +62,7 @@ def reference(mag):
     dY = {t: np.zeros((mag["n"][t], len(b) * d)) for t, b in blocks.items()}
     for name, r in mag["rels"].items():
         ts, tt = r["src_type"], r["dst_type"]
-        ik, im, iq = col[("k", name)][1], col[("m", name)][1], col[("q", name)][1]
+        ik, im, iq = col[("k", name)][1], col[("m", name)][1], col[("q", tt)][1]
         Ws, Wt = par["W"][ts], par["W"][tt]
         res = op.hgt_relation(mag["h"][ts], mag["h"][tt], Ws[ik * d:(ik + 1) * d],
                               Ws[im * d:(im + 1) * d], Wt[iq * d:(iq + 1) * d], mag["key"][ts],
