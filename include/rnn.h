@@ -132,7 +132,7 @@ rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64_t* e_dst_k
 /* A3/A4. Fused gather - combine - segmented reduce, forward                             */
 /* ===================================================================================== */
 
-typedef enum { RNN_AGG_SUM = 0, RNN_AGG_MEAN = 1, RNN_AGG_SOFTMAX = 2 } rnn_agg;
+typedef enum { RNN_AGG_SUM = 0, RNN_AGG_MEAN = 1, RNN_AGG_SOFTMAX = 2, RNN_AGG_MAX = 3 } rnn_agg;
 typedef enum {
   RNN_COMBINE_SRC = 0,   /* w * z_s ; w = scalar edge operand (dim 1) or 1 (GCN norm, a*v)  */
   RNN_COMBINE_MUL = 1,   /* z_s (.) z_e (.) z_t of the present operands (q*k, DHN product)  */
@@ -194,6 +194,22 @@ rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rnn_lifted_qu
                                   float* d_src_key, float* d_edge, float* d_dst,
                                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* MAX aggregate (PAPER.md:209 "sum, mean, or max", :755): agg
+ * RNN_AGG_MAX with combine SRC, value w_p * z_s (edge: optional scalar weight, by row or by
+ * position).  out[g, c] = max over the group's join rows; argmax[g, c] (int32 [G, ld_arg]) =
+ * the LOWEST join position attaining it (ties broken deterministically); an empty group gives
+ * out 0 and argmax -1 (scatter_max convention).  Backward (subgradient: everything to the
+ * arg-max row): d_src[s, c] = sum of w_p d_out[g, c] over the (g, c) whose arg-max row p has
+ * src_row[p] = s (source-major over the transposed CSR, no atomics; rows never referenced
+ * get 0), d_edge[p] = sum over c with argmax[g, c] = p of d_out[g, c] z_s[s_p, c] (written;
+ * needs the edge weight).  d_src / d_edge use their operand's ld; either may be NULL. */
+rnn_status rnn_join_aggregate_max_fwd(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                      float* out, int64_t ld_out, int32_t* argmax, int64_t ld_arg,
+                                      void* stream);
+rnn_status rnn_join_aggregate_max_bwd(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                      const int32_t* argmax, int64_t ld_arg, const float* d_out,
+                                      int64_t ld_dout, float* d_src, float* d_edge, void* stream);
+
 /* Standalone grouped softmax over materialised scores [E', heads] in group-major order (the
  * ATT relation of Fig. 4), and its backward ds = p (dp - sum_q p dp). */
 rnn_status rnn_group_softmax(const rnn_join_index* idx, const float* scores, int32_t heads,
@@ -201,6 +217,76 @@ rnn_status rnn_group_softmax(const rnn_join_index* idx, const float* scores, int
 rnn_status rnn_group_softmax_bwd(const rnn_join_index* idx, const float* probs,
                                  const float* d_probs, int32_t heads, float* d_scores,
                                  void* stream);
+
+/* ===================================================================================== */
+/* Node epilogues: bias, activation, gated residual                */
+/* ===================================================================================== */
+/* The per-node transformation a rule applies after the aggregate or the projection:
+ *   y = gate * act(x + bias) + (1 - gate) * resid          (resid == NULL: y = act(x + bias))
+ * GCN layers: bias then ReLU (hidden) / bias only (last) -- PyG GCNConv, PAPER.md:865 (O7);
+ * the HGT skip connection: gate = sigmoid(skip_tau), resid = the previous layer's H
+ * (PAPER.md:1392-1394 [src-only]); GELU for HGT's target-specific aggregation (:1356 ff).
+ *   bias  [dim] or NULL;  resid [rows, ld_resid] (row order of x) or NULL;
+ *   pre   [rows, ld_pre] or NULL: x + bias saved for the backward (needed for GELU, and for
+ *         RELU when resid is given; for RELU without resid the output's sign suffices).   */
+typedef enum { RNN_ACT_NONE = 0, RNN_ACT_RELU = 1, RNN_ACT_GELU = 2 } rnn_activation;
+typedef struct {
+  const float* bias;
+  int32_t act;           /* rnn_activation (GELU: x * Phi(x), erf form) */
+  float gate;            /* used when resid != NULL, in [0, 1] */
+  const float* resid;
+  int64_t ld_resid;
+  float* pre;
+  int64_t ld_pre;
+} rnn_epilogue;
+
+/* The forward LJA with the epilogue fused into its final store (the lean SRC/MUL gather path;
+ * other paths run the aggregate, then the epilogue in place).  Arguments as
+ * rnn_join_aggregate_fwd; beta must be 0 (a union is accumulated first and the epilogue
+ * applied once with rnn_epilogue_fwd); SUM / MEAN only. */
+rnn_status rnn_join_aggregate_fwd_epi(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                      const rnn_epilogue* epi, float* out, int64_t ld_out,
+                                      void* workspace, size_t workspace_bytes, void* stream);
+/* Standalone epilogue over x [rows, dim] -> y (y may alias x; epi->pre may alias neither). */
+rnn_status rnn_epilogue_fwd(const float* x, int64_t ldx, int64_t rows, int32_t dim,
+                            const rnn_epilogue* epi, float* y, int64_t ldy, void* stream);
+/* Backward of the epilogue: from dy [rows, dim] and the forward's y / epi->pre:
+ *   dx = dy * gate * act'(x + bias)   (gate = 1 without resid)   [rows, ld_dx], may alias dy
+ *   d_bias = sum over rows of dx      [dim] or NULL   (fixed-order two-stage reduction)
+ *   d_resid = (1 - gate) * dy         [rows, ld_dresid] or NULL
+ *   d_gate = sum dy * (act(x + bias) - resid)   scalar or NULL (needs pre and resid)
+ * workspace: rnn_epilogue_bwd_workspace_size (host-only). */
+rnn_status rnn_epilogue_bwd_workspace_size(int64_t rows, int32_t dim, size_t* bytes);
+rnn_status rnn_epilogue_bwd(const float* dy, int64_t lddy, const float* y, int64_t ldy,
+                            int64_t rows, int32_t dim, const rnn_epilogue* epi, float* dx,
+                            int64_t lddx, float* d_bias, float* d_resid, int64_t ld_dresid,
+                            float* d_gate, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ===================================================================================== */
+/* Training step: the loss relation and the fit optimiser           */
+/* ===================================================================================== */
+/* Loss(; CrossEntropyLoss()(Cls(z_p), z_l)): loss (device scalar) = mean over
+ * the rows with label >= 0 of -log softmax(logits_i)[label_i]; d_logits [n, ld_dlogits]
+ * (nullable) = (softmax - onehot) / n_labelled on labelled rows, 0 on the others.  label
+ * int64 [n] (device; -1 = unlabelled, < C).  Fixed-order reductions (deterministic).
+ * workspace: rnn_softmax_xent_workspace_size (host-only). */
+rnn_status rnn_softmax_xent_workspace_size(int64_t n, size_t* bytes);
+rnn_status rnn_softmax_xent(const float* logits, int64_t n, int32_t C, int64_t ld,
+                            const int64_t* label, float* loss, float* d_logits, int64_t ld_dlogits,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/* ?fit <lr, weight_decay, ...>: one Adam step on a parameter matrix
+ * (Kingma & Ba, bias-corrected; weight decay added to the gradient as L2, torch.optim.Adam):
+ *   g' = g + wd p;  m = b1 m + (1 - b1) g';  v = b2 v + (1 - b2) g'^2;
+ *   p -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ * param [rows, ld_param] (updated in place), grad [rows, ld_grad], m / v dense [rows, cols]
+ * (zero before the first step).  t = *step (device int64, >= 1), advanced once per training
+ * step by rnn_adam_tick -- kept on the device so the whole step can be graph-captured. */
+typedef struct { float lr, beta1, beta2, eps, weight_decay; } rnn_adam_config;
+rnn_status rnn_adam_tick(int64_t* step, void* stream);
+rnn_status rnn_adam(float* param, int64_t rows, int32_t cols, int64_t ld_param, const float* grad,
+                    int64_t ld_grad, float* m, float* v, const rnn_adam_config* cfg,
+                    const int64_t* step, void* stream);
 
 /* ===================================================================================== */
 /* A2. Dense per-relation projection on tcgen05 tensor cores                             */

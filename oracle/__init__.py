@@ -18,6 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRC2 = os.path.join(_HERE, "oracle_next.c")
 _HDR = os.path.join(_HERE, "oracle.h")
 _LIB = os.path.join(_HERE, "_build", "liboracle.so")
 
@@ -29,11 +30,11 @@ def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (plain -O2, no fast-math) into oracle/_build/liboracle.so."""
     os.makedirs(os.path.dirname(_LIB), exist_ok=True)
     stale = (not os.path.exists(_LIB)) or any(
-        os.path.getmtime(p) > os.path.getmtime(_LIB) for p in (_SRC, _HDR))
+        os.path.getmtime(p) > os.path.getmtime(_LIB) for p in (_SRC, _SRC2, _HDR))
     if force or stale:
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall", "-Werror",
-                               "-fno-fast-math", "-o", tmp, _SRC, "-lm"])
+                               "-fno-fast-math", "-o", tmp, _SRC, _SRC2, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -54,6 +55,17 @@ def lib():
     global _lib
     if _lib is None:
         L = C.CDLL(build())
+        L.ora_epilogue_fwd.argtypes = [PD, C.c_int64, C.c_int, C.c_int64, PD, C.c_int, C.c_double,
+                                       PD, C.c_int64, PD, C.c_int64]
+        L.ora_epilogue_bwd.argtypes = [PD, PD, C.c_int64, C.c_int, PD, C.c_int, C.c_double, PD, PD,
+                                       PD, PD, PD]
+        L.ora_lja_max_fwd.argtypes = [P64, C.c_int64, P32, P32, PD, C.c_int64, C.c_int, PD, C.c_int,
+                                      PD, C.c_int64, P64]
+        L.ora_lja_max_bwd.argtypes = [P64, C.c_int64, P32, P32, PD, C.c_int64, C.c_int, PD, C.c_int,
+                                      P64, PD, C.c_int64, C.c_int64, C.c_int64, PD, PD]
+        L.ora_softmax_xent.argtypes = [PD, C.c_int64, C.c_int, C.c_int64, P64, PD, PD]
+        L.ora_adam.argtypes = [PD, PD, PD, PD, C.c_int64, C.c_double, C.c_double, C.c_double,
+                               C.c_double, C.c_double, C.c_int64]
         L.ora_build_join_index.argtypes = [P64, P64, C.c_int64, P64, C.c_int64, P64, C.c_int64,
                                            C.c_int, P64, P64, P64, P64, P32, P32, P32, P64, P32]
         L.ora_lja_fwd.argtypes = [P64, C.c_int64, P32, P32, P32, C.c_int, C.c_int, C.c_int,
@@ -285,3 +297,87 @@ def hash_partition(keys, P, seed):
 
 def splitmix64(x: int) -> int:
     return int(lib().ora_splitmix64(x))
+
+
+# ---- SURVEY sec 8f rows (oracle_next.c) ----
+ACT = {"none": 0, "relu": 1, "gelu": 2}
+
+
+def epilogue_fwd(x, bias=None, act="none", gate=1.0, resid=None):
+    """y = gate * act(x + b) + (1 - gate) * resid (resid None: act(x + b))."""
+    x = _f64(x)
+    rows, dim = x.shape
+    y = np.zeros((max(rows, 1), dim))
+    b = None if bias is None else _f64(np.asarray(bias).reshape(-1))
+    r = None if resid is None else _f64(resid)
+    _check(lib().ora_epilogue_fwd(_p(x, PD), rows, dim, dim, _p(b, PD), ACT[act], float(gate),
+                                  _p(r, PD), dim, _p(y, PD), dim))
+    return y[:rows]
+
+
+def epilogue_bwd(dy, x, bias=None, act="none", gate=1.0, resid=None):
+    """(dx, d_bias, d_resid, d_gate) of epilogue_fwd at x."""
+    dy, x = _f64(dy), _f64(x)
+    rows, dim = x.shape
+    dx = np.zeros((max(rows, 1), dim))
+    db = np.zeros(dim)
+    b = None if bias is None else _f64(np.asarray(bias).reshape(-1))
+    r = None if resid is None else _f64(resid)
+    dr = np.zeros((max(rows, 1), dim)) if r is not None else None
+    dg = np.zeros(1)
+    _check(lib().ora_epilogue_bwd(_p(dy, PD), _p(x, PD), rows, dim, _p(b, PD), ACT[act],
+                                  float(gate), _p(r, PD), _p(dx, PD), _p(db, PD), _p(dr, PD),
+                                  _p(dg, PD) if r is not None else None))
+    return dx[:rows], db, (None if dr is None else dr[:rows]), (float(dg[0]) if r is not None else None)
+
+
+def lja_max_fwd(idx, z, w=None, w_by_pos=True):
+    """MAX aggregate of w * z_s per group and column; returns (out [G, d], argmax [G, d])."""
+    z = _f64(z)
+    d = z.shape[1]
+    G = idx["n_groups"]
+    out = np.zeros((max(G, 1), d))
+    am = np.zeros((max(G, 1), d), np.int64)
+    wv = None if w is None else _f64(np.asarray(w).reshape(-1))
+    _check(lib().ora_lja_max_fwd(_p(idx["group_ptr"], P64), G, _p(_i32(idx["src_row"]), P32),
+                                 _p(_i32(idx["edge_row"]), P32), _p(z, PD), d, d, _p(wv, PD),
+                                 1 if w_by_pos else 0, _p(out, PD), d, _p(am, P64)))
+    return out[:G], am[:G]
+
+
+def lja_max_bwd(idx, z, argmax, d_out, w=None, w_by_pos=True):
+    """(d_z [n_src, d], d_w or None) of lja_max_fwd."""
+    z, d_out = _f64(z), _f64(d_out)
+    n_s, d = z.shape
+    G = idx["n_groups"]
+    wv = None if w is None else _f64(np.asarray(w).reshape(-1))
+    dz = np.zeros((max(n_s, 1), d))
+    n_w = 0 if wv is None else len(wv)
+    dw = np.zeros(max(n_w, 1))
+    am = np.ascontiguousarray(argmax, np.int64)
+    _check(lib().ora_lja_max_bwd(_p(idx["group_ptr"], P64), G, _p(_i32(idx["src_row"]), P32),
+                                 _p(_i32(idx["edge_row"]), P32), _p(z, PD), d, d, _p(wv, PD),
+                                 1 if w_by_pos else 0, _p(am, P64), _p(d_out, PD), d, n_s, n_w,
+                                 _p(dz, PD), _p(dw, PD) if wv is not None else None))
+    return dz[:n_s], (dw[:n_w] if wv is not None else None)
+
+
+def softmax_xent(logits, label):
+    """(mean cross-entropy over rows with label >= 0, d_logits)."""
+    x = _f64(logits)
+    n, Cn = x.shape
+    lab = np.ascontiguousarray(label, np.int64)
+    loss = np.zeros(1)
+    dl = np.zeros((max(n, 1), Cn))
+    _check(lib().ora_softmax_xent(_p(x, PD), n, Cn, Cn, _p(lab, P64), _p(loss, PD), _p(dl, PD)))
+    return float(loss[0]), dl[:n]
+
+
+def adam(p, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, wd=0.0):
+    """One Adam step in place on float64 arrays p, m, v (returns them)."""
+    for a in (p, m, v):
+        assert a.dtype == np.float64 and a.flags.c_contiguous
+    gg = _f64(g)
+    _check(lib().ora_adam(_p(p, PD), _p(gg, PD), _p(m, PD), _p(v, PD), p.size, lr, b1, b2, eps,
+                          wd, t))
+    return p, m, v

@@ -129,6 +129,28 @@ int ora_dhn_bwd(int k, const int64_t* group_ptr, int64_t n_groups, const int32_t
                 const double* const* f, int64_t ldf, int d,
                 const double* d_out, int64_t ld_dout, double* const* d_f);
 
+/* ---- SURVEY sec 8f rows (oracle_next.c) ---- */
+/* node epilogue y = gate act(x + b) + (1 - gate) r  (act 0 none, 1 ReLU, 2 GELU; r nullable) */
+int ora_epilogue_fwd(const double* x, int64_t rows, int dim, int64_t ldx, const double* bias,
+                     int act, double gate, const double* resid, int64_t ld_resid, double* y,
+                     int64_t ldy);
+int ora_epilogue_bwd(const double* dy, const double* x, int64_t rows, int dim, const double* bias,
+                     int act, double gate, const double* resid, double* dx, double* d_bias,
+                     double* d_resid, double* d_gate);
+/* MAX aggregate of w * z_s; argmax [G, dim] (lowest position, -1 empty) */
+int ora_lja_max_fwd(const int64_t* group_ptr, int64_t n_groups, const int32_t* src_row,
+                    const int32_t* edge_row, const double* z, int64_t ldz, int dim,
+                    const double* w, int w_by_pos, double* out, int64_t ld_out, int64_t* argmax);
+int ora_lja_max_bwd(const int64_t* group_ptr, int64_t n_groups, const int32_t* src_row,
+                    const int32_t* edge_row, const double* z, int64_t ldz, int dim,
+                    const double* w, int w_by_pos, const int64_t* argmax, const double* d_out,
+                    int64_t ld_dout, int64_t n_src_rows, int64_t n_w, double* d_z, double* d_w);
+/* Loss(; CrossEntropyLoss()(logits, label)) and one Adam step (fit, :554) */
+int ora_softmax_xent(const double* logits, int64_t n, int C, int64_t ld, const int64_t* label,
+                     double* loss, double* d_logits);
+int ora_adam(double* p, const double* g, double* m, double* v, int64_t n, double lr, double b1,
+             double b2, double eps, double wd, int64_t t);
+
 /* Multi-GPU ownership: owner(key) = splitmix64(key ^ seed) mod P. */
 int ora_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed, int32_t* owner);
 uint64_t ora_splitmix64(uint64_t x);

@@ -5,13 +5,42 @@ Only oracle functions are used; nothing here imports the product package.
 import numpy as np
 
 import oracle
-def gcn_step(graph, layers=None):
+def gcn_fit(graph, labels, epochs, lr=0.01, weight_decay=5e-4):
+    """fit: `epochs` full-batch steps of Loss = CrossEntropy(H^L, label)
+    with Adam on every W and b; returns the per-epoch losses and the final parameters."""
+    g = dict(graph)
+    g["W"] = [np.asarray(w, np.float64).copy() for w in graph["W"]]
+    g["b"] = [np.asarray(b, np.float64).copy() for b in graph["b"]]
+    key = graph["nodes"]["key"]
+    o1 = oracle.build_join_index(graph["edges"]["src"], graph["edges"]["dst"], key, key)
+    lab = np.asarray(labels, np.int64)[o1["group_dst_row"]]     # logits rows: group order
+    state = [(np.zeros_like(p), np.zeros_like(p)) for p in g["W"] + g["b"]]
+    losses = []
+    for t in range(1, epochs + 1):
+        ex = {}
+        g["d_out"] = None
+        H, _, _ = gcn_step(g, out=ex, forward_only=True)
+        loss, dl = oracle.softmax_xent(H[-1], lab)
+        losses.append(loss)
+        g["d_out"] = dl
+        ex = {}
+        _, dW, _ = gcn_step(g, out=ex)
+        grads = dW + ex["db"]
+        for p, gr, (m, v) in zip(g["W"] + g["b"], grads, state):
+            oracle.adam(p.reshape(-1) if p.ndim == 1 else p, np.asarray(gr).reshape(p.shape),
+                        m, v, lr, t, wd=weight_decay)
+    return losses, g["W"], g["b"]
+
+
+def gcn_step(graph, layers=None, out=None, forward_only=False):
     """O7: fp64 forward + backward of the L-layer GCN program (reading #1).
 
     Same rules as paper_2605_24207_b200.programs.GCNProgram, evaluated with the plain oracle
-    functions: AEdge join index, w = deg^-1/2 deg^-1/2, H^{l+1} = sum_s w (H^l W_l^T)[s].
+    functions: AEdge join index, w = deg^-1/2 deg^-1/2, A^l = sum_s w (H^l W_l^T)[s], and when
+    the graph carries biases "b" the PyG GCNConv epilogue H^{l+1} = ReLU(A^l + b_l) on hidden
+    layers, A^L + b_L on the last; else H^{l+1} = A^l.
     `layers` limits the evaluation to the first layers (bounded CPU-baseline samples).
-    """
+    `out` (a dict) receives the bias gradients "db" and the activations "H"."""
     nodes, edges = graph["nodes"], graph["edges"]
     key = nodes["key"]
     L = len(graph["W"]) if layers is None else layers
@@ -20,20 +49,29 @@ def gcn_step(graph, layers=None):
     if L > 1:
         o2 = oracle.build_join_index(edges["src"], edges["dst"], o1["group_key"], o1["group_key"])
         w2 = oracle.gcn_norm(o2, len(o1["group_key"]))
+    bias = graph.get("b")
+    act = lambda l: "relu" if l < len(graph["W"]) - 1 else "none"
     H = [np.asarray(nodes["x"], np.float64)]
-    Z = []
+    Z, A = [], []
     for l in range(L):
         Z.append(oracle.project(H[l], graph["W"][l]))
         o, w = (o1, w1) if l == 0 else (o2, w2)
-        H.append(oracle.lja_fwd(o, "src", "sum", src=Z[l], edge=w, edge_mode=1)[0])
+        A.append(oracle.lja_fwd(o, "src", "sum", src=Z[l], edge=w, edge_mode=1)[0])
+        H.append(A[l] if bias is None else oracle.epilogue_fwd(A[l], bias[l], act(l)))
+    if forward_only:
+        return H, None, None
     G = o1["n_groups"]
     dY = np.asarray(graph["d_out"][:G, : H[-1].shape[1]], np.float64)
-    dW, dH0 = [None] * L, None
+    dW, dH0, db = [None] * L, None, [None] * L
     for l in reversed(range(L)):
         o, w = (o1, w1) if l == 0 else (o2, w2)
+        if bias is not None:
+            dY, db[l], _, _ = oracle.epilogue_bwd(dY, A[l], bias[l], act(l))
         dZ = oracle.lja_bwd(o, dY, "src", "sum", src=Z[l], edge=w, edge_mode=1, want=("src",))["src"]
         dX, dW[l], _ = oracle.project_bwd(H[l], graph["W"][l], dZ, want_db=False)
         dY = dX
+    if out is not None:
+        out.update(db=db, H=H)
     return H, dW, dY
 
 

@@ -1,0 +1,206 @@
+// epilogue.cu -- node epilogues: y = gate * act(x + bias) + (1 - gate) * resid
+//
+// The per-node transformation of a rule after its aggregate or projection: GCN's bias and ReLU
+// (PyG GCNConv, O7), the HGT skip gate sigmoid(skip) over the previous layer's
+// H (PAPER.md:1392-1394 [src-only]), GELU.  The forward is normally fused into the LJA's final
+// store (rowsplit.cuh lean_store); this file holds the standalone forward (other LJA paths, a
+// projection output, a union accumulated first) and the backward: dx, d_bias (fixed-order
+// two-stage column sums, deterministic), d_resid and d_gate.
+#include "lja.cuh"
+
+namespace rnn {
+namespace {
+
+constexpr int EPI_CHUNK = 2048;   // rows per partial of the column / gate sums
+
+EpiD epi_dev(const rnn_epilogue* e) {
+  EpiD d{};
+  if (!e) return d;
+  d.on = 1;
+  d.bias = e->bias;
+  d.act = e->act;
+  d.gate = e->resid ? e->gate : 1.f;
+  d.resid = e->resid;
+  d.ld_resid = e->ld_resid;
+  d.pre = e->pre;
+  d.ld_pre = e->ld_pre;
+  return d;
+}
+
+__global__ void epi_fwd_kernel(const float* __restrict__ x, int64_t ldx, int64_t rows, int dim,
+                               EpiD e, float* y, int64_t ldy) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows * dim) return;
+  const int64_t r = i / dim;
+  const int c = (int)(i % dim);
+  float v = x[r * ldx + c];
+  if (e.bias) v += e.bias[c];
+  if (e.pre) e.pre[r * e.ld_pre + c] = v;
+  v = epi_act(e.act, v);
+  if (e.resid) v = e.gate * v + (1.f - e.gate) * e.resid[r * e.ld_resid + c];
+  y[r * ldy + c] = v;
+}
+
+// one block per (32-column slab, row chunk): thread (tx, ty) walks rows ty, ty + 8, ... of the
+// chunk for column c0 + tx; per-chunk column partials of dx and per-chunk gate partials
+__global__ void __launch_bounds__(256) epi_bwd_kernel(const float* __restrict__ dy, int64_t lddy,
+                                                      const float* __restrict__ y, int64_t ldy,
+                                                      int64_t rows, int dim, EpiD e,
+                                                      float* dx, int64_t lddx,
+                                                      float* __restrict__ dres, int64_t ldres,
+                                                      float* __restrict__ part_b,
+                                                      float* __restrict__ part_g) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + tx;
+  const int64_t r0 = (int64_t)blockIdx.y * EPI_CHUNK;
+  const int64_t r1 = r0 + EPI_CHUNK < rows ? r0 + EPI_CHUNK : rows;
+  float sb = 0.f, sg = 0.f;
+  if (c < dim) {
+    for (int64_t r = r0 + ty; r < r1; r += 8) {
+      const float g = dy[r * lddy + c];
+      float xb;          // x + bias (pre-activation)
+      if (e.pre) xb = e.pre[r * e.ld_pre + c];
+      else xb = y[r * ldy + c];   // act none / ReLU without resid: y decides act'
+      const float d = g * e.gate * epi_dact(e.act, xb);
+      if (dx) dx[r * lddx + c] = d;
+      if (dres) dres[r * ldres + c] = (1.f - e.gate) * g;
+      if (part_g) sg += g * (epi_act(e.act, xb) - e.resid[r * e.ld_resid + c]);
+      sb += d;
+    }
+  }
+  __shared__ float sh_b[8][33];
+  __shared__ float sh_g[256];
+  sh_b[ty][tx] = sb;
+  sh_g[threadIdx.x] = sg;
+  __syncthreads();
+  if (ty == 0 && c < dim && part_b) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += sh_b[k][tx];
+    part_b[(int64_t)blockIdx.y * dim + c] = t;
+  }
+  if (part_g) {   // fixed tree over the block, one partial per block
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) sh_g[threadIdx.x] += sh_g[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part_g[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = sh_g[0];
+  }
+}
+
+__global__ void epi_colsum_final(const float* __restrict__ part, int64_t chunks, int dim,
+                                 float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= dim) return;
+  float t = 0.f;
+  for (int64_t k = 0; k < chunks; ++k) t += part[k * dim + c];
+  out[c] = t;
+}
+
+__global__ void epi_sum_final(const float* __restrict__ part, int64_t n, float* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  float t = 0.f;
+  for (int64_t k = 0; k < n; ++k) t += part[k];
+  *out = t;
+}
+
+rnn_status check_epi(const rnn_epilogue* e, int dim, bool need_pre_for_bwd) {
+  RNN_REQUIRE(e, RNN_ERR_INVALID_ARGUMENT, "epilogue is NULL");
+  RNN_REQUIRE(e->act >= RNN_ACT_NONE && e->act <= RNN_ACT_GELU, RNN_ERR_INVALID_ARGUMENT,
+              "unknown activation %d", (int)e->act);
+  RNN_REQUIRE(!e->resid || (e->gate >= 0.f && e->gate <= 1.f && e->ld_resid >= dim),
+              RNN_ERR_INVALID_ARGUMENT, "resid needs gate in [0, 1] and ld_resid >= dim");
+  RNN_REQUIRE(!e->pre || e->ld_pre >= dim, RNN_ERR_INVALID_ARGUMENT, "ld_pre < dim");
+  if (need_pre_for_bwd)
+    RNN_REQUIRE(e->pre || (e->act != RNN_ACT_GELU && !(e->act == RNN_ACT_RELU && e->resid)),
+                RNN_ERR_INVALID_ARGUMENT,
+                "the backward of GELU (or ReLU with a residual) needs the saved pre-activation");
+  return RNN_OK;
+}
+
+}  // namespace
+
+rnn_status epilogue_inplace(float* y, int64_t ldy, int64_t rows, int dim, const EpiD& e,
+                            cudaStream_t st) {
+  if (rows == 0 || dim == 0) return RNN_OK;
+  epi_fwd_kernel<<<(unsigned)ceil_div(rows * dim, 256), 256, 0, st>>>(y, ldy, rows, dim, e, y, ldy);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+EpiD epi_from_abi(const rnn_epilogue* e) { return epi_dev(e); }
+
+}  // namespace rnn
+
+using namespace rnn;
+
+extern "C" rnn_status rnn_epilogue_fwd(const float* x, int64_t ldx, int64_t rows, int32_t dim,
+                                       const rnn_epilogue* epi, float* y, int64_t ldy,
+                                       void* stream) {
+  clear_error();
+  RNN_TRY(check_epi(epi, dim, false));
+  RNN_REQUIRE(rows >= 0 && dim >= 1 && ldx >= dim && ldy >= dim &&
+                  (rows == 0 || (x && y)),
+              RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  if (rows == 0) return RNN_OK;
+  const EpiD e = epi_dev(epi);
+  epi_fwd_kernel<<<(unsigned)ceil_div(rows * dim, 256), 256, 0, as_stream(stream)>>>(
+      x, ldx, rows, dim, e, y, ldy);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_epilogue_bwd_workspace_size(int64_t rows, int32_t dim, size_t* bytes) {
+  clear_error();
+  RNN_REQUIRE(bytes && rows >= 0 && dim >= 1, RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  const int64_t chunks = ceil_div(rows > 0 ? rows : 1, EPI_CHUNK);
+  const int64_t slabs = ceil_div(dim, 32);
+  *bytes = sizeof(float) * (size_t)(chunks * dim + chunks * slabs) + 256;
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_epilogue_bwd(const float* dy, int64_t lddy, const float* y, int64_t ldy,
+                                       int64_t rows, int32_t dim, const rnn_epilogue* epi,
+                                       float* dx, int64_t lddx, float* d_bias, float* d_resid,
+                                       int64_t ld_dresid, float* d_gate, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_TRY(check_epi(epi, dim, true));
+  RNN_REQUIRE(rows >= 0 && dim >= 1 && lddy >= dim && (rows == 0 || dy), RNN_ERR_INVALID_ARGUMENT,
+              "bad argument");
+  RNN_REQUIRE(epi->pre || y || rows == 0, RNN_ERR_INVALID_ARGUMENT,
+              "the forward output y is needed without a saved pre-activation");
+  RNN_REQUIRE(!dx || lddx >= dim, RNN_ERR_INVALID_ARGUMENT, "lddx < dim");
+  RNN_REQUIRE(!d_resid || (epi->resid && ld_dresid >= dim), RNN_ERR_INVALID_ARGUMENT,
+              "d_resid needs a residual and ld_dresid >= dim");
+  RNN_REQUIRE(!d_gate || (epi->resid && epi->pre), RNN_ERR_INVALID_ARGUMENT,
+              "d_gate needs the residual and the saved pre-activation");
+  size_t need = 0;
+  RNN_TRY(rnn_epilogue_bwd_workspace_size(rows, dim, &need));
+  RNN_REQUIRE(workspace && workspace_bytes >= need, RNN_ERR_WORKSPACE_TOO_SMALL,
+              "epilogue backward workspace %zu < %zu bytes", workspace_bytes, need);
+  cudaStream_t st = as_stream(stream);
+  if (rows == 0) {
+    if (d_bias) RNN_CUDA(cudaMemsetAsync(d_bias, 0, sizeof(float) * dim, st));
+    if (d_gate) RNN_CUDA(cudaMemsetAsync(d_gate, 0, sizeof(float), st));
+    return RNN_OK;
+  }
+  const EpiD e = epi_dev(epi);
+  const int64_t chunks = ceil_div(rows, EPI_CHUNK);
+  const int64_t slabs = ceil_div(dim, 32);
+  float* part_b = reinterpret_cast<float*>(workspace);
+  float* part_g = part_b + chunks * dim;
+  dim3 grid((unsigned)slabs, (unsigned)chunks);
+  epi_bwd_kernel<<<grid, 256, 0, st>>>(dy, lddy, y, ldy, rows, dim, e, dx, lddx, d_resid,
+                                       ld_dresid, d_bias ? part_b : nullptr,
+                                       d_gate ? part_g : nullptr);
+  RNN_LAUNCH_CHECK();
+  if (d_bias) {
+    epi_colsum_final<<<(unsigned)ceil_div(dim, 128), 128, 0, st>>>(part_b, chunks, dim, d_bias);
+    RNN_LAUNCH_CHECK();
+  }
+  if (d_gate) {
+    epi_sum_final<<<1, 32, 0, st>>>(part_g, chunks * slabs, d_gate);
+    RNN_LAUNCH_CHECK();
+  }
+  return RNN_OK;
+}

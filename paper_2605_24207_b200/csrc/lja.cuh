@@ -11,6 +11,47 @@ struct OpndD {
   int mode;
 };
 
+// node epilogue (rnn_epilogue) in device form: y = gate * act(x + bias) + (1 - gate) * resid
+struct EpiD {
+  int on;
+  const float* bias;
+  int act;               // 0 none, 1 ReLU, 2 GELU
+  float gate;
+  const float* resid;
+  int64_t ld_resid;
+  float* pre;
+  int64_t ld_pre;
+};
+
+__device__ __forceinline__ float epi_act(int act, float x) {
+  if (act == 1) return fmaxf(x, 0.f);
+  if (act == 2) return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+  return x;
+}
+__device__ __forceinline__ float epi_dact(int act, float x) {   // d act / dx at x
+  if (act == 1) return x > 0.f ? 1.f : 0.f;
+  if (act == 2) {
+    const float cdf = 0.5f * (1.f + erff(x * 0.70710678118654752f));
+    const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+    return cdf + x * pdf;
+  }
+  return 1.f;
+}
+// the epilogue of row g, columns c .. c+3 (x already holds the aggregate)
+__device__ __forceinline__ float4 epi_apply4(const EpiD& e, float4 x, int64_t g, int c) {
+  if (e.bias) x = f4_add(x, *reinterpret_cast<const float4*>(e.bias + c));
+  if (e.pre) *reinterpret_cast<float4*>(e.pre + g * e.ld_pre + c) = x;
+  x = make_float4(epi_act(e.act, x.x), epi_act(e.act, x.y), epi_act(e.act, x.z),
+                  epi_act(e.act, x.w));
+  if (e.resid) {
+    const float4 r = *reinterpret_cast<const float4*>(e.resid + g * e.ld_resid + c);
+    const float a = e.gate;
+    x = make_float4(a * x.x + (1.f - a) * r.x, a * x.y + (1.f - a) * r.y,
+                    a * x.z + (1.f - a) * r.z, a * x.w + (1.f - a) * r.w);
+  }
+  return x;
+}
+
 struct LjaArgs {
   const int64_t* group_ptr;
   const int32_t* src_row;
@@ -24,6 +65,8 @@ struct LjaArgs {
   int D;
   float beta;
   float* lse;
+  EpiD epi;        // node epilogue fused into the lean store (epi.on == 0: none)
+  int* epi_done;   // host flag: set when a launcher fused the epilogue
 };
 
 struct QueryInfo {
@@ -171,7 +214,11 @@ inline rnn_status lja_fwd_ws(const rnn_join_index* idx, const rnn_lifted_query* 
 
 rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
                         int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
-                        cudaStream_t st);
+                        cudaStream_t st,
+                        const EpiD* epi = nullptr);
+rnn_status epilogue_inplace(float* y, int64_t ldy, int64_t rows, int dim, const EpiD& e,
+                            cudaStream_t st);
+EpiD epi_from_abi(const rnn_epilogue* e);
 rnn_status lja_bwd_ws(const rnn_join_index* idx, const rnn_lifted_query* q, size_t* b);
 
 }  // namespace rnn

@@ -364,7 +364,8 @@ rnn_status launch_rs_mode(const LjaArgs& a, const RSCtx& cx, cudaStream_t st) {
                       (a.combine == RNN_COMBINE_MUL && (!a.edge.p || a.edge.dim == 1));
   if (scaled && !a.dst.p && a.D == 128 * VEC && a.ld_out % 4 == 0) {
     LeanFwdMeta mp{a.src_row, a.edge_row, a.group_ptr, a.edge.p, a.edge.ld, a.edge.mode, a.mean};
-    LeanOut o{a.src.p, a.src.ld, a.out, a.ld_out, a.beta};
+    LeanOut o{a.src.p, a.src.ld, a.out, a.ld_out, a.beta, a.epi};
+    if (a.epi.on && a.epi_done) *a.epi_done = 1;
     return launch_lean<LeanFwdMeta, VEC>(mp, cx, o, st);
   }
   const bool ev = a.edge.p && a.edge.dim > 1;
@@ -440,9 +441,32 @@ rnn_status launch_softmax(const LjaArgs& a, int heads, float scale, const SegCtx
 
 }  // namespace
 
+rnn_status lja_fwd_core(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
+                        int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
+                        cudaStream_t st, const EpiD* epi, int* epi_done);
+
 rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
                         int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
-                        cudaStream_t st) {
+                        cudaStream_t st, const EpiD* epi) {
+  if (epi && epi->on) {
+    // the aggregate, with the epilogue fused into the lean store where that path runs, else
+    // applied in place afterwards (one extra pass over [G, D])
+    int done = 0;
+    EpiD e = *epi;
+    RNN_TRY(lja_fwd_core(idx, q, out, ld_out, beta, lse, ws, ws_bytes, st, &e, &done));
+    if (!done && idx->n_groups > 0) {
+      QueryInfo qi;
+      RNN_TRY(check_query(idx, q, &qi));
+      RNN_TRY(epilogue_inplace(out, ld_out, idx->n_groups, qi.D, e, st));
+    }
+    return RNN_OK;
+  }
+  return lja_fwd_core(idx, q, out, ld_out, beta, lse, ws, ws_bytes, st, nullptr, nullptr);
+}
+
+rnn_status lja_fwd_core(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
+                        int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
+                        cudaStream_t st, const EpiD* epi, int* epi_done) {
   QueryInfo qi;
   RNN_TRY(check_query(idx, q, &qi));
   if (idx->n_groups == 0) return RNN_OK;
@@ -467,6 +491,10 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
     return RNN_OK;
   }
   LjaArgs a = make_args(idx, q, out, ld_out, beta, lse, qi.D);
+  if (epi) {
+    a.epi = *epi;
+    a.epi_done = epi_done;
+  }
   if (qi.concat) {
     fwd_concat_kernel<<<(unsigned)ceil_div(idx->n_groups, 8), 256, 0, st>>>(a, idx->n_groups);
     RNN_LAUNCH_CHECK();
@@ -533,4 +561,26 @@ extern "C" rnn_status rnn_join_aggregate_fwd(const rnn_join_index* idx, const rn
   rnn::clear_error();
   return rnn::lja_fwd_impl(idx, q, out, ld_out, beta, lse, workspace, workspace_bytes,
                            rnn::as_stream(stream));
+}
+
+extern "C" rnn_status rnn_join_aggregate_fwd_epi(const rnn_join_index* idx,
+                                                 const rnn_lifted_query* q,
+                                                 const rnn_epilogue* epi, float* out,
+                                                 int64_t ld_out, void* workspace,
+                                                 size_t workspace_bytes, void* stream) {
+  rnn::clear_error();
+  RNN_REQUIRE(epi, RNN_ERR_INVALID_ARGUMENT, "epilogue is NULL");
+  RNN_REQUIRE(q && q->agg != RNN_AGG_SOFTMAX, RNN_ERR_UNSUPPORTED,
+              "the fused epilogue takes SUM / MEAN aggregates");
+  RNN_REQUIRE(epi->act >= RNN_ACT_NONE && epi->act <= RNN_ACT_GELU, RNN_ERR_INVALID_ARGUMENT,
+              "unknown activation");
+  RNN_REQUIRE(!epi->resid || (epi->gate >= 0.f && epi->gate <= 1.f), RNN_ERR_INVALID_ARGUMENT,
+              "gate outside [0, 1]");
+  RNN_REQUIRE((!epi->bias || rnn::aligned16(epi->bias)) && (!epi->pre || (rnn::aligned16(epi->pre) &&
+              epi->ld_pre % 4 == 0)) && (!epi->resid || (rnn::aligned16(epi->resid) &&
+              epi->ld_resid % 4 == 0)), RNN_ERR_INVALID_ARGUMENT,
+              "epilogue operands must be 16-byte aligned with ld %% 4 == 0");
+  const rnn::EpiD e = rnn::epi_from_abi(epi);
+  return rnn::lja_fwd_impl(idx, q, out, ld_out, 0.f, nullptr, workspace, workspace_bytes,
+                           rnn::as_stream(stream), &e);
 }

@@ -191,6 +191,7 @@ struct LeanOut {
   float* out;      // [n_seg, ldo]
   int64_t ldo;
   float beta;
+  EpiD epi;        // node epilogue fused into the store (epi.on == 0: none)
 };
 
 template <int VEC>
@@ -201,6 +202,7 @@ __device__ __forceinline__ void lean_store(const LeanOut& o, int64_t g, const fl
     float4* p = reinterpret_cast<float4*>(o.out + g * o.ldo) + lane + 32 * w;
     float4 x = acc[w];
     if (o.beta != 0.f) x = f4_fma(o.beta, *p, x);
+    if (o.epi.on) x = epi_apply4(o.epi, x, g, 4 * (lane + 32 * w));
     *p = x;
   }
 }

@@ -137,6 +137,18 @@ class GCNProgram(_Program):
         self.d_out = _dev_f32(graph["d_out"][: self.G, : self.dims[-1]], dev)
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
+        self.ws_e = rnn.Workspace(dev)
+        # O7 node epilogue (PyG GCNConv): bias then ReLU on hidden layers, bias
+        # only on the last, fused into the LJA's store; graphs without "b" run the bare LJA
+        self.b = [torch.as_tensor(np.asarray(b, np.float32)).to(dev) for b in graph["b"]] \
+            if graph.get("b") is not None else None
+        self.epi, self.dP, self.db = [], [], []
+        if self.b is not None:
+            for l in range(self.L):
+                act = "relu" if l < self.L - 1 else "none"
+                self.epi.append(rnn.make_epilogue(bias=self.b[l], act=act))
+                self.dP.append(_empty(self.G, self.dims[l + 1], dev))
+                self.db.append(torch.empty(self.dims[l + 1], dtype=torch.float32, device=dev))
         self.q = []
         for l in range(self.L):
             idx, w = (self.idx1, self.w1) if l == 0 else (self.idx2, self.w2)
@@ -186,7 +198,10 @@ class GCNProgram(_Program):
             self._t("proj_fwd_end")
             idx, q = self.q[l]
             self._t("lja_fwd")
-            rnn.join_aggregate_fwd(idx, q, out=self.H[l + 1], ws=self.ws)
+            if self.b is not None:
+                rnn.join_aggregate_fwd_epi(idx, q, self.epi[l], out=self.H[l + 1], ws=self.ws)
+            else:
+                rnn.join_aggregate_fwd(idx, q, out=self.H[l + 1], ws=self.ws)
             self._t("lja_fwd_end")
         return self.H[-1]
 
@@ -194,6 +209,13 @@ class GCNProgram(_Program):
         dY = self.d_out if d_out is None else d_out
         for l in reversed(range(self.L)):
             idx, q = self.q[l]
+            if self.b is not None:
+                # epilogue backward: d(pre-activation) and d(bias) from the layer output's sign
+                self._t("epi_bwd")
+                rnn.epilogue_bwd(dY, self.H[l + 1], self.epi[l], dx=self.dP[l], ws=self.ws_e,
+                                 db_out=self.db[l])
+                self._t("epi_bwd_end")
+                dY = self.dP[l]
             self._t("lja_bwd")
             g = self._lja_bwd_into(idx, q, dY, self.dZ[l])
             self._t("lja_bwd_end")
@@ -203,6 +225,41 @@ class GCNProgram(_Program):
             self._t("proj_bwd_end")
             dY = self.dH[l]
         return self.dW, self.dH[0]
+
+    # ---- fit (SURVEY sec 8f item 3; PAPER.md:549 Loss, :554 ?fit) ----
+    def setup_training(self, labels, lr=0.01, weight_decay=5e-4, learn_embeddings=False):
+        """Loss(; CrossEntropyLoss()(H^L, label)) over the labelled nodes and an Adam fit of
+        every W and b (and, with learn_embeddings, of the per-tuple input embeddings X0 --
+        PAPER.md:568).  labels: int64 per node row (-1 = unlabelled); the logits are H^L in
+        group (key) order, so the labels are permuted to that order once here."""
+        dev = self.device
+        lab = np.asarray(labels, np.int64)
+        row = self.idx1.group_dst_row.cpu().numpy()
+        self.labels_g = torch.as_tensor(lab[row]).to(dev)
+        self.loss = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.d_logits = _empty(self.G, self.dims[-1], dev)
+        self.ws_x = rnn.Workspace(dev)
+        params, self._grads = list(self.W), list(self.dW)
+        if self.b is not None:
+            params += self.b
+            self._grads += self.db
+        if learn_embeddings:
+            params.append(self.X0)
+            self._grads.append(self.dH[0])
+        self.opt = rnn.Adam(params, lr=lr, weight_decay=weight_decay)
+
+    def train_step(self):
+        """One epoch of full-batch training: forward, loss, backward, Adam (all on device)."""
+        self.forward()
+        self._t("loss")
+        rnn.softmax_xent(self.H[-1], self.labels_g, loss=self.loss, d_logits=self.d_logits,
+                         ws=self.ws_x)
+        self._t("loss_end")
+        self.backward(d_out=self.d_logits)
+        self._t("adam")
+        self.opt.step(self._grads)
+        self._t("adam_end")
+        return self.loss
 
     def _lja_bwd_into(self, idx, q, d_out, d_src):
         import ctypes as C
@@ -646,13 +703,14 @@ class CapturedStep:
     the program brackets (prog.timers), so per-step and per-kernel device times can be read
     after every replay (`times()`)."""
 
-    def __init__(self, prog, timed=False, warmup=2):
+    def __init__(self, prog, timed=False, warmup=2, step_fn=None):
         self.prog = prog
+        step = step_fn or prog.step
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
             for _ in range(warmup):       # workspaces reach their final size before capture
-                prog.step()
+                step()
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         self.graph = torch.cuda.CUDAGraph()
@@ -663,7 +721,7 @@ class CapturedStep:
             if timed:
                 self.t0 = torch.cuda.Event(enable_timing=True, external=True)
                 self.t0.record()
-            prog.step()
+            step()
             if timed:
                 self.t1 = torch.cuda.Event(enable_timing=True, external=True)
                 self.t1.record()

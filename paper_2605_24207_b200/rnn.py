@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("RNN_LIB") or os.path.join(_HERE, "librnn.so")
 
 # enums (include/rnn.h)
 RNN_OK = 0
-AGG = {"sum": 0, "mean": 1, "softmax": 2}
+AGG = {"sum": 0, "mean": 1, "softmax": 2, "max": 3}
 COMBINE = {"src": 0, "mul": 1, "add": 2, "concat": 3}
 BY_ROW, BY_POSITION = 0, 1
 IDX_VALIDATE, IDX_WITHIN_GROUP_BY_SRC_KEY, IDX_NO_TRANSPOSE, IDX_DENSE_GROUPS = 1, 2, 4, 8
@@ -53,6 +53,30 @@ class OperandC(C.Structure):
 class QueryC(C.Structure):
     _fields_ = [("combine", C.c_int), ("agg", C.c_int), ("heads", C.c_int32), ("scale", C.c_float),
                 ("src", OperandC), ("src_key", OperandC), ("edge", OperandC), ("dst", OperandC)]
+
+
+class AdamC(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float),
+                ("weight_decay", C.c_float)]
+
+
+class EpilogueC(C.Structure):
+    """rnn_epilogue: y = gate * act(x + bias) + (1 - gate) * resid."""
+    _fields_ = [("bias", C.c_void_p), ("act", C.c_int32), ("gate", C.c_float),
+                ("resid", C.c_void_p), ("ld_resid", C.c_int64), ("pre", C.c_void_p),
+                ("ld_pre", C.c_int64)]
+
+
+ACT = {"none": 0, "relu": 1, "gelu": 2}
+
+
+def make_epilogue(bias=None, act="none", gate=1.0, resid=None, pre=None) -> EpilogueC:
+    e = EpilogueC(None if bias is None else bias.data_ptr(), ACT[act], float(gate),
+                  None if resid is None else resid.data_ptr(),
+                  0 if resid is None else resid.stride(0),
+                  None if pre is None else pre.data_ptr(), 0 if pre is None else pre.stride(0))
+    e.keep = (bias, resid, pre)
+    return e
 
 
 _lib = None
@@ -89,6 +113,27 @@ def lib():
         L.rnn_accumulate.argtypes = [vp, i64, vp, i64, i64, i32, C.c_float, vp]
         L.rnn_accumulate.restype = C.c_int
         L.rnn_gather_rows.argtypes = [vp, i64, vp, i64, vp, i64, i32, vp]
+        L.rnn_softmax_xent_workspace_size.argtypes = [i64, C.POINTER(sz)]
+        L.rnn_softmax_xent.argtypes = [vp, i64, i32, i64, vp, vp, vp, i64, vp, sz, vp]
+        L.rnn_adam_tick.argtypes = [vp, vp]
+        L.rnn_adam.argtypes = [vp, i64, i32, i64, vp, i64, vp, vp, C.POINTER(AdamC), vp, vp]
+        for f in ("rnn_softmax_xent_workspace_size", "rnn_softmax_xent", "rnn_adam_tick", "rnn_adam"):
+            getattr(L, f).restype = C.c_int
+        L.rnn_join_aggregate_max_fwd.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp, i64,
+                                                 vp, i64, vp]
+        L.rnn_join_aggregate_max_bwd.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp, i64,
+                                                 vp, i64, vp, vp, vp]
+        L.rnn_join_aggregate_max_fwd.restype = C.c_int
+        L.rnn_join_aggregate_max_bwd.restype = C.c_int
+        L.rnn_join_aggregate_fwd_epi.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC),
+                                                 C.POINTER(EpilogueC), vp, i64, vp, sz, vp]
+        L.rnn_epilogue_fwd.argtypes = [vp, i64, i64, i32, C.POINTER(EpilogueC), vp, i64, vp]
+        L.rnn_epilogue_bwd_workspace_size.argtypes = [i64, i32, C.POINTER(sz)]
+        L.rnn_epilogue_bwd.argtypes = [vp, i64, vp, i64, i64, i32, C.POINTER(EpilogueC), vp, i64,
+                                       vp, vp, i64, vp, vp, sz, vp]
+        for f in ("rnn_join_aggregate_fwd_epi", "rnn_epilogue_fwd",
+                  "rnn_epilogue_bwd_workspace_size", "rnn_epilogue_bwd"):
+            getattr(L, f).restype = C.c_int
         L.rnn_gather_rows.restype = C.c_int
         L.rnn_dhn_workspace_size.argtypes = [C.POINTER(JoinIndexC), i32, i32, C.POINTER(sz)]
         L.rnn_dhn_fwd.argtypes = [C.POINTER(JoinIndexC), i32, C.POINTER(OperandC), vp, i64, vp, sz, vp]
@@ -536,3 +581,114 @@ def dhn_path_counters(reset=False):
     if lib().rnn_internal_dhn_stats(buf, 1 if reset else 0, 0) != 0:
         raise RuntimeError("rnn_internal_dhn_stats failed")
     return dict(zip(DHN_PATHS, [int(x) for x in buf[:len(DHN_PATHS)]]))
+
+
+# ------------------------------------------------------------------------------------------
+# node epilogues
+# ------------------------------------------------------------------------------------------
+def join_aggregate_fwd_epi(idx: JoinIndex, q: QueryC, epi: EpilogueC, out=None, ws=None,
+                           stream=None):
+    """The SUM/MEAN LJA with the epilogue fused into its store (rnn_join_aggregate_fwd_epi)."""
+    dev = idx.group_ptr.device
+    D = out_width(q)
+    if out is None:
+        out = torch.empty(max(idx.n_groups, 1), (D + 3) // 4 * 4, dtype=torch.float32, device=dev)[: idx.n_groups, :D]
+    fb, _ = lja_workspace_size(idx, q)
+    w = ws.get(fb) if ws is not None else _ws(fb, dev)
+    _check(lib().rnn_join_aggregate_fwd_epi(C.byref(idx.c), C.byref(q), C.byref(epi), _ptr(out),
+                                            out.stride(0), _ptr(w), w.numel(), _stream(stream)))
+    return out
+
+
+def epilogue_fwd(x, epi: EpilogueC, out=None, stream=None):
+    rows, dim = x.shape
+    y = out if out is not None else torch.empty_like(x)
+    _check(lib().rnn_epilogue_fwd(_ptr(x), x.stride(0), rows, dim, C.byref(epi), _ptr(y),
+                                  y.stride(0), _stream(stream)))
+    return y
+
+
+def epilogue_bwd(dy, y, epi: EpilogueC, dx=None, want_bias=True, want_resid=False,
+                 want_gate=False, ws=None, stream=None, db_out=None):
+    """(dx, d_bias, d_resid, d_gate) of the epilogue (rnn_epilogue_bwd); y = the forward output."""
+    rows, dim = dy.shape
+    dev = dy.device
+    dx = dx if dx is not None else torch.empty_like(dy)
+    db = db_out if db_out is not None else (
+        torch.empty(dim, dtype=torch.float32, device=dev) if want_bias else None)
+    dr = torch.empty_like(dy) if want_resid else None
+    dg = torch.empty(1, dtype=torch.float32, device=dev) if want_gate else None
+    nb = C.c_size_t(0)
+    _check(lib().rnn_epilogue_bwd_workspace_size(rows, dim, C.byref(nb)))
+    w = ws.get(nb.value) if ws is not None else _ws(nb.value, dev)
+    _check(lib().rnn_epilogue_bwd(_ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0),
+                                  rows, dim, C.byref(epi), _ptr(dx), dx.stride(0), _ptr(db),
+                                  _ptr(dr), 0 if dr is None else dr.stride(0), _ptr(dg), _ptr(w),
+                                  w.numel(), _stream(stream)))
+    return dx, db, dr, dg
+
+
+def join_aggregate_max_fwd(idx: JoinIndex, q: QueryC, out=None, argmax=None, stream=None):
+    """MAX aggregate (rnn_join_aggregate_max_fwd): (out [G, D], argmax int32 [G, D])."""
+    dev = idx.group_ptr.device
+    D = q.src.dim
+    G = idx.n_groups
+    if out is None:
+        out = torch.empty(max(G, 1), (D + 3) // 4 * 4, dtype=torch.float32, device=dev)[:G, :D]
+    if argmax is None:
+        argmax = torch.empty(max(G, 1), D, dtype=torch.int32, device=dev)[:G]
+    _check(lib().rnn_join_aggregate_max_fwd(C.byref(idx.c), C.byref(q), _ptr(out), out.stride(0),
+                                            _ptr(argmax), argmax.stride(0), _stream(stream)))
+    return out, argmax
+
+
+def join_aggregate_max_bwd(idx: JoinIndex, q: QueryC, argmax, d_out, want_edge=False,
+                           stream=None):
+    """(d_src, d_edge) of the MAX aggregate (rnn_join_aggregate_max_bwd)."""
+    dev = idx.group_ptr.device
+    d_src = _grad_like(q.src, idx.n_src_rows, dev)
+    ne = idx.c.n_edge_rows if q.edge.mode == BY_ROW else idx.n_join_rows
+    d_edge = _grad_like(q.edge, ne, dev) if want_edge else None
+    _check(lib().rnn_join_aggregate_max_bwd(C.byref(idx.c), C.byref(q), _ptr(argmax),
+                                            argmax.stride(0), _ptr(d_out), d_out.stride(0),
+                                            _ptr(d_src), _ptr(d_edge), _stream(stream)))
+    return d_src, d_edge
+
+
+# ------------------------------------------------------------------------------------------
+# training step (SURVEY sec 8f item 3)
+# ------------------------------------------------------------------------------------------
+def softmax_xent(logits, label, loss=None, d_logits=None, ws=None, stream=None):
+    """(loss device scalar, d_logits) of the mean cross-entropy over labelled rows."""
+    n, Cn = logits.shape
+    dev = logits.device
+    loss = loss if loss is not None else torch.empty(1, dtype=torch.float32, device=dev)
+    d_logits = d_logits if d_logits is not None else torch.empty_like(logits)
+    nb = C.c_size_t(0)
+    _check(lib().rnn_softmax_xent_workspace_size(n, C.byref(nb)))
+    w = ws.get(nb.value) if ws is not None else _ws(nb.value, dev)
+    _check(lib().rnn_softmax_xent(_ptr(logits), n, Cn, logits.stride(0), _ptr(label), _ptr(loss),
+                                  _ptr(d_logits), d_logits.stride(0), _ptr(w), w.numel(),
+                                  _stream(stream)))
+    return loss, d_logits
+
+
+class Adam:
+    """rnn_adam over a list of parameter tensors (2-D views or 1-D vectors), with the step
+    counter on the device (rnn_adam_tick), so a training step is graph-capturable."""
+
+    def __init__(self, params, lr=0.01, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.0):
+        self.params = [p if p.dim() == 2 else p.view(1, -1) for p in params]
+        dev = self.params[0].device
+        self.m = [torch.zeros(p.shape, dtype=torch.float32, device=dev) for p in self.params]
+        self.v = [torch.zeros(p.shape, dtype=torch.float32, device=dev) for p in self.params]
+        self.t = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.cfg = AdamC(lr, betas[0], betas[1], eps, weight_decay)
+
+    def step(self, grads, stream=None):
+        _check(lib().rnn_adam_tick(_ptr(self.t), _stream(stream)))
+        for p, g, m, v in zip(self.params, grads, self.m, self.v):
+            g = g if g.dim() == 2 else g.view(1, -1)
+            _check(lib().rnn_adam(_ptr(p), p.shape[0], p.shape[1], p.stride(0), _ptr(g),
+                                  g.stride(0), _ptr(m), _ptr(v), C.byref(self.cfg), _ptr(self.t),
+                                  _stream(stream)))

@@ -156,7 +156,21 @@ class ShardedGCNProgram:
         d_out = np.zeros((n_pad, dp[-1]), np.float32)
         d_out[: self.n_own, : self.dims[-1]] = np.asarray(graph["d_out"], np.float32)[rank_of, : self.dims[-1]]
         self.d_out = be.tensor(d_out)
+        # O7 node epilogue (bias then ReLU on hidden layers, bias on the last), when the graph
+        # carries biases: fused into the owned rows' LJA store; d bias all-reduced
+        self.bias = None
+        if graph.get("b") is not None:
+            self.bias, self.dP, self.db = [], [], []
+            for l in range(self.L):
+                bp = np.zeros((1, dp[l + 1]), np.float32)
+                bp[0, : self.dims[l + 1]] = np.asarray(graph["b"][l], np.float32)
+                self.bias.append(be.tensor(bp)[0])
+                self.dP.append(be.zeros(n_pad, dp[l + 1]))
+                self.db.append(be.zeros(1, dp[l + 1])[0])
         self.timers = None
+
+    def _act(self, l):
+        return "relu" if l < self.L - 1 else "none"
 
     @property
     def join_rows_per_step(self):
@@ -189,7 +203,11 @@ class ShardedGCNProgram:
             all_gather_rows(self.Zall[l], self.Z[l], g)
             self._t("allgather_end")
             self._t("lja_fwd")
-            be.lja_fwd(self.idx, self.Zall[l], self.w, self.H[l + 1])
+            if self.bias is not None:
+                be.lja_fwd_epi(self.idx, self.Zall[l], self.w, self.H[l + 1], self.bias[l],
+                               self._act(l))
+            else:
+                be.lja_fwd(self.idx, self.Zall[l], self.w, self.H[l + 1])
             self._t("lja_fwd_end")
         return self.H[-1]
 
@@ -197,6 +215,12 @@ class ShardedGCNProgram:
         be, g = self.be, self.group
         dY = self.d_out
         for l in reversed(range(self.L)):
+            if self.bias is not None:
+                be.epilogue_bwd(dY, self.H[l + 1], self.bias[l], self._act(l), self.dP[l],
+                                self.db[l], self.n_own)
+                if self.P > 1:
+                    dist.all_reduce(self.db[l], group=g)
+                dY = self.dP[l]
             self._t("lja_bwd")
             be.lja_bwd_src(self.idx, self.Zall[l], self.w, dY, self.dZall[l])
             self._t("lja_bwd_end")
@@ -361,6 +385,16 @@ class RnnBackend:
 
     def lja_fwd(self, idx, Z, w, out):
         self.rnn.join_aggregate_fwd(idx, self._query(idx, Z, w), out=out, ws=self.ws)
+
+    def lja_fwd_epi(self, idx, Z, w, out, bias, act):
+        G = idx.n_groups
+        epi = self.rnn.make_epilogue(bias=bias, act=act)
+        self.rnn.join_aggregate_fwd_epi(idx, self._query(idx, Z, w), epi, out=out[:G], ws=self.ws)
+
+    def epilogue_bwd(self, dy, y, bias, act, dx, db, rows):
+        """dx / db over the first `rows` (owned) rows; padding rows of dx are left 0."""
+        epi = self.rnn.make_epilogue(bias=bias, act=act)
+        self.rnn.epilogue_bwd(dy[:rows], y[:rows], epi, dx=dx[:rows], ws=self.ws, db_out=db)
 
     def lja_bwd_src(self, idx, Z, w, d_out, d_src):
         from .programs import _lja_src_grad

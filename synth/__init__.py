@@ -137,7 +137,20 @@ def cora_like(seed=42):
               _normal_f32(rng, (7, 16), 1.0 / np.sqrt(16))]
     g["d_out"] = _normal_f32(rng, (2708, 7), 1.0)
     g["dims"] = [1433, 16, 7]
+    _gcn_extras(g, rng)
     return g
+
+
+def _gcn_extras(g, rng):
+    """Drawn after everything else (the earlier draws are unchanged): per-layer biases of the
+    O7 epilogue ~ N(0, 0.1^2), class labels uniform over the last width, and a training mask of
+    the first 5% of node rows (Cora's public split labels 140 of 2,708 nodes)."""
+    dims = g["dims"]
+    g["b"] = [_normal_f32(rng, (dims[l + 1],), 0.1) for l in range(len(dims) - 1)]
+    n = len(g["nodes"]["key"])
+    lab = rng.integers(0, dims[-1], n).astype(np.int64)
+    lab[max(1, n // 20):] = -1
+    g["labels"] = lab
 
 
 def arxiv_like(seed=42, n_nodes=169343, n_edges=1166243, d=128, layers=3):
@@ -147,6 +160,7 @@ def arxiv_like(seed=42, n_nodes=169343, n_edges=1166243, d=128, layers=3):
     g["W"] = [_normal_f32(rng, (d, d), 1.0 / np.sqrt(d)) for _ in range(layers)]
     g["d_out"] = _normal_f32(rng, (n_nodes, d), 1.0)
     g["dims"] = [d] * (layers + 1)
+    _gcn_extras(g, rng)
     return g
 
 

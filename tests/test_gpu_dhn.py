@@ -228,7 +228,10 @@ def test_root_subset(rnn, k):
     rnn.dhn_fwd(gi, k, fg, out=out, walk_sum=ws, roots=roots)
     o = np_(out)
     full = np_(rnn.dhn_fwd(gi, k, fg))
-    np.testing.assert_array_equal(o[sel], full[sel])
+    if k == 3:
+        np.testing.assert_array_equal(o[sel], full[sel])       # deterministic walk
+    else:
+        assert_close(o[sel], full[sel], FP32_TOL, "C4 subset")  # fp32 atomics: order only
     others = np.setdiff1d(np.arange(gi.n_groups), sel)
     assert np.all(np.isnan(o[others]))
     d_out = rng.standard_normal((gi.n_groups, d)).astype(np.float32)

@@ -383,3 +383,80 @@ def test_empty_join_dense_groups(R, agg):
     for k in ("src", "src_key", "dst"):
         if g.get(k) is not None:
             assert torch.count_nonzero(g[k]) == 0, k
+
+
+@pytest.mark.parametrize("D", [128, 16, 256])
+@pytest.mark.parametrize("act", ["none", "relu", "gelu"])
+@pytest.mark.parametrize("gated", [False, True])
+def test_epilogue_fused_parity(R, ora, D, act, gated):
+    """rnn_join_aggregate_fwd_epi: y = gate act(LJA + b) + (1 - gate) r fused into the lean
+    store (D = 128, 256) or applied after the aggregate (D = 16); rnn_epilogue_bwd: dx, d_bias,
+    d_resid, d_gate -- against oracle.lja_fwd + oracle.epilogue_fwd / _bwd."""
+    rng = np.random.default_rng(D + 7 * gated + len(act))
+    db = make_case(rng, n_s=300, n_t=200, n_e=5000, d=4)
+    gi = R.build_join_index(cu(db["e_src"]), cu(db["e_dst"]), cu(db["s_key"]), cu(db["t_key"]),
+                            rows_per_item=16, dense_groups=True)
+    oi = ora.build_join_index(db["e_src"], db["e_dst"], db["s_key"], db["t_key"])
+    z = rng.standard_normal((300, D)).astype(np.float32)
+    w = rng.uniform(0.5, 1.5, gi.n_join_rows).astype(np.float32)
+    b = (rng.standard_normal(D) * 0.5).astype(np.float32)
+    G = gi.n_groups
+    r = rng.standard_normal((G, D)).astype(np.float32) if gated else None
+    gate = 0.35 if gated else 1.0
+    pre = padded(np.full((G, D), np.nan, np.float32))
+    zg, bg, rg = padded(z), cu(b), (padded(r) if gated else None)
+    epi = R.make_epilogue(bias=bg, act=act, gate=gate, resid=rg, pre=pre)
+    q = R.make_query("src", "sum", src=zg, edge=cu(w), edge_mode=R.BY_POSITION)
+    out = R.join_aggregate_fwd_epi(gi, q, epi)
+    # oracle: compact groups sit at their key's rank among the dense groups; empty ones
+    # aggregate to 0 before the epilogue
+    rows = np.searchsorted(np.sort(db["t_key"]), oi["group_key"])
+    agg = np.zeros((G, D))
+    ow = np.zeros(oi["n_join_rows"])
+    ow[:] = w[: oi["n_join_rows"]]
+    agg[rows], _ = ora.lja_fwd(oi, "src", "sum", src=z, edge=ow, edge_mode=1)
+    ref = ora.epilogue_fwd(agg, b, act, gate, r)
+    assert_close(np_(out), ref, FP32_TOL, "y")
+    assert_close(np_(pre), agg + b, FP32_TOL, "pre")
+    dy = rng.standard_normal((G, D)).astype(np.float32)
+    dx, dbias, dres, dgate = R.epilogue_bwd(padded(dy), out, epi, want_resid=gated, want_gate=gated)
+    # the activation's kink is a floating-point decision: take it from the GPU's pre
+    rdx, rdb, rdr, rdg = ora.epilogue_bwd(dy, np_(pre) - b, b, act, gate, r)
+    assert_close(np_(dx), rdx, FP32_TOL, "dx")
+    assert_close(np_(dbias), rdb, FP32_TOL, "d_bias")
+    if gated:
+        assert_close(np_(dres), rdr, FP32_TOL, "d_resid")
+        assert abs(float(dgate.item()) - rdg) <= FP32_TOL * max(1.0, abs(rdg))
+
+
+@pytest.mark.parametrize("D,wmode,dense", [(16, 1, False), (128, 0, True), (7, 1, True),
+                                           (200, None, False)])
+def test_max_aggregate_parity(R, ora, D, wmode, dense):
+    """RNN_AGG_MAX: out and the arg-max bit-exact against the oracle
+    (integer-valued features and weights in {0.5, 1, 2}: every product is exact in fp32, so
+    both sides take each max / tie decision on the same values; ties go to the lowest join
+    position), empty dense groups 0 / -1, and the backward to the arg-max rows only."""
+    rng = np.random.default_rng(D + 3 * (wmode or 0))
+    db = make_case(rng, n_s=300, n_t=200, n_e=6000, d=4)
+    gi = R.build_join_index(cu(db["e_src"]), cu(db["e_dst"]), cu(db["s_key"]), cu(db["t_key"]),
+                            dense_groups=dense)
+    oi = ora.build_join_index(db["e_src"], db["e_dst"], db["s_key"], db["t_key"])
+    z = rng.integers(-6, 7, (300, D)).astype(np.float32)
+    n_w = oi["n_join_rows"] if wmode == 1 else len(db["e_src"])
+    w = rng.choice([0.5, 1.0, 2.0], n_w).astype(np.float32) if wmode is not None else None
+    q = R.make_query("src", "max", src=padded(z), edge=None if w is None else cu(w),
+                     edge_mode=wmode or 0)
+    out, am = R.join_aggregate_max_fwd(gi, q)
+    ro, ram = ora.lja_max_fwd(oi, z, w, w_by_pos=wmode == 1)
+    rows = np.searchsorted(np.sort(db["t_key"]), oi["group_key"]) if dense else np.arange(oi["n_groups"])
+    np.testing.assert_array_equal(np_(out)[rows], ro)
+    np.testing.assert_array_equal(np_(am)[rows], ram)
+    if dense:
+        empty = np.setdiff1d(np.arange(gi.n_groups), rows)
+        assert len(empty) and np.all(np_(out)[empty] == 0) and np.all(np_(am)[empty] == -1)
+    dO = rng.standard_normal((gi.n_groups, D)).astype(np.float32)
+    d_src, d_edge = R.join_aggregate_max_bwd(gi, q, am, padded(dO), want_edge=w is not None)
+    rdz, rdw = ora.lja_max_bwd(oi, z, ram, dO[rows], w, w_by_pos=wmode == 1)
+    assert_close(np_(d_src), rdz, FP32_TOL, "d_src")
+    if w is not None:
+        assert_close(np_(d_edge).reshape(-1), rdw, FP32_TOL, "d_edge")

@@ -29,11 +29,14 @@ def test_gcn_cora_full(P, prec):
     prog = P.GCNProgram(g, prec=prec)
     prog.step()
     torch.cuda.synchronize()
-    H, dW, dX0 = op.gcn_step(g)
+    extra = {}
+    H, dW, dX0 = op.gcn_step(g, out=extra)
     tol = FP32_TOL if prec == "3xtf32" else TF32_TOL
     assert_close(np_(prog.H[-1]), H[-1], tol, "out")
+    assert_close(np_(prog.H[1]), H[1], tol, "H1 (bias + ReLU)")
     for l in range(len(dW)):
         assert_close(np_(prog.dW[l]), dW[l], tol, f"dW{l}")
+        assert_close(np_(prog.db[l]), extra["db"][l], tol, f"db{l}")
     assert_close(np_(prog.dH[0]), dX0, tol, "dX0")
 
 
@@ -76,16 +79,25 @@ def test_gcn_arxiv_full_size_sampled(P):
     sizes = np.diff(o1["group_ptr"])
     sel = np.unique(np.concatenate([rng.choice(o1["n_groups"], 3000, replace=False),
                                     np.argsort(sizes)[-20:]]))          # + the 20 largest hubs
-    # layer 1 forward on the projection the GPU produced
+    # layer 1 forward on the projection the GPU produced: the LJA, then the O7 epilogue
+    # (bias + ReLU) fused into its store
     Z0 = np_(prog.Z[0])
+    b0 = g["b"][0]
     ref, _ = oracle.lja_fwd(o1, "src", "sum", src=Z0, edge=w1, edge_mode=1, sel=sel)
-    assert_close(np_(prog.H[1])[sel], ref, FP32_TOL, "H1 sampled")
+    assert_close(np_(prog.H[1])[sel], oracle.epilogue_fwd(ref, b0, "relu"), FP32_TOL, "H1 sampled")
     # projection (tcgen05 3xTF32) on sampled rows
     rows = rng.choice(len(key), 2000, replace=False)
     assert_close(Z0[rows], oracle.project(g["nodes"]["x"][rows], g["W"][0]), FP32_TOL, "Z0 rows")
-    # layer 1 backward: every source row, on the upstream gradient the GPU used
-    dY1 = np_(prog.dH[1])
-    dZ0 = oracle.lja_bwd(o1, dY1, "src", "sum", src=Z0, edge=w1, edge_mode=1, want=("src",))["src"]
+    # layer 1 backward: the epilogue backward on every row (from the GPU's upstream dH1), then
+    # the LJA backward on every source row from the GPU's d(pre-activation)
+    # (the ReLU mask is a decision taken in floating point: both sides take it from the GPU's
+    # fp32 output -- pre = H1 - b, which is the pre-activation where H1 > 0 and gives the
+    # zero derivative where H1 = 0)
+    dP0, db0, _, _ = oracle.epilogue_bwd(np_(prog.dH[1]), np_(prog.H[1]) - b0, b0, "relu")
+    assert_close(np_(prog.dP[0]), dP0, FP32_TOL, "dP0 all rows")
+    assert_close(np_(prog.db[0]), db0, FP32_TOL, "db0")
+    dZ0 = oracle.lja_bwd(o1, np_(prog.dP[0]), "src", "sum", src=Z0, edge=w1, edge_mode=1,
+                         want=("src",))["src"]
     assert_close(np_(prog.dZ[0]), dZ0, FP32_TOL, "dZ0 all rows")
     # dW of layer 1 on the GPU's own dZ
     _, dW0, _ = oracle.project_bwd(g["nodes"]["x"], g["W"][0], np_(prog.dZ[0]), want_dx=False, want_db=False)

@@ -71,14 +71,28 @@ class OracleBackend:
                            edge=w, edge_mode=1, want=("src",))["src"]
         d_src[:] = torch.from_numpy(g)
 
+    def lja_fwd_epi(self, idx, Z, w, out, bias, act):
+        self.lja_fwd(idx, Z, w, out)
+        G = idx["n_groups"]
+        out[:G] = torch.from_numpy(oracle.epilogue_fwd(out[:G].numpy(), bias.numpy(), act))
+
+    def epilogue_bwd(self, dy, y, bias, act, dx, db, rows):
+        # the pre-activation from the output: y - b (ReLU: where y = 0 it gives -b, i.e. pre
+        # = 0, whose derivative is 0 like any pre <= 0)
+        b = bias.numpy()
+        d, bb, _, _ = oracle.epilogue_bwd(dy[:rows].numpy(), y[:rows].numpy() - b, b, act)
+        dx[:rows] = torch.from_numpy(d)
+        db[:] = torch.from_numpy(bb)
+
     def project_bwd(self, X, W, dY, dX, dW):
         a, b, _ = oracle.project_bwd(X.numpy(), W.numpy(), dY.numpy(), want_db=False)
         dX[:] = torch.from_numpy(a)
         dW[:] = torch.from_numpy(b)
 
 
-def graph_with_weights(dims=(12, 8, 4)):
-    """Small GCN; dims (13, 6, 7) gives Cora-like widths that are not multiples of 4."""
+def graph_with_weights(dims=(12, 8, 4), bias=False):
+    """Small GCN; dims (13, 6, 7) gives Cora-like widths that are not multiples of 4; bias:
+    the O7 epilogue's per-layer biases."""
     g = synth.gcn_graph(7, n_nodes=400, n_edge_tuples=2400, d_in=dims[0], undirected=True,
                         cap_ratio=50.0)
     rng = np.random.default_rng(3)
@@ -86,6 +100,9 @@ def graph_with_weights(dims=(12, 8, 4)):
     g["W"] = [(rng.standard_normal((dims[l + 1], dims[l])) / 3).astype(np.float32)
               for l in range(len(dims) - 1)]
     g["d_out"] = rng.standard_normal((400, dims[-1])).astype(np.float32)
+    if bias:
+        g["b"] = [(rng.standard_normal(dims[l + 1]) * 0.3).astype(np.float32)
+                  for l in range(len(dims) - 1)]
     return g
 
 
@@ -170,3 +187,28 @@ def test_world_size_2_gloo_ragged_widths():
         res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
     g = graph_with_weights(dims)
     check(res, reference(g), g)
+
+
+def test_world_size_2_gloo_with_epilogue():
+    """O7 epilogue (bias + ReLU hidden, bias last) in the sharded step: fused on the owned
+    rows, backward through the epilogue, d bias all-reduced (checked through dW / dX)."""
+    dims = (12, 8, 4)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker_b, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    g = graph_with_weights(dims, bias=True)
+    check(res, reference(g), g)
+
+
+def _worker_b(rank, world, port, path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = graph_with_weights((12, 8, 4), bias=True)
+        prog = ShardedGCNProgram(g, backend=OracleBackend())
+        prog.step()
+        np.savez(os.path.join(path, f"r{rank}.npz"), keys=prog.plan.my_keys, rows=prog.plan.my_rows,
+                 out=prog.owned_output(), dx=prog.owned_dx(),
+                 **{f"dW{l}": prog.dW[l].numpy() for l in range(prog.L)})
+    finally:
+        dist.destroy_process_group()
