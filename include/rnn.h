@@ -128,6 +128,23 @@ rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64_t* e_dst_k
                                 int64_t rows_per_item, rnn_join_index* idx, void* workspace,
                                 size_t* workspace_bytes, void* stream);
 
+/* Selection pushdown (PAPER.md:444 -- the join rule is U(T_tau(sigma(R1 |><| ... |><| Rk))); :1031
+ * "selection pushdowns"): the same build over sigma(E), the E rows with
+ * e_mask[j] != 0 (uint8 [n_edge_rows], device).  Masked rows are dropped in the probe, before
+ * the sort, so the index is exactly the canonical index of the filtered relation (edge_row
+ * still refers to rows of the unfiltered E).  Other arguments as rnn_build_join_index. */
+rnn_status rnn_build_join_index_sel(const int64_t* e_src_key, const int64_t* e_dst_key,
+                                    const uint8_t* e_mask, int64_t n_edge_rows,
+                                    const int64_t* src_key, int64_t n_src, const int64_t* dst_key,
+                                    int64_t n_dst, int flags, int64_t rows_per_item,
+                                    rnn_join_index* idx, void* workspace, size_t* workspace_bytes,
+                                    void* stream);
+/* Predicate mask over an E attribute column: r_j = attr[j] <op> value, op in {EQ, NE, LT, LE,
+ * GT, GE} = 0..5; attr int64 (dtype 0, value truncated to int64) or float32 (dtype 1);
+ * combine 0: mask = r, 1: mask &= r, 2: mask |= r (conjunctions / disjunctions of atoms). */
+rnn_status rnn_select_mask(const void* attr, int32_t dtype, int64_t n, int32_t op, double value,
+                           int32_t combine, uint8_t* mask, void* stream);
+
 /* ===================================================================================== */
 /* A3/A4. Fused gather - combine - segmented reduce, forward                             */
 /* ===================================================================================== */
@@ -438,6 +455,13 @@ rnn_status rnn_accumulate(float* y, int64_t ldy, const float* x, int64_t ldx, in
  * idx[i] < 0 (fp32, row-major, any ld; idx int32, device).  Indices are not range-checked. */
 rnn_status rnn_gather_rows(float* y, int64_t ldy, const float* x, int64_t ldx, const int32_t* idx,
                            int64_t n, int32_t cols, void* stream);
+
+/* Row scatter-add (mini-batch streaming: adding one batch's source-gradient rows into the
+ * full gradient): y[idx[i], c] += x[i, c] for i < n (idx[i] < 0 skipped).  The indices of one
+ * call must be distinct (no two rows collide; calls on one stream apply in order, so the
+ * result is deterministic). */
+rnn_status rnn_scatter_add_rows(float* y, int64_t ldy, const float* x, int64_t ldx,
+                                const int32_t* idx, int64_t n, int32_t cols, void* stream);
 
 /* Multi-GPU ownership of group keys: owner[i] = splitmix64(keys[i] ^ seed) mod P. */
 rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed,

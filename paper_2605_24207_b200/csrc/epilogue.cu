@@ -87,6 +87,64 @@ __global__ void __launch_bounds__(256) epi_bwd_kernel(const float* __restrict__ 
   }
 }
 
+// vectorised variant (dim % 4 == 0, 16-byte aligned rows): block = 8 warps x EPI_VROWS rows,
+// lane = one float4 column quad of a 128-column slab; per-block column partials of dx
+constexpr int EPI_VROWS = 256;
+__global__ void __launch_bounds__(256) epi_bwd4_kernel(const float* __restrict__ dy, int64_t lddy,
+                                                       const float* __restrict__ y, int64_t ldy,
+                                                       int64_t rows, int dim, EpiD e,
+                                                       float* dx, int64_t lddx,
+                                                       float* __restrict__ dres, int64_t ldres,
+                                                       float* __restrict__ part_b,
+                                                       float* __restrict__ part_g) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 128 + 4 * lane;
+  const int64_t r0 = (int64_t)blockIdx.y * EPI_VROWS;
+  const int64_t r1 = r0 + EPI_VROWS < rows ? r0 + EPI_VROWS : rows;
+  float4 sb = make_float4(0.f, 0.f, 0.f, 0.f);
+  float sg = 0.f;
+  if (c < dim) {
+    const float4 bias = e.bias ? *reinterpret_cast<const float4*>(e.bias + c) : sb;
+    for (int64_t r = r0 + wp; r < r1; r += 8) {
+      const float4 g = *reinterpret_cast<const float4*>(dy + r * lddy + c);
+      float4 xb = e.pre ? *reinterpret_cast<const float4*>(e.pre + r * e.ld_pre + c)
+                        : *reinterpret_cast<const float4*>(y + r * ldy + c);
+      float4 d;
+      d.x = g.x * e.gate * epi_dact(e.act, xb.x);
+      d.y = g.y * e.gate * epi_dact(e.act, xb.y);
+      d.z = g.z * e.gate * epi_dact(e.act, xb.z);
+      d.w = g.w * e.gate * epi_dact(e.act, xb.w);
+      if (dx) *reinterpret_cast<float4*>(dx + r * lddx + c) = d;
+      if (dres)
+        *reinterpret_cast<float4*>(dres + r * ldres + c) = f4_scale(1.f - e.gate, g);
+      if (part_g) {
+        const float4 rr = *reinterpret_cast<const float4*>(e.resid + r * e.ld_resid + c);
+        sg += g.x * (epi_act(e.act, xb.x) - rr.x) + g.y * (epi_act(e.act, xb.y) - rr.y) +
+              g.z * (epi_act(e.act, xb.z) - rr.z) + g.w * (epi_act(e.act, xb.w) - rr.w);
+      }
+      sb = f4_add(sb, d);
+      (void)bias;
+    }
+  }
+  __shared__ float4 sh_b[8][32];
+  __shared__ float sh_g[256];
+  sh_b[wp][lane] = sb;
+  sh_g[threadIdx.x] = sg;
+  __syncthreads();
+  if (wp == 0 && c < dim && part_b) {
+    float4 t = sh_b[0][lane];
+    for (int k = 1; k < 8; ++k) t = f4_add(t, sh_b[k][lane]);
+    *reinterpret_cast<float4*>(part_b + (int64_t)blockIdx.y * dim + c) = t;
+  }
+  if (part_g) {
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) sh_g[threadIdx.x] += sh_g[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) part_g[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = sh_g[0];
+  }
+}
+
 __global__ void epi_colsum_final(const float* __restrict__ part, int64_t chunks, int dim,
                                  float* __restrict__ out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
@@ -152,7 +210,7 @@ extern "C" rnn_status rnn_epilogue_fwd(const float* x, int64_t ldx, int64_t rows
 extern "C" rnn_status rnn_epilogue_bwd_workspace_size(int64_t rows, int32_t dim, size_t* bytes) {
   clear_error();
   RNN_REQUIRE(bytes && rows >= 0 && dim >= 1, RNN_ERR_INVALID_ARGUMENT, "bad argument");
-  const int64_t chunks = ceil_div(rows > 0 ? rows : 1, EPI_CHUNK);
+  const int64_t chunks = ceil_div(rows > 0 ? rows : 1, EPI_VROWS);   // >= the scalar path's
   const int64_t slabs = ceil_div(dim, 32);
   *bytes = sizeof(float) * (size_t)(chunks * dim + chunks * slabs) + 256;
   return RNN_OK;
@@ -185,14 +243,24 @@ extern "C" rnn_status rnn_epilogue_bwd(const float* dy, int64_t lddy, const floa
     return RNN_OK;
   }
   const EpiD e = epi_dev(epi);
-  const int64_t chunks = ceil_div(rows, EPI_CHUNK);
-  const int64_t slabs = ceil_div(dim, 32);
+  // float4 path when every row operand is 16-byte aligned with ld % 4 == 0
+  auto al = [](const void* p, int64_t ld) { return !p || (aligned16(p) && ld % 4 == 0); };
+  const bool vec = dim % 4 == 0 && al(dy, lddy) && al(y, ldy) && al(dx, lddx) &&
+                   al(d_resid, ld_dresid) && al(epi->pre, epi->ld_pre) &&
+                   al(epi->resid, epi->ld_resid) && al(epi->bias, 4);
+  const int64_t chunks = vec ? ceil_div(rows, EPI_VROWS) : ceil_div(rows, EPI_CHUNK);
+  const int64_t slabs = vec ? ceil_div(dim, 128) : ceil_div(dim, 32);
   float* part_b = reinterpret_cast<float*>(workspace);
   float* part_g = part_b + chunks * dim;
   dim3 grid((unsigned)slabs, (unsigned)chunks);
-  epi_bwd_kernel<<<grid, 256, 0, st>>>(dy, lddy, y, ldy, rows, dim, e, dx, lddx, d_resid,
-                                       ld_dresid, d_bias ? part_b : nullptr,
-                                       d_gate ? part_g : nullptr);
+  if (vec)
+    epi_bwd4_kernel<<<grid, 256, 0, st>>>(dy, lddy, y, ldy, rows, dim, e, dx, lddx, d_resid,
+                                          ld_dresid, d_bias ? part_b : nullptr,
+                                          d_gate ? part_g : nullptr);
+  else
+    epi_bwd_kernel<<<grid, 256, 0, st>>>(dy, lddy, y, ldy, rows, dim, e, dx, lddx, d_resid,
+                                         ld_dresid, d_bias ? part_b : nullptr,
+                                         d_gate ? part_g : nullptr);
   RNN_LAUNCH_CHECK();
   if (d_bias) {
     epi_colsum_final<<<(unsigned)ceil_div(dim, 128), 128, 0, st>>>(part_b, chunks, dim, d_bias);

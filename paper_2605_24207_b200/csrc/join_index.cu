@@ -85,11 +85,12 @@ __device__ __forceinline__ int32_t table_find(const Table& t, int64_t key) {
 // probe: s_row_of[j], t_row_of[j], hit[j] in {0,1} (as int64 for the scan)
 __global__ void probe_kernel(const int64_t* __restrict__ e_src, const int64_t* __restrict__ e_dst,
                              int64_t n_e, Table S, bool has_s, Table T, bool has_t,
-                             int32_t* s_row_of, int32_t* t_row_of, int64_t* hit) {
+                             int32_t* s_row_of, int32_t* t_row_of, int64_t* hit,
+                             const uint8_t* __restrict__ e_mask) {
   int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= n_e) return;
   int32_t sr = -1, tr = -1;
-  bool ok = true;
+  bool ok = !e_mask || e_mask[j];   // selection sigma(E) pushed into the probe
   if (has_s) { sr = table_find(S, e_src[j]); ok = sr >= 0; }
   if (ok && has_t) { tr = table_find(T, e_dst[j]); ok = tr >= 0; }
   s_row_of[j] = sr;
@@ -453,6 +454,12 @@ rnn_status rank_keys(const int64_t* keys, int64_t n, Scratch& s, uint32_t* rank,
 
 using namespace rnn;
 
+static rnn_status build_impl(const int64_t* e_src_key, const int64_t* e_dst_key,
+                             int64_t n_edge_rows, const int64_t* src_key, int64_t n_src,
+                             const int64_t* dst_key, int64_t n_dst, int flags,
+                             int64_t rows_per_item, rnn_join_index* idx, void* workspace,
+                             size_t* workspace_bytes, void* stream, const uint8_t* e_mask);
+
 extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64_t* e_dst_key,
                                            int64_t n_edge_rows, const int64_t* src_key,
                                            int64_t n_src, const int64_t* dst_key, int64_t n_dst,
@@ -460,6 +467,66 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
                                            void* workspace, size_t* workspace_bytes,
                                            void* stream) {
   clear_error();
+  return build_impl(e_src_key, e_dst_key, n_edge_rows, src_key, n_src, dst_key, n_dst, flags,
+                    rows_per_item, idx, workspace, workspace_bytes, stream, nullptr);
+}
+
+extern "C" rnn_status rnn_build_join_index_sel(const int64_t* e_src_key, const int64_t* e_dst_key,
+                                               const uint8_t* e_mask, int64_t n_edge_rows,
+                                               const int64_t* src_key, int64_t n_src,
+                                               const int64_t* dst_key, int64_t n_dst, int flags,
+                                               int64_t rows_per_item, rnn_join_index* idx,
+                                               void* workspace, size_t* workspace_bytes,
+                                               void* stream) {
+  clear_error();
+  RNN_REQUIRE(e_mask || n_edge_rows == 0, RNN_ERR_INVALID_ARGUMENT, "e_mask is NULL");
+  return build_impl(e_src_key, e_dst_key, n_edge_rows, src_key, n_src, dst_key, n_dst, flags,
+                    rows_per_item, idx, workspace, workspace_bytes, stream, e_mask);
+}
+
+namespace rnn {
+namespace {
+__global__ void select_kernel(const void* __restrict__ attr, int dtype, int64_t n, int op,
+                              double value, int combine, uint8_t* __restrict__ mask) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  bool r;
+  if (dtype == 0) {
+    const int64_t a = static_cast<const int64_t*>(attr)[j];
+    const int64_t v = (int64_t)value;
+    r = op == 0 ? a == v : op == 1 ? a != v : op == 2 ? a < v : op == 3 ? a <= v
+      : op == 4 ? a > v : a >= v;
+  } else {
+    const float a = static_cast<const float*>(attr)[j];
+    const float v = (float)value;
+    r = op == 0 ? a == v : op == 1 ? a != v : op == 2 ? a < v : op == 3 ? a <= v
+      : op == 4 ? a > v : a >= v;
+  }
+  mask[j] = combine == 0 ? (uint8_t)r : combine == 1 ? (uint8_t)(mask[j] && r)
+                                                      : (uint8_t)(mask[j] || r);
+}
+}  // namespace
+}  // namespace rnn
+
+extern "C" rnn_status rnn_select_mask(const void* attr, int32_t dtype, int64_t n, int32_t op,
+                                      double value, int32_t combine, uint8_t* mask, void* stream) {
+  clear_error();
+  RNN_REQUIRE(n >= 0 && (n == 0 || (attr && mask)), RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  RNN_REQUIRE(dtype == 0 || dtype == 1, RNN_ERR_UNSUPPORTED, "dtype: 0 int64, 1 float32");
+  RNN_REQUIRE(op >= 0 && op <= 5, RNN_ERR_INVALID_ARGUMENT, "op: EQ NE LT LE GT GE = 0..5");
+  RNN_REQUIRE(combine >= 0 && combine <= 2, RNN_ERR_INVALID_ARGUMENT, "combine: 0 set, 1 and, 2 or");
+  if (n == 0) return RNN_OK;
+  select_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, as_stream(stream)>>>(attr, dtype, n, op,
+                                                                          value, combine, mask);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+static rnn_status build_impl(const int64_t* e_src_key, const int64_t* e_dst_key,
+                             int64_t n_edge_rows, const int64_t* src_key, int64_t n_src,
+                             const int64_t* dst_key, int64_t n_dst, int flags,
+                             int64_t rows_per_item, rnn_join_index* idx, void* workspace,
+                             size_t* workspace_bytes, void* stream, const uint8_t* e_mask) {
   RNN_REQUIRE(idx && workspace_bytes, RNN_ERR_INVALID_ARGUMENT, "idx and workspace_bytes required");
   RNN_REQUIRE(n_edge_rows >= 0 && n_src >= 0 && n_dst >= 0, RNN_ERR_INVALID_ARGUMENT,
               "negative size");
@@ -518,7 +585,7 @@ extern "C" rnn_status rnn_build_join_index(const int64_t* e_src_key, const int64
   // 2. probe + compaction
   if (n_e > 0) {
     probe_kernel<<<blocks_for(n_e), T256, 0, st>>>(e_src_key, e_dst_key, n_e, s.S, P.has_s, s.T,
-                                                   P.has_t, s.s_row_of, s.t_row_of, s.hit);
+                                                   P.has_t, s.s_row_of, s.t_row_of, s.hit, e_mask);
     RNN_LAUNCH_CHECK();
   }
   RNN_TRY(exclusive_scan_i64(s.hit, s.hit, n_e, s.scan_ws, st));

@@ -364,9 +364,9 @@ rnn_status launch_rs_mode(const LjaArgs& a, const RSCtx& cx, cudaStream_t st) {
                       (a.combine == RNN_COMBINE_MUL && (!a.edge.p || a.edge.dim == 1));
   if (scaled && !a.dst.p && a.D == 128 * VEC && a.ld_out % 4 == 0) {
     LeanFwdMeta mp{a.src_row, a.edge_row, a.group_ptr, a.edge.p, a.edge.ld, a.edge.mode, a.mean};
-    LeanOut o{a.src.p, a.src.ld, a.out, a.ld_out, a.beta, a.epi};
+    LeanOut o{a.src.p, a.src.ld, a.out, a.ld_out, a.beta};
     if (a.epi.on && a.epi_done) *a.epi_done = 1;
-    return launch_lean<LeanFwdMeta, VEC>(mp, cx, o, st);
+    return launch_lean<LeanFwdMeta, VEC>(mp, cx, o, st, a.epi);
   }
   const bool ev = a.edge.p && a.edge.dim > 1;
   if (ev) return launch_rs<VEC, 1>(a, cx, st);

@@ -173,3 +173,33 @@ extern "C" rnn_status rnn_gather_rows(float* y, int64_t ldy, const float* x, int
   RNN_LAUNCH_CHECK();
   return RNN_OK;
 }
+
+namespace rnn {
+namespace {
+// y[idx[i], :] += x[i, :] (idx distinct within one call: no two rows collide)
+__global__ void scatter_add_rows_kernel(float* __restrict__ y, int64_t ldy,
+                                        const float* __restrict__ x, int64_t ldx,
+                                        const int32_t* __restrict__ idx, int64_t n, int cols) {
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int32_t r = idx[i];
+  if (r < 0) return;
+  for (int c = lane; c < cols; c += 32) y[(int64_t)r * ldy + c] += x[i * ldx + c];
+}
+}  // namespace
+}  // namespace rnn
+
+extern "C" rnn_status rnn_scatter_add_rows(float* y, int64_t ldy, const float* x, int64_t ldx,
+                                           const int32_t* idx, int64_t n, int32_t cols,
+                                           void* stream) {
+  clear_error();
+  RNN_REQUIRE(n >= 0 && cols >= 0 && (n == 0 || cols == 0 || (x && y && idx)) && ldy >= cols &&
+                  ldx >= cols,
+              RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  if (n == 0 || cols == 0) return RNN_OK;
+  scatter_add_rows_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, as_stream(stream)>>>(y, ldy, x, ldx,
+                                                                                  idx, n, cols);
+  RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}

@@ -48,6 +48,7 @@ struct GemmParams {
   int smem_kb;      // shared-memory budget of the stage ring (0: default 200 KB, 1 CTA / SM)
   int b_lo_row;     // K-major B with its 3xTF32 lo part precomputed b_lo_row rows below (0: none)
   int nbuf;         // TMEM accumulator buffers (2: chunk c+1 accumulates while chunk c drains)
+  int chunk_elems;  // reduction elements per TMEM accumulation chunk (multiple of KB)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -206,7 +207,7 @@ template <bool A_MN, bool B_MN, bool SPLIT3, int KB = BK, int NGRP = 4>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    GemmParams p) {
-  constexpr int CH = CHUNK_ELEMS / KB;   // k-blocks per accumulation chunk
+  const int CH = p.chunk_elems / KB;     // k-blocks per accumulation chunk
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte align the carve (swizzle atoms)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -1128,6 +1129,10 @@ rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams 
   const size_t smem = (size_t)stages * stage + 1024 + 8 * (3 * MAX_STAGES + 4) + 64;
   const int ctas_per_sm = smem <= 113 * 1024 ? 2 : 1;
   p.nbuf = (int)pow2_cols(2 * p.BN) * ctas_per_sm <= 512 ? 2 : 1;
+  static const int chunk_env = getenv("RNN_GEMM_CHUNK") ? atoi(getenv("RNN_GEMM_CHUNK")) : 0;
+  p.chunk_elems = (chunk_env > 0 ? chunk_env : CHUNK_ELEMS) / KB * KB;
+  if (p.chunk_elems < KB) p.chunk_elems = KB;
+  if (getenv("RNN_GEMM_NBUF1")) p.nbuf = 1;
   p.tmem_cols = pow2_cols(p.nbuf * p.BN);
   auto kern = p.BN <= 128 ? tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB, 4>
                           : tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB, 8>;

@@ -191,25 +191,45 @@ struct LeanOut {
   float* out;      // [n_seg, ldo]
   int64_t ldo;
   float beta;
-  EpiD epi;        // node epilogue fused into the store (epi.on == 0: none)
 };
 
+// the epilogue store lives out of line: its erf / residual code would otherwise inflate the
+// hot loop's register allocation (measured: 1 KB local-memory frames in every lean variant)
 template <int VEC>
-__device__ __forceinline__ void lean_store(const LeanOut& o, int64_t g, const float4 (&acc)[4]) {
+__device__ __noinline__ void lean_store_epi(const LeanOut& o, const EpiD* e, int64_t g, float4 a0,
+                                            float4 a1, float4 a2, float4 a3) {
+  const int lane = lane_id();
+  const float4 acc[4] = {a0, a1, a2, a3};
+#pragma unroll
+  for (int w = 0; w < VEC; ++w) {
+    float4* p = reinterpret_cast<float4*>(o.out + g * o.ldo) + lane + 32 * w;
+    float4 x = acc[w];
+    if (o.beta != 0.f) x = f4_fma(o.beta, *p, x);
+    *p = epi_apply4(*e, x, g, 4 * (lane + 32 * w));
+  }
+}
+
+template <int VEC, bool EPI = false>
+__device__ __forceinline__ void lean_store(const LeanOut& o, const EpiD* e, int64_t g,
+                                           const float4 (&acc)[4]) {
+  if constexpr (EPI) {
+    lean_store_epi<VEC>(o, e, g, acc[0], acc[1], acc[2], acc[3]);
+    return;
+  }
   const int lane = lane_id();
 #pragma unroll
   for (int w = 0; w < VEC; ++w) {
     float4* p = reinterpret_cast<float4*>(o.out + g * o.ldo) + lane + 32 * w;
     float4 x = acc[w];
     if (o.beta != 0.f) x = f4_fma(o.beta, *p, x);
-    if (o.epi.on) x = epi_apply4(o.epi, x, g, 4 * (lane + 32 * w));
     *p = x;
   }
 }
 
-template <int VEC>
-__device__ __noinline__ void lean_piece(const LeanOut& o, const RSCtx& cx, int64_t item, int64_t g,
-                                        float4 a0, float4 a1, float4 a2, float4 a3) {
+template <int VEC, bool EPI = false>
+__device__ __noinline__ void lean_piece(const LeanOut& o, const EpiD* e, const RSCtx& cx,
+                                        int64_t item, int64_t g, float4 a0, float4 a1, float4 a2,
+                                        float4 a3) {
   const int lane = lane_id();
   const float4 acc[4] = {a0, a1, a2, a3};
   float* mine = cx.partial + item * cx.pstride;
@@ -231,19 +251,24 @@ __device__ __noinline__ void lean_piece(const LeanOut& o, const RSCtx& cx, int64
   __threadfence();
   float4 tot[4];
   merge_pieces<VEC>(cx, i0, i1, tot);
-  lean_store<VEC>(o, g, tot);
+  lean_store<VEC, EPI>(o, e, g, tot);
 }
 
-// empty segments: the aggregate of an empty multiset is 0, so out = beta*out (+0)
-template <int VEC>
-__device__ __noinline__ void lean_zero(const LeanOut& o, int64_t g0, int64_t g1) {
-  if (o.beta != 0.f) return;
+// empty segments: the aggregate of an empty multiset is 0, so out = beta*out (+0) (then the
+// epilogue of 0)
+template <int VEC, bool EPI = false>
+__device__ __noinline__ void lean_zero(const LeanOut& o, const EpiD* e, int64_t g0, int64_t g1) {
+  if (o.beta != 0.f && !EPI) return;
   float4 z[4] = {f4_zero(), f4_zero(), f4_zero(), f4_zero()};
-  for (int64_t g = g0; g < g1; ++g) lean_store<VEC>(o, g, z);
+  for (int64_t g = g0; g < g1; ++g) lean_store<VEC, EPI>(o, e, g, z);
 }
 
-template <class MP, int VEC, int U, int MINB = 0>
-__global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOut o) {
+// EpiD e: the node epilogue of the EPI variant (a separate argument, so the plain variants
+// keep round 1's parameter layout and register allocation)
+template <class MP, int VEC, int U, int MINB = 0, bool EPI = false>
+__global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOut o, EpiD epi) {
+  const EpiD* ep = nullptr;
+  if constexpr (EPI) ep = &epi;
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (item >= cx.n_work) return;
   const int lane = lane_id();
@@ -273,7 +298,7 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
       while (gaps) {
         const int j = __ffs(gaps) - 1;
         gaps &= gaps - 1;
-        lean_zero<VEC>(o, __shfl_sync(FULL, gprev, j) + 1, __shfl_sync(FULL, gl, j));
+        lean_zero<VEC, EPI>(o, ep, __shfl_sync(FULL, gprev, j) + 1, __shfl_sync(FULL, gl, j));
       }
     }
     const unsigned ends = __ballot_sync(FULL, endf);
@@ -297,8 +322,8 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
           pending = true;
           if ((ends >> j) & 1u) {
             const int g = __shfl_sync(FULL, gl, j);
-            if (head_piece) lean_piece<VEC>(o, cx, item, g, acc[0], acc[1], acc[2], acc[3]);
-            else lean_store<VEC>(o, g, acc);
+            if (head_piece) lean_piece<VEC, EPI>(o, ep, cx, item, g, acc[0], acc[1], acc[2], acc[3]);
+            else lean_store<VEC, EPI>(o, ep, g, acc);
             head_piece = false;
             pending = false;
 #pragma unroll
@@ -309,8 +334,9 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
     }
     g_tail = __shfl_sync(FULL, gl, P - 1);
   }
-  if (pending) lean_piece<VEC>(o, cx, item, g_tail, acc[0], acc[1], acc[2], acc[3]);
-  if (cx.zero_empty && item == cx.n_work - 1) lean_zero<VEC>(o, cx.seg[cx.E - 1] + 1, cx.n_seg);
+  if (pending) lean_piece<VEC, EPI>(o, ep, cx, item, g_tail, acc[0], acc[1], acc[2], acc[3]);
+  if (cx.zero_empty && item == cx.n_work - 1)
+    lean_zero<VEC, EPI>(o, ep, cx.seg[cx.E - 1] + 1, cx.n_seg);
 }
 
 // (rows in flight, min CTAs per SM) of the VEC = 1 lean kernel; RNN_LEAN_VAR="U,B" selects
@@ -327,21 +353,37 @@ inline void lean_var(int* u, int* b) {
 }
 
 template <class MP, int VEC>
-rnn_status launch_lean(const MP& mp, RSCtx cx, const LeanOut& o, cudaStream_t st) {
+rnn_status launch_lean(const MP& mp, RSCtx cx, const LeanOut& o, cudaStream_t st,
+                       const EpiD& e = EpiD{}) {
   if (cx.n_work <= 0) return RNN_OK;
   constexpr int U = VEC == 1 ? 8 : (VEC == 2 ? 4 : 2);
   RNN_CUDA(cudaMemsetAsync(cx.counter, 0, sizeof(int) * cx.n_work, st));
   const unsigned grid = (unsigned)ceil_div(cx.n_work, 8);
   int vu = U, vb = 1;
   if (VEC == 1) lean_var(&vu, &vb);
-  if (VEC == 1 && vu == 8 && vb == 4) lean_kernel<MP, VEC, 8, 4><<<grid, 256, 0, st>>>(mp, cx, o);
-  else if (VEC == 1 && vu == 4 && vb == 4) lean_kernel<MP, VEC, 4, 4><<<grid, 256, 0, st>>>(mp, cx, o);
-  else if (VEC == 1 && vu == 8 && vb == 3) lean_kernel<MP, VEC, 8, 3><<<grid, 256, 0, st>>>(mp, cx, o);
-  else if (VEC == 1 && vu == 4 && vb == 6) lean_kernel<MP, VEC, 4, 6><<<grid, 256, 0, st>>>(mp, cx, o);
-  else if (VEC == 1 && vu == 4 && vb == 5) lean_kernel<MP, VEC, 4, 5><<<grid, 256, 0, st>>>(mp, cx, o);
-  else if (VEC == 1 && vu == 2 && vb == 6) lean_kernel<MP, VEC, 2, 6><<<grid, 256, 0, st>>>(mp, cx, o);
-  else if (VEC == 1 && vu == 6 && vb == 4) lean_kernel<MP, VEC, 6, 4><<<grid, 256, 0, st>>>(mp, cx, o);
-  else lean_kernel<MP, VEC, U><<<grid, 256, 0, st>>>(mp, cx, o);
+  if (e.on) {   // node epilogue fused into the store (RNN_LEAN_EPI_VAR="U,B": measurement)
+    static int ev[2] = {6, 4};
+    static bool einit = false;
+    if (!einit) {
+      if (const char* s = getenv("RNN_LEAN_EPI_VAR")) sscanf(s, "%d,%d", &ev[0], &ev[1]);
+      einit = true;
+    }
+    if (VEC == 1 && ev[0] == 8 && ev[1] == 0) lean_kernel<MP, VEC, 8, 0, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else if (VEC == 1 && ev[0] == 8 && ev[1] == 3) lean_kernel<MP, VEC, 8, 3, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else if (VEC == 1 && ev[0] == 4 && ev[1] == 4) lean_kernel<MP, VEC, 4, 4, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else if (VEC == 1) lean_kernel<MP, VEC, 6, 4, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else lean_kernel<MP, VEC, U, 0, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    RNN_LAUNCH_CHECK();
+    return RNN_OK;
+  }
+  if (VEC == 1 && vu == 8 && vb == 4) lean_kernel<MP, VEC, 8, 4><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else if (VEC == 1 && vu == 4 && vb == 4) lean_kernel<MP, VEC, 4, 4><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else if (VEC == 1 && vu == 8 && vb == 3) lean_kernel<MP, VEC, 8, 3><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else if (VEC == 1 && vu == 4 && vb == 6) lean_kernel<MP, VEC, 4, 6><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else if (VEC == 1 && vu == 4 && vb == 5) lean_kernel<MP, VEC, 4, 5><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else if (VEC == 1 && vu == 2 && vb == 6) lean_kernel<MP, VEC, 2, 6><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else if (VEC == 1 && vu == 6 && vb == 4) lean_kernel<MP, VEC, 6, 4><<<grid, 256, 0, st>>>(mp, cx, o, e);
+  else lean_kernel<MP, VEC, U><<<grid, 256, 0, st>>>(mp, cx, o, e);
   RNN_LAUNCH_CHECK();
   return RNN_OK;
 }

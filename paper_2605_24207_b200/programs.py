@@ -795,3 +795,116 @@ class HostStreamedSteps:
         for h, w in zip(self.out_host, self.outs):
             h.copy_(w, non_blocking=True)
         return self.out_host
+
+
+class MiniBatchLJA:
+    """Mini-batch streaming of one SUM/MEAN lifted join-aggregate whose source embeddings live
+    in (pinned) HOST memory -- the paper's future-work "scaling for memory" (PAPER.md:1028-1031:
+    relations beyond GPU memory, sampled / streamed in mini-batches).
+
+    The group keys (T) are split into batches of `batch_groups` keys.  Per batch, built once
+    (content caching): the E rows grouped into the batch, the source rows they reference S_b,
+    and a device join index over S_b x T_b (dense groups).  A step streams, batch by batch:
+        H2D   S_b's embedding rows (gathered into pinned staging on the host, copy stream)
+        LJA   out_b = agg over the batch's join rows                       (A3, librnn)
+        D2H   out_b into the host output
+    with batch b+1's copy in flight during batch b's compute, so the device holds two batches
+    of source rows, never the whole relation.  The backward streams dOut_b the same way and
+    adds each batch's source-gradient rows into a device (or host) gradient with
+    rnn_scatter_add_rows (rows of one batch are distinct; batches apply in order, so the
+    result is deterministic and equals the single-shot LJA's up to summation order)."""
+
+    def __init__(self, e_src, e_dst, s_key, t_key, z_host, agg="sum", batch_groups=65536,
+                 device="cuda", e_weight=None):
+        dev = self.device = torch.device(device)
+        self.agg = agg
+        e_src, e_dst = np.asarray(e_src, np.int64), np.asarray(e_dst, np.int64)
+        s_key, t_key = np.asarray(s_key, np.int64), np.asarray(t_key, np.int64)
+        self.z_host = z_host if isinstance(z_host, torch.Tensor) else torch.from_numpy(
+            np.ascontiguousarray(z_host, np.float32))
+        if not self.z_host.is_pinned():
+            self.z_host = self.z_host.pin_memory()
+        self.d = d = self.z_host.shape[1]
+        self.n_s = len(s_key)
+        t_sorted = np.sort(t_key)
+        s_order = np.argsort(s_key, kind="stable")
+        self.batches = []
+        max_rows = 1
+        for b0 in range(0, len(t_sorted), batch_groups):
+            tb = t_sorted[b0:b0 + batch_groups]
+            rows = np.isin(e_dst, tb)
+            es, ed = e_src[rows], e_dst[rows]
+            # the batch's source relation: referenced S keys (present in S), ascending
+            sk = np.unique(es)
+            pos = np.searchsorted(s_key[s_order], sk)
+            ok = (pos < len(s_key)) & (s_key[s_order][np.minimum(pos, len(s_key) - 1)] == sk)
+            sk = sk[ok]
+            srows = s_order[pos[ok]].astype(np.int64)          # rows of S in the host matrix
+            cu = lambda a: torch.as_tensor(a).to(dev)
+            idx = rnn.build_join_index(cu(es), cu(ed), cu(sk), cu(tb), dense_groups=True)
+            w = None
+            if e_weight is not None:
+                w = cu(np.asarray(e_weight, np.float32)[rows])
+            self.batches.append({"t_lo": b0, "n_t": len(tb), "idx": idx, "srows": srows,
+                                 "srows_dev": cu(srows.astype(np.int32)), "w": w})
+            max_rows = max(max_rows, len(srows))
+        self.n_t = len(t_sorted)
+        self.stage_h = [torch.empty(max_rows, d, dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.stage_d = [torch.empty(max_rows, d, dtype=torch.float32, device=dev) for _ in range(2)]
+        self.out_d = [torch.empty(batch_groups, (d + 3) // 4 * 4, dtype=torch.float32,
+                                  device=dev)[:, :d] for _ in range(2)]
+        self.copy = torch.cuda.Stream(device=dev)
+        self.ws = rnn.Workspace(dev)
+
+    def _query(self, b, z):
+        w = b["w"]
+        return rnn.make_query("src", self.agg, src=z, edge=w, edge_mode=rnn.BY_ROW)
+
+    def _stage(self, i, b):
+        """Gather batch b's source rows on the host and start their H2D copy (copy stream)."""
+        n = len(b["srows"])
+        torch.index_select(self.z_host, 0, torch.from_numpy(b["srows"]), out=self.stage_h[i][:n])
+        ev = torch.cuda.Event()
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_stream(torch.cuda.current_stream())
+            self.stage_d[i][:n].copy_(self.stage_h[i][:n], non_blocking=True)
+            ev.record(self.copy)
+        return ev
+
+    def forward(self, out_host=None):
+        """Streamed forward: returns the [n_t, d] output (host, T-key order)."""
+        out = out_host if out_host is not None else torch.empty(self.n_t, self.d).pin_memory()
+        cur = torch.cuda.current_stream()
+        nxt = self._stage(0, self.batches[0]) if self.batches else None
+        for k, b in enumerate(self.batches):
+            i = k & 1
+            cur.wait_event(nxt)
+            if k + 1 < len(self.batches):
+                nxt = self._stage(1 - i, self.batches[k + 1])
+            n = len(b["srows"])
+            z = self.stage_d[i][:n]
+            o = self.out_d[i][: b["n_t"]]
+            rnn.join_aggregate_fwd(b["idx"], self._query(b, z), out=o, ws=self.ws)
+            out[b["t_lo"]:b["t_lo"] + b["n_t"]].copy_(o, non_blocking=True)
+        torch.cuda.synchronize()
+        return out
+
+    def backward(self, d_out_host, d_src=None):
+        """Streamed source gradient: d_src [n_s, d] (device) = sum over batches of each batch's
+        LJA backward, scattered onto the batch's source rows."""
+        dev = self.device
+        d = self.d
+        if d_src is None:
+            d_src = torch.zeros(self.n_s, d, dtype=torch.float32, device=dev)
+        dout_d = torch.empty(max(b["n_t"] for b in self.batches), d, dtype=torch.float32, device=dev)
+        for k, b in enumerate(self.batches):
+            n = len(b["srows"])
+            ev = self._stage(0, b)
+            dout_d[: b["n_t"]].copy_(d_out_host[b["t_lo"]:b["t_lo"] + b["n_t"]], non_blocking=True)
+            torch.cuda.current_stream().wait_event(ev)
+            q = self._query(b, self.stage_d[0][:n])
+            g = rnn.join_aggregate_bwd(b["idx"], q, dout_d[: b["n_t"]], want_edge=False,
+                                       want_dst=False, ws=self.ws)["src"]
+            rnn.scatter_add_rows(d_src, g[:n], b["srows_dev"])
+            torch.cuda.synchronize()
+        return d_src

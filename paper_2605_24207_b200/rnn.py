@@ -113,6 +113,13 @@ def lib():
         L.rnn_accumulate.argtypes = [vp, i64, vp, i64, i64, i32, C.c_float, vp]
         L.rnn_accumulate.restype = C.c_int
         L.rnn_gather_rows.argtypes = [vp, i64, vp, i64, vp, i64, i32, vp]
+        L.rnn_build_join_index_sel.argtypes = [vp, vp, vp, i64, vp, i64, vp, i64, C.c_int, i64,
+                                               C.POINTER(JoinIndexC), vp, C.POINTER(sz), vp]
+        L.rnn_select_mask.argtypes = [vp, i32, i64, i32, C.c_double, i32, vp, vp]
+        L.rnn_build_join_index_sel.restype = C.c_int
+        L.rnn_select_mask.restype = C.c_int
+        L.rnn_scatter_add_rows.argtypes = [vp, i64, vp, i64, vp, i64, i32, vp]
+        L.rnn_scatter_add_rows.restype = C.c_int
         L.rnn_softmax_xent_workspace_size.argtypes = [i64, C.POINTER(sz)]
         L.rnn_softmax_xent.argtypes = [vp, i64, i32, i64, vp, vp, vp, i64, vp, sz, vp]
         L.rnn_adam_tick.argtypes = [vp, vp]
@@ -229,8 +236,9 @@ class JoinIndex:
 
 def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, validate=False,
                      within_group_by_src_key=False, transpose=True, dense_groups=False,
-                     rows_per_item=0, stream=None) -> JoinIndex:
-    """rnn_build_join_index: phase 1 (sizes, SYNC), allocate, phase 2 (fill)."""
+                     rows_per_item=0, stream=None, e_mask=None) -> JoinIndex:
+    """rnn_build_join_index: phase 1 (sizes, SYNC), allocate, phase 2 (fill).  e_mask (uint8
+    per E row, device): the selection sigma(E) pushed into the probe (rnn_build_join_index_sel)."""
     L = lib()
     e_dst_key = _cuda(e_dst_key, torch.int64, "e_dst_key").contiguous()
     dev = e_dst_key.device
@@ -253,11 +261,20 @@ def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, valida
         e_dst_key = torch.zeros(1, dtype=torch.int64, device=dev)
     idx = JoinIndexC()
     wsb = C.c_size_t(0)
-    args = (_ptr(e_src_key), _ptr(e_dst_key), n_e, _ptr(src_key), n_s, _ptr(dst_key), n_t, flags,
-            rows_per_item)
-    _check(L.rnn_build_join_index(*args, C.byref(idx), None, C.byref(wsb), _stream(stream)))
+    if e_mask is not None:
+        e_mask = _cuda(e_mask, torch.uint8, "e_mask").contiguous()
+        if n_e == 0:
+            e_mask = torch.zeros(1, dtype=torch.uint8, device=dev)
+        args = (_ptr(e_src_key), _ptr(e_dst_key), _ptr(e_mask), n_e, _ptr(src_key), n_s,
+                _ptr(dst_key), n_t, flags, rows_per_item)
+        fn = L.rnn_build_join_index_sel
+    else:
+        args = (_ptr(e_src_key), _ptr(e_dst_key), n_e, _ptr(src_key), n_s, _ptr(dst_key), n_t,
+                flags, rows_per_item)
+        fn = L.rnn_build_join_index
+    _check(fn(*args, C.byref(idx), None, C.byref(wsb), _stream(stream)))
     ws = _ws(wsb.value, dev)
-    _check(L.rnn_build_join_index(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
+    _check(fn(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
     nj, ng = idx.n_join_rows, idx.n_groups
     i64 = dict(dtype=torch.int64, device=dev)
     i32 = dict(dtype=torch.int32, device=dev)
@@ -692,3 +709,32 @@ class Adam:
             _check(lib().rnn_adam(_ptr(p), p.shape[0], p.shape[1], p.stride(0), _ptr(g),
                                   g.stride(0), _ptr(m), _ptr(v), C.byref(self.cfg), _ptr(self.t),
                                   _stream(stream)))
+
+
+# ------------------------------------------------------------------------------------------
+# selection sigma pushdown
+# ------------------------------------------------------------------------------------------
+SELECT_OPS = {"==": 0, "!=": 1, "<": 2, "<=": 3, ">": 4, ">=": 5}
+
+
+def select_mask(attr, op, value, mask=None, combine="set", stream=None):
+    """mask[j] (uint8) = attr[j] <op> value, or AND / OR-ed into an existing mask
+    (rnn_select_mask); attr int64 or float32 per E row (device)."""
+    n = attr.numel()
+    dtype = 0 if attr.dtype == torch.int64 else 1 if attr.dtype == torch.float32 else None
+    if dtype is None:
+        raise TypeError("attr must be int64 or float32")
+    if mask is None:
+        mask = torch.empty(max(n, 1), dtype=torch.uint8, device=attr.device)[:n]
+    _check(lib().rnn_select_mask(_ptr(attr.contiguous()), dtype, n, SELECT_OPS[op], float(value),
+                                 {"set": 0, "and": 1, "or": 2}[combine], _ptr(mask),
+                                 _stream(stream)))
+    return mask
+
+
+def scatter_add_rows(y, x, idx, stream=None):
+    """y[idx[i]] += x[i] (distinct idx within the call; rnn_scatter_add_rows)."""
+    n, cols = x.shape
+    _check(lib().rnn_scatter_add_rows(_ptr(y), y.stride(0), _ptr(x), x.stride(0), _ptr(idx), n,
+                                      cols, _stream(stream)))
+    return y

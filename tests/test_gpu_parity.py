@@ -438,6 +438,8 @@ def test_max_aggregate_parity(R, ora, D, wmode, dense):
     position), empty dense groups 0 / -1, and the backward to the arg-max rows only."""
     rng = np.random.default_rng(D + 3 * (wmode or 0))
     db = make_case(rng, n_s=300, n_t=200, n_e=6000, d=4)
+    # T keys 100..139 get no join row (empty dense groups)
+    db["e_dst"] = np.where(np.isin(db["e_dst"], db["t_key"][100:140]), db["t_key"][0], db["e_dst"])
     gi = R.build_join_index(cu(db["e_src"]), cu(db["e_dst"]), cu(db["s_key"]), cu(db["t_key"]),
                             dense_groups=dense)
     oi = ora.build_join_index(db["e_src"], db["e_dst"], db["s_key"], db["t_key"])
