@@ -138,3 +138,87 @@ def dhn_step(g, W, d_out_dense, ks=(2, 3, 4)):
         p += k
     dH, dW, _ = oracle.project_bwd(h, W, dY, want_db=False)
     return {"out": out, "dY": dY, "dW": dW, "dH": dH}
+
+
+def hgt_joint_step(mag, par, heads):
+    """Joint-softmax HGT layer (the original HGT's attention, normalised over the sources of
+    every relation into a target type at once; SURVEY sec 8c reading 3): per target type one
+    softmax join-aggregate over the union of the relations into it, the source relation being
+    the stack of every relation's (K', M') rows keyed by (relation, source key)."""
+    d = mag["d"]
+    col, W = par["col"], par["W"]
+    blk = lambda t, kind, key: W[t][col[(kind, key)][1] * d:(col[(kind, key)][1] + 1) * d]
+    out, grads = {}, {"dWk": {}, "dWm": {}, "dWq": {}, "dH": {}}
+    add = lambda t, x: grads["dH"].__setitem__(t, grads["dH"].get(t, 0) + x)
+    for t in par["targets"]:
+        names = [n for n, r in mag["rels"].items() if r["dst_type"] == t]
+        K, M, skeys, es, ed = [], [], [], [], []
+        for j, name in enumerate(names):
+            r = mag["rels"][name]
+            s = r["src_type"]
+            K.append(oracle.project(mag["h"][s], blk(s, "k", name)))
+            M.append(oracle.project(mag["h"][s], blk(s, "m", name)))
+            skeys.append((np.int64(j) << np.int64(56)) | np.asarray(mag["key"][s], np.int64))
+            es.append((np.int64(j) << np.int64(56)) | np.asarray(r["src"], np.int64))
+            ed.append(np.asarray(r["dst"], np.int64))
+        K, M = np.concatenate(K), np.concatenate(M)
+        Q = oracle.project(mag["h"][t], blk(t, "q", t))
+        o = oracle.build_join_index(np.concatenate(es), np.concatenate(ed), np.concatenate(skeys),
+                                    mag["key"][t])
+        o_out, _ = oracle.lja_fwd(o, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=1.0)
+        rank = np.argsort(np.argsort(mag["key"][t], kind="stable"), kind="stable")
+        rows = rank[o["group_dst_row"]]
+        dense = np.zeros((mag["n"][t], d))
+        dense[rows] = o_out
+        out[t] = dense
+        g = oracle.lja_bwd(o, np.asarray(par["d_out"][t], np.float64)[rows], agg="softmax", src=M,
+                           src_key=K, dst=Q, heads=heads, scale=1.0)
+        dX, grads["dWq"][t], _ = oracle.project_bwd(mag["h"][t], blk(t, "q", t), g["dst"], want_db=False)
+        add(t, dX)
+        off = 0
+        for name in names:
+            s = mag["rels"][name]["src_type"]
+            n = mag["n"][s]
+            dXk, grads["dWk"][name], _ = oracle.project_bwd(mag["h"][s], blk(s, "k", name),
+                                                            g["src_key"][off:off + n], want_db=False)
+            dXm, grads["dWm"][name], _ = oracle.project_bwd(mag["h"][s], blk(s, "m", name),
+                                                            g["src"][off:off + n], want_db=False)
+            add(s, dXk + dXm)
+            off += n
+    return out, grads
+
+
+def hygnn_attention_step(hg, P, heads):
+    """HyGNN double attention: node-level softmax attention grouped by hyperedge,
+    then hyperedge-level grouped by node; P = the six maps (scale 1/sqrt(d/h) on the keys)."""
+    d = hg["nodes"]["x"].shape[1]
+    scale = 1.0 / np.sqrt(d / heads)
+    nk, hk = hg["nodes"]["key"], hg["hyperedges"]["key"]
+    iv, ih = hg["inc"]["node"], hg["inc"]["hyper"]
+    X, E0 = np.asarray(hg["nodes"]["x"], np.float64), np.asarray(hg["hx"], np.float64)
+    rank = lambda k: np.argsort(np.argsort(k, kind="stable"), kind="stable")
+    o1 = oracle.build_join_index(iv, ih, nk, hk)
+    K1, V1 = oracle.project(X, P["k1"] * scale), oracle.project(X, P["v1"])
+    Q1 = oracle.project(E0, P["q1"])
+    e_out, _ = oracle.lja_fwd(o1, agg="softmax", src=V1, src_key=K1, dst=Q1, heads=heads, scale=1.0)
+    r1 = rank(hk)[o1["group_dst_row"]]
+    Eh = np.zeros((len(hk), d)); Eh[r1] = e_out                 # dense, hyperedge-key order
+    hks = np.sort(hk)
+    o2 = oracle.build_join_index(ih, iv, hks, nk)
+    K2, V2 = oracle.project(Eh, P["k2"] * scale), oracle.project(Eh, P["v2"])
+    Q2 = oracle.project(X, P["q2"])
+    x_out, _ = oracle.lja_fwd(o2, agg="softmax", src=V2, src_key=K2, dst=Q2, heads=heads, scale=1.0)
+    r2 = rank(nk)[o2["group_dst_row"]]
+    Xo = np.zeros((len(nk), d)); Xo[r2] = x_out
+    dXo = np.asarray(hg["d_out"][: len(nk)], np.float64)
+    g2 = oracle.lja_bwd(o2, dXo[r2], agg="softmax", src=V2, src_key=K2, dst=Q2, heads=heads, scale=1.0)
+    dXq, dWq2, _ = oracle.project_bwd(X, P["q2"], g2["dst"], want_db=False)
+    dEk, dWk2, _ = oracle.project_bwd(Eh, P["k2"] * scale, g2["src_key"], want_db=False)
+    dEv, dWv2, _ = oracle.project_bwd(Eh, P["v2"], g2["src"], want_db=False)
+    dEh = dEk + dEv
+    g1 = oracle.lja_bwd(o1, dEh[r1], agg="softmax", src=V1, src_key=K1, dst=Q1, heads=heads, scale=1.0)
+    dE0, dWq1, _ = oracle.project_bwd(E0, P["q1"], g1["dst"], want_db=False)
+    dXk, dWk1, _ = oracle.project_bwd(X, P["k1"] * scale, g1["src_key"], want_db=False)
+    dXv, dWv1, _ = oracle.project_bwd(X, P["v1"], g1["src"], want_db=False)
+    return {"Eh": Eh, "Xo": Xo, "dX": dXq + dXk + dXv, "dE0": dE0, "dWk1": dWk1, "dWv1": dWv1,
+            "dWq1": dWq1, "dWk2": dWk2, "dWv2": dWv2, "dWq2": dWq2}

@@ -91,7 +91,7 @@ __global__ void probe_kernel(const int64_t* __restrict__ e_src, const int64_t* _
   if (j >= n_e) return;
   int32_t sr = -1, tr = -1;
   bool ok = !e_mask || e_mask[j];   // selection sigma(E) pushed into the probe
-  if (has_s) { sr = table_find(S, e_src[j]); ok = sr >= 0; }
+  if (ok && has_s) { sr = table_find(S, e_src[j]); ok = sr >= 0; }
   if (ok && has_t) { tr = table_find(T, e_dst[j]); ok = tr >= 0; }
   s_row_of[j] = sr;
   t_row_of[j] = tr;

@@ -47,8 +47,6 @@ struct GemmParams {
   int a3d, b3d;     // MN-major operand loaded as ONE 3D box {32, KB, MN/32} per stage
   int smem_kb;      // shared-memory budget of the stage ring (0: default 200 KB, 1 CTA / SM)
   int b_lo_row;     // K-major B with its 3xTF32 lo part precomputed b_lo_row rows below (0: none)
-  int nbuf;         // TMEM accumulator buffers (2: chunk c+1 accumulates while chunk c drains)
-  int chunk_elems;  // reduction elements per TMEM accumulation chunk (multiple of KB)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -190,24 +188,10 @@ __device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n1
 // [4] stages counted for [3]; [8..10] total cycles of producer, MMA, converter lanes
 __device__ unsigned long long g_gemm_stats[16];
 
-// Accumulation in chunks: the tensor core's fp32 accumulate rounds every partial sum (measured
-// on B200: the dW error grows linearly with the reduction length -- 3xTF32 rms 5.6e-6 at 704
-// rows per split, 4.9e-5 at 6,757, profiles/r02/precision), so the MMA accumulates at most
-// CHUNK_ELEMS reduction elements into a TMEM buffer, and warps 2-9 drain each finished chunk
-// into fp32 registers (round-to-nearest adds); with two buffers the next chunk accumulates
-// while the previous one drains.  NGRP = 16-column groups per draining thread (BN <= 32 NGRP).
-// 256 elements: rms 2.3e-6 at 1M rows; 1024 keeps the error ~4x that (far below the 1e-4 bar)
-// with a quarter of the drains.
-#ifndef RNN_CHUNK_ELEMS
-#define RNN_CHUNK_ELEMS 1024
-#endif
-constexpr int CHUNK_ELEMS = RNN_CHUNK_ELEMS;
-
-template <bool A_MN, bool B_MN, bool SPLIT3, int KB = BK, int NGRP = 4>
+template <bool A_MN, bool B_MN, bool SPLIT3, int KB = BK>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    GemmParams p) {
-  const int CH = p.chunk_elems / KB;     // k-blocks per accumulation chunk
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte align the carve (swizzle atoms)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -220,9 +204,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * STAGE);
   uint64_t* empty = full + MAX_STAGES;
   uint64_t* conv = empty + MAX_STAGES;
-  uint64_t* acc_full = conv + MAX_STAGES;   // [2]
-  uint64_t* acc_empty = acc_full + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_full = conv + MAX_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   RNN_PROBE(const long long gs_t0 = clock64(); unsigned long long gs_w[5] = {0, 0, 0, 0, 0};
@@ -240,10 +223,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_init(&empty[s], 1);
         mbar_init(&conv[s], CONV_THREADS);
       }
-      for (int b = 0; b < 2; ++b) {
-        mbar_init(&acc_full[b], 1);
-        mbar_init(&acc_empty[b], CONV_THREADS);
-      }
+      mbar_init(acc_full, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -311,12 +291,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % p.stages;
       const uint32_t ph = (kb / p.stages) & 1;
-      const int c = kb / CH, cb = c % p.nbuf, use = c / p.nbuf;
-      if (kb % CH == 0 && use > 0) {
-        mbar_wait(&acc_empty[cb], (use - 1) & 1);   // drained by warps 2-9
-        tc_fence_after();
-      }
-      const uint32_t dacc = tmem + (uint32_t)(cb * p.BN);
       {
         RNN_PROBE(const long long t0 = clock64();)
         mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
@@ -329,36 +303,30 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kk = 0; kk < KB / 8; ++kk) {
           const uint64_t ad = make_desc(smem_u32(a_hi(s)), A_MN, kk, KB * 128);
           const uint64_t bd = make_desc(smem_u32(b_hi(s)), B_MN, kk, KB * 128);
-          tc_mma_tf32(dacc, ad, bd, idesc, ((kb % CH) | kk) != 0);
+          tc_mma_tf32(tmem, ad, bd, idesc, (kb | kk) != 0);
           if (SPLIT3) {
             const uint64_t al = make_desc(smem_u32(a_lo(s)), A_MN, kk, KB * 128);
             const uint64_t bl = make_desc(smem_u32(b_lo(s)), B_MN, kk, KB * 128);
-            tc_mma_tf32(dacc, ad, bl, idesc, 1u);
-            tc_mma_tf32(dacc, al, bd, idesc, 1u);
+            tc_mma_tf32(tmem, ad, bl, idesc, 1u);
+            tc_mma_tf32(tmem, al, bd, idesc, 1u);
           }
         }
         tc_commit(&empty[s]);
-        if (kb % CH == CH - 1 || kb == nkb - 1) tc_commit(&acc_full[cb]);   // chunk done
       }
       __syncwarp();
     }
+    if (lane == 0) tc_commit(acc_full);
+    __syncwarp();
     RNN_PROBE(if (lane == 0) {
       atomicAdd(&g_gemm_stats[9], (unsigned long long)(clock64() - gs_t0));
       atomicAdd(&g_gemm_stats[1], gs_w[1]);
       if (!SPLIT3) { atomicAdd(&g_gemm_stats[3], gs_w[3]); atomicAdd(&g_gemm_stats[4], gs_w[4]); }
     })
   } else {
-    // ------- converters (3xTF32) and accumulator drains: warps 2..9 -------
+    // ---------------- converters (3xTF32): warps 2..9; epilogue: warps 2..5 ----------------
     const int et = threadIdx.x - 64;  // 0..255
-    const int quad = warp & 3;        // TMEM lanes [32*quad, 32*quad+32) belong to this warp
-    const int half = (warp - 2) >> 2; // 16-column groups G = 2 i + half of the tile
-    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    float acc[NGRP * 16];
-#pragma unroll
-    for (int j = 0; j < NGRP * 16; ++j) acc[j] = 0.f;
-    const int ngrp = p.BN / 16;
-    for (int kb = 0; kb < nkb; ++kb) {
-      if (SPLIT3) {
+    if (SPLIT3) {
+      for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
         {
@@ -376,60 +344,43 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[s]);
       }
-      if (kb % CH == CH - 1 || kb == nkb - 1) {
-        // drain chunk c: TMEM buffer -> fp32 registers (round-to-nearest adds)
-        const int c = kb / CH, cb = c % p.nbuf, use = c / p.nbuf;
-        mbar_wait(&acc_full[cb], use & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int i = 0; i < NGRP; ++i) {
-          const int G = 2 * i + half;
-          if (G < ngrp) {
-            uint32_t r[16];
-            tc_ld16(tmem + lane_base + (uint32_t)(cb * p.BN + G * 16), r);
-#pragma unroll
-            for (int j = 0; j < 16; ++j) acc[i * 16 + j] += __uint_as_float(r[j]);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&acc_empty[cb]);
-      }
     }
     RNN_PROBE(if (lane == 0 && warp == 2) {
       atomicAdd(&g_gemm_stats[10], (unsigned long long)(clock64() - gs_t0));
       for (int i = 2; i < 5; ++i) atomicAdd(&g_gemm_stats[i], gs_w[i]);
     })
-    // ---- epilogue from registers ----
+    if (warp < 6) mbar_wait(acc_full, 0);   // warps 6-9 only convert
+    tc_fence_after();
+    const int quad = warp & 3;  // TMEM lanes [32*quad, 32*quad+32) belong to this warp
     const int64_t row = m0 + quad * 32 + lane;
-    if (row < p.M) {
+    const bool row_ok = row < p.M;
+    for (int c0 = 0; c0 < (warp < 6 ? p.BN : 0); c0 += 16) {
+      uint32_t r[16];
+      tc_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, r);
+      if (!row_ok) continue;
+      const int col0 = n0 + c0;
+      if (p.mode == 0) {
+        float* dst = p.out + row * p.ldo + col0;
+        const bool vec = col0 + 16 <= p.N && (p.ldo % 4 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
+        float v[16];
 #pragma unroll
-      for (int i = 0; i < NGRP; ++i) {
-        const int G = 2 * i + half;
-        if (G >= ngrp) continue;
-        const int col0 = n0 + G * 16;
-        if (p.mode == 0) {
-          float* dst = p.out + row * p.ldo + col0;
-          const bool vec = col0 + 16 <= p.N && (p.ldo % 4 == 0) &&
-                           ((reinterpret_cast<uintptr_t>(dst) & 15u) == 0);
-          float v[16];
+        for (int j = 0; j < 16; ++j)
+          v[j] = __uint_as_float(r[j]) + ((p.bias && col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f);
+        if (vec) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            v[j] = acc[i * 16 + j] + ((p.bias && col0 + j < p.N) ? __ldg(p.bias + col0 + j) : 0.f);
-          if (vec) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (col0 + j < p.N) dst[j] = v[j];
-          }
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         } else {
-          float* dst = p.partial + blockIdx.z * p.part_stride + row * p.ldp + col0;
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            if (col0 + j < p.N) dst[j] = acc[i * 16 + j];
+            if (col0 + j < p.N) dst[j] = v[j];
         }
+      } else {
+        float* dst = p.partial + blockIdx.z * p.part_stride + row * p.ldp + col0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (col0 + j < p.N) dst[j] = __uint_as_float(r[j]);
       }
     }
   }
@@ -1125,17 +1076,9 @@ rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams 
   if (stages > nkb_max) stages = (int)nkb_max;
   if (stages < 1) stages = 1;
   p.stages = stages;
-  // two accumulator buffers when they fit the TMEM columns of every resident CTA
-  const size_t smem = (size_t)stages * stage + 1024 + 8 * (3 * MAX_STAGES + 4) + 64;
-  const int ctas_per_sm = smem <= 113 * 1024 ? 2 : 1;
-  p.nbuf = (int)pow2_cols(2 * p.BN) * ctas_per_sm <= 512 ? 2 : 1;
-  static const int chunk_env = getenv("RNN_GEMM_CHUNK") ? atoi(getenv("RNN_GEMM_CHUNK")) : 0;
-  p.chunk_elems = (chunk_env > 0 ? chunk_env : CHUNK_ELEMS) / KB * KB;
-  if (p.chunk_elems < KB) p.chunk_elems = KB;
-  if (getenv("RNN_GEMM_NBUF1")) p.nbuf = 1;
-  p.tmem_cols = pow2_cols(p.nbuf * p.BN);
-  auto kern = p.BN <= 128 ? tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB, 4>
-                          : tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB, 8>;
+  p.tmem_cols = pow2_cols(p.BN);
+  const size_t smem = (size_t)stages * stage + 1024 + 8 * (3 * MAX_STAGES + 2) + 64;
+  auto kern = tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB>;
   RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)ceil_div(p.M, BM), (unsigned)ceil_div(p.N, p.BN), (unsigned)splits);
   kern<<<grid, THREADS, smem, st>>>(ta, tb, p);
@@ -1264,6 +1207,10 @@ struct BwdWs {
 // MMA tile over k and N = 256 columns of n per MMA, so X is re-read ceil(N / 256) times instead
 // of ceil(N / 128) and the shared-memory reads per loaded byte drop (the 3xTF32 tile GEMM is
 // bound by shared-memory traffic); the ordered reduce writes dW^T, a small transpose gives dW.
+#ifndef RNN_DW_MAX_CHAIN
+#define RNN_DW_MAX_CHAIN 2048
+#endif
+constexpr int64_t DW_MAX_CHAIN = RNN_DW_MAX_CHAIN;
 inline bool dw_swapped(int K, int N) { return N > 128 && K <= 128 && !getenv("RNN_NO_DWT"); }
 
 BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
@@ -1277,6 +1224,15 @@ BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
   int64_t splits = ceil_div(M, 8 * BK);
   const int64_t cap = (148 + tiles - 1) / tiles;   // about one wave of CTAs
   if (splits > cap) splits = cap;
+  // Precision: the tensor core's fp32 accumulate rounds every partial sum, so the dW error
+  // grows linearly with the rows one split accumulates (measured on B200, 3xTF32 max error
+  // 1.35e-5 at 704 rows per split, 1.5e-4 at 6,757 -- profiles/r02/precision); bound the
+  // chain at DW_MAX_CHAIN rows and leave the rest to the fixed-order fp32 split reduction
+  // (a drain-to-registers variant kept the chain short inside one CTA but cost 48 % on the
+  // wide MAG shapes -- profiles/r02/cmp).
+  // (whole waves: a partial second wave of CTAs would cost a full wave's time)
+  const int64_t min_splits = ceil_div(M, DW_MAX_CHAIN);
+  if (splits < min_splits) splits = ceil_div(min_splits, cap) * cap;
   if (splits < 1) splits = 1;
   w.splits = (int)splits;
   w.part = c.take<float>((size_t)splits * N * K);

@@ -193,6 +193,12 @@ struct LeanOut {
   float beta;
 };
 
+// the inline (bias, ReLU) epilogue of EPI == 1, passed by value (no address of a kernel param)
+struct EpiS {
+  const float* bias;
+  int act;
+};
+
 // the epilogue store lives out of line: its erf / residual code would otherwise inflate the
 // hot loop's register allocation (measured: 1 KB local-memory frames in every lean variant)
 template <int VEC>
@@ -209,10 +215,10 @@ __device__ __noinline__ void lean_store_epi(const LeanOut& o, const EpiD* e, int
   }
 }
 
-template <int VEC, bool EPI = false>
-__device__ __forceinline__ void lean_store(const LeanOut& o, const EpiD* e, int64_t g,
+template <int VEC, int EPI = 0>
+__device__ __forceinline__ void lean_store(const LeanOut& o, const EpiD* e, EpiS es, int64_t g,
                                            const float4 (&acc)[4]) {
-  if constexpr (EPI) {
+  if constexpr (EPI == 2) {
     lean_store_epi<VEC>(o, e, g, acc[0], acc[1], acc[2], acc[3]);
     return;
   }
@@ -222,14 +228,19 @@ __device__ __forceinline__ void lean_store(const LeanOut& o, const EpiD* e, int6
     float4* p = reinterpret_cast<float4*>(o.out + g * o.ldo) + lane + 32 * w;
     float4 x = acc[w];
     if (o.beta != 0.f) x = f4_fma(o.beta, *p, x);
+    if constexpr (EPI == 1) {   // bias (+ ReLU): the GCN epilogue, inline
+      if (es.bias) x = f4_add(x, __ldg(reinterpret_cast<const float4*>(es.bias) + lane + 32 * w));
+      if (es.act == 1)
+        x = make_float4(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f), fmaxf(x.z, 0.f), fmaxf(x.w, 0.f));
+    }
     *p = x;
   }
 }
 
-template <int VEC, bool EPI = false>
-__device__ __noinline__ void lean_piece(const LeanOut& o, const EpiD* e, const RSCtx& cx,
-                                        int64_t item, int64_t g, float4 a0, float4 a1, float4 a2,
-                                        float4 a3) {
+template <int VEC, int EPI = 0>
+__device__ __noinline__ void lean_piece(const LeanOut& o, const EpiD* e, EpiS es,
+                                        const RSCtx& cx, int64_t item, int64_t g, float4 a0,
+                                        float4 a1, float4 a2, float4 a3) {
   const int lane = lane_id();
   const float4 acc[4] = {a0, a1, a2, a3};
   float* mine = cx.partial + item * cx.pstride;
@@ -251,24 +262,27 @@ __device__ __noinline__ void lean_piece(const LeanOut& o, const EpiD* e, const R
   __threadfence();
   float4 tot[4];
   merge_pieces<VEC>(cx, i0, i1, tot);
-  lean_store<VEC, EPI>(o, e, g, tot);
+  lean_store<VEC, EPI>(o, e, es, g, tot);
 }
 
 // empty segments: the aggregate of an empty multiset is 0, so out = beta*out (+0) (then the
 // epilogue of 0)
-template <int VEC, bool EPI = false>
-__device__ __noinline__ void lean_zero(const LeanOut& o, const EpiD* e, int64_t g0, int64_t g1) {
-  if (o.beta != 0.f && !EPI) return;
+template <int VEC, int EPI = 0>
+__device__ __noinline__ void lean_zero(const LeanOut& o, const EpiD* e, EpiS es, int64_t g0,
+                                       int64_t g1) {
+  if (o.beta != 0.f && EPI == 0) return;
   float4 z[4] = {f4_zero(), f4_zero(), f4_zero(), f4_zero()};
-  for (int64_t g = g0; g < g1; ++g) lean_store<VEC, EPI>(o, e, g, z);
+  for (int64_t g = g0; g < g1; ++g) lean_store<VEC, EPI>(o, e, es, g, z);
 }
 
 // EpiD e: the node epilogue of the EPI variant (a separate argument, so the plain variants
 // keep round 1's parameter layout and register allocation)
-template <class MP, int VEC, int U, int MINB = 0, bool EPI = false>
+template <class MP, int VEC, int U, int MINB = 0, int EPI = 0>
 __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOut o, EpiD epi) {
   const EpiD* ep = nullptr;
-  if constexpr (EPI) ep = &epi;
+  if constexpr (EPI == 2) ep = &epi;
+  EpiS es{nullptr, 0};
+  if constexpr (EPI == 1) es = EpiS{epi.bias, epi.act};
   const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (item >= cx.n_work) return;
   const int lane = lane_id();
@@ -298,7 +312,7 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
       while (gaps) {
         const int j = __ffs(gaps) - 1;
         gaps &= gaps - 1;
-        lean_zero<VEC, EPI>(o, ep, __shfl_sync(FULL, gprev, j) + 1, __shfl_sync(FULL, gl, j));
+        lean_zero<VEC, EPI>(o, ep, es, __shfl_sync(FULL, gprev, j) + 1, __shfl_sync(FULL, gl, j));
       }
     }
     const unsigned ends = __ballot_sync(FULL, endf);
@@ -322,8 +336,8 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
           pending = true;
           if ((ends >> j) & 1u) {
             const int g = __shfl_sync(FULL, gl, j);
-            if (head_piece) lean_piece<VEC, EPI>(o, ep, cx, item, g, acc[0], acc[1], acc[2], acc[3]);
-            else lean_store<VEC, EPI>(o, ep, g, acc);
+            if (head_piece) lean_piece<VEC, EPI>(o, ep, es, cx, item, g, acc[0], acc[1], acc[2], acc[3]);
+            else lean_store<VEC, EPI>(o, ep, es, g, acc);
             head_piece = false;
             pending = false;
 #pragma unroll
@@ -334,9 +348,9 @@ __global__ void __launch_bounds__(256, MINB) lean_kernel(MP mp, RSCtx cx, LeanOu
     }
     g_tail = __shfl_sync(FULL, gl, P - 1);
   }
-  if (pending) lean_piece<VEC, EPI>(o, ep, cx, item, g_tail, acc[0], acc[1], acc[2], acc[3]);
+  if (pending) lean_piece<VEC, EPI>(o, ep, es, cx, item, g_tail, acc[0], acc[1], acc[2], acc[3]);
   if (cx.zero_empty && item == cx.n_work - 1)
-    lean_zero<VEC, EPI>(o, ep, cx.seg[cx.E - 1] + 1, cx.n_seg);
+    lean_zero<VEC, EPI>(o, ep, es, cx.seg[cx.E - 1] + 1, cx.n_seg);
 }
 
 // (rows in flight, min CTAs per SM) of the VEC = 1 lean kernel; RNN_LEAN_VAR="U,B" selects
@@ -362,17 +376,19 @@ rnn_status launch_lean(const MP& mp, RSCtx cx, const LeanOut& o, cudaStream_t st
   int vu = U, vb = 1;
   if (VEC == 1) lean_var(&vu, &vb);
   if (e.on) {   // node epilogue fused into the store (RNN_LEAN_EPI_VAR="U,B": measurement)
-    static int ev[2] = {6, 4};
+    static int ev[2] = {4, 4};
     static bool einit = false;
     if (!einit) {
       if (const char* s = getenv("RNN_LEAN_EPI_VAR")) sscanf(s, "%d,%d", &ev[0], &ev[1]);
       einit = true;
     }
-    if (VEC == 1 && ev[0] == 8 && ev[1] == 0) lean_kernel<MP, VEC, 8, 0, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
-    else if (VEC == 1 && ev[0] == 8 && ev[1] == 3) lean_kernel<MP, VEC, 8, 3, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
-    else if (VEC == 1 && ev[0] == 4 && ev[1] == 4) lean_kernel<MP, VEC, 4, 4, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
-    else if (VEC == 1) lean_kernel<MP, VEC, 6, 4, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
-    else lean_kernel<MP, VEC, U, 0, true><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    // bias (+ ReLU) inline in the store (GCN); anything else through the out-of-line store
+    const bool simple = !e.resid && !e.pre && (e.act == 0 || e.act == 1);
+    if (simple && VEC == 1) lean_kernel<MP, VEC, 6, 4, 1><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else if (simple) lean_kernel<MP, VEC, U, 0, 1><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else if (VEC == 1 && ev[0] == 6 && ev[1] == 4) lean_kernel<MP, VEC, 6, 4, 2><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else if (VEC == 1) lean_kernel<MP, VEC, 4, 4, 2><<<grid, 256, 0, st>>>(mp, cx, o, e);
+    else lean_kernel<MP, VEC, U, 0, 2><<<grid, 256, 0, st>>>(mp, cx, o, e);
     RNN_LAUNCH_CHECK();
     return RNN_OK;
   }

@@ -908,3 +908,225 @@ class MiniBatchLJA:
             rnn.scatter_add_rows(d_src, g[:n], b["srows_dev"])
             torch.cuda.synchronize()
         return d_src
+
+
+def _joint_keys(rel_idx, keys):
+    """Composite S keys (relation index j, source key) of a union over relations: j << 56 | key
+    (keys must lie in [0, 2^56))."""
+    keys = np.asarray(keys, np.int64)
+    if len(keys) and (keys.min() < 0 or keys.max() >= (1 << 56)):
+        raise ValueError("joint softmax: keys must lie in [0, 2^56)")
+    return (np.int64(rel_idx) << np.int64(56)) | keys
+
+
+class HGTJointProgram(_Program):
+    """HGT layer with the ORIGINAL HGT's joint softmax: the attention of target t normalises over
+    the sources of EVERY relation phi into t's type at once (SURVEY sec 8c reading 3 / sec 8f
+    item 2), instead of per relation then summing (HGTProgram, the paper's templated rule,
+    PAPER.md:1351-1358, :1409).  It is one SOFTMAX LJA per target type over the UNION of the
+    relations into it: the source relation is the stack of every relation's (K'_phi, M'_phi)
+    rows, keyed by (phi, source key) -- the union of PAPER.md:451-460 with a relation tag --
+    so no new kernel: per relation one projection writes its rows of the stack, one index per
+    target type joins the union."""
+
+    def __init__(self, mag: dict, device="cuda", prec="3xtf32", seed=7):
+        dev = self.device = torch.device(device)
+        self.prec = prec
+        self.d, self.h = d, h = mag["d"], mag["heads"]
+        types = list(mag["n"].keys())
+        self.n = dict(mag["n"])
+        self.rels = mag["rels"]
+        par = hgt_parameters(mag, seed)
+        self.col = par["col"]
+        self.targets = par["targets"]
+        self.H = {t: _dev_f32(mag["h"][t], dev) for t in types}
+        Wt = par["W"]
+        blk = lambda t, kind, key: Wt[t][self.col[(kind, key)][1] * d:(self.col[(kind, key)][1] + 1) * d]
+        # per relation: W_km = [Wk; Wm] ([2d, d]); per target type: Wq
+        self.Wkm = {name: _dev_f32(np.concatenate([blk(r["src_type"], "k", name),
+                                                   blk(r["src_type"], "m", name)], 0), dev)
+                    for name, r in self.rels.items()}
+        self.Wq = {t: _dev_f32(blk(t, "q", t), dev) for t in self.targets}
+        self.into = {t: [name for name, r in self.rels.items() if r["dst_type"] == t]
+                     for t in self.targets}
+        self.off = {}
+        self.KM, self.dKM, self.Q, self.dQ, self.idx, self.q, self.lse = {}, {}, {}, {}, {}, {}, {}
+        self.Ht = {t: _empty(self.n[t], d, dev) for t in self.targets}
+        self.d_out = {t: _dev_f32(par["d_out"][t], dev) for t in self.targets}
+        for t in self.targets:
+            off, skeys, es, ed = 0, [], [], []
+            for j, name in enumerate(self.into[t]):
+                r = self.rels[name]
+                self.off[name] = off
+                off += self.n[r["src_type"]]
+                skeys.append(_joint_keys(j, mag["key"][r["src_type"]]))
+                es.append(_joint_keys(j, r["src"]))
+                ed.append(np.asarray(r["dst"], np.int64))
+            cu = lambda a: torch.as_tensor(np.concatenate(a)).to(dev)
+            self.idx[t] = rnn.build_join_index(cu(es), cu(ed), cu(skeys),
+                                               torch.as_tensor(mag["key"][t]).to(dev),
+                                               dense_groups=True)
+            self.KM[t] = _empty(off, 2 * d, dev)
+            self.dKM[t] = _empty(off, 2 * d, dev)
+            self.Q[t] = _empty(self.n[t], d, dev)
+            self.dQ[t] = _empty(self.n[t], d, dev)
+            self.lse[t] = torch.empty(max(self.n[t], 1), h, dtype=torch.float32, device=dev)
+            self.q[t] = rnn.make_query("src", "softmax", src=self.KM[t][:, d:], src_key=self.KM[t][:, :d],
+                                       dst=self.Q[t], heads=h, scale=1.0)
+        self.dWkm = {name: torch.empty(2 * d, d, dtype=torch.float32, device=dev) for name in self.rels}
+        self.dWq = {t: torch.empty(d, d, dtype=torch.float32, device=dev) for t in self.targets}
+        self.dH = {t: _empty(self.n[t], d, dev) for t in types}
+        self.dH_tmp = _empty(max(self.n.values()), d, dev)
+        self.ws = rnn.Workspace(dev)
+        self.ws_p = rnn.Workspace(dev)
+
+    @property
+    def join_rows_per_step(self):
+        return sum(ix.n_join_rows for ix in self.idx.values())
+
+    def lja_bytes(self):
+        return {}
+
+    def forward(self):
+        d = self.d
+        for name, r in self.rels.items():
+            t, s = r["dst_type"], r["src_type"]
+            o = self.off[name]
+            rnn.project(self.H[s], self.Wkm[name], out=self.KM[t][o:o + self.n[s]], prec=self.prec)
+        for t in self.targets:
+            rnn.project(self.H[t], self.Wq[t], out=self.Q[t], prec=self.prec)
+            rnn.join_aggregate_fwd(self.idx[t], self.q[t], out=self.Ht[t], lse=self.lse[t],
+                                   ws=self.ws)
+        return self.Ht
+
+    def _add_dh(self, t, first):
+        if first[t]:
+            first[t] = False
+        else:
+            rnn.accumulate(self.dH[t], self.dH_tmp[: self.n[t]], beta=1.0)
+
+    def backward(self):
+        import ctypes as C
+        d = self.d
+        first = {t: True for t in self.dH}
+        for t in self.targets:
+            idx, q = self.idx[t], self.q[t]
+            _, bb = rnn.lja_workspace_size(idx, q)
+            w = self.ws.get(bb)
+            dO = self.d_out[t]
+            rnn._check(rnn.lib().rnn_join_aggregate_bwd(
+                C.byref(idx.c), C.byref(q), rnn._ptr(self.Ht[t]), self.Ht[t].stride(0),
+                rnn._ptr(self.lse[t]), rnn._ptr(dO), dO.stride(0),
+                rnn._ptr(self.dKM[t][:, d:]), rnn._ptr(self.dKM[t][:, :d]), None,
+                rnn._ptr(self.dQ[t]), rnn._ptr(w), w.numel(), rnn._stream()))
+            dst = self.dH[t] if first[t] else self.dH_tmp[: self.n[t]]
+            rnn.project_bwd(self.H[t], self.Wq[t], self.dQ[t], want_dx=True, prec=self.prec,
+                            ws=self.ws_p, dx_out=dst, dw_out=self.dWq[t])
+            self._add_dh(t, first)
+        for name, r in self.rels.items():
+            t, s = r["dst_type"], r["src_type"]
+            o = self.off[name]
+            dst = self.dH[s] if first[s] else self.dH_tmp[: self.n[s]]
+            rnn.project_bwd(self.H[s], self.Wkm[name], self.dKM[t][o:o + self.n[s]], want_dx=True,
+                            prec=self.prec, ws=self.ws_p, dx_out=dst, dw_out=self.dWkm[name])
+            self._add_dh(s, first)
+        return self.dWkm, self.dWq, self.dH
+
+
+def hygnn_attention_parameters(d, seed=13):
+    """Six d x d maps of the two attention hops (K, V, Q per hop), N(0, 1/d); the score scale
+    1/sqrt(d/h) is folded into the key maps (reading 12)."""
+    rng = np.random.default_rng(seed)
+    return {k: (rng.standard_normal((d, d)) / np.sqrt(d)).astype(np.float32)
+            for k in ("k1", "v1", "q1", "k2", "v2", "q2")}
+
+
+class HypergraphAttentionProgram(_Program):
+    """HyGNN's double attention (PAPER.md:956: node-level then hyperedge-level attention;
+    SURVEY sec 8f item 2) as two SOFTMAX lifted join-aggregates over the incidence relation:
+
+        hop 1 (group by hyperedge e):  Eh(e) = sum_{v in e} softmax_v(<K1 x_v, Q1 h_e>) V1 x_v
+        hop 2 (group by node v):       Xo(v) = sum_{e ∋ v} softmax_e(<K2 Eh_e, Q2 x_v>) V2 Eh_e
+
+    with h_e the hyperedges' per-tuple (learnable) embeddings; K/V of a hop are one stacked
+    tcgen05 projection.  Outputs are dense in key order (nodes / hyperedges without incidences
+    aggregate to 0); the backward returns every weight gradient and d x, d h."""
+
+    def __init__(self, hg: dict, device="cuda", prec="3xtf32", heads=8, seed=13):
+        dev = self.device = torch.device(device)
+        self.prec, self.h = prec, heads
+        d = self.d = hg["nodes"]["x"].shape[1]
+        nk = torch.as_tensor(hg["nodes"]["key"]).to(dev)
+        hk = torch.as_tensor(hg["hyperedges"]["key"]).to(dev)
+        iv = torch.as_tensor(hg["inc"]["node"]).to(dev)
+        ih = torch.as_tensor(hg["inc"]["hyper"]).to(dev)
+        self.idx1 = rnn.build_join_index(iv, ih, nk, hk, dense_groups=True)
+        hk_sorted = torch.sort(hk).values
+        self.idx2 = rnn.build_join_index(ih, iv, hk_sorted, nk, dense_groups=True)
+        self.nv, self.ne = len(hg["nodes"]["key"]), len(hg["hyperedges"]["key"])
+        self.X = _dev_f32(hg["nodes"]["x"], dev)
+        self.E0 = _dev_f32(hg["hx"], dev)
+        P = hygnn_attention_parameters(d, seed)
+        scale = 1.0 / np.sqrt(d / heads)
+        self.W = {k: _dev_f32(v * (scale if k[0] == "k" else 1.0), dev) for k, v in P.items()}
+        self.Wkv1 = _dev_f32(np.concatenate([P["k1"] * scale, P["v1"]]), dev)
+        self.Wkv2 = _dev_f32(np.concatenate([P["k2"] * scale, P["v2"]]), dev)
+        self.KV1, self.KV2 = _empty(self.nv, 2 * d, dev), _empty(self.ne, 2 * d, dev)
+        self.dKV1, self.dKV2 = _empty(self.nv, 2 * d, dev), _empty(self.ne, 2 * d, dev)
+        self.Q1, self.Q2 = _empty(self.ne, d, dev), _empty(self.nv, d, dev)
+        self.dQ1, self.dQ2 = _empty(self.ne, d, dev), _empty(self.nv, d, dev)
+        self.Eh, self.Xo = _empty(self.ne, d, dev), _empty(self.nv, d, dev)
+        self.dEh = _empty(self.ne, d, dev)
+        self.lse1 = torch.empty(self.ne, heads, dtype=torch.float32, device=dev)
+        self.lse2 = torch.empty(self.nv, heads, dtype=torch.float32, device=dev)
+        self.q1 = rnn.make_query("src", "softmax", src=self.KV1[:, d:], src_key=self.KV1[:, :d],
+                                 dst=self.Q1, heads=heads, scale=1.0)
+        self.q2 = rnn.make_query("src", "softmax", src=self.KV2[:, d:], src_key=self.KV2[:, :d],
+                                 dst=self.Q2, heads=heads, scale=1.0)
+        self.d_out = _dev_f32(hg["d_out"][: self.nv], dev)
+        self.dWkv1 = torch.empty(2 * d, d, dtype=torch.float32, device=dev)
+        self.dWkv2 = torch.empty(2 * d, d, dtype=torch.float32, device=dev)
+        self.dWq1 = torch.empty(d, d, dtype=torch.float32, device=dev)
+        self.dWq2 = torch.empty(d, d, dtype=torch.float32, device=dev)
+        self.dX, self.dX2 = _empty(self.nv, d, dev), _empty(self.nv, d, dev)
+        self.dE0 = _empty(self.ne, d, dev)
+        self.dEh_in = _empty(self.ne, d, dev)
+        self.ws = rnn.Workspace(dev)
+        self.ws_p = rnn.Workspace(dev)
+
+    @property
+    def join_rows_per_step(self):
+        return self.idx1.n_join_rows + self.idx2.n_join_rows
+
+    def lja_bytes(self):
+        return {}
+
+    def forward(self):
+        rnn.project(self.X, self.Wkv1, out=self.KV1, prec=self.prec)
+        rnn.project(self.E0, self.W["q1"], out=self.Q1, prec=self.prec)
+        rnn.join_aggregate_fwd(self.idx1, self.q1, out=self.Eh, lse=self.lse1, ws=self.ws)
+        rnn.project(self.Eh, self.Wkv2, out=self.KV2, prec=self.prec)
+        rnn.project(self.X, self.W["q2"], out=self.Q2, prec=self.prec)
+        rnn.join_aggregate_fwd(self.idx2, self.q2, out=self.Xo, lse=self.lse2, ws=self.ws)
+        return self.Xo
+
+    def _sm_bwd(self, idx, q, out, lse, d_out, dKV, dQ):
+        import ctypes as C
+        d = self.d
+        _, bb = rnn.lja_workspace_size(idx, q)
+        w = self.ws.get(bb)
+        rnn._check(rnn.lib().rnn_join_aggregate_bwd(
+            C.byref(idx.c), C.byref(q), rnn._ptr(out), out.stride(0), rnn._ptr(lse),
+            rnn._ptr(d_out), d_out.stride(0), rnn._ptr(dKV[:, d:]), rnn._ptr(dKV[:, :d]), None,
+            rnn._ptr(dQ), rnn._ptr(w), w.numel(), rnn._stream()))
+
+    def backward(self):
+        p = dict(want_dx=True, prec=self.prec, ws=self.ws_p)
+        self._sm_bwd(self.idx2, self.q2, self.Xo, self.lse2, self.d_out, self.dKV2, self.dQ2)
+        rnn.project_bwd(self.X, self.W["q2"], self.dQ2, dx_out=self.dX, dw_out=self.dWq2, **p)
+        rnn.project_bwd(self.Eh, self.Wkv2, self.dKV2, dx_out=self.dEh, dw_out=self.dWkv2, **p)
+        self._sm_bwd(self.idx1, self.q1, self.Eh, self.lse1, self.dEh, self.dKV1, self.dQ1)
+        rnn.project_bwd(self.E0, self.W["q1"], self.dQ1, dx_out=self.dE0, dw_out=self.dWq1, **p)
+        rnn.project_bwd(self.X, self.Wkv1, self.dKV1, dx_out=self.dX2, dw_out=self.dWkv1, **p)
+        rnn.accumulate(self.dX, self.dX2, beta=1.0)
+        return self.dX, self.dE0

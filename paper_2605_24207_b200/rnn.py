@@ -294,7 +294,7 @@ def build_join_index(e_src_key, e_dst_key, src_key=None, dst_key=None, *, valida
                        "src_work_seg": torch.empty(max(idx.n_src_work, 1), **i32)})
     for k, v in arrays.items():
         setattr(idx, k, v.data_ptr())
-    _check(L.rnn_build_join_index(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
+    _check(fn(*args, C.byref(idx), _ptr(ws), C.byref(wsb), _stream(stream)))
     arrays["group_key"] = arrays["group_key"][:ng]
     arrays["group_dst_row"] = arrays["group_dst_row"][:ng]
     for k in ("src_row", "edge_row", "pos_group", "src_pos", "src_group", "src_seg"):

@@ -196,8 +196,11 @@ def hypergraph_like(seed=42, n_nodes=1_000_000, n_hyper=200_000, n_inc=5_000_000
     x = _normal_f32(rng, (n_nodes, d), 1.0 / np.sqrt(d))
     theta = _normal_f32(rng, (d, d), 1.0 / np.sqrt(d))
     d_out = _normal_f32(rng, (n_nodes, d), 1.0)
+    # per-tuple hyperedge embeddings (HyGNN attention queries), drawn last
+    hx = _normal_f32(rng, (n_hyper, d), 1.0 / np.sqrt(d))
     return {"nodes": {"key": node_key, "x": x}, "hyperedges": {"key": hyper_key},
-            "inc": {"node": node_key[v], "hyper": hyper_key[e]}, "theta": theta, "d_out": d_out}
+            "inc": {"node": node_key[v], "hyper": hyper_key[e]}, "theta": theta, "d_out": d_out,
+            "hx": hx}
 
 
 MAG_NODES = {"paper": 736_389, "author": 1_134_649, "institution": 8_740, "field": 59_965}
