@@ -348,7 +348,8 @@ def run_ours(args):
         return float(np.mean(v)) if v else None
 
     model = first["model"]
-    per = {k: kernel_ms(k) for k in ["proj_fwd", "proj_bwd", "allgather", "reduce_scatter"] + list(model)}
+    per = {k: kernel_ms(k) for k in ["proj_fwd", "proj_bwd", "epi_bwd", "allgather", "reduce_scatter"]
+           + list(model)}
     n_steps = args.steps * len(seeds)
 
     # ---- roofline of the dominant hot-path kernel (the fused LJA) ----

@@ -66,6 +66,10 @@ def lib():
         L.ora_softmax_xent.argtypes = [PD, C.c_int64, C.c_int, C.c_int64, P64, PD, PD]
         L.ora_adam.argtypes = [PD, PD, PD, PD, C.c_int64, C.c_double, C.c_double, C.c_double,
                                C.c_double, C.c_double, C.c_int64]
+        L.ora_rgcn_fwd.argtypes = [P64, C.c_int64, P32, P32, P32, P32, C.c_int, PD, C.c_int64,
+                                   C.c_int, PD, C.c_int, PD, C.c_int64]
+        L.ora_rgcn_bwd.argtypes = [P64, C.c_int64, P32, P32, P32, P32, C.c_int, PD, C.c_int64,
+                                   C.c_int64, C.c_int, PD, C.c_int, PD, C.c_int64, PD, PD]
         L.ora_build_join_index.argtypes = [P64, P64, C.c_int64, P64, C.c_int64, P64, C.c_int64,
                                            C.c_int, P64, P64, P64, P64, P32, P32, P32, P64, P32]
         L.ora_lja_fwd.argtypes = [P64, C.c_int64, P32, P32, P32, C.c_int, C.c_int, C.c_int,
@@ -381,3 +385,33 @@ def adam(p, g, m, v, lr, t, b1=0.9, b2=0.999, eps=1e-8, wd=0.0):
     _check(lib().ora_adam(_p(p, PD), _p(gg, PD), _p(m, PD), _p(v, PD), p.size, lr, b1, b2, eps,
                           wd, t))
     return p, m, v
+
+
+def rgcn_fwd(idx, rel, x, W):
+    """R-GCN layer with per-join-row W_rel x_s (no pushdown): W [n_rel + 1, d_out, d_in]
+    (W[0] self-loop); rel int per E row.  Returns out [G, d_out]."""
+    x, W = _f64(x), np.ascontiguousarray(W, np.float64)
+    n_rel = W.shape[0] - 1
+    d_out, d_in = W.shape[1], W.shape[2]
+    G = idx["n_groups"]
+    out = np.zeros((max(G, 1), d_out))
+    _check(lib().ora_rgcn_fwd(_p(idx["group_ptr"], P64), G, _p(_i32(idx["src_row"]), P32),
+                              _p(_i32(idx["edge_row"]), P32), _p(_i32(idx["group_dst_row"]), P32),
+                              _p(_i32(rel), P32), n_rel, _p(x, PD), x.shape[1], d_in, _p(W, PD),
+                              d_out, _p(out, PD), d_out))
+    return out[:G]
+
+
+def rgcn_bwd(idx, rel, x, W, d_out):
+    """(d_x [n, d_in], d_W [n_rel + 1, d_out, d_in]) of rgcn_fwd."""
+    x, W, d_out = _f64(x), np.ascontiguousarray(W, np.float64), _f64(d_out)
+    n_rel = W.shape[0] - 1
+    do, di = W.shape[1], W.shape[2]
+    dx = np.zeros((max(x.shape[0], 1), di))
+    dW = np.zeros(W.shape)
+    _check(lib().ora_rgcn_bwd(_p(idx["group_ptr"], P64), idx["n_groups"],
+                              _p(_i32(idx["src_row"]), P32), _p(_i32(idx["edge_row"]), P32),
+                              _p(_i32(idx["group_dst_row"]), P32), _p(_i32(rel), P32), n_rel,
+                              _p(x, PD), x.shape[1], x.shape[0], di, _p(W, PD), do, _p(d_out, PD),
+                              d_out.shape[1], _p(dx, PD), _p(dW, PD)))
+    return dx[: x.shape[0]], dW

@@ -151,6 +151,17 @@ int ora_softmax_xent(const double* logits, int64_t n, int C, int64_t ld, const i
 int ora_adam(double* p, const double* g, double* m, double* v, int64_t n, double lr, double b1,
              double b2, double eps, double wd, int64_t t);
 
+/* R-GCN layer, per-join-row transform W_rel x_s with no pushdown:
+ * out[g] = W0 x_t + sum_p c_p W_{rel(p)} x_{s(p)}, c_p = 1 / (rows of g with p's relation). */
+int ora_rgcn_fwd(const int64_t* group_ptr, int64_t n_groups, const int32_t* src_row,
+                 const int32_t* edge_row, const int32_t* group_dst_row, const int32_t* rel,
+                 int n_rel, const double* x, int64_t ldx, int d_in, const double* W, int d_out,
+                 double* out, int64_t ld_out);
+int ora_rgcn_bwd(const int64_t* group_ptr, int64_t n_groups, const int32_t* src_row,
+                 const int32_t* edge_row, const int32_t* group_dst_row, const int32_t* rel,
+                 int n_rel, const double* x, int64_t ldx, int64_t n_x, int d_in, const double* W,
+                 int d_out, const double* d_out_g, int64_t ld_dout, double* d_x, double* d_W);
+
 /* Multi-GPU ownership: owner(key) = splitmix64(key ^ seed) mod P. */
 int ora_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed, int32_t* owner);
 uint64_t ora_splitmix64(uint64_t x);

@@ -155,3 +155,81 @@ int ora_adam(double* p, const double* g, double* m, double* v, int64_t n, double
   }
   return ORA_OK;
 }
+
+/* R-GCN layer with per-join-row transformations, NO pushdown (the per-row T_tau of the join rule,
+ * PAPER.md:444; R-GCN PAPER.md:890, :897 -- one weight matrix per relation type):
+ *   out[g] = W0 x[t_g] + sum over join rows p of group g of  c_p W_{rel_p} x[s_p],
+ *   c_p = 1 / |{p' in g : rel_p' = rel_p}|   (R-GCN's per-relation neighbour normalisation)
+ * W [n_rel + 1][d_out][d_in] (W[0] = the self-loop map, W[1 + r] relation r's), x [n, ld_x].
+ * Every join row's W_rel x_s is formed and added in double, then the self term. */
+int ora_rgcn_fwd(const int64_t* group_ptr, int64_t n_groups, const int32_t* src_row,
+                 const int32_t* edge_row, const int32_t* group_dst_row, const int32_t* rel,
+                 int n_rel, const double* x, int64_t ldx, int d_in, const double* W, int d_out,
+                 double* out, int64_t ld_out) {
+  int64_t* cnt = (int64_t*)calloc((size_t)(n_rel > 0 ? n_rel : 1), sizeof(int64_t));
+  if (!cnt) return ORA_ERR_NOMEM;
+  for (int64_t g = 0; g < n_groups; ++g) {
+    double* o = out + g * ld_out;
+    for (int k = 0; k < n_rel; ++k) cnt[k] = 0;
+    for (int64_t p = group_ptr[g]; p < group_ptr[g + 1]; ++p) {
+      const int r = rel[edge_row[p]];
+      if (r < 0 || r >= n_rel) { free(cnt); return ORA_ERR_BAD_ARG; }
+      cnt[r] += 1;
+    }
+    const double* xt = x + (int64_t)group_dst_row[g] * ldx;
+    for (int i = 0; i < d_out; ++i) {
+      double acc = 0.0;
+      for (int k = 0; k < d_in; ++k) acc += W[(size_t)i * d_in + k] * xt[k];
+      o[i] = acc;
+    }
+    for (int64_t p = group_ptr[g]; p < group_ptr[g + 1]; ++p) {
+      const int r = rel[edge_row[p]];
+      const double c = 1.0 / (double)cnt[r];
+      const double* Wr = W + (size_t)(1 + r) * d_out * d_in;
+      const double* xs = x + (int64_t)src_row[p] * ldx;
+      for (int i = 0; i < d_out; ++i) {
+        double y = 0.0;                      /* tau_p: W_rel x_s for this join row */
+        for (int k = 0; k < d_in; ++k) y += Wr[(size_t)i * d_in + k] * xs[k];
+        o[i] += c * y;
+      }
+    }
+  }
+  free(cnt);
+  return ORA_OK;
+}
+
+/* backward of ora_rgcn_fwd: d_x [n, d_in] and d_W [(n_rel + 1) d_out d_in], both written. */
+int ora_rgcn_bwd(const int64_t* group_ptr, int64_t n_groups, const int32_t* src_row,
+                 const int32_t* edge_row, const int32_t* group_dst_row, const int32_t* rel,
+                 int n_rel, const double* x, int64_t ldx, int64_t n_x, int d_in, const double* W,
+                 int d_out, const double* d_out_g, int64_t ld_dout, double* d_x, double* d_W) {
+  int64_t* cnt = (int64_t*)calloc((size_t)(n_rel > 0 ? n_rel : 1), sizeof(int64_t));
+  if (!cnt) return ORA_ERR_NOMEM;
+  memset(d_x, 0, sizeof(double) * (size_t)(n_x * d_in));
+  memset(d_W, 0, sizeof(double) * (size_t)(n_rel + 1) * d_out * d_in);
+  for (int64_t g = 0; g < n_groups; ++g) {
+    const double* dO = d_out_g + g * ld_dout;
+    for (int k = 0; k < n_rel; ++k) cnt[k] = 0;
+    for (int64_t p = group_ptr[g]; p < group_ptr[g + 1]; ++p) cnt[rel[edge_row[p]]] += 1;
+    const int64_t t = group_dst_row[g];
+    for (int i = 0; i < d_out; ++i)
+      for (int k = 0; k < d_in; ++k) {
+        d_W[(size_t)i * d_in + k] += dO[i] * x[t * ldx + k];
+        d_x[t * d_in + k] += W[(size_t)i * d_in + k] * dO[i];
+      }
+    for (int64_t p = group_ptr[g]; p < group_ptr[g + 1]; ++p) {
+      const int r = rel[edge_row[p]];
+      const double c = 1.0 / (double)cnt[r];
+      const double* Wr = W + (size_t)(1 + r) * d_out * d_in;
+      double* dWr = d_W + (size_t)(1 + r) * d_out * d_in;
+      const int64_t s = src_row[p];
+      for (int i = 0; i < d_out; ++i)
+        for (int k = 0; k < d_in; ++k) {
+          dWr[(size_t)i * d_in + k] += c * dO[i] * x[s * ldx + k];
+          d_x[s * d_in + k] += c * Wr[(size_t)i * d_in + k] * dO[i];
+        }
+    }
+  }
+  free(cnt);
+  return ORA_OK;
+}

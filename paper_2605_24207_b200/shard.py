@@ -70,6 +70,80 @@ class ShardPlan:
         self.e_dst = e_dst[mine]
 
 
+class HaloPlan:
+    """Halo-only exchange of a hash-partitioned source relation (SURVEY sec 8e "Mitigations":
+    every rank receives only the rows its join rows reference, not the whole relation;
+    0.44x the all-gather rows at P = 8 on arxiv).  Built identically on every rank from the
+    global relation (host, numpy, setup time).
+
+    Rank r's source relation S_r = [its owned keys, padded to n_pad | halo keys it needs from
+    rank q, q = 0..P-1, q != r, each ascending] -- its join index is built over S_r once.
+      send_idx  int32 [sum_q send_counts[q]]: rows of r's owned block sent to q, q ascending
+      send_counts[q] = |need(r <- ... q wants from r)|, recv_counts[q] = |need(q -> r)|"""
+
+    def __init__(self, owned, n_pad, referenced, rank):
+        P = len(owned)
+        self.P, self.rank, self.n_pad = P, rank, n_pad
+        pos = [{int(k): i for i, k in enumerate(o)} for o in owned]
+        need = [[np.intersect1d(referenced[q], owned[o], assume_unique=True) if o != q
+                 else np.zeros(0, np.int64) for o in range(P)] for q in range(P)]
+        # need[q][o] = keys rank q needs from owner o
+        self.recv_counts = [len(need[rank][o]) for o in range(P)]
+        self.send_counts = [len(need[q][rank]) for q in range(P)]
+        self.send_idx = np.concatenate([np.array([pos[rank][int(k)] for k in need[q][rank]],
+                                                 np.int32) for q in range(P)]) \
+            if sum(self.send_counts) else np.zeros(0, np.int32)
+        self.halo_keys = np.concatenate([need[rank][o] for o in range(P)]) \
+            if sum(self.recv_counts) else np.zeros(0, np.int64)
+        self.n_halo = len(self.halo_keys)
+        # bytes moved per exchanged row set, against the all-gather's (P - 1) n_pad rows
+        self.rows_recv = int(sum(self.recv_counts))
+        self.rows_allgather = (P - 1) * n_pad
+
+    def s_keys(self, own_block_keys):
+        return np.concatenate([own_block_keys, self.halo_keys])
+
+
+def _all_to_all_rows(out, x, out_splits, in_splits, group=None):
+    """all_to_all_single over rows; backends without it for device tensors (gloo + CUDA, the
+    1-GPU functional tests) exchange through host copies."""
+    try:
+        dist.all_to_all_single(out, x, output_split_sizes=out_splits, input_split_sizes=in_splits,
+                               group=group)
+    except (RuntimeError, NotImplementedError):
+        o = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_to_all_single(o, x.cpu(), output_split_sizes=out_splits,
+                               input_split_sizes=in_splits, group=group)
+        out.copy_(o)
+
+
+def halo_exchange_fwd(be, plan, Zs, send_buf, group=None):
+    """Zs [n_pad + n_halo, d]: rows [:n_pad] are this rank's own (filled); the halo rows are
+    received from their owners (all_to_all_single of the gathered send rows)."""
+    n_pad = plan.n_pad
+    if plan.P == 1 or not dist.is_initialized():
+        return
+    if len(plan.send_idx):
+        be.gather_rows(send_buf, Zs[:n_pad], plan.send_idx_dev)
+    _all_to_all_rows(Zs[n_pad:], send_buf, plan.recv_counts, plan.send_counts, group)
+
+
+def halo_exchange_bwd(be, plan, dZs, back_buf, group=None):
+    """dZs [n_pad + n_halo, d]: partial source gradients of own and halo rows; the halo rows'
+    partials go back to their owners and are added onto the owned rows they came from (one
+    scatter per destination: rows within one destination's list are distinct -> no collisions,
+    fixed order -> deterministic).  Leaves the result in dZs[:n_pad]."""
+    n_pad = plan.n_pad
+    if plan.P == 1 or not dist.is_initialized():
+        return
+    _all_to_all_rows(back_buf, dZs[n_pad:], plan.send_counts, plan.recv_counts, group)
+    off = 0
+    for q, c in enumerate(plan.send_counts):
+        if c:
+            be.scatter_add_rows(dZs[:n_pad], back_buf[off:off + c], plan.send_idx_dev[off:off + c])
+        off += c
+
+
 def all_gather_rows(out, x, group=None):
     """out[P * n, d] <- concat over ranks of x[n, d] (contiguous tensors)."""
     if not dist.is_initialized():
@@ -108,7 +182,8 @@ class ShardedGCNProgram:
     backend: the compute primitives (``RnnBackend`` = librnn.so on this rank's GPU; the CPU
     tests plug in an fp64 backend built from the oracle to check the sharding logic)."""
 
-    def __init__(self, graph: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32"):
+    def __init__(self, graph: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32",
+                 halo=True):
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
@@ -117,6 +192,14 @@ class ShardedGCNProgram:
         keys = np.asarray(nodes["key"], np.int64)
         owner = be.hash_partition(keys, self.P, seed)
         plan = self.plan = ShardPlan(keys, edges["src"], edges["dst"], owner, self.P, self.rank)
+        # halo exchange (default): only the referenced source rows cross the links
+        self.halo = None
+        if halo and self.P > 1:
+            e_src, e_dst = np.asarray(edges["src"], np.int64), np.asarray(edges["dst"], np.int64)
+            o_dst = _owner_of(keys, owner, e_dst)
+            referenced = [np.intersect1d(np.unique(e_src[o_dst == q]), keys) for q in range(self.P)]
+            self.halo = HaloPlan(plan.owned_keys, plan.n_pad, referenced, self.rank)
+            self.halo.send_idx_dev = be.index_i32(self.halo.send_idx)
         # layer widths padded to a multiple of 4 (rnn_project / the LJA need ld % 4 == 0 and
         # the collectives contiguous rows): W, features and d_out are zero-padded, so padded
         # columns stay exactly 0 and the real columns are unchanged (Cora: 1,433 -> 16 -> 7)
@@ -125,13 +208,27 @@ class ShardedGCNProgram:
         self.L = len(self.dims) - 1
         n_pad, P = plan.n_pad, self.P
         self.n_own = int(plan.counts[self.rank])
-        self.idx = be.build_index(plan.e_src, plan.e_dst, plan.s_keys, plan.my_keys)
+        r0 = self.rank * n_pad
+        if self.halo is not None:
+            s_keys = self.halo.s_keys(plan.s_keys[r0:r0 + n_pad])
+        else:
+            s_keys = plan.s_keys
+        self.n_s = len(s_keys)
+        self.idx = be.build_index(plan.e_src, plan.e_dst, s_keys, plan.my_keys)
         assert be.n_groups(self.idx) == self.n_own, "every owned node needs a self-loop"
-        # normalisation: deg(s) from its owner (all-gathered group sizes)
+        # normalisation: deg(s) from its owner (all-gathered group sizes, setup time)
+        own_idx = be.build_index(plan.e_src, plan.e_dst, plan.s_keys, plan.my_keys) \
+            if self.halo is not None else self.idx
         own_deg = be.zeros_i32(n_pad)
-        be.group_sizes(self.idx, own_deg)
+        be.group_sizes(own_idx, own_deg)
         all_deg = be.zeros_i32(P * n_pad)
         all_gather_rows(all_deg, own_deg, group)
+        if self.halo is not None:
+            # S-row degrees of the halo layout: own block, then every halo key's owner row
+            pos = {int(k): i for i, k in enumerate(plan.s_keys)}
+            rows = np.concatenate([np.arange(r0, r0 + n_pad),
+                                   [pos[int(k)] for k in self.halo.halo_keys]]).astype(np.int64)
+            all_deg = all_deg[torch.as_tensor(rows, device=all_deg.device)].contiguous()
         self.w = be.gcn_norm_src_deg(self.idx, all_deg)
         # activations (rows >= n_own stay zero: padding of the gathered blocks)
         x0 = np.zeros((n_pad, dp[0]), np.float32)
@@ -144,8 +241,11 @@ class ShardedGCNProgram:
             Wp.append(be.tensor(wp))
         self.W = Wp
         self.Z = [be.zeros(n_pad, dp[l + 1]) for l in range(self.L)]
-        self.Zall = [be.zeros(P * n_pad, dp[l + 1]) for l in range(self.L)]
-        self.dZall = [be.zeros(P * n_pad, dp[l + 1]) for l in range(self.L)]
+        # the layer's source relation: all-gathered [P n_pad] or own + halo [n_pad + n_halo]
+        self.Zall = [be.zeros(self.n_s, dp[l + 1]) for l in range(self.L)]
+        self.dZall = [be.zeros(self.n_s, dp[l + 1]) for l in range(self.L)]
+        if self.halo is not None:
+            self.send = [be.zeros(max(len(self.halo.send_idx), 1), dp[l + 1]) for l in range(self.L)]
         self.dZ = [be.zeros(n_pad, dp[l + 1]) for l in range(self.L)]
         self.dH = [be.zeros(n_pad, dp[l]) for l in range(self.L)]
         self._dW = [be.zeros(dp[l + 1], dp[l]) for l in range(self.L)]
@@ -200,7 +300,12 @@ class ShardedGCNProgram:
             be.project(self.H[l], self.W[l], self.Z[l])
             self._t("proj_fwd_end")
             self._t("allgather")
-            all_gather_rows(self.Zall[l], self.Z[l], g)
+            if self.halo is not None:
+                n_pad = self.plan.n_pad
+                self.Zall[l][:n_pad].copy_(self.Z[l])
+                halo_exchange_fwd(be, self.halo, self.Zall[l], self.send[l][: len(self.halo.send_idx)], g)
+            else:
+                all_gather_rows(self.Zall[l], self.Z[l], g)
             self._t("allgather_end")
             self._t("lja_fwd")
             if self.bias is not None:
@@ -225,7 +330,12 @@ class ShardedGCNProgram:
             be.lja_bwd_src(self.idx, self.Zall[l], self.w, dY, self.dZall[l])
             self._t("lja_bwd_end")
             self._t("reduce_scatter")
-            reduce_scatter_rows(self.dZ[l], self.dZall[l], g)
+            if self.halo is not None:
+                n_pad = self.plan.n_pad
+                halo_exchange_bwd(be, self.halo, self.dZall[l], self.send[l][: len(self.halo.send_idx)], g)
+                self.dZ[l].copy_(self.dZall[l][:n_pad])
+            else:
+                reduce_scatter_rows(self.dZ[l], self.dZall[l], g)
             self._t("reduce_scatter_end")
             self._t("proj_bwd")
             be.project_bwd(self.H[l], self.W[l], self.dZ[l], self.dH[l], self._dW[l])
@@ -349,6 +459,9 @@ class RnnBackend:
 
     def gather_rows(self, out, x, idx):
         self.rnn.gather_rows(out, x, idx)
+
+    def scatter_add_rows(self, y, x, idx):
+        self.rnn.scatter_add_rows(y, x, idx)
 
     def dhn_fwd(self, idx, k, f, roots, out, walk_sum):
         self.rnn.dhn_fwd(idx, k, f, out=out, ws=self.ws, walk_sum=walk_sum, roots=roots)
@@ -570,13 +683,14 @@ class ShardedHGTProgram:
     each relation's join rows live on the owner of their TARGET key (the GROUP BY key), with
     dense groups over the rank's owned target keys.  Per step:
 
-        Y_own[t]  = H_own[t] W[t]^T                 stacked K', M', Q blocks, owned rows
-        Y_all[s]  = all_gather(Y_own[s])            for every source type s
-        O_phi     = softmax-LJA(K' = Y_all[s][k], M' = Y_all[s][m], Q = Y_own[t][q])
+        KM_own[t] = H_own[t] Wkm[t]^T               stacked K', M' blocks, owned rows
+        Q_own[t]  = H_own[t] Wq[t]^T                 the target type's queries (stay local)
+        KM_all[s] = all_gather(KM_own[s])            for every source type s: ONLY K'/M'
+        O_phi     = softmax-LJA(K' = KM_all[s][k], M' = KM_all[s][m], Q = Q_own[t])
         Ht[t]     = sum_phi O_phi                    (rnn_accumulate)
-      backward: per phi dK', dM' over all source rows into dY_all[s] (disjoint column blocks)
-      and dQ into dY_own[t]; reduce_scatter(dY_all[s]) added to dY_own[s]; projection
-      backward on owned rows; all_reduce(dW[t])."""
+      backward: per phi dK', dM' over all source rows into dKM_all[s] (disjoint column
+      blocks) and dQ summed into dQ_own[t]; reduce_scatter(dKM_all[s]) added to dKM_own[s];
+      both projection backwards on owned rows; all_reduce(dW[t])."""
 
     def __init__(self, mag: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32",
                  param_seed=7):
@@ -602,22 +716,29 @@ class ShardedHGTProgram:
             self.my_rows[t] = order[np.searchsorted(k[order], owned[r])]
         self.n_own = {t: len(self.my_keys[t]) for t in types}
         self.sources = sorted({x["src_type"] for x in self.rels.values()})
-        self.H, self.W, self.Y, self.dY, self.dW, self.dH = {}, {}, {}, {}, {}, {}
+        self.H, self.W, self.dW, self.dH, self.dH2 = {}, {}, {}, {}, {}
+        self.Y, self.dY, self.Yq, self.dYq = {}, {}, {}, {}      # Y / dY: the K'/M' blocks
         self.Yall, self.dYall, self.R = {}, {}, {}
+        self.nkm = {t: sum(k != "q" for k, _ in self.blocks[t]) for t in types}
         for t in types:
-            nb = len(self.blocks[t])
+            nb, nkm = len(self.blocks[t]), self.nkm[t]
             x = np.zeros((self.n_pad[t], d), np.float32)
             x[: self.n_own[t]] = np.asarray(mag["h"][t], np.float32)[self.my_rows[t]]
             self.H[t] = be.tensor(x)
             self.W[t] = be.tensor(par["W"][t])
-            self.Y[t] = be.zeros(self.n_pad[t], nb * d)
-            self.dY[t] = be.zeros(self.n_pad[t], nb * d)
             self.dW[t] = be.zeros(nb * d, d)
             self.dH[t] = be.zeros(self.n_pad[t], d)
+            self.dH2[t] = be.zeros(self.n_pad[t], d)
+            if nkm:
+                self.Y[t] = be.zeros(self.n_pad[t], nkm * d)
+                self.dY[t] = be.zeros(self.n_pad[t], nkm * d)
+            if nkm < nb:
+                self.Yq[t] = be.zeros(self.n_pad[t], d)
+                self.dYq[t] = be.zeros(self.n_pad[t], d)
             if t in self.sources:
-                self.Yall[t] = be.zeros(P * self.n_pad[t], nb * d)
-                self.dYall[t] = be.zeros(P * self.n_pad[t], nb * d)
-                self.R[t] = be.zeros(self.n_pad[t], nb * d)
+                self.Yall[t] = be.zeros(P * self.n_pad[t], nkm * d)
+                self.dYall[t] = be.zeros(P * self.n_pad[t], nkm * d)
+                self.R[t] = be.zeros(self.n_pad[t], nkm * d)
         self.idx, self.O, self.lse = {}, {}, {}
         for name, x in self.rels.items():
             ts, tt = x["src_type"], x["dst_type"]
@@ -627,9 +748,8 @@ class ShardedHGTProgram:
             self.O[name] = be.zeros(self.n_pad[tt], d)
             self.lse[name] = be.zeros(self.n_pad[tt], h)
         self.Ht = {t: be.zeros(self.n_pad[t], d) for t in self.targets}
-        # per-relation dQ, summed into the target type's single query-gradient block (a
-        # gradient buffer takes its operand's ld -- here the stacked Y[t]'s -- rnn.h)
-        self.dQ = {t: be.zeros(self.n_pad[t], len(self.blocks[t]) * d)[:, :d] for t in self.targets}
+        # per-relation dQ, summed into the target type's query gradient
+        self.dQ = {t: be.zeros(self.n_pad[t], d) for t in self.targets}
         self.d_out = {}
         for t in self.targets:
             full = np.asarray(par["d_out"][t], np.float32)       # T-key order of all keys
@@ -640,8 +760,15 @@ class ShardedHGTProgram:
         self.timers = None
 
     def _blk(self, buf, t, kind, name):
-        i = self.col[(kind, name)][1]
+        if kind == "q":
+            return buf[t]
+        i = self.col[(kind, name)][1]               # K'/M' blocks precede Q (hgt_parameters)
         return buf[t][:, i * self.d:(i + 1) * self.d]
+
+    def _w(self, t, q):
+        """W[t] rows of the K'/M' blocks (q False) or of the query block (q True); likewise dW."""
+        k = self.nkm[t] * self.d
+        return (self.W[t][k:], self.dW[t][k:]) if q else (self.W[t][:k], self.dW[t][:k])
 
     @property
     def join_rows_per_step(self):
@@ -672,17 +799,20 @@ class ShardedHGTProgram:
         be, g = self.be, self.group
         self._t("proj_fwd")
         for t in self.blocks:
-            be.project(self.H[t], self.W[t], self.Y[t])
+            if t in self.Y:
+                be.project(self.H[t], self._w(t, False)[0], self.Y[t])
+            if t in self.Yq:
+                be.project(self.H[t], self._w(t, True)[0], self.Yq[t])
         self._t("proj_fwd_end")
         for s in self.sources:
-            all_gather_rows(self.Yall[s], self.Y[s], g)
+            all_gather_rows(self.Yall[s], self.Y[s], g)          # K'/M' only
         first = {t: True for t in self.targets}
         for name, x in self.rels.items():
             ts, tt = x["src_type"], x["dst_type"]
             n = self.n_own[tt]
             self._t("lja_fwd")
             be.lja_sm_fwd(self.idx[name], self._blk(self.Yall, ts, "m", name),
-                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", tt),
+                          self._blk(self.Yall, ts, "k", name), self._blk(self.Yq, tt, "q", tt),
                           self.h, self.O[name][:n], self.lse[name][:n])
             self._t("lja_fwd_end")
             be.accumulate(self.Ht[tt][:n], self.O[name][:n], 0.0 if first[tt] else 1.0)
@@ -692,24 +822,35 @@ class ShardedHGTProgram:
     def backward(self):
         be, g = self.be, self.group
         for t in self.blocks:
-            be.fill_zero(self.dY[t])
+            if t in self.dY:
+                be.fill_zero(self.dY[t])
+            if t in self.dYq:
+                be.fill_zero(self.dYq[t])
         for name, x in self.rels.items():
             ts, tt = x["src_type"], x["dst_type"]
             n = self.n_own[tt]
             self._t("lja_bwd")
             be.lja_sm_bwd(self.idx[name], self._blk(self.Yall, ts, "m", name),
-                          self._blk(self.Yall, ts, "k", name), self._blk(self.Y, tt, "q", tt),
+                          self._blk(self.Yall, ts, "k", name), self._blk(self.Yq, tt, "q", tt),
                           self.h, self.O[name][:n], self.lse[name][:n], self.d_out[tt][:n],
                           self._blk(self.dYall, ts, "m", name), self._blk(self.dYall, ts, "k", name),
                           self.dQ[tt][:n])
             self._t("lja_bwd_end")
-            be.accumulate(self._blk(self.dY, tt, "q", tt)[:n], self.dQ[tt][:n], 1.0)
+            be.accumulate(self.dYq[tt][:n], self.dQ[tt][:n], 1.0)
         for s in self.sources:
             reduce_scatter_rows(self.R[s], self.dYall[s], g)
             be.accumulate(self.dY[s], self.R[s], 1.0)
         self._t("proj_bwd")
         for t in self.blocks:
-            be.project_bwd(self.H[t], self.W[t], self.dY[t], self.dH[t], self.dW[t])
+            first = True
+            for q, dY in ((False, self.dY.get(t)), (True, self.dYq.get(t))):
+                if dY is None:
+                    continue
+                W, dW = self._w(t, q)
+                be.project_bwd(self.H[t], W, dY, self.dH[t] if first else self.dH2[t], dW)
+                if not first:
+                    be.accumulate(self.dH[t], self.dH2[t], 1.0)
+                first = False
         self._t("proj_bwd_end")
         if self.P > 1:
             for t in self.blocks:

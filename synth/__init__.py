@@ -267,3 +267,25 @@ def random_db(rng, n_s, n_t, n_e, key_space=None, dangling=0.2, d_s=4, d_e=1, d_
             "z_s": _normal_f32(rng, (n_s, d_s), 1.0),
             "z_e": _normal_f32(rng, (n_e, d_e), 1.0),
             "z_t": _normal_f32(rng, (n_t, d_t), 1.0)}
+
+
+def rgcn_like(seed=42, n_nodes=8285, n_pairs=29043, n_rel=45, d=16):
+    """AIFB-shaped multi-relational graph for R-GCN: power-law Chung-Lu
+    pairs, each with a relation type (Zipf-like: a few types hold most edges), stored in both
+    directions with the inverse as its own type (2 n_rel types, the R-GCN convention);
+    dense node features ~ N(0, 1/d)."""
+    rng = rng_for(seed)
+    w = powerlaw_weights(rng, n_nodes, cap_ratio=200.0)
+    s, t = chung_lu(rng, w, w, n_pairs, same_set=True, undirected=False)
+    p = 1.0 / np.arange(1, n_rel + 1) ** 1.2
+    rel = rng.choice(n_rel, size=n_pairs, p=p / p.sum())
+    src = np.concatenate([s, t]); dst = np.concatenate([t, s])
+    rel = np.concatenate([rel, rel + n_rel])
+    perm = rng.permutation(len(src))
+    key = rng.permutation(n_nodes).astype(np.int64)
+    x = _normal_f32(rng, (n_nodes, d), 1.0 / np.sqrt(d))
+    W = _normal_f32(rng, (2 * n_rel + 1, d, d), 1.0 / np.sqrt(d))
+    d_out = _normal_f32(rng, (n_nodes, d), 1.0)
+    return {"nodes": {"key": key, "x": x},
+            "edges": {"src": key[src[perm]], "dst": key[dst[perm]], "rel": rel[perm].astype(np.int32)},
+            "n_rel": 2 * n_rel, "W": W, "d_out": d_out}

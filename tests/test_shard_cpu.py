@@ -71,6 +71,16 @@ class OracleBackend:
                            edge=w, edge_mode=1, want=("src",))["src"]
         d_src[:] = torch.from_numpy(g)
 
+    def index_i32(self, a):
+        return torch.as_tensor(np.asarray(a, np.int32))
+
+    def gather_rows(self, out, x, idx):
+        i = idx.numpy()
+        out[:] = x[torch.as_tensor(i.astype(np.int64))]
+
+    def scatter_add_rows(self, y, x, idx):
+        y[torch.as_tensor(idx.numpy().astype(np.int64))] += x
+
     def lja_fwd_epi(self, idx, Z, w, out, bias, act):
         self.lja_fwd(idx, Z, w, out)
         G = idx["n_groups"]
@@ -112,12 +122,14 @@ def reference(g):
     return {"out_keys": np.sort(keys), "out": H[-1], "dW": dW, "dH0": dH0}
 
 
-def _worker(rank, world, port, path, dims=(12, 8, 4)):
+def _worker(rank, world, port, path, dims=(12, 8, 4), halo=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         g = graph_with_weights(dims)
-        prog = ShardedGCNProgram(g, backend=OracleBackend())
+        prog = ShardedGCNProgram(g, backend=OracleBackend(), halo=halo)
+        if halo and world > 1:
+            assert prog.halo is not None and prog.halo.rows_recv < prog.halo.rows_allgather
         prog.step()
         np.savez(os.path.join(path, f"r{rank}.npz"), keys=prog.plan.my_keys, rows=prog.plan.my_rows,
                  out=prog.owned_output(), dx=prog.owned_dx(),
@@ -212,3 +224,20 @@ def _worker_b(rank, world, port, path):
                  **{f"dW{l}": prog.dW[l].numpy() for l in range(prog.L)})
     finally:
         dist.destroy_process_group()
+
+
+def test_world_size_2_gloo_allgather():
+    """The all-gather exchange (halo=False) gives the same result as the halo exchange."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, (12, 8, 4), False), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    g = graph_with_weights()
+    check(res, reference(g), g)
+
+
+def test_world_size_3_gloo_halo():
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(3, _free_port(), d), nprocs=3, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(3)]
+    g = graph_with_weights()
+    check(res, reference(g), g)
