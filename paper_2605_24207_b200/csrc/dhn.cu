@@ -84,7 +84,8 @@ __device__ __forceinline__ int64_t dhn_next_root(const DhnArgs& a, int* s_root) 
 //   [0] C3 roots, [1] C3 roots on the global mark array (in-degree > H3_MAX_INDEG),
 //   [2] C4 roots, [3] C4 (root, partition) passes, [4] of them in chunked mode,
 //   [5] C4 long runs queued for phase B, [6] long runs past the queue (walked inline),
-//   [7] C4 roots with hash partitions (P > 1).
+//   [7] C4 roots with hash partitions (P > 1), [8] C4 keys refused by a full value table
+//   (shared-memory variant; must stay 0).
 // Counted per CTA (registers / shared memory) and added once per CTA at exit.
 __device__ unsigned long long g_dhn_paths[16];
 
@@ -319,33 +320,42 @@ constexpr int H4_LONG_MAX = 512;             // long runs queued per sweep (over
 // compact id of key w in the C4 table (inserted if absent): the CAS winner draws the next id
 // (so a root's S1 rows are a dense prefix of the CTA's slab and stay L2-resident); a lane
 // that finds w already present waits for the winner to publish the id.
+// CAP: hash slots; MAXID: value rows (ids >= MAXID are refused: -2 is published so waiting
+// lanes give up too, and the overflow is counted -- the shared-memory variant sizes its
+// partitions so this does not happen, tests assert it)
+template <int CAP = H4_CAP, int MAXID = (1 << 30)>
 __device__ __forceinline__ int h4_insert(int* keys, int* ids, int* n_ids, int w) {
-  uint32_t s = dhn_hash((uint32_t)w) & (uint32_t)(H4_CAP - 1);
-  for (int t = 0; t < H4_CAP; ++t) {
+  uint32_t s = dhn_hash((uint32_t)w) & (uint32_t)(CAP - 1);
+  for (int t = 0; t < CAP; ++t) {
     const int prev = atomicCAS(&keys[s], -1, w);
     if (prev == -1) {
-      const int id = atomicAdd(n_ids, 1);
+      int id = atomicAdd(n_ids, 1);
+      if (id >= MAXID) {
+        id = -2;
+        atomicAdd(&g_dhn_paths[8], 1ull);
+      }
       atomicExch(&ids[s], id);
-      return id;
+      return id < 0 ? -1 : id;
     }
     if (prev == w) {
       int id;
-      do { id = *((volatile int*)&ids[s]); } while (id < 0);
-      return id;
+      do { id = *((volatile int*)&ids[s]); } while (id == -1);
+      return id < 0 ? -1 : id;
     }
-    s = (s + 1) & (uint32_t)(H4_CAP - 1);
+    s = (s + 1) & (uint32_t)(CAP - 1);
   }
   return -1;
 }
 
 // One 32-entry chunk of a run: OUT inserts w and adds f1(v) to S1(w) (one 128-byte red per
 // entry); IN finds w and sums G(w) into t (8 slab rows in flight per round).
-template <bool OUT>
+template <bool OUT, int CAP = H4_CAP, int MAXID = (1 << 30), bool DUAL = false>
 __device__ __forceinline__ void h4_chunk(int* keys, int* ids, int* n_ids, float* S, int32_t w,
                                          bool in, float fv, float& t, int lane,
-                                         const float* F2c, int d) {
+                                         const float* F2c, int d, float* tb = nullptr,
+                                         const float* F2bc = nullptr) {
   if (OUT) {
-    const int sl = (in && w >= 0) ? h4_insert(keys, ids, n_ids, w) : -1;
+    const int sl = (in && w >= 0) ? h4_insert<CAP, MAXID>(keys, ids, n_ids, w) : -1;
     unsigned bal = __ballot_sync(FULL, sl >= 0);
     while (bal) {
       const int q = __ffs(bal) - 1;
@@ -353,22 +363,26 @@ __device__ __forceinline__ void h4_chunk(int* keys, int* ids, int* n_ids, float*
       atomicAdd(&S[__shfl_sync(FULL, sl, q) * 32 + lane], fv);
     }
   } else {
-    int sl = (in && w >= 0) ? hs_find(keys, H4_CAP - 1, w) : -1;
+    int sl = (in && w >= 0) ? hs_find(keys, CAP - 1, w) : -1;
     if (sl >= 0) sl = ids[sl];
     unsigned bal = __ballot_sync(FULL, sl >= 0);
     while (bal) {   // G(w) = f2(w) (.) S1(w) formed on the fly, 8 hits in flight
-      float x[8], y[8];
+      float x[8], y[8], yb[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         int q = -1;
         if (bal) { q = __ffs(bal) - 1; bal &= bal - 1; }
         const int slq = __shfl_sync(FULL, sl, q < 0 ? 0 : q);
         const int wq = __shfl_sync(FULL, w, q < 0 ? 0 : q);
-        x[u] = q >= 0 ? __ldcg(&S[slq * 32 + lane]) : 0.f;
+        x[u] = q >= 0 ? S[slq * 32 + lane] : 0.f;
         y[u] = q >= 0 ? F2c[(int64_t)wq * d] : 0.f;
+        if (DUAL) yb[u] = q >= 0 ? F2bc[(int64_t)wq * d] : 0.f;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t = fmaf(x[u], y[u], t);
+      for (int u = 0; u < 8; ++u) {
+        t = fmaf(x[u], y[u], t);
+        if (DUAL) *tb = fmaf(x[u], yb[u], *tb);
+      }
     }
   }
 }
@@ -453,7 +467,7 @@ struct H4Root {
 // serves neighbours (one per warp, or 32 per step in chunked mode) and walks their runs of
 // this partition; runs longer than H4_LONG are queued.  Phase B: every queued run is split
 // over all warps.  Returns this thread's contribution to the root's accumulator (IN).
-template <bool OUT, bool V4, bool DUAL = false>
+template <bool OUT, bool V4, bool DUAL = false, int CAP = H4_CAP, int MAXID = (1 << 30)>
 __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* ids, int* n_ids,
                           float* S, int* cur, int* q_i, int64_t* q_b, int64_t* q_e, int* q_n,
                           int* grab, int c, bool cok, int* s_cnt, float4* acc_b = nullptr) {
@@ -462,6 +476,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
   const float* Fv = OUT ? a.F1 : a.F3;
   const int d = a.d;
   const float* F2c = a.F2 + (cok ? c : 0);   // f2 column of this lane (rows gathered by w)
+  const float* F2bc = DUAL ? a.F2b + (cok ? c : 0) : nullptr;
   // V4: this lane's channel quad c0 + 4 (lane % 8) .. + 3
   const int cq4 = (c - lane) + 4 * (lane & 7);
   const bool cok4 = cq4 < d;
@@ -527,7 +542,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         }
         if (lane == 0) atomicAdd(&s_cnt[1], 1);   // queue full: walk this long run inline
       }
-      float fv = 0.f, t = 0.f;
+      float fv = 0.f, t = 0.f, tb = 0.f;
       float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4, t4b = fv4;
       if (V4) fv4 = ld_fv4(uj);
       else fv = cok ? Fv[(int64_t)uj * d + c] : 0.f;
@@ -538,14 +553,17 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         const bool in = tt < ej && (h4_top(w) >> R.sh) == R.part;
         const unsigned im = __ballot_sync(FULL, in);
         if (V4) h4_chunk4<OUT, DUAL>(keys, ids, n_ids, S, w, in, fv4, t4, lane, F2q, d, &t4b, F2bq);
-        else h4_chunk<OUT>(keys, ids, n_ids, S, w, in, fv, t, lane, F2c, d);
+        else h4_chunk<OUT, CAP, MAXID, DUAL>(keys, ids, n_ids, S, w, in, fv, t, lane, F2c, d, &tb, F2bc);
         t0 += __popc(im);
         if (im != FULL) break;
       }
       if (!OUT) {
         if (V4) fma4(acc4, fv4, t4);
         else acc += fv * t;
-        if (DUAL) fma4(*acc_b, fv4, t4b);
+        if (DUAL) {
+          if (V4) fma4(*acc_b, fv4, t4b);
+          else acc_b->x += fv * tb;
+        }
       }
       if (R.cur_ok && lane == 0) cur[ij] = (int)(t0 - sj);
     }
@@ -559,7 +577,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
     int k = 0;            // current item (items are walked in order; chunk ids are global)
     int64_t k_end = 0;    // first global chunk id after item k
     int64_t k_beg = 0;
-    float fv = 0.f, t = 0.f;
+    float fv = 0.f, t = 0.f, tb = 0.f;
     float4 fv4 = make_float4(0.f, 0.f, 0.f, 0.f), t4 = fv4, t4b = fv4;
     int32_t uk = -1;
     for (;;) {
@@ -572,9 +590,13 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
         if (uk >= 0 && !OUT) {
           if (V4) fma4(acc4, fv4, t4);
           else acc += fv * t;
-          if (DUAL) fma4(*acc_b, fv4, t4b);
+          if (DUAL) {
+            if (V4) fma4(*acc_b, fv4, t4b);
+            else acc_b->x += fv * tb;
+          }
         }
         t = 0.f;
+        tb = 0.f;
         t4 = make_float4(0.f, 0.f, 0.f, 0.f);
         t4b = t4;
         uk = -1;
@@ -591,7 +613,7 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
       const int64_t tt = qb + (g - k_beg) * 32 + lane;
       const int32_t w = tt < qe ? L[tt] : -1;
       if (V4) h4_chunk4<OUT, DUAL>(keys, ids, n_ids, S, w, tt < qe, fv4, t4, lane, F2q, d, &t4b, F2bq);
-      else h4_chunk<OUT>(keys, ids, n_ids, S, w, tt < qe, fv, t, lane, F2c, d);
+      else h4_chunk<OUT, CAP, MAXID, DUAL>(keys, ids, n_ids, S, w, tt < qe, fv, t, lane, F2c, d, &tb, F2bc);
     }
   }
   __syncthreads();
@@ -601,23 +623,41 @@ __device__ float4 h4_sweep(const DhnArgs& a, const H4Root& R, int* keys, int* id
   return acc4;
 }
 
-template <bool V4, bool DUAL = false>
+// SMEMS: the S1 values live in SHARED memory (H4S_KEYS rows of 32 floats, one conflict-free
+// warp-wide smem atomic per wedge) with partitions sized for H4S_PART distinct keys, instead
+// of the per-CTA L2 slab (one 128-byte L2 reduction per wedge)
+constexpr int H4S_CAP = 2048;    // hash slots
+constexpr int H4S_KEYS = 1024;   // value rows (32 floats each: 128 KB)
+constexpr int H4S_PART = 384;    // expected distinct keys per partition (bound-based)
+constexpr int H4S_DEG_CAP = 4096;
+
+template <bool V4, bool DUAL = false, bool SMEMS = false>
 __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
+  constexpr int CAP = SMEMS ? H4S_CAP : H4_CAP;
+  constexpr int MAXID = SMEMS ? H4S_KEYS : (1 << 30);
+  constexpr int PART = SMEMS ? H4S_PART : H4_PART;
+  constexpr int DEGCAP = SMEMS ? H4S_DEG_CAP : H4_DEG_CAP;
   extern __shared__ int h4[];
   int* keys = h4;
-  int* ids = h4 + H4_CAP;                                  // compact id of each slot
-  float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;  // [H4_CAP][32] by compact id
-  float* s_red = reinterpret_cast<float*>(ids + H4_CAP);   // [H4_WARPS][32]
-  int* cur_out = reinterpret_cast<int*>(s_red + H4_WARPS * 32);   // [H4_DEG_CAP]
-  int* cur_in = cur_out + H4_DEG_CAP;                               // [H4_DEG_CAP]
-  int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
+  int* ids = h4 + CAP;                                     // compact id of each slot
+  float* s_red = reinterpret_cast<float*>(ids + CAP);      // [H4_WARPS][32]
+  int* cur_out = reinterpret_cast<int*>(s_red + H4_WARPS * 32);   // [DEGCAP]
+  int* cur_in = cur_out + DEGCAP;                                   // [DEGCAP]
+  int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + DEGCAP);      // [H4_LONG_MAX]
   int64_t* q_e = q_b + H4_LONG_MAX;
   int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
+  // S1 values by compact id: shared (SMEMS, after the queue) or the CTA's L2 slab
+  float* S = SMEMS ? reinterpret_cast<float*>(
+                         (reinterpret_cast<uintptr_t>(q_i + H4_LONG_MAX) + 15) & ~uintptr_t(15))
+                   : a.slab + (int64_t)blockIdx.x * a.cta_stride;
   __shared__ int s_root, q_n, n_ids, grab;
   __shared__ int s_cnt[2];   // long runs queued / walked inline (queue full)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int d = a.d;
-  for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
+  for (int i = threadIdx.x; i < CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
+  if (SMEMS)
+    for (int i = threadIdx.x; i < H4S_KEYS * 8; i += H4_THREADS)
+      reinterpret_cast<float4*>(S)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (threadIdx.x == 0) { q_n = 0; n_ids = 0; grab = 0; s_cnt[0] = 0; s_cnt[1] = 0; }
   RNN_PROBE(long long t_last = clock64();)
   unsigned long long c_roots = 0, c_parts = 0, c_chunked = 0, c_multi = 0;   // thread 0
@@ -629,10 +669,10 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
     const int64_t ib = a.sp[r], ie = a.sp[r + 1];
     const int64_t pb = a.gp[n], pe = a.gp[n + 1];
     const int deg_out = (int)(pe - pb), deg_in = (int)(ie - ib);
-    const bool cur_ok = deg_out <= H4_DEG_CAP && deg_in <= H4_DEG_CAP;
+    const bool cur_ok = deg_out <= DEGCAP && deg_in <= DEGCAP;
     const int64_t bound = a.wout[n] < (uint32_t)a.G ? (int64_t)a.wout[n] : a.G;
     int bits = 0;
-    while (bits < H4_HBITS && ((int64_t)H4_PART << bits) < bound) ++bits;
+    while (bits < H4_HBITS && ((int64_t)PART << bits) < bound) ++bits;
     H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
     // lanes test 32 neighbours per step only when a neighbour's list has under one entry
     // per partition on average (hubs); otherwise one neighbour per warp
@@ -654,21 +694,27 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
         c_chunked += R.chunked;
         // (1) S1(w) += f1(v) over out-wedges n -> v -> w of this partition
         R.deg = deg_out;
-        h4_sweep<true, V4>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c, cok,
-                           s_cnt);
+        h4_sweep<true, V4, false, CAP, MAXID>(a, R, keys, ids, &n_ids, S, cur_out, q_i, q_b, q_e,
+                                              &q_n, &grab, c, cok, s_cnt);
         H4_T(1);
         // (3) acc += f3(p) (.) G(w) over in-wedges w -> p -> n of this partition
         R.deg = deg_in;
         {
-          const float4 r4 = h4_sweep<false, V4, DUAL>(a, R, keys, ids, &n_ids, S, cur_in, q_i, q_b,
-                                                      q_e, &q_n, &grab, c, cok, s_cnt, &acc_b);
+          const float4 r4 = h4_sweep<false, V4, DUAL, CAP, MAXID>(a, R, keys, ids, &n_ids, S, cur_in,
+                                                                  q_i, q_b, q_e, &q_n, &grab, c,
+                                                                  cok, s_cnt, &acc_b);
           acc.x += r4.x; acc.y += r4.y; acc.z += r4.z; acc.w += r4.w;
         }
         H4_T(3);
         // (4) clear the table for the next partition / root
-        for (int i = threadIdx.x; i < n_ids * 8; i += H4_THREADS)   // dense prefix, float4
-          __stcg(reinterpret_cast<float4*>(S) + i, make_float4(0.f, 0.f, 0.f, 0.f));
-        for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
+        {
+          const int nz = (n_ids < MAXID ? n_ids : MAXID) * 8;
+          for (int i = threadIdx.x; i < nz; i += H4_THREADS) {   // dense prefix, float4
+            if (SMEMS) reinterpret_cast<float4*>(S)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            else __stcg(reinterpret_cast<float4*>(S) + i, make_float4(0.f, 0.f, 0.f, 0.f));
+          }
+        }
+        for (int i = threadIdx.x; i < CAP; i += H4_THREADS) { keys[i] = -1; ids[i] = -1; }
         __syncthreads();
         if (threadIdx.x == 0) n_ids = 0;
         __syncthreads();
@@ -693,13 +739,17 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
         if (cok) dhn_store(a, n, c, s);
       }
       __syncthreads();
-      if (DUAL) {   // the second middle operand's result (V4 layout, no root multiplier)
+      if (DUAL) {   // the second middle operand's result (no root multiplier)
+        if (V4) {
 #pragma unroll
-        for (int m = 8; m < 32; m <<= 1) {
-          acc_b.x += __shfl_xor_sync(FULL, acc_b.x, m); acc_b.y += __shfl_xor_sync(FULL, acc_b.y, m);
-          acc_b.z += __shfl_xor_sync(FULL, acc_b.z, m); acc_b.w += __shfl_xor_sync(FULL, acc_b.w, m);
+          for (int m = 8; m < 32; m <<= 1) {
+            acc_b.x += __shfl_xor_sync(FULL, acc_b.x, m); acc_b.y += __shfl_xor_sync(FULL, acc_b.y, m);
+            acc_b.z += __shfl_xor_sync(FULL, acc_b.z, m); acc_b.w += __shfl_xor_sync(FULL, acc_b.w, m);
+          }
+          if (lane < 8) *reinterpret_cast<float4*>(&s_red[warp * 32 + 4 * lane]) = acc_b;
+        } else {
+          s_red[warp * 32 + lane] = acc_b.x;
         }
-        if (lane < 8) *reinterpret_cast<float4*>(&s_red[warp * 32 + 4 * lane]) = acc_b;
         __syncthreads();
         if (warp == 0) {
           float s = 0.f;
@@ -1088,6 +1138,19 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
   } else {
     a.wout = b.wout; a.nbrh = b.nbrh; a.sgh = b.sgh;
     a.slab = reinterpret_cast<float*>(b.cta);
+    // shared-memory S1 (default) or the L2 slab (RNN_DHN_L2SLAB=1, the round-1 design)
+    static const bool l2slab = getenv("RNN_DHN_L2SLAB") != nullptr;
+    if (!l2slab) {
+      const size_t smem_s = 2 * H4S_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
+                            2 * H4S_DEG_CAP * sizeof(int) +
+                            H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) + 16 +
+                            (size_t)H4S_KEYS * 32 * sizeof(float);
+      auto kern = a.F2b ? dhn4_kernel<false, true, true> : dhn4_kernel<false, false, true>;
+      RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+      kern<<<P.n_cta, H4_THREADS, smem_s, st>>>(a);
+      RNN_LAUNCH_CHECK();
+      return RNN_OK;
+    }
     const size_t smem = 2 * H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                         2 * H4_DEG_CAP * sizeof(int) + H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
     // four hits per instruction (float4 per lane) when rows are whole float4s

@@ -588,7 +588,7 @@ def dhn_count(adj: JoinIndex, k, out=None, stream=None):
 
 
 DHN_PATHS = ("c3_roots", "c3_mark_roots", "c4_roots", "c4_passes", "c4_chunked_passes",
-             "c4_long_runs", "c4_long_overflow", "c4_partitioned_roots")
+             "c4_long_runs", "c4_long_overflow", "c4_partitioned_roots", "c4_value_overflow")
 
 
 def dhn_path_counters(reset=False):

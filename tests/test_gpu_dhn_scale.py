@@ -128,6 +128,7 @@ def check_walks(rnn, keys, e_n, e_v, k, d, seed, ks_count=True, dyadic=False):
     rnn.dhn_path_counters(reset=True)
     out = np_(rnn.dhn_fwd(gi, k, fg))
     paths = rnn.dhn_path_counters()
+    assert paths["c4_value_overflow"] == 0, paths
     assert_close(out[rows], oracle.dhn_fwd(k, oi, keys, f), FP32_TOL, f"C{k} fwd")
     d_out = rng.standard_normal((gi.n_groups, d)).astype(np.float32)
     grads = rnn.dhn_bwd(gi, k, fg, cu(d_out))
@@ -243,6 +244,7 @@ def test_products_full_scale_sampled(rnn, products):
     g4 = rnn.dhn_bwd(gi, 4, fg, cu(d_out), want=[False, True, False, False])[1]
     g4 = np_(g4)
     assert paths["c4_roots"] == G and paths["c4_partitioned_roots"] > 0, paths
+    assert paths["c4_value_overflow"] == 0, paths
     # sampled roots: 48 random + 8 of degree 200-600 (C3 also gets the 4 largest hubs)
     pick = rng.choice(G, 48, replace=False)
     mid = np.nonzero((deg >= 200) & (deg <= 600))[0]
