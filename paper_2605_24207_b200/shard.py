@@ -693,7 +693,7 @@ class ShardedHGTProgram:
       both projection backwards on owned rows; all_reduce(dW[t])."""
 
     def __init__(self, mag: dict, backend=None, group=None, seed=0x5EED, prec="3xtf32",
-                 param_seed=7):
+                 param_seed=7, halo=True):
         from .programs import hgt_parameters
         self.group = group
         self.P = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -735,10 +735,37 @@ class ShardedHGTProgram:
             if nkm < nb:
                 self.Yq[t] = be.zeros(self.n_pad[t], d)
                 self.dYq[t] = be.zeros(self.n_pad[t], d)
+        # halo exchange per source type (default at P > 1): rank r receives only the K'/M'
+        # rows its join rows reference (union over the relations leaving the type)
+        self.halo = {}
+        if halo and P > 1:
+            for t in self.sources:
+                k = np.asarray(mag["key"][t], np.int64)
+                owned_t = [np.sort(k[self.owner[t] == q]) for q in range(P)]
+                refs = []
+                for q in range(P):
+                    srcs = []
+                    for x in self.rels.values():
+                        if x["src_type"] != t:
+                            continue
+                        tt = x["dst_type"]
+                        mine = _owner_of(mag["key"][tt], self.owner[tt], x["dst"]) == q
+                        srcs.append(np.asarray(x["src"], np.int64)[mine])
+                    refs.append(np.intersect1d(np.unique(np.concatenate(srcs)), k))
+                hp = HaloPlan(owned_t, self.n_pad[t], refs, r)
+                hp.send_idx_dev = be.index_i32(hp.send_idx)
+                self.halo[t] = hp
+                r0 = r * self.n_pad[t]
+                self.s_keys[t] = hp.s_keys(self.s_keys[t][r0:r0 + self.n_pad[t]])
+        for t in types:
+            nkm = self.nkm[t]
             if t in self.sources:
-                self.Yall[t] = be.zeros(P * self.n_pad[t], nkm * d)
-                self.dYall[t] = be.zeros(P * self.n_pad[t], nkm * d)
+                n_s = len(self.s_keys[t])      # all-gathered P n_pad rows, or own + halo rows
+                self.Yall[t] = be.zeros(n_s, nkm * d)
+                self.dYall[t] = be.zeros(n_s, nkm * d)
                 self.R[t] = be.zeros(self.n_pad[t], nkm * d)
+                if t in self.halo:
+                    self.R[t] = be.zeros(max(len(self.halo[t].send_idx), 1), nkm * d)
         self.idx, self.O, self.lse = {}, {}, {}
         for name, x in self.rels.items():
             ts, tt = x["src_type"], x["dst_type"]
@@ -805,7 +832,12 @@ class ShardedHGTProgram:
                 be.project(self.H[t], self._w(t, True)[0], self.Yq[t])
         self._t("proj_fwd_end")
         for s in self.sources:
-            all_gather_rows(self.Yall[s], self.Y[s], g)          # K'/M' only
+            if s in self.halo:                                   # K'/M' of referenced rows
+                hp = self.halo[s]
+                self.Yall[s][: hp.n_pad].copy_(self.Y[s])
+                halo_exchange_fwd(be, hp, self.Yall[s], self.R[s][: len(hp.send_idx)], g)
+            else:
+                all_gather_rows(self.Yall[s], self.Y[s], g)      # K'/M' only
         first = {t: True for t in self.targets}
         for name, x in self.rels.items():
             ts, tt = x["src_type"], x["dst_type"]
@@ -838,8 +870,13 @@ class ShardedHGTProgram:
             self._t("lja_bwd_end")
             be.accumulate(self.dYq[tt][:n], self.dQ[tt][:n], 1.0)
         for s in self.sources:
-            reduce_scatter_rows(self.R[s], self.dYall[s], g)
-            be.accumulate(self.dY[s], self.R[s], 1.0)
+            if s in self.halo:
+                hp = self.halo[s]
+                halo_exchange_bwd(be, hp, self.dYall[s], self.R[s][: len(hp.send_idx)], g)
+                be.accumulate(self.dY[s], self.dYall[s][: hp.n_pad], 1.0)
+            else:
+                reduce_scatter_rows(self.R[s], self.dYall[s], g)
+                be.accumulate(self.dY[s], self.R[s], 1.0)
         self._t("proj_bwd")
         for t in self.blocks:
             first = True

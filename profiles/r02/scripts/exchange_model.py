@@ -47,17 +47,30 @@ def main():
         print(f"| arxiv GCN | {P} | {a:,} | {h:,} | {h / a:.2f} | {la * 1e3:.3f} | {lh * 1e3:.3f} | {hb * 1e3:.3f} |")
     mag = synth.mag_like(42)
     d = 128
+    blocks = {"paper": 4, "author": 4}          # K'/M' blocks per source type
     for P in (2, 4, 8):
-        rows = {}
-        for t, k in mag["key"].items():
-            rows[t] = np.bincount(owner(k, P), minlength=P).max()
-        # HGT: K'/M' blocks of each source type (2 per relation leaving it) all-gathered,
-        # gradients reduce-scattered: 2 x (P-1) n_pad rows x blocks x d x 4 per step
-        blocks = {"paper": 4, "author": 4}
-        b = sum(2 * (P - 1) * rows[t] * nb * d * 4 for t, nb in blocks.items())
-        b_old = sum(2 * (P - 1) * rows[t] * (nb + (1 if t == "paper" else 0) + (1 if t == "paper" else 0)) * d * 4
-                    for t, nb in blocks.items())
-        print(f"| MAG HGT (K'/M' only; was K'/M'/Q x2) | {P} | - | - | {b / b_old:.2f} | {b_old / LINK * 1e3:.3f} | {b / LINK * 1e3:.3f} | {75.9e9 / P / HBM * 1e3:.3f} |")
+        own = {t: owner(k, P) for t, k in mag["key"].items()}
+        n_pad = {t: np.bincount(o, minlength=P).max() for t, o in own.items()}
+        allg = sum(2 * (P - 1) * n_pad[t] * nb * d * 4 for t, nb in blocks.items())
+        halo = 0
+        for t, nb in blocks.items():
+            keys = mag["key"][t]
+            kp = np.argsort(keys)
+            worst = 0
+            for r in range(P):
+                srcs = []
+                for x in mag["rels"].values():
+                    if x["src_type"] != t:
+                        continue
+                    tk = mag["key"][x["dst_type"]]
+                    tp = np.argsort(tk)
+                    od = own[x["dst_type"]][tp[np.searchsorted(tk[tp], x["dst"])]]
+                    srcs.append(x["src"][od == r])
+                ref = np.unique(np.concatenate(srcs))
+                osrc = own[t][kp[np.searchsorted(keys[kp], ref)]]
+                worst = max(worst, int((osrc != r).sum()))
+            halo += 2 * worst * nb * d * 4
+        print(f"| MAG HGT (K'/M' rows) | {P} | {allg // (2 * d * 4 * 8):,} | {halo // (2 * d * 4 * 8):,} | {halo / allg:.2f} | {allg / LINK * 1e3:.3f} | {halo / LINK * 1e3:.3f} | {75.9e9 / P / HBM * 1e3:.3f} |")
 
 
 if __name__ == "__main__":

@@ -1,4 +1,5 @@
-"""Tiny-tier run of every kernel family of librnn.so for compute-sanitizer (memcheck,
+"""Tiny-tier run of every kernel family (SANITIZE_PART=index|lja|proj|dhn|train selects one
+family; default all) of librnn.so for compute-sanitizer (memcheck,
 racecheck, synccheck): index build (+ selection), SUM/MEAN/softmax LJA fwd + bwd (split hub
 groups), epilogue fused + backward, MAX, projection fwd/bwd (tf32 + 3xTF32, wide dY), DHN
 C2/C3/C4 fwd + bwd + counts, xent + Adam, gather / scatter rows."""
@@ -9,6 +10,9 @@ sys.path.insert(0, ".")
 import synth
 from paper_2605_24207_b200 import rnn
 
+import os
+PART = os.environ.get("SANITIZE_PART", "all")
+want = lambda p: PART in ("all", p)
 cu = lambda a: torch.as_tensor(np.ascontiguousarray(a)).cuda()
 rng = np.random.default_rng(0)
 db = synth.random_db(rng, 300, 200, 4000, d_s=16)
@@ -18,23 +22,26 @@ gi = rnn.build_join_index(cu(db["e_src"]), cu(db["e_dst"]), cu(db["s_key"]), cu(
                           rows_per_item=16, e_mask=m, dense_groups=True)
 z = cu(rng.standard_normal((300, 128)).astype(np.float32))
 w = cu(rng.random(gi.n_join_rows).astype(np.float32))
-for agg in ("sum", "mean"):
+for agg in (("sum", "mean") if want("lja") else ()):
     q = rnn.make_query("src", agg, src=z, edge=w, edge_mode=rnn.BY_POSITION)
     out = rnn.join_aggregate_fwd(gi, q)
     rnn.join_aggregate_bwd(gi, q, out.contiguous())
 b = cu(rng.standard_normal(128).astype(np.float32))
 epi = rnn.make_epilogue(bias=b, act="relu")
-y = rnn.join_aggregate_fwd_epi(gi, rnn.make_query("src", "sum", src=z, edge=w, edge_mode=rnn.BY_POSITION), epi)
-rnn.epilogue_bwd(y.contiguous(), y, epi)
-qm = rnn.make_query("src", "max", src=z)
-o, am = rnn.join_aggregate_max_fwd(gi, qm)
-rnn.join_aggregate_max_bwd(gi, qm, am, o.contiguous())
-K = cu(rng.standard_normal((300, 128)).astype(np.float32))
-Q = cu(rng.standard_normal((200, 128)).astype(np.float32))
-qs = rnn.make_query("src", "softmax", src=z, src_key=K, dst=Q, heads=8, scale=0.25)
-o, lse = rnn.join_aggregate_fwd(gi, qs)
-rnn.join_aggregate_bwd(gi, qs, o.contiguous(), out=o, lse=lse)
-for prec in ("tf32", "3xtf32"):
+if not want("lja"):
+    epi = None
+if want("lja"):
+    y = rnn.join_aggregate_fwd_epi(gi, rnn.make_query("src", "sum", src=z, edge=w, edge_mode=rnn.BY_POSITION), epi)
+    rnn.epilogue_bwd(y.contiguous(), y, epi)
+    qm = rnn.make_query("src", "max", src=z)
+    o, am = rnn.join_aggregate_max_fwd(gi, qm)
+    rnn.join_aggregate_max_bwd(gi, qm, am, o.contiguous())
+    K = cu(rng.standard_normal((300, 128)).astype(np.float32))
+    Q = cu(rng.standard_normal((200, 128)).astype(np.float32))
+    qs = rnn.make_query("src", "softmax", src=z, src_key=K, dst=Q, heads=8, scale=0.25)
+    o, lse = rnn.join_aggregate_fwd(gi, qs)
+    rnn.join_aggregate_bwd(gi, qs, o.contiguous(), out=o, lse=lse)
+for prec in (("tf32", "3xtf32") if want("proj") else ()):
     for (M, Kd, N) in [(1000, 128, 128), (700, 64, 384), (300, 200, 48)]:
         X = cu(rng.standard_normal((M, Kd)).astype(np.float32))
         W = cu(rng.standard_normal((N, Kd)).astype(np.float32))
@@ -46,16 +53,17 @@ ok = s != t
 e_n, e_v = np.concatenate([s[ok], t[ok]]), np.concatenate([t[ok], s[ok]])
 adj = rnn.build_join_index(cu(keys[e_v]), cu(keys[e_n]), cu(keys), cu(keys), dense_groups=True)
 f = [cu(rng.standard_normal((120, 32)).astype(np.float32)) for _ in range(4)]
-for k in (2, 3, 4):
+for k in ((2, 3, 4) if want("dhn") else ()):
     ws = torch.empty(adj.n_groups, 32, device="cuda")
     o = rnn.dhn_fwd(adj, k, f[:k], walk_sum=ws)
     rnn.dhn_bwd(adj, k, f[:k], o.contiguous(), walk_sum=ws, symmetric=True)
     rnn.dhn_count(adj, k)
 x = cu(rng.standard_normal((500, 7)).astype(np.float32))
-lab = cu(rng.integers(-1, 7, 500).astype(np.int64))
-loss, d = rnn.softmax_xent(x, lab)
-opt = rnn.Adam([x], lr=0.01, weight_decay=5e-4)
-opt.step([d])
+if want("train"):
+    lab = cu(rng.integers(-1, 7, 500).astype(np.int64))
+    loss, d = rnn.softmax_xent(x, lab)
+    opt = rnn.Adam([x], lr=0.01, weight_decay=5e-4)
+    opt.step([d])
 idx = cu(rng.permutation(500)[:100].astype(np.int32))
 yb = torch.zeros(100, 7, device="cuda")
 rnn.gather_rows(yb, x, idx)

@@ -130,7 +130,10 @@ def check_walks(rnn, keys, e_n, e_v, k, d, seed, ks_count=True, dyadic=False):
     paths = rnn.dhn_path_counters()
     assert paths["c4_value_overflow"] == 0, paths
     assert_close(out[rows], oracle.dhn_fwd(k, oi, keys, f), FP32_TOL, f"C{k} fwd")
-    d_out = rng.standard_normal((gi.n_groups, d)).astype(np.float32)
+    if dyadic:
+        d_out = (rng.integers(-8, 9, (gi.n_groups, d)) / 8.0).astype(np.float32)
+    else:
+        d_out = rng.standard_normal((gi.n_groups, d)).astype(np.float32)
     grads = rnn.dhn_bwd(gi, k, fg, cu(d_out))
     ref_g = oracle.dhn_bwd(k, oi, keys, f, d_out[rows])
     for i in range(k):

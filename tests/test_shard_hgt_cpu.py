@@ -78,8 +78,10 @@ def reference(mag):
     return {"Ht": Ht, "dW": dW, "dH": dH}
 
 
-def _run(mag, backend):
-    prog = ShardedHGTProgram(mag, backend=backend)
+def _run(mag, backend, halo=True):
+    prog = ShardedHGTProgram(mag, backend=backend, halo=halo)
+    if halo and prog.P > 1:      # the halo exchange moves fewer K'/M' rows than the all-gather
+        assert all(h.rows_recv <= h.rows_allgather for h in prog.halo.values())
     prog.step()
     nm = prog.be.numpy
     out = {}
@@ -115,11 +117,11 @@ def test_world_size_1():
     check([_run(mag, HGTOracleBackend())], mag)
 
 
-def _worker(rank, world, port, path):
+def _worker(rank, world, port, path, halo=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        np.savez(os.path.join(path, f"r{rank}.npz"), **_run(small_mag(), HGTOracleBackend()))
+        np.savez(os.path.join(path, f"r{rank}.npz"), **_run(small_mag(), HGTOracleBackend(), halo))
     finally:
         dist.destroy_process_group()
 
@@ -127,5 +129,13 @@ def _worker(rank, world, port, path):
 def test_world_size_2_gloo():
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
+    check(res, small_mag())
+
+
+def test_world_size_2_gloo_allgather():
+    """K'/M' all-gather (halo=False) gives the same result as the per-type halo exchange."""
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(2, _free_port(), d, False), nprocs=2, join=True)
         res = [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(2)]
     check(res, small_mag())
