@@ -43,16 +43,21 @@ def parse():
                     help="workload (default: MAG-shaped HGT, the largest single-GPU config)")
     ap.add_argument("--dhn-scale", type=float, default=1.0,
                     help="fraction of the ogbn-products-shaped graph for --config dhn")
-    ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32"])
+    ap.add_argument("--prec", default="3xtf32", choices=["3xtf32", "tf32", "bf16"])
     ap.add_argument("--seeds", default=None,
                     help="comma-separated input seeds (default 42..46, PAPER.md:851; dhn: 42)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true",
                     help="launch the step kernel by kernel instead of replaying its CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l2-window", action="store_true",
+                    help="experiment (GCN configs, implies --eager): persisting-L2 window over "
+                         "each LJA's gathered matrix")
     ap.add_argument("--profile-launches", action="store_true",
                     help="count kernel launches with torch.profiler (untimed pass)")
     a = ap.parse_args()
+    if a.l2_window:
+        a.eager = True
     if a.seeds is None:
         a.seeds = "42" if a.config == "dhn" else "42,43,44,45,46"
     return a
@@ -305,6 +310,8 @@ def run_ours(args):
     first = None
     for si, seed in enumerate(seeds):
         prog, rows, sharded = _build(args, seed, world, dev)
+        if args.l2_window:
+            prog.l2_window = True
         graphed = not args.eager and (not sharded or args.config != "dhn")
         if si == 0:
             sampler.start()                   # clocks sampled during the timed regions
@@ -392,6 +399,8 @@ def run_ours(args):
                "projection_precision": args.prec, "l2": "flushed between timed steps",
                "step_launch": "one CUDA graph replay" if first["graphed"] else "eager launches",
                "seeds": seeds,
+               **({"l2_window": "persisting window over each LJA's gathered matrix"}
+                  if args.l2_window else {}),
                "parallelism": (f"hash-partition by group key x{world} ({SHARD_DESC[args.config]})"
                                if sharded else f"replica x{world}" if world > 1 else "single")}
         result = {

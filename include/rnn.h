@@ -315,9 +315,13 @@ rnn_status rnn_adam(float* param, int64_t rows, int32_t cols, int64_t ld_param, 
  * are one GEMM with their weights stacked).  Precision:
  *   RNN_PREC_TF32   : one kind::tf32 MMA per tile (operands truncated to tf32).
  *   RNN_PREC_3XTF32 : split-operand 3xTF32 (hi*hi + hi*lo + lo*hi), ~fp32 accuracy.
+ *   RNN_PREC_BF16   : both operands rounded to bf16 (round-to-nearest-even) on chip, exact
+ *                     bf16 x bf16 products, fp32 accumulation (north_star's bf16 projection,
+ *                     tolerance 1e-2); storage stays fp32 (the embeddings are fp32), so the
+ *                     rounded operands run through the kind::tf32 MMA, in which bf16 is exact.
  * Backward: dX = dY . W (may be NULL), dW = dY^T . X (required), db = colsum(dY) (may be NULL),
  * all written.  workspace: dW partials (deterministic split-M reduction). */
-typedef enum { RNN_PREC_TF32 = 0, RNN_PREC_3XTF32 = 1 } rnn_precision;
+typedef enum { RNN_PREC_TF32 = 0, RNN_PREC_3XTF32 = 1, RNN_PREC_BF16 = 2 } rnn_precision;
 rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t ldx, const float* W,
                        int32_t N, int64_t ldw, const float* bias, float* Y, int64_t ldy,
                        rnn_precision prec, void* stream);
@@ -326,6 +330,19 @@ rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, co
                            int32_t N, int64_t ldw, const float* dY, int64_t lddy, float* dX,
                            int64_t lddx, float* dW, float* db, rnn_precision prec,
                            void* workspace, size_t workspace_bytes, void* stream);
+/* Backward of a projection whose input is the output of a ReLU epilogue, X = ReLU(P) (the
+ * hidden layers of the GCN program, H^l = ReLU(A Z + b); rnn_epilogue_fwd with
+ * RNN_ACT_RELU): as rnn_project_bwd, but dX (required) receives the gradient at the epilogue's
+ * input, dP = (dY . W) (.) [X > 0], and d_in_bias (nullable) receives colsum(dP), the epilogue's
+ * bias gradient -- i.e. rnn_project_bwd followed by rnn_epilogue_bwd(relu) on dX, in one pass
+ * where dY has <= 128 columns (the mask is applied in the tensor-core kernel's store).  Same
+ * workspace as rnn_project_bwd; results equal that two-call sequence up to summation order of
+ * d_in_bias (fixed order, deterministic). */
+rnn_status rnn_project_bwd_relu(const float* X, int64_t M, int32_t K, int64_t ldx, const float* W,
+                                int32_t N, int64_t ldw, const float* dY, int64_t lddy, float* dX,
+                                int64_t lddx, float* dW, float* db, float* d_in_bias,
+                                rnn_precision prec, void* workspace, size_t workspace_bytes,
+                                void* stream);
 
 /* ===================================================================================== */
 /* A6. Multi-way cyclic joins: DHN closed-walk pattern aggregates                        */
@@ -466,6 +483,14 @@ rnn_status rnn_scatter_add_rows(float* y, int64_t ldy, const float* x, int64_t l
 /* Multi-GPU ownership of group keys: owner[i] = splitmix64(keys[i] ^ seed) mod P. */
 rnn_status rnn_hash_partition(const int64_t* keys, int64_t n, int32_t P, uint64_t seed,
                               int32_t* owner, void* stream);
+
+/* Residency hint for the gathered embedding matrix (north_star: "keep hot rows on chip"):
+ * sets `stream`'s L2 access-policy window to [base, base + bytes) with the given hit ratio
+ * (hits persisting, misses streaming) and reserves min(bytes * hit_ratio, device maximum)
+ * of L2 for persisting lines; bytes = 0 clears the window and resets persisting lines.
+ * Kernels launched on the stream afterwards (and kernel nodes captured from it) carry the
+ * window.  SYNC for the limit change (cudaDeviceSetLimit). */
+rnn_status rnn_stream_l2_window(void* stream, const void* base, size_t bytes, float hit_ratio);
 
 #ifdef __cplusplus
 }

@@ -107,8 +107,10 @@ __global__ void __launch_bounds__(256) epi_bwd4_kernel(const float* __restrict__
     const float4 bias = e.bias ? *reinterpret_cast<const float4*>(e.bias + c) : sb;
     for (int64_t r = r0 + wp; r < r1; r += 8) {
       const float4 g = *reinterpret_cast<const float4*>(dy + r * lddy + c);
-      float4 xb = e.pre ? *reinterpret_cast<const float4*>(e.pre + r * e.ld_pre + c)
-                        : *reinterpret_cast<const float4*>(y + r * ldy + c);
+      // act none without the gate's sum: act' = 1, the forward output is not read
+      float4 xb = (e.act == 0 && !part_g) ? make_float4(0.f, 0.f, 0.f, 0.f)
+                  : e.pre ? *reinterpret_cast<const float4*>(e.pre + r * e.ld_pre + c)
+                          : *reinterpret_cast<const float4*>(y + r * ldy + c);
       float4 d;
       d.x = g.x * e.gate * epi_dact(e.act, xb.x);
       d.y = g.y * e.gate * epi_dact(e.act, xb.y);

@@ -1,5 +1,6 @@
 // misc.cu -- program helpers: GCN normalisation weights and the multi-GPU hash partition.
 #include "common.cuh"
+#include <algorithm>
 
 namespace rnn {
 namespace {
@@ -201,5 +202,39 @@ extern "C" rnn_status rnn_scatter_add_rows(float* y, int64_t ldy, const float* x
   scatter_add_rows_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, as_stream(stream)>>>(y, ldy, x, ldx,
                                                                                   idx, n, cols);
   RNN_LAUNCH_CHECK();
+  return RNN_OK;
+}
+
+extern "C" rnn_status rnn_stream_l2_window(void* stream, const void* base, size_t bytes,
+                                           float hit_ratio) {
+  clear_error();
+  RNN_REQUIRE((bytes == 0 || base) && hit_ratio >= 0.f && hit_ratio <= 1.f,
+              RNN_ERR_INVALID_ARGUMENT, "bad argument");
+  cudaStream_t st = as_stream(stream);
+  int dev = 0, max_persist = 0, max_window = 0;
+  RNN_CUDA(cudaGetDevice(&dev));
+  RNN_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  RNN_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  cudaStreamAttrValue v{};
+  if (bytes == 0) {
+    v.accessPolicyWindow.base_ptr = nullptr;
+    v.accessPolicyWindow.num_bytes = 0;
+    v.accessPolicyWindow.hitRatio = 0.f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyNormal;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+    RNN_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
+    RNN_CUDA(cudaCtxResetPersistingL2Cache());
+    RNN_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0));
+    return RNN_OK;
+  }
+  const size_t win = std::min(bytes, (size_t)max_window);
+  const size_t want = (size_t)((double)win * hit_ratio);
+  RNN_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(want, (size_t)max_persist)));
+  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = hit_ratio;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  RNN_CUDA(cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &v));
   return RNN_OK;
 }

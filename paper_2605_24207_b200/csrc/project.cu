@@ -16,6 +16,7 @@
 // latter gives dW = dY^T X without materialising transposes (smem descriptor major bit).
 // Split-K over z with partial tiles reduced in a fixed order keeps dW deterministic.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -182,16 +183,41 @@ __device__ __forceinline__ void lo_tile(const float4* x, float4* lo, uint32_t n1
   for (; i < n16; i += NT) lo[i] = lo_part(x[i]);
 }
 
+// RNN_PREC_BF16: operands rounded to bf16 (round-to-nearest-even) in shared memory; a bf16 value
+// is exact in tf32 (8-bit exponent, 7 <= 10 mantissa bits), so the kind::tf32 MMA then forms the
+// exact bf16 x bf16 products with fp32 accumulation -- numerically a bf16 GEMM over fp32 storage
+__device__ __forceinline__ float bf16_rn(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+__device__ __forceinline__ float4 bf16_rn4(float4 v) {
+  return make_float4(bf16_rn(v.x), bf16_rn(v.y), bf16_rn(v.z), bf16_rn(v.w));
+}
+template <int NT = 128>
+__device__ __forceinline__ void bf16_tile(float4* x, uint32_t n16, int t) {
+  uint32_t i = t;
+  for (; i + 7 * NT < n16; i += 8 * NT) {
+    float4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = x[i + u * NT];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[i + u * NT] = bf16_rn4(v[u]);
+  }
+  for (; i < n16; i += NT) x[i] = bf16_rn4(x[i]);
+}
+
+// precision modes of the tensor-core kernels (template argument PM = rnn_precision)
+constexpr int PM_TF32 = 0, PM_3X = 1, PM_BF16 = 2;
+
 // per-role wait cycles of tc_gemm_kernel (internal hook rnn_internal_gemm_stats): [0] producer
 // waits for a free slot, [1] MMA waits for a ready stage, [2] converter waits for a landed
 // stage, [3] TMA latency (issue -> landed, summed over stages, converter / MMA side),
 // [4] stages counted for [3]; [8..10] total cycles of producer, MMA, converter lanes
 __device__ unsigned long long g_gemm_stats[16];
 
-template <bool A_MN, bool B_MN, bool SPLIT3, int KB = BK>
+template <bool A_MN, bool B_MN, int PM, int KB = BK>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    GemmParams p) {
+  constexpr bool SPLIT3 = PM == PM_3X;   // hi/lo split tiles
+  constexpr bool CONV = PM != PM_TF32;   // a converter pass over every landed stage
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte align the carve (swizzle atoms)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -293,7 +319,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t ph = (kb / p.stages) & 1;
       {
         RNN_PROBE(const long long t0 = clock64();)
-        mbar_wait(SPLIT3 ? &conv[s] : &full[s], ph);
+        mbar_wait(CONV ? &conv[s] : &full[s], ph);
         RNN_PROBE(const long long t1 = clock64(); gs_w[1] += t1 - t0;
                   if (!SPLIT3) { gs_w[3] += t1 - *(volatile long long*)&gs_issue[s]; gs_w[4] += 1; })
       }
@@ -325,7 +351,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else {
     // ---------------- converters (3xTF32): warps 2..9; epilogue: warps 2..5 ----------------
     const int et = threadIdx.x - 64;  // 0..255
-    if (SPLIT3) {
+    if (CONV) {
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % p.stages;
         const uint32_t ph = (kb / p.stages) & 1;
@@ -335,12 +361,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           RNN_PROBE(const long long t1 = clock64(); gs_w[2] += t1 - t0;
                     gs_w[3] += t1 - *(volatile long long*)&gs_issue[s]; gs_w[4] += 1;)
         }
-        // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
-        lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(a_hi(s)),
-                              reinterpret_cast<float4*>(a_lo(s)), A_BYTES / 16, et);
-        if (B_MN || p.b_lo_row == 0)   // else B's lo part was precomputed and loaded by TMA
-          lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(b_hi(s)),
-                                reinterpret_cast<float4*>(b_lo(s)), B_BYTES / 16, et);
+        if (SPLIT3) {
+          // lo = x - trunc_tf32(x); the raw tile is the hi part (the MMA truncates)
+          lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(a_hi(s)),
+                                reinterpret_cast<float4*>(a_lo(s)), A_BYTES / 16, et);
+          if (B_MN || p.b_lo_row == 0)   // else B's lo part was precomputed and loaded by TMA
+            lo_tile<CONV_THREADS>(reinterpret_cast<const float4*>(b_hi(s)),
+                                  reinterpret_cast<float4*>(b_lo(s)), B_BYTES / 16, et);
+        } else {
+          bf16_tile<CONV_THREADS>(reinterpret_cast<float4*>(a_hi(s)), A_BYTES / 16, et);
+          bf16_tile<CONV_THREADS>(reinterpret_cast<float4*>(b_hi(s)), B_BYTES / 16, et);
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&conv[s]);
       }
@@ -429,10 +460,11 @@ __device__ __forceinline__ void split_tile(float4* hi, float4* lo, uint32_t n16,
   }
 }
 
-template <bool SPLIT3>
+template <int PM>
 __global__ void __launch_bounds__(PT_THREADS, 1)
     tc_proj_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                    ProjParams p) {
+  constexpr bool SPLIT3 = PM == PM_3X, CONV = PM != PM_TF32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -506,7 +538,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     }
   } else if (warp == 1) {
     const uint32_t idesc = make_idesc(p.BN, false, false);
-    mbar_wait(SPLIT3 ? b_conv : b_full, 0);
+    mbar_wait(CONV ? b_conv : b_full, 0);
     tc_fence_after();
     int64_t it = 0;
     int j = 0;
@@ -518,7 +550,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
       for (int kb = 0; kb < p.nkb; ++kb, ++it) {
         const int s = (int)(it % p.stages);
         const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-        mbar_wait(SPLIT3 ? &a_conv[s] : &a_full[s], ph);
+        mbar_wait(CONV ? &a_conv[s] : &a_full[s], ph);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t ah = smem_u32(a_base + s * A_STAGE);
@@ -543,10 +575,13 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
       __syncwarp();
     }
   } else if (warp < 6) {
-    if (SPLIT3) {
+    if (CONV) {
       const int t = threadIdx.x - 64;
       mbar_wait(b_full, 0);
-      split_tile(reinterpret_cast<float4*>(b_hi), reinterpret_cast<float4*>(b_lo), B_RES / 16, t);
+      if (SPLIT3)
+        split_tile(reinterpret_cast<float4*>(b_hi), reinterpret_cast<float4*>(b_lo), B_RES / 16, t);
+      else
+        bf16_tile(reinterpret_cast<float4*>(b_hi), B_RES / 16, t);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(b_conv);
       int64_t it = 0;
@@ -556,8 +591,11 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
           const uint32_t ph = (uint32_t)((it / p.stages) & 1);
           mbar_wait(&a_full[s], ph);
           uint8_t* a = a_base + s * A_STAGE;
-          split_tile(reinterpret_cast<float4*>(a), reinterpret_cast<float4*>(a + A_BYTES),
-                     A_BYTES / 16, t);
+          if (SPLIT3)
+            split_tile(reinterpret_cast<float4*>(a), reinterpret_cast<float4*>(a + A_BYTES),
+                       A_BYTES / 16, t);
+          else
+            bf16_tile(reinterpret_cast<float4*>(a), A_BYTES / 16, t);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_arrive(&a_conv[s]);
         }
@@ -652,6 +690,11 @@ struct ProjTParams {
   const float* W; int64_t ldw;   // [N, K] row-major
   float* out; int64_t ldo;
   const float* bias;
+  // fused ReLU backward of the layer that produced the GEMM's reduction input (dX of a
+  // projection whose input X = ReLU(pre)): out *= [relu_src > 0], per-CTA column sums of the
+  // masked output into colsum[blockIdx.x][N] (the producing epilogue's bias gradient)
+  const float* relu_src; int64_t ld_relu;
+  float* colsum;
 };
 
 __device__ __forceinline__ void tc_mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
@@ -671,10 +714,11 @@ __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&r)[16])
       : "memory");
 }
 
-template <bool SPLIT3>
+template <int PM>
 __global__ void __launch_bounds__(PT_THREADS, 1)
     tc_projt_kernel(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap ty,
                     ProjTParams p) {
+  constexpr bool SPLIT3 = PM == PM_3X, CONV = PM != PM_TF32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -752,7 +796,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
       for (int kb = 0; kb < p.nkb; ++kb, ++it) {
         const int s = (int)(it % p.stages);
         const uint32_t ph = (uint32_t)((it / p.stages) & 1);
-        PT_WAIT(3, mbar_wait(SPLIT3 ? &x_conv[s] : &x_full[s], ph));
+        PT_WAIT(3, mbar_wait(CONV ? &x_conv[s] : &x_full[s], ph));
         tc_fence_after();
         if (lane == 0) {
           const uint32_t xs = smem_u32(smem + s * X_STAGE);
@@ -775,7 +819,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
       __syncwarp();
     }
   } else if (warp < 6) {
-    if (SPLIT3) {
+    if (CONV) {
       const int t = threadIdx.x - 64;
       int64_t it = 0;
       for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep) {
@@ -784,8 +828,11 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
           const uint32_t ph = (uint32_t)((it / p.stages) & 1);
           PT_WAIT(4, mbar_wait(&x_full[s], ph));
           uint8_t* x = smem + s * X_STAGE;
-          lo_tile(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(x + X_BYTES),
-                  X_BYTES / 16, t);
+          if (SPLIT3)
+            lo_tile(reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(x + X_BYTES),
+                    X_BYTES / 16, t);
+          else
+            bf16_tile(reinterpret_cast<float4*>(x), X_BYTES / 16, t);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           mbar_arrive(&x_conv[s]);
         }
@@ -835,7 +882,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const float w = tp[lane * 65 + h + q];
+          const float w = PM == PM_BF16 ? bf16_rn(tp[lane * 65 + h + q]) : tp[lane * 65 + h + q];
           hi[q] = __float_as_uint(w);
           lo[q] = __float_as_uint(w - __uint_as_float(__float_as_uint(w) & 0xFFFFE000u));
         }
@@ -851,6 +898,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
     // output staging (2 x 4 KB per warp) aliases the W transpose tiles, which are done
     float* stage_out = reinterpret_cast<float*>(smem + p.stages * X_STAGE + 1024) + quad * 2 * 32 * 32;
     const float bf = (p.bias && f < p.N) ? __ldg(p.bias + f) : 0.f;
+    float csum = 0.f;   // fused ReLU backward: this thread's column sum (feature f)
     int j = 0;
     for (int64_t mt = mt0; mt < p.n_tiles_m; mt += mstep, ++j) {
       const int buf = j & 1;
@@ -873,8 +921,26 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         float* st = stage_out + sb * 32 * 32;
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
+        if (p.relu_src) {
+          // d pre = dX (.) [X > 0]: the mask row of the producing layer's output, 32 rows per
+          // chunk, each load one coalesced 128-byte row segment across the warp
+          const bool fok = f < p.N;
+          float mk[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) st[q * 32 + lane] = __uint_as_float(r[q]) + bf;
+          for (int q = 0; q < 32; ++q) {
+            const int64_t row = r0 + c0 + q;
+            mk[q] = (fok && row < p.M) ? __ldg(p.relu_src + row * p.ld_relu + f) : 0.f;
+          }
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const float v = mk[q] > 0.f ? __uint_as_float(r[q]) + bf : 0.f;
+            csum += v;
+            st[q * 32 + lane] = v;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) st[q * 32 + lane] = __uint_as_float(r[q]) + bf;
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) {
@@ -890,6 +956,7 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
       mbar_arrive(&acc_empty[buf]);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (p.colsum && f < p.N) p.colsum[(int64_t)blockIdx.x * p.N + f] = csum;
   }
   RNN_PROBE(if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 6)) {
     const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : 3;
@@ -979,6 +1046,25 @@ __global__ void colsum_final(const float* __restrict__ part, int64_t chunks, int
   for (int64_t k = 0; k < chunks; ++k) s += part[k * N + c];
   out[c] = s;
 }
+// column sums of the fused ReLU backward (tc_projt_kernel colsum): CTA c wrote the features of
+// column block c % n_tiles_n, so feature f sums the CTAs nt(f), nt(f) + n_tiles_n, ... in order
+__global__ void projt_colsum_final(const float* __restrict__ part, int grid, int n_tiles_n, int N,
+                                   float* __restrict__ out) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= N) return;
+  float s = 0.f;
+  for (int c = f / 128; c < grid; c += n_tiles_n) s += part[(int64_t)c * N + f];
+  out[f] = s;
+}
+// dX *= [X > 0] (the unfused path of rnn_project_bwd_relu)
+__global__ void relu_mask_kernel(float* __restrict__ dx, int64_t lddx, const float* __restrict__ x,
+                                 int64_t ldx, int64_t M, int K) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= M * K) return;
+  const int64_t r = i / K;
+  const int k = (int)(i % K);
+  if (!(x[r * ldx + k] > 0.f)) dx[r * lddx + k] = 0.f;
+}
 
 // Wt[k, n] = W[n, k] (hi, rows 0..K-1) and Wt[K + k, n] = lo part (3xTF32 B operand)
 __global__ void transpose_hilo_kernel(const float* __restrict__ W, int N, int K, int64_t ldw,
@@ -1063,9 +1149,10 @@ uint32_t pow2_cols(int bn) {
   return c;
 }
 
-template <bool A_MN, bool B_MN, bool SPLIT3>
+template <bool A_MN, bool B_MN, int PM>
 rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams p, int splits,
                        cudaStream_t st) {
+  constexpr bool SPLIT3 = PM == PM_3X;
   constexpr int KB = (A_MN && B_MN) ? 16 : BK;
   const uint32_t stage = (uint32_t)(BM * KB * 4 + p.BN * KB * 4) * (SPLIT3 ? 2u : 1u);
   const int64_t nkb_max = ceil_div(p.k_split, KB);
@@ -1078,7 +1165,7 @@ rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams 
   p.stages = stages;
   p.tmem_cols = pow2_cols(p.BN);
   const size_t smem = (size_t)stages * stage + 1024 + 8 * (3 * MAX_STAGES + 2) + 64;
-  auto kern = tc_gemm_kernel<A_MN, B_MN, SPLIT3, KB>;
+  auto kern = tc_gemm_kernel<A_MN, B_MN, PM, KB>;
   RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)ceil_div(p.M, BM), (unsigned)ceil_div(p.N, p.BN), (unsigned)splits);
   kern<<<grid, THREADS, smem, st>>>(ta, tb, p);
@@ -1089,8 +1176,9 @@ rnn_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, GemmParams 
 template <bool A_MN, bool B_MN>
 rnn_status gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmParams& p, int splits,
                 rnn_precision prec, cudaStream_t st) {
-  if (prec == RNN_PREC_3XTF32) return launch_gemm<A_MN, B_MN, true>(ta, tb, p, splits, st);
-  return launch_gemm<A_MN, B_MN, false>(ta, tb, p, splits, st);
+  if (prec == RNN_PREC_3XTF32) return launch_gemm<A_MN, B_MN, PM_3X>(ta, tb, p, splits, st);
+  if (prec == RNN_PREC_BF16) return launch_gemm<A_MN, B_MN, PM_BF16>(ta, tb, p, splits, st);
+  return launch_gemm<A_MN, B_MN, PM_TF32>(ta, tb, p, splits, st);
 }
 
 __global__ void bias_fill(float* Y, int64_t M, int N, int64_t ldy, const float* b) {
@@ -1098,11 +1186,20 @@ __global__ void bias_fill(float* Y, int64_t M, int N, int64_t ldy, const float* 
   if (i < M * N) Y[(i / N) * ldy + i % N] = b ? b[i % N] : 0.f;
 }
 
+// Fused ReLU backward for the TMEM-resident kernel (rnn_project_bwd_relu): Y *= [relu_src > 0]
+// and per-CTA column sums into colsum; `fused` reports whether that kernel ran (else the caller
+// masks and sums Y itself).
+struct ReluBwd {
+  const float* src; int64_t ld;
+  float* colsum;
+  bool fused; int grid, n_tiles_n;
+};
+
 // Y[M, N] = A[M, Kred] B[N, Kred]^T (+bias), both K-major
 // b_has_lo: rows N .. 2N-1 of B hold lo = B - trunc_tf32(B) (precomputed by the caller)
 rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const float* B, int N,
                    int64_t ldb, const float* bias, float* Y, int64_t ldy, rnn_precision prec,
-                   cudaStream_t st, bool b_has_lo = false) {
+                   cudaStream_t st, bool b_has_lo = false, ReluBwd* rb = nullptr) {
   if (M == 0 || N == 0) return RNN_OK;
   if (Kred == 0) {
     bias_fill<<<(unsigned)ceil_div(M * N, 256), 256, 0, st>>>(Y, M, N, ldy, bias);
@@ -1123,6 +1220,7 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
     const size_t budget = 227 * 1024 - 1024 - 256 - tscratch;
     q.stages = (int)std::min<size_t>(PX_STAGES, budget / x_stage);
     q.W = B; q.ldw = ldb; q.out = Y; q.ldo = ldy; q.bias = bias;
+    if (rb) { q.relu_src = rb->src; q.ld_relu = rb->ld; q.colsum = rb->colsum; }
     CUtensorMap tx, ty;
     RNN_TRY(make_map(&tx, A, Kred, M, lda, BK, BM));
     RNN_TRY(make_map(&ty, Y, N, M, ldy, 32, 32, false, /*swizzle=*/false));
@@ -1130,10 +1228,12 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
         std::max<int64_t>(1, std::min<int64_t>(num_sms() / q.n_tiles_n, q.n_tiles_m));
     const unsigned grid = (unsigned)(per_n * q.n_tiles_n);
     const size_t smem = q.stages * x_stage + 1024 + tscratch;
-    auto kern = s3 ? tc_projt_kernel<true> : tc_projt_kernel<false>;
+    auto kern = s3 ? tc_projt_kernel<PM_3X>
+                : prec == RNN_PREC_BF16 ? tc_projt_kernel<PM_BF16> : tc_projt_kernel<PM_TF32>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, PT_THREADS, smem, st>>>(tx, ty, q);
     RNN_LAUNCH_CHECK();
+    if (rb) { rb->fused = true; rb->grid = (int)grid; rb->n_tiles_n = q.n_tiles_n; }
     return RNN_OK;
   }
   {
@@ -1159,7 +1259,8 @@ rnn_status gemm_kk(const float* A, int64_t M, int64_t Kred, int64_t lda, const f
       const int64_t per_n = std::max<int64_t>(1, std::min<int64_t>(num_sms() / n_tiles_n, q.n_tiles_m));
       const unsigned grid = (unsigned)(per_n * n_tiles_n);
       const size_t smem = b_res + q.stages * a_stage + 1024 + 8 * (3 * PT_MAX_STAGES + 6) + 64;
-      auto kern = s3 ? tc_proj_kernel<true> : tc_proj_kernel<false>;
+      auto kern = s3 ? tc_proj_kernel<PM_3X>
+                  : prec == RNN_PREC_BF16 ? tc_proj_kernel<PM_BF16> : tc_proj_kernel<PM_TF32>;
       RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<grid, PT_THREADS, smem, st>>>(ta, tb, q);
       RNN_LAUNCH_CHECK();
@@ -1192,14 +1293,15 @@ extern "C" rnn_status rnn_project(const float* X, int64_t M, int32_t K, int64_t 
   RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 0 && K <= 8192 && N >= 1 && N <= 8192,
               RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, K <= 8192, 1 <= N <= 8192");
   RNN_REQUIRE(ldx >= K && ldw >= K && ldy >= N, RNN_ERR_INVALID_ARGUMENT, "ld too small");
-  RNN_REQUIRE(prec == RNN_PREC_TF32 || prec == RNN_PREC_3XTF32, RNN_ERR_INVALID_ARGUMENT,
+  RNN_REQUIRE(prec == RNN_PREC_TF32 || prec == RNN_PREC_3XTF32 || prec == RNN_PREC_BF16,
+              RNN_ERR_INVALID_ARGUMENT,
               "precision");
   return gemm_kk(X, M, K, ldx, W, N, ldw, bias, Y, ldy, prec, as_stream(stream));
 }
 
 namespace {
 struct BwdWs {
-  float* Wt; float* dWt; float* part; float* part2; float* cpart;
+  float* Wt; float* dWt; float* part; float* part2; float* cpart; float* rpart;
   size_t bytes;
   int splits; int64_t chunks;
 };
@@ -1211,6 +1313,7 @@ struct BwdWs {
 #define RNN_DW_MAX_CHAIN 2048
 #endif
 constexpr int64_t DW_MAX_CHAIN = RNN_DW_MAX_CHAIN;
+constexpr int64_t RELU_PART_ROWS = 1024;   // >= the fused kernel's grid (SMs, or column blocks)
 inline bool dw_swapped(int K, int N) { return N > 128 && K <= 128 && !getenv("RNN_NO_DWT"); }
 
 BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
@@ -1239,6 +1342,9 @@ BwdWs bwd_ws(int64_t M, int K, int N, void* base) {
   w.part2 = c.take<float>((size_t)ceil_div(splits, 8) * N * K);
   w.chunks = ceil_div(M > 0 ? M : 1, 4096);
   w.cpart = c.take<float>((size_t)w.chunks * N);
+  // ReLU-input column sums: one row per CTA of the fused kernel (<= RELU_PART_ROWS) or per
+  // 4096-row chunk of the unfused path
+  w.rpart = c.take<float>((size_t)std::max<int64_t>(RELU_PART_ROWS, w.chunks) * K);
   w.bytes = c.used + 1024;
   return w;
 }
@@ -1252,13 +1358,14 @@ extern "C" rnn_status rnn_project_bwd_workspace_size(int64_t M, int32_t K, int32
   return RNN_OK;
 }
 
-extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx,
-                                      const float* W, int32_t N, int64_t ldw, const float* dY,
-                                      int64_t lddy, float* dX, int64_t lddx, float* dW, float* db,
-                                      rnn_precision prec, void* workspace,
-                                      size_t workspace_bytes, void* stream) {
-  clear_error();
+namespace {
+rnn_status project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, const float* W, int32_t N,
+                       int64_t ldw, const float* dY, int64_t lddy, float* dX, int64_t lddx,
+                       float* dW, float* db, bool relu_in, float* d_in_bias, rnn_precision prec,
+                       void* workspace, size_t workspace_bytes, void* stream) {
   RNN_REQUIRE(X && W && dY && dW, RNN_ERR_INVALID_ARGUMENT, "X, W, dY, dW required");
+  RNN_REQUIRE(prec == RNN_PREC_TF32 || prec == RNN_PREC_3XTF32 || prec == RNN_PREC_BF16,
+              RNN_ERR_INVALID_ARGUMENT, "precision");
   RNN_REQUIRE(M >= 0 && M < (int64_t(1) << 31) && K >= 1 && K <= 8192 && N >= 1 && N <= 8192,
               RNN_ERR_UNSUPPORTED, "shape outside M < 2^31, 1 <= K <= 8192, 1 <= N <= 8192");
   RNN_REQUIRE(ldx >= K && ldw >= K && lddy >= N && (!dX || lddx >= K), RNN_ERR_INVALID_ARGUMENT,
@@ -1273,7 +1380,30 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
     transpose_hilo_kernel<<<(unsigned)ceil_div((int64_t)N * K, 256), 256, 0, st>>>(W, N, K, ldw, w.Wt,
                                                                              ldt);
     RNN_LAUNCH_CHECK();
-    RNN_TRY(gemm_kk(dY, M, N, lddy, w.Wt, K, ldt, nullptr, dX, lddx, prec, st, true));
+    ReluBwd rb{X, ldx, w.rpart, false, 0, 0};
+    RNN_TRY(gemm_kk(dY, M, N, lddy, w.Wt, K, ldt, nullptr, dX, lddx, prec, st, true,
+                    relu_in ? &rb : nullptr));
+    if (relu_in && M > 0) {
+      if (!rb.fused) {
+        relu_mask_kernel<<<(unsigned)ceil_div(M * K, 256), 256, 0, st>>>(dX, lddx, X, ldx, M, K);
+        RNN_LAUNCH_CHECK();
+      }
+      if (d_in_bias) {
+        if (rb.fused) {
+          RNN_REQUIRE(rb.grid <= RELU_PART_ROWS, RNN_ERR_UNSUPPORTED, "fused grid %d", rb.grid);
+          projt_colsum_final<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(w.rpart, rb.grid,
+                                                                        rb.n_tiles_n, K, d_in_bias);
+        } else {
+          dim3 g1((unsigned)ceil_div(K, 32), (unsigned)w.chunks);
+          colsum_partial<<<g1, 256, 0, st>>>(dX, M, K, lddx, 4096, w.rpart);
+          colsum_final<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(w.rpart, w.chunks, K,
+                                                                   d_in_bias);
+        }
+        RNN_LAUNCH_CHECK();
+      }
+    } else if (relu_in && d_in_bias) {
+      RNN_CUDA(cudaMemsetAsync(d_in_bias, 0, sizeof(float) * K, st));
+    }
   }
   // dW = dY^T X : both operands MN-major, split over M, ordered reduction
   if (M == 0) {
@@ -1348,6 +1478,29 @@ extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int6
     }
   }
   return RNN_OK;
+}
+}  // namespace
+
+extern "C" rnn_status rnn_project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx,
+                                      const float* W, int32_t N, int64_t ldw, const float* dY,
+                                      int64_t lddy, float* dX, int64_t lddx, float* dW, float* db,
+                                      rnn_precision prec, void* workspace,
+                                      size_t workspace_bytes, void* stream) {
+  clear_error();
+  return project_bwd(X, M, K, ldx, W, N, ldw, dY, lddy, dX, lddx, dW, db, false, nullptr, prec,
+                     workspace, workspace_bytes, stream);
+}
+
+extern "C" rnn_status rnn_project_bwd_relu(const float* X, int64_t M, int32_t K, int64_t ldx,
+                                           const float* W, int32_t N, int64_t ldw,
+                                           const float* dY, int64_t lddy, float* dX, int64_t lddx,
+                                           float* dW, float* db, float* d_in_bias,
+                                           rnn_precision prec, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  clear_error();
+  RNN_REQUIRE(dX, RNN_ERR_INVALID_ARGUMENT, "dX is required");
+  return project_bwd(X, M, K, ldx, W, N, ldw, dY, lddy, dX, lddx, dW, db, true, d_in_bias, prec,
+                     workspace, workspace_bytes, stream);
 }
 
 // Internal test hook (not part of include/rnn.h): C[M, N] = A . B with A given K-major

@@ -112,6 +112,9 @@ def _comp_bwd(idx, d, weighted=False):
 
 class GCNProgram(_Program):
     """L-layer GCN as lifted queries; step() = forward + backward of every layer."""
+    # experiment knob (profiles/r02/l2window): a persisting-L2 window over each LJA's gathered
+    # matrix (eager steps only: the limit change is not capturable)
+    l2_window = False
 
     def __init__(self, graph: dict, device="cuda", prec="3xtf32", rows_per_item=0):
         self.device = torch.device(device)
@@ -197,6 +200,8 @@ class GCNProgram(_Program):
             rnn.project(self.H[l], self.W[l], out=self.Z[l], prec=self.prec)
             self._t("proj_fwd_end")
             idx, q = self.q[l]
+            if self.l2_window:
+                rnn.stream_l2_window(self.Z[l])      # the gathered matrix of this layer
             self._t("lja_fwd")
             if self.b is not None:
                 rnn.join_aggregate_fwd_epi(idx, q, self.epi[l], out=self.H[l + 1], ws=self.ws)
@@ -206,24 +211,37 @@ class GCNProgram(_Program):
         return self.H[-1]
 
     def backward(self, d_out=None):
+        """With the O7 epilogue: the last layer's (bias only) backward is d bias = colsum(dY)
+        and dY passes through unchanged; every hidden layer's ReLU backward is fused into the
+        next layer's projection backward (rnn_project_bwd_relu: its input H^l is the ReLU
+        output, so dX comes out as d(pre-activation) and the bias gradient as its column sums).
+        Without it, dH^l = dZ^l W^l as in the bare lifted query."""
         dY = self.d_out if d_out is None else d_out
         for l in reversed(range(self.L)):
             idx, q = self.q[l]
-            if self.b is not None:
-                # epilogue backward: d(pre-activation) and d(bias) from the layer output's sign
+            if self.b is not None and l == self.L - 1:
                 self._t("epi_bwd")
-                rnn.epilogue_bwd(dY, self.H[l + 1], self.epi[l], dx=self.dP[l], ws=self.ws_e,
-                                 db_out=self.db[l])
+                rnn.epilogue_bwd(dY, self.H[l + 1], self.epi[l], ws=self.ws_e, db_out=self.db[l],
+                                 want_dx=False)
                 self._t("epi_bwd_end")
-                dY = self.dP[l]
+            if self.l2_window:
+                rnn.stream_l2_window(dY)              # gathered by the source-major backward
             self._t("lja_bwd")
             g = self._lja_bwd_into(idx, q, dY, self.dZ[l])
             self._t("lja_bwd_end")
             self._t("proj_bwd")
-            rnn.project_bwd(self.H[l], self.W[l], g, want_dx=True, prec=self.prec, ws=self.ws_p,
-                            dx_out=self.dH[l], dw_out=self.dW[l])
+            if self.b is not None and l > 0:
+                rnn.project_bwd(self.H[l], self.W[l], g, want_dx=True, prec=self.prec,
+                                ws=self.ws_p, dx_out=self.dP[l - 1], dw_out=self.dW[l],
+                                relu_in=True, d_in_bias=self.db[l - 1])
+                dY = self.dP[l - 1]
+            else:
+                rnn.project_bwd(self.H[l], self.W[l], g, want_dx=True, prec=self.prec,
+                                ws=self.ws_p, dx_out=self.dH[l], dw_out=self.dW[l])
+                dY = self.dH[l]
             self._t("proj_bwd_end")
-            dY = self.dH[l]
+        if self.l2_window:
+            rnn.stream_l2_window(None)
         return self.dW, self.dH[0]
 
     # ---- fit (SURVEY sec 8f item 3; PAPER.md:549 Loss, :554 ?fit) ----
@@ -447,7 +465,9 @@ class HGTProgram(_Program):
             self.q[name] = rnn.make_query("src", "softmax", src=self._blk("m", name),
                                           src_key=self._blk("k", name), dst=self._blk("q", tt),
                                           heads=self.h, scale=1.0)
-            self.O[name] = _empty(self.n[tt], d, dev)
+            # a target type reached by ONE relation: H_tilda is that relation's output itself
+            n_into = sum(x["dst_type"] == tt for x in rels.values())
+            self.O[name] = self.Ht[tt] if n_into == 1 else _empty(self.n[tt], d, dev)
             self.lse[name] = torch.empty(max(self.n[tt], 1), self.h, dtype=torch.float32, device=dev)
         # dQ of the second and later relations into a target type: written here, then added
         # onto the type's query-gradient block (the shared Q's gradient is the sum over phi).
@@ -523,7 +543,8 @@ class HGTProgram(_Program):
             rnn.join_aggregate_fwd(self.idx[name], self.q[name], out=self.O[name],
                                    lse=self.lse[name], ws=self.ws)
             self._t("lja_fwd_end")
-            rnn.accumulate(self.Ht[tt], self.O[name], beta=0.0 if first[tt] else 1.0)
+            if self.O[name] is not self.Ht[tt]:     # union over the relations into tt
+                rnn.accumulate(self.Ht[tt], self.O[name], beta=0.0 if first[tt] else 1.0)
             first[tt] = False
         return self.Ht
 

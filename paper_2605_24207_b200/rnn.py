@@ -23,7 +23,7 @@ AGG = {"sum": 0, "mean": 1, "softmax": 2, "max": 3}
 COMBINE = {"src": 0, "mul": 1, "add": 2, "concat": 3}
 BY_ROW, BY_POSITION = 0, 1
 IDX_VALIDATE, IDX_WITHIN_GROUP_BY_SRC_KEY, IDX_NO_TRANSPOSE, IDX_DENSE_GROUPS = 1, 2, 4, 8
-PREC = {"tf32": 0, "3xtf32": 1}
+PREC = {"tf32": 0, "3xtf32": 1, "bf16": 2}
 
 
 class RnnError(RuntimeError):
@@ -108,6 +108,10 @@ def lib():
         L.rnn_project_bwd_workspace_size.argtypes = [i64, i32, i32, C.POINTER(sz)]
         L.rnn_project_bwd.argtypes = [vp, i64, i32, i64, vp, i32, i64, vp, i64, vp, i64, vp, vp,
                                       C.c_int, vp, sz, vp]
+        L.rnn_project_bwd_relu.argtypes = [vp, i64, i32, i64, vp, i32, i64, vp, i64, vp, i64, vp,
+                                           vp, vp, C.c_int, vp, sz, vp]
+        L.rnn_stream_l2_window.argtypes = [vp, vp, sz, C.c_float]
+        L.rnn_stream_l2_window.restype = C.c_int
         L.rnn_gcn_norm.argtypes = [C.POINTER(JoinIndexC), vp, vp, sz, vp]
         L.rnn_hash_partition.argtypes = [vp, i64, i32, C.c_uint64, vp, vp]
         L.rnn_accumulate.argtypes = [vp, i64, vp, i64, i64, i32, C.c_float, vp]
@@ -168,7 +172,7 @@ def lib():
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
                   "rnn_join_aggregate_bwd", "rnn_group_softmax", "rnn_group_softmax_bwd",
                   "rnn_project", "rnn_project_bwd_workspace_size", "rnn_project_bwd",
-                  "rnn_gcn_norm", "rnn_hash_partition"):
+                  "rnn_project_bwd_relu", "rnn_gcn_norm", "rnn_hash_partition"):
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -425,7 +429,10 @@ def project(X, W, bias=None, out=None, prec="3xtf32", stream=None):
 
 
 def project_bwd(X, W, dY, want_dx=True, want_db=False, prec="3xtf32", ws=None, stream=None,
-                dx_out=None, dw_out=None):
+                dx_out=None, dw_out=None, relu_in=False, d_in_bias=None):
+    """dX = dY W, dW = dY^T X, db = colsum(dY).  relu_in: X is a ReLU epilogue's output, dX
+    becomes the gradient at that epilogue's input (dY W) * [X > 0] and d_in_bias (a [K]
+    tensor, optional) its bias gradient (rnn_project_bwd_relu)."""
     M, K = X.shape
     N = W.shape[0]
     dev = X.device
@@ -437,6 +444,14 @@ def project_bwd(X, W, dY, want_dx=True, want_db=False, prec="3xtf32", ws=None, s
     nb = C.c_size_t(0)
     _check(lib().rnn_project_bwd_workspace_size(M, K, N, C.byref(nb)))
     w = ws.get(nb.value) if ws is not None else _ws(nb.value, dev)
+    if relu_in:
+        if dX is None:
+            raise ValueError("relu_in needs dX (want_dx=True)")
+        _check(lib().rnn_project_bwd_relu(
+            _ptr(X), M, K, X.stride(0), _ptr(W), N, W.stride(0), _ptr(dY), dY.stride(0), _ptr(dX),
+            dX.stride(0), _ptr(dW), _ptr(db), _ptr(d_in_bias), PREC[prec], _ptr(w), w.numel(),
+            _stream(stream)))
+        return dX, dW, db
     _check(lib().rnn_project_bwd(_ptr(X), M, K, X.stride(0), _ptr(W), N, W.stride(0), _ptr(dY),
                                  dY.stride(0), _ptr(dX), 0 if dX is None else dX.stride(0), _ptr(dW),
                                  _ptr(db), PREC[prec], _ptr(w), w.numel(), _stream(stream)))
@@ -446,6 +461,15 @@ def project_bwd(X, W, dY, want_dx=True, want_db=False, prec="3xtf32", ws=None, s
 # ------------------------------------------------------------------------------------------
 # helpers
 # ------------------------------------------------------------------------------------------
+def stream_l2_window(t=None, hit_ratio=1.0, stream=None):
+    """Persisting-L2 window over tensor t on the stream (rnn_stream_l2_window); t=None clears."""
+    if t is None:
+        _check(lib().rnn_stream_l2_window(_stream(stream), None, 0, 0.0))
+    else:
+        span = (1 + sum((n - 1) * st for n, st in zip(t.shape, t.stride()))) * t.element_size()
+        _check(lib().rnn_stream_l2_window(_stream(stream), _ptr(t), span, float(hit_ratio)))
+
+
 def gcn_norm(idx: JoinIndex, stream=None):
     dev = idx.group_ptr.device
     w = torch.empty(max(idx.n_join_rows, 1), dtype=torch.float32, device=dev)
@@ -626,11 +650,12 @@ def epilogue_fwd(x, epi: EpilogueC, out=None, stream=None):
 
 
 def epilogue_bwd(dy, y, epi: EpilogueC, dx=None, want_bias=True, want_resid=False,
-                 want_gate=False, ws=None, stream=None, db_out=None):
-    """(dx, d_bias, d_resid, d_gate) of the epilogue (rnn_epilogue_bwd); y = the forward output."""
+                 want_gate=False, ws=None, stream=None, db_out=None, want_dx=True):
+    """(dx, d_bias, d_resid, d_gate) of the epilogue (rnn_epilogue_bwd); y = the forward output.
+    want_dx=False skips dx (e.g. the bias-only epilogue, where dx would be a copy of dy)."""
     rows, dim = dy.shape
     dev = dy.device
-    dx = dx if dx is not None else torch.empty_like(dy)
+    dx = dx if dx is not None else (torch.empty_like(dy) if want_dx else None)
     db = db_out if db_out is not None else (
         torch.empty(dim, dtype=torch.float32, device=dev) if want_bias else None)
     dr = torch.empty_like(dy) if want_resid else None
@@ -639,7 +664,8 @@ def epilogue_bwd(dy, y, epi: EpilogueC, dx=None, want_bias=True, want_resid=Fals
     _check(lib().rnn_epilogue_bwd_workspace_size(rows, dim, C.byref(nb)))
     w = ws.get(nb.value) if ws is not None else _ws(nb.value, dev)
     _check(lib().rnn_epilogue_bwd(_ptr(dy), dy.stride(0), _ptr(y), 0 if y is None else y.stride(0),
-                                  rows, dim, C.byref(epi), _ptr(dx), dx.stride(0), _ptr(db),
+                                  rows, dim, C.byref(epi), _ptr(dx),
+                                  dim if dx is None else dx.stride(0), _ptr(db),
                                   _ptr(dr), 0 if dr is None else dr.stride(0), _ptr(dg), _ptr(w),
                                   w.numel(), _stream(stream)))
     return dx, db, dr, dg

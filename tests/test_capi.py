@@ -59,6 +59,22 @@ def test_host_side_checks_without_gpu(lib):
     assert lib.rnn_hash_partition(None, 10, 0, 0, None, None) == 1
 
 
+def test_round2_entry_points_host_checks(lib):
+    """Host-side checks of the round-2 entry points: unknown precision, the fused ReLU backward
+    without dX, an out-of-range L2 hit ratio -- all rejected before any device work."""
+    v = C.c_void_p(16)
+    # precision 3 does not exist (0 tf32, 1 3xtf32, 2 bf16)
+    assert lib.rnn_project(v, 10, 8, 8, v, 8, 8, None, v, 8, 3, None) == 1
+    assert b"precision" in lib.rnn_last_error()
+    assert lib.rnn_project_bwd(v, 10, 8, 8, v, 8, 8, v, 8, v, 8, v, None, 3, v, 1 << 20, None) == 1
+    # rnn_project_bwd_relu needs dX
+    assert lib.rnn_project_bwd_relu(v, 10, 8, 8, v, 8, 8, v, 8, None, 8, v, None, None, 1, v,
+                                    1 << 20, None) == 1
+    assert b"dX" in lib.rnn_last_error()
+    assert lib.rnn_stream_l2_window(None, v, 1024, C.c_float(1.5)) == 1
+    assert lib.rnn_stream_l2_window(None, None, 1024, C.c_float(0.5)) == 1
+
+
 def test_dhn_saved_entry_points_host_checks(lib):
     """rnn_dhn_fwd_save / rnn_dhn_bwd_saved reject a missing walk sum and unknown flags before
     any device work (an empty index has no groups, so no pointer is dereferenced)."""

@@ -281,6 +281,46 @@ def test_projection_parity(R, ora, M, K, N, prec):
     assert_close(np_(db), rdb, FP32_TOL, "db")
 
 
+def bf16_rne(a):
+    """fp32 -> nearest bf16 (ties to even), returned as fp32 (test-side input rounding, SURVEY
+    O5: 'inputs rounded to tf32/bf16 first when checking the reduced-precision path')."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+@pytest.mark.parametrize("M,K,N", [(300, 128, 128), (60001, 128, 384), (5001, 200, 100),
+                                   (2708, 1433, 16), (1000, 40, 200), (77, 8, 3)])
+def test_projection_bf16(R, ora, M, K, N):
+    """RNN_PREC_BF16 (north_star: 1e-2 for bf16 projections) on every kernel family (TMEM-resident
+    W, resident-B, tile GEMM; dW split-K): within 1e-2 of the exact product, and within fp32
+    tolerance of the oracle on bf16-rounded inputs -- which pins the rounding (RNE to bf16, not a
+    tf32 truncation) and the exactness of the products."""
+    rng = np.random.default_rng(11 * M + K + N)
+    X = (rng.standard_normal((M, K)) / np.sqrt(K)).astype(np.float32)
+    W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    b = rng.standard_normal(N).astype(np.float32)
+    dY = rng.standard_normal((M, N)).astype(np.float32)
+    Y = np_(R.project(padded(X), padded(W), cu(b), prec="bf16"))
+    assert_close(Y, ora.project(X, W, b), TF32_TOL, "Y vs exact")
+    assert_close(Y, ora.project(bf16_rne(X), bf16_rne(W), b), FP32_TOL, "Y vs rounded inputs")
+    dX, dW, db = R.project_bwd(padded(X), padded(W), padded(dY), want_db=True, prec="bf16")
+    rdX, rdW, rdb = ora.project_bwd(X, W, dY)
+    assert_close(np_(dX), rdX, TF32_TOL, "dX vs exact")
+    assert_close(np_(dW), rdW, TF32_TOL, "dW vs exact")
+    qdX, qdW, _ = ora.project_bwd(bf16_rne(X), bf16_rne(W), bf16_rne(dY))
+    assert_close(np_(dX), qdX, FP32_TOL, "dX vs rounded inputs")
+    assert_close(np_(dW), qdW, FP32_TOL, "dW vs rounded inputs")
+    assert_close(np_(db), rdb, FP32_TOL, "db (fp32 column sums)")
+
+
+def test_bf16_rne_helper():
+    x = np.array([1.0, 1 + 2 ** -8, 1 + 3 * 2 ** -8, 1 + 2 ** -7, -2.5, 3e-39], np.float32)
+    # 1 + 2^-8 is a tie -> even (1.0); 1 + 3 * 2^-8 is a tie -> even (1 + 2^-6)
+    np.testing.assert_array_equal(bf16_rne(x)[:5], np.array([1.0, 1.0, 1 + 2 ** -6, 1 + 2 ** -7, -2.5],
+                                                            np.float32))
+
+
 @pytest.mark.parametrize("M,K,N,ldx,lddy", [(5000, 40, 100, 64, 128), (70001, 128, 48, 128, 64),
                                              (3000, 96, 16, 96, 32)])
 def test_projection_bwd_wide_ld(R, ora, M, K, N, ldx, lddy):
@@ -294,6 +334,34 @@ def test_projection_bwd_wide_ld(R, ora, M, K, N, ldx, lddy):
     rdX, rdW, _ = ora.project_bwd(X, W, dY)
     assert_close(np_(dX), rdX, FP32_TOL, "dX")
     assert_close(np_(dW), rdW, FP32_TOL, "dW")
+
+
+@pytest.mark.parametrize("M,K,N", [(300, 128, 40), (100000, 128, 40), (5001, 256, 7), (77, 8, 3),
+                                   (60001, 384, 128), (2708, 16, 7),
+                                   # N > 128: unfused path (mask + column-sum kernels)
+                                   (3000, 64, 200)])
+def test_projection_bwd_relu_parity(R, ora, M, K, N):
+    """rnn_project_bwd_relu = rnn_project_bwd then the ReLU epilogue backward on dX (reading
+     of the GCN hidden layer): dP = (dY W) * [X > 0], d_in_bias = colsum(dP).
+    X is a ReLU output (about half exact zeros), so the mask is the same decision on both sides."""
+    rng = np.random.default_rng(3 * M + K + N)
+    X = np.maximum(rng.standard_normal((M, K)) / np.sqrt(K), 0).astype(np.float32)
+    W = (rng.standard_normal((N, K)) / np.sqrt(K)).astype(np.float32)
+    dY = rng.standard_normal((M, N)).astype(np.float32)
+    dbi = torch.full((K,), float("nan"), device="cuda")
+    dX, dW, db = R.project_bwd(padded(X), padded(W), padded(dY), want_db=True, relu_in=True,
+                               d_in_bias=dbi)
+    rdX, rdW, rdb = ora.project_bwd(X, W, dY)
+    rdP, rdbi, _, _ = ora.epilogue_bwd(rdX, X, np.zeros(K), "relu")
+    assert_close(np_(dX), rdP, FP32_TOL, "dP")
+    assert (np_(dX)[X == 0] == 0).all()
+    assert_close(np_(dbi), rdbi, FP32_TOL, "d_in_bias")
+    assert_close(np_(dW), rdW, FP32_TOL, "dW")
+    assert_close(np_(db), rdb, FP32_TOL, "db")
+    # deterministic: the fused column sums are reduced in a fixed order
+    dbi2 = torch.empty_like(dbi)
+    R.project_bwd(padded(X), padded(W), padded(dY), relu_in=True, d_in_bias=dbi2)
+    assert torch.equal(dbi, dbi2)
 
 
 def test_gcn_norm_and_partition(R, ora):

@@ -88,12 +88,14 @@ def test_gcn_arxiv_full_size_sampled(P):
     # projection (tcgen05 3xTF32) on sampled rows
     rows = rng.choice(len(key), 2000, replace=False)
     assert_close(Z0[rows], oracle.project(g["nodes"]["x"][rows], g["W"][0]), FP32_TOL, "Z0 rows")
-    # layer 1 backward: the epilogue backward on every row (from the GPU's upstream dH1), then
-    # the LJA backward on every source row from the GPU's d(pre-activation)
+    # layer 1 backward: the layer-2 projection backward dH1 = dZ1 W1 (from the GPU's dZ1), the
+    # epilogue backward on every row (fused into that projection on the GPU), then the LJA
+    # backward on every source row from the GPU's d(pre-activation)
     # (the ReLU mask is a decision taken in floating point: both sides take it from the GPU's
     # fp32 output -- pre = H1 - b, which is the pre-activation where H1 > 0 and gives the
     # zero derivative where H1 = 0)
-    dP0, db0, _, _ = oracle.epilogue_bwd(np_(prog.dH[1]), np_(prog.H[1]) - b0, b0, "relu")
+    dH1, _, _ = oracle.project_bwd(np_(prog.H[1]), g["W"][1], np_(prog.dZ[1]), want_db=False)
+    dP0, db0, _, _ = oracle.epilogue_bwd(dH1, np_(prog.H[1]) - b0, b0, "relu")
     assert_close(np_(prog.dP[0]), dP0, FP32_TOL, "dP0 all rows")
     assert_close(np_(prog.db[0]), db0, FP32_TOL, "db0")
     dZ0 = oracle.lja_bwd(o1, np_(prog.dP[0]), "src", "sum", src=Z0, edge=w1, edge_mode=1,
