@@ -1138,9 +1138,11 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
   } else {
     a.wout = b.wout; a.nbrh = b.nbrh; a.sgh = b.sgh;
     a.slab = reinterpret_cast<float*>(b.cta);
-    // shared-memory S1 (default) or the L2 slab (RNN_DHN_L2SLAB=1, the round-1 design)
-    static const bool l2slab = getenv("RNN_DHN_L2SLAB") != nullptr;
-    if (!l2slab) {
+    // the L2 slab (default) or shared-memory S1 values (RNN_DHN_SMEM_S1=1; measured 5.8x
+    // slower on the products graph, profiles/r02/dhn: the 384-key partitions multiply the
+    // passes over every adjacency list and the 128 KB value table leaves one CTA per SM)
+    const bool smem_s1 = getenv("RNN_DHN_SMEM_S1") != nullptr;
+    if (smem_s1) {
       const size_t smem_s = 2 * H4S_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4S_DEG_CAP * sizeof(int) +
                             H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) + 16 +

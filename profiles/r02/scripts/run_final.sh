@@ -29,3 +29,15 @@ for c in mag arxiv hyper; do
   ncu -i /tmp/ncu/prof_$c.ncu-rep --page raw --csv > $O/prof_${c}_raw.csv 2>&1
 done
 cp /tmp/ncu/prof_mag.ncu-rep $O/ 2>/dev/null
+# DHN C3 / C4 (L2-slab default) full captures, 0.03-scale products graph (the 0.1-scale C4 replay timed out in ncu)
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:dhn4_kernel -c 1 -o /tmp/ncu/dhn4_l2 -f \
+  python bench.py --config dhn --dhn-scale 0.03 --steps 1 --warmup 0 --seeds 42 --no-cpu-baseline --no-e2e --eager > $O/ncu_dhn4.log 2>&1
+ncu -i /tmp/ncu/dhn4_l2.ncu-rep --page raw --csv > $O/dhn4_l2_raw.csv 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:dhn3_kernel -c 1 -o /tmp/ncu/dhn3 -f \
+  python bench.py --config dhn --dhn-scale 0.03 --steps 1 --warmup 0 --seeds 42 --no-cpu-baseline --no-e2e --eager > $O/ncu_dhn3.log 2>&1
+ncu -i /tmp/ncu/dhn3.ncu-rep --page raw --csv > $O/dhn3_raw.csv 2>&1
+# sanitizers: first-launch report probe, DHN racecheck per k on a 40-node graph
+SANITIZE_FIRST=gather CUDA_MODULE_LOADING=EAGER timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python profiles/r02/scripts/sanitize_tiny.py > $O/memcheck_first_gather.log 2>&1; echo "exit $?" >> $O/memcheck_first_gather.log
+for k in 2 3 4; do
+  SANITIZE_PART=dhn SANITIZE_DHN_N=40 SANITIZE_DHN_K=$k timeout 900 compute-sanitizer --tool racecheck --print-limit 20 python profiles/r02/scripts/sanitize_tiny.py > $O/racecheck_dhn_k$k.log 2>&1; echo "exit $?" >> $O/racecheck_dhn_k$k.log
+done

@@ -168,7 +168,18 @@ def test_c3_mark_array_path(rnn):
     assert paths["c3_mark_roots"] >= 1, paths
 
 
-def test_c4_partitioned_chunked_path(rnn):
+@pytest.fixture(params=["l2slab", "smem_s1"])
+def c4_variant(request, monkeypatch):
+    """Both C4 S1-value layouts: the L2 slab (default) and shared-memory values
+    (RNN_DHN_SMEM_S1, read by the library at every launch)."""
+    if request.param == "smem_s1":
+        monkeypatch.setenv("RNN_DHN_SMEM_S1", "1")
+    else:
+        monkeypatch.delenv("RNN_DHN_SMEM_S1", raising=False)
+    return request.param
+
+
+def test_c4_partitioned_chunked_path(rnn, c4_variant):
     """Leaves see 8,300 two-hop keys through the hub (> 8,192: hash partitions of w); the hub
     itself has 8,300 neighbours (> H4_DEG_CAP: no smem cursors, binary-searched partition
     starts) and walks its neighbours 32 at a time (chunked mode)."""
@@ -179,7 +190,7 @@ def test_c4_partitioned_chunked_path(rnn):
     assert paths["c4_passes"] > paths["c4_roots"], paths
 
 
-def test_c4_long_run_overflow(rnn):
+def test_c4_long_run_overflow(rnn, c4_variant):
     """Root n -> 600 neighbours v_i, each v_i -> w0 with multiplicity 200 (one long run per
     v_i in w0's partition; 600 > the 512-entry queue), w0 -> p0 -> n closes the walks.
     Directed multigraph plus random noise edges."""
