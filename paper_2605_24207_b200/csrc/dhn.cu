@@ -24,9 +24,19 @@
 namespace rnn {
 namespace {
 
-constexpr int DHN_THREADS = 1024;
+// C3 CTA shape (compile-time; -D overrides for measurement builds, profiles/build_variant.py)
+#ifndef DHN_THREADS_CFG
+#define DHN_THREADS_CFG 1024
+#endif
+#ifndef DHN_CTAS_CFG
+#define DHN_CTAS_CFG 1
+#endif
+#ifndef H3_CAP_CFG
+#define H3_CAP_CFG 8192
+#endif
+constexpr int DHN_THREADS = DHN_THREADS_CFG;
 constexpr int DHN_WARPS = DHN_THREADS / 32;
-constexpr int DHN_CTAS_PER_SM = 1;
+constexpr int DHN_CTAS_PER_SM = DHN_CTAS_CFG;
 
 struct DhnArgs {
   int64_t G;
@@ -59,6 +69,7 @@ struct DhnArgs {
   const float* F2b;       // k=4, optional second middle operand (symmetric Edge)
   const float* F1b;       // k=3, optional second first-hop operand (symmetric Edge)
   float* out_b;           // its result (same layout as out, no root multiplier)
+  int part_keys;          // k=4 slot-indexed walk: target distinct keys per partition (0: H4_PART)
 };
 
 __device__ __forceinline__ void dhn_store(const DhnArgs& a, int64_t n, int c, float v) {
@@ -123,15 +134,16 @@ __device__ __forceinline__ int hs_find(const int* keys, int cap_mask, int w) {
 // n -> v -> w with lanes over w, probe the set, and the hits gather f1(v) (.) f2(w) with
 // lane = channel.  Roots whose in-degree exceeds the set use a per-CTA global mark array.
 // -------------------------------------------------------------------------------------
-constexpr int H3_CAP = 8192;                 // slots (keys + counts: 64 KB)
-constexpr int H3_MAX_INDEG = 6144;           // load factor <= 0.75
+constexpr int H3_CAP = H3_CAP_CFG;           // slots (keys + counts: 64 KB at 8,192)
+constexpr int H3_MAX_INDEG = H3_CAP / 4 * 3; // load factor <= 0.75
 
 template <int DPL, bool DUAL = false>
-__global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
+__global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnArgs a) {
   extern __shared__ int h3[];
   int* keys = h3;
   int* cnt = h3 + H3_CAP;
-  float* s_acc = reinterpret_cast<float*>(cnt + H3_CAP);   // [DHN_WARPS][DPL * 32]
+  int* used = cnt + H3_CAP;                                  // [H3_MAX_INDEG] slots taken
+  float* s_acc = reinterpret_cast<float*>(used + H3_MAX_INDEG);   // [DHN_WARPS][DPL * 32]
   __shared__ int s_root;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* mark = a.mark + (int64_t)blockIdx.x * a.cta_stride;
@@ -147,8 +159,11 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
     ++c_roots;
     c_mark += !hashed;
     if (hashed) {
-      for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS)
-        atomicAdd(&cnt[hs_insert(keys, H3_CAP - 1, a.sg[q])], 1);
+      for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) {
+        const int sl = hs_insert(keys, H3_CAP - 1, a.sg[q]);
+        atomicAdd(&cnt[sl], 1);
+        used[q - ib] = sl;
+      }
     } else {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) atomicAdd(&mark[a.sg[q]], 1);
     }
@@ -168,18 +183,26 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
         f1bv[j] = DUAL && c < d ? a.F1b[(int64_t)v * d + c] : 0.f;
       }
       const int64_t we = a.gp[v + 1];
-      for (int64_t i0 = a.gp[v]; i0 < we; i0 += 32) {
-        const int64_t i = i0 + lane;
-        const int32_t w = i < we ? a.nbr[i] : -1;
-        int m = 0;
-        if (w >= 0) {
-          if (hashed) {
-            const int sl = hs_find(keys, H3_CAP - 1, w);
-            m = sl >= 0 ? cnt[sl] : 0;
-          } else {
-            m = __ldcg(&mark[w]);
+      // two 32-entry chunks of N(v) per step: both loads in flight before either probe
+      for (int64_t i0 = a.gp[v]; i0 < we; i0 += 64) {
+        const int32_t w2[2] = {i0 + lane < we ? a.nbr[i0 + lane] : -1,
+                               i0 + 32 + lane < we ? a.nbr[i0 + 32 + lane] : -1};
+        int m2[2] = {0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (w2[h] >= 0) {
+            if (hashed) {
+              const int sl = hs_find(keys, H3_CAP - 1, w2[h]);
+              m2[h] = sl >= 0 ? cnt[sl] : 0;
+            } else {
+              m2[h] = __ldcg(&mark[w2[h]]);
+            }
           }
         }
+#pragma unroll
+        for (int hc = 0; hc < 2; ++hc) {
+        const int32_t w = w2[hc];
+        const int m = m2[hc];
         unsigned bal = __ballot_sync(FULL, m != 0);
         while (bal) {
           // up to 4 hits per round so their row loads are in flight together
@@ -210,6 +233,7 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
             }
           }
         }
+        }
       }
     }
 #pragma unroll
@@ -232,8 +256,11 @@ __global__ void __launch_bounds__(DHN_THREADS, 1) dhn3_kernel(DhnArgs a) {
         a.out_b[orow * a.ld_out + c] = s;
       }
     }
-    if (hashed) {
-      for (int i = threadIdx.x; i < H3_CAP; i += DHN_THREADS) { keys[i] = -1; cnt[i] = 0; }
+    if (hashed) {   // exactly the slots the inserts took (a repeated key clears twice)
+      for (int64_t q = threadIdx.x; q < ie - ib; q += DHN_THREADS) {
+        keys[used[q]] = -1;
+        cnt[used[q]] = 0;
+      }
     } else {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) mark[a.sg[q]] = 0;
     }
@@ -772,6 +799,331 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
   }
 }
 
+// -------------------------------------------------------------------------------------
+// C4, slot-indexed (the default when rows are whole float4s): the partitioned walk of
+// dhn4_kernel with three changes that remove its serialised per-hit work (ncu, 0.03-scale
+// products graph: the walk issued ~35 warp instructions per wedge, half of them in the
+// ballot / ffs hit selection and the id-publication spin of h4_insert):
+//  * the S1 value row of key w IS its hash slot (rows [CAP][32] per CTA): an insert is one
+//    shared-memory CAS, with no compact id to draw and publish;
+//  * ONE hash of w gives both the partition (top bits; the lists are sorted by them) and the
+//    slot (low bits);
+//  * a run sorted by partition enters the current partition as a lane PREFIX of every
+//    32-entry chunk, so round r's lane group sub = lane / 8 serves hit 4 r + sub directly.
+// Two chunks of a run are loaded per step.  The table is cleared row by row (occupied slots).
+// -------------------------------------------------------------------------------------
+#ifndef H4S_INFLIGHT
+#define H4S_INFLIGHT 2   // IN sweep: hits per lane group in flight per round (x4 per warp)
+#endif
+__device__ __forceinline__ uint32_t h4s_hash(int32_t w) { return dhn_hash((uint32_t)w ^ 0x5bd1e995u); }
+__device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w) {
+  uint32_t s = H & (uint32_t)(H4_CAP - 1);
+  for (int t = 0; t < H4_CAP; ++t) {
+    const int prev = atomicCAS(&keys[s], -1, w);
+    if (prev == -1 || prev == w) return (int)s;
+    s = (s + 1) & (uint32_t)(H4_CAP - 1);
+  }
+  return -1;
+}
+__device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w) {
+  uint32_t s = H & (uint32_t)(H4_CAP - 1);
+  for (int t = 0; t < H4_CAP; ++t) {
+    const int k = keys[s];
+    if (k == w) return (int)s;
+    if (k == -1) return -1;
+    s = (s + 1) & (uint32_t)(H4_CAP - 1);
+  }
+  return -1;
+}
+
+// one 32-entry chunk whose first cnt lanes are in the partition.  OUT: insert w, add f1(v) to
+// row slot(w) (one red.global.add.v4.f32 per lane: lane group sub carries hit 4 r + sub,
+// lane % 8 its channel quad).  IN: find w, t += S1(w) (.) f2(w) (8 hits in flight).
+template <bool OUT, bool DUAL>
+__device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32_t H, bool in,
+                                          int cnt, const float4& fv4, float4& t4, float4& t4b,
+                                          int lane, const float* F2q, const float* F2bq, int d) {
+  const int sub = lane >> 3, cq = lane & 7;
+  if (OUT) {
+    const int sl = (in && w >= 0) ? h4s_insert(keys, H, w) : -1;
+    if (in && w >= 0 && sl < 0) atomicAdd(&g_dhn_paths[8], 1ull);   // table full (tests: 0)
+    for (int q0 = 0; q0 < cnt; q0 += 4) {
+      const int q = q0 + sub;
+      const int slq = __shfl_sync(FULL, sl, q & 31);
+      if (q < cnt && slq >= 0)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(S + slq * 32 + 4 * cq),
+                     "f"(fv4.x), "f"(fv4.y), "f"(fv4.z), "f"(fv4.w)
+                     : "memory");
+    }
+  } else {
+    const int sl = (in && w >= 0) ? h4s_find(keys, H, w) : -1;
+    for (int q0 = 0; q0 < cnt; q0 += 4 * H4S_INFLIGHT) {
+      float4 x[H4S_INFLIGHT], y[H4S_INFLIGHT], yb[H4S_INFLIGHT];
+#pragma unroll
+      for (int u = 0; u < H4S_INFLIGHT; ++u) {
+        const int q = q0 + 4 * u + sub;
+        const int slq = __shfl_sync(FULL, sl, q & 31);
+        const int wq = __shfl_sync(FULL, w, q & 31);
+        const bool ok = q < cnt && slq >= 0;
+        x[u] = ok ? __ldcg(reinterpret_cast<const float4*>(S + slq * 32 + 4 * cq)) : f4_zero();
+        y[u] = ok ? __ldg(reinterpret_cast<const float4*>(F2q + (int64_t)wq * d)) : f4_zero();
+        if (DUAL)
+          yb[u] = ok ? __ldg(reinterpret_cast<const float4*>(F2bq + (int64_t)wq * d)) : f4_zero();
+      }
+#pragma unroll
+      for (int u = 0; u < H4S_INFLIGHT; ++u) {
+        t4.x = fmaf(x[u].x, y[u].x, t4.x); t4.y = fmaf(x[u].y, y[u].y, t4.y);
+        t4.z = fmaf(x[u].z, y[u].z, t4.z); t4.w = fmaf(x[u].w, y[u].w, t4.w);
+        if (DUAL) {
+          t4b.x = fmaf(x[u].x, yb[u].x, t4b.x); t4b.y = fmaf(x[u].y, yb[u].y, t4b.y);
+          t4b.z = fmaf(x[u].z, yb[u].z, t4b.z); t4b.w = fmaf(x[u].w, yb[u].w, t4b.w);
+        }
+      }
+    }
+  }
+}
+
+// One side of one partition (as h4_sweep): phase A walks the runs of the neighbours the warps
+// grab, queueing runs longer than H4_LONG; phase B splits the queued runs over all warps.
+template <bool OUT, bool DUAL>
+__device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float* S, int* cur,
+                            int* q_i, int64_t* q_b, int64_t* q_e, int* q_n, int* grab, int c0,
+                            int* s_cnt, float4* acc_b) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* L = OUT ? a.nbrh : a.sgh;
+  const float* Fv = OUT ? a.F1 : a.F3;
+  const int d = a.d;
+  const int cq4 = c0 + 4 * (lane & 7);   // this lane's channel quad
+  const bool cok4 = cq4 < d;
+  const float* F2q = a.F2 + (cok4 ? cq4 : 0);
+  const float* F2bq = DUAL ? a.F2b + (cok4 ? cq4 : 0) : nullptr;
+  float4 acc4 = f4_zero();
+  auto ld_fv4 = [&](int32_t u) {
+    return cok4 ? __ldg(reinterpret_cast<const float4*>(Fv + (int64_t)u * d + cq4)) : f4_zero();
+  };
+  auto fma4 = [](float4& acc_, const float4& f, const float4& t_) {
+    acc_.x = fmaf(f.x, t_.x, acc_.x); acc_.y = fmaf(f.y, t_.y, acc_.y);
+    acc_.z = fmaf(f.z, t_.z, acc_.z); acc_.w = fmaf(f.w, t_.w, acc_.w);
+  };
+  auto in_part = [&](uint32_t H) { return ((H >> 16) >> R.sh) == R.part; };
+  const int step = R.chunked ? 32 : 1;
+  for (;;) {
+    int base = 0;
+    if (lane == 0) base = atomicAdd(grab, step);
+    base = __shfl_sync(FULL, base, 0);
+    if (base >= R.deg) break;
+    const int i = R.chunked ? base + lane : base;
+    int32_t u = -1;
+    int64_t b0 = 0, e0 = 0, s0 = 0;
+    bool has = false;
+    if (i < R.deg && (R.chunked || lane == 0)) {
+      if (OUT) {
+        u = a.nbr[R.pb + i];
+        if (u >= 0) { s0 = a.gp[u]; e0 = a.gp[u + 1]; }
+      } else {
+        u = a.sg[R.ib + i];
+        const int32_t ru = a.row_of[u];
+        s0 = a.sp[ru];
+        e0 = a.sp[ru + 1];
+      }
+      if (u >= 0) {
+        b0 = R.cur_ok ? s0 + cur[i] : h4_lower(L, s0, e0, R.part, R.sh);
+        has = b0 < e0 && (h4_top(L[b0]) >> R.sh) == R.part;
+      }
+    }
+    unsigned hb = __ballot_sync(FULL, has);
+    while (hb) {
+      const int j = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const int32_t uj = __shfl_sync(FULL, u, j);
+      const int64_t bj = __shfl_sync(FULL, b0, j), ej = __shfl_sync(FULL, e0, j);
+      const int64_t sj = __shfl_sync(FULL, s0, j);
+      const int ij = __shfl_sync(FULL, i, j);
+      int64_t re = -1;
+      if (ej - bj > H4_LONG) {
+        re = R.P == 1 ? ej : h4_lower(L, bj, ej, R.part + 1, R.sh);
+        if (re - bj <= H4_LONG) re = -1;
+      }
+      if (re >= 0) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(q_n, 1);
+        slot = __shfl_sync(FULL, slot, 0);
+        if (slot < H4_LONG_MAX) {
+          if (lane == 0) { q_i[slot] = uj; q_b[slot] = bj; q_e[slot] = re; atomicAdd(&s_cnt[0], 1); }
+          if (R.cur_ok && lane == 0) cur[ij] = (int)(re - sj);
+          continue;
+        }
+        if (lane == 0) atomicAdd(&s_cnt[1], 1);
+      }
+      const float4 fv4 = ld_fv4(uj);
+      float4 t4 = f4_zero(), t4b = f4_zero();
+      int64_t t0 = bj;
+      for (;;) {
+        const int64_t ta = t0 + lane, tb = ta + 32;
+        const int32_t wa = ta < ej ? L[ta] : -1;
+        const int32_t wb = tb < ej ? L[tb] : -1;
+        const uint32_t Ha = h4s_hash(wa), Hb = h4s_hash(wb);
+        const bool ina = ta < ej && in_part(Ha);
+        const bool inb = tb < ej && in_part(Hb);
+        const unsigned ma = __ballot_sync(FULL, ina), mb = __ballot_sync(FULL, inb);
+        const int ca = __popc(ma), cb = __popc(mb);
+        h4s_chunk<OUT, DUAL>(keys, S, wa, Ha, ina, ca, fv4, t4, t4b, lane, F2q, F2bq, d);
+        if (cb) h4s_chunk<OUT, DUAL>(keys, S, wb, Hb, inb, cb, fv4, t4, t4b, lane, F2q, F2bq, d);
+        t0 += ca + cb;
+        if (mb != FULL) break;
+      }
+      if (!OUT) {
+        fma4(acc4, fv4, t4);
+        if (DUAL) fma4(*acc_b, fv4, t4b);
+      }
+      if (R.cur_ok && lane == 0) cur[ij] = (int)(t0 - sj);
+    }
+  }
+  __syncthreads();
+  // phase B: the 32-entry chunks of all queued long runs (every entry in the partition)
+  const int nq = *q_n < H4_LONG_MAX ? *q_n : H4_LONG_MAX;
+  if (nq > 0) {
+    if (threadIdx.x == 0) *grab = 0;
+    __syncthreads();
+    int k = 0;
+    int64_t k_end = 0, k_beg = 0;
+    float4 fv4 = f4_zero(), t4 = f4_zero(), t4b = f4_zero();
+    int32_t uk = -1;
+    for (;;) {
+      int g = 0;
+      if (lane == 0) g = atomicAdd(grab, 1);
+      g = __shfl_sync(FULL, g, 0);
+      bool done = false;
+      while (g >= k_end) {
+        if (uk >= 0 && !OUT) {
+          fma4(acc4, fv4, t4);
+          if (DUAL) fma4(*acc_b, fv4, t4b);
+        }
+        t4 = f4_zero();
+        t4b = f4_zero();
+        uk = -1;
+        if (k >= nq) { done = true; break; }
+        k_beg = k_end;
+        k_end += (q_e[k] - q_b[k] + 31) / 32;
+        uk = q_i[k];
+        fv4 = ld_fv4(uk);
+        ++k;
+      }
+      if (done) break;
+      const int64_t qb = q_b[k - 1], qe = q_e[k - 1];
+      const int64_t tt = qb + (g - k_beg) * 32 + lane;
+      const int32_t w = tt < qe ? L[tt] : -1;
+      const bool in = tt < qe;
+      const int cnt = __popc(__ballot_sync(FULL, in));
+      h4s_chunk<OUT, DUAL>(keys, S, w, h4s_hash(w), in, cnt, fv4, t4, t4b, lane, F2q, F2bq, d);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) { *q_n = 0; *grab = 0; }
+  __syncthreads();
+  return acc4;
+}
+
+template <bool DUAL>
+__global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
+  extern __shared__ int h4[];
+  int* keys = h4;
+  float* s_red = reinterpret_cast<float*>(keys + H4_CAP);          // [H4_WARPS][32]
+  int* cur_out = reinterpret_cast<int*>(s_red + H4_WARPS * 32);     // [H4_DEG_CAP]
+  int* cur_in = cur_out + H4_DEG_CAP;                               // [H4_DEG_CAP]
+  int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
+  int64_t* q_e = q_b + H4_LONG_MAX;
+  int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
+  float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;          // [H4_CAP][32], zero
+  __shared__ int s_root, q_n, grab;
+  __shared__ int s_cnt[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int d = a.d;
+  const int64_t part_keys = a.part_keys > 0 ? a.part_keys : H4_PART;
+  for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) keys[i] = -1;
+  if (threadIdx.x == 0) { q_n = 0; grab = 0; s_cnt[0] = 0; s_cnt[1] = 0; }
+  unsigned long long c_roots = 0, c_parts = 0, c_chunked = 0, c_multi = 0;   // thread 0
+  for (;;) {
+    const int64_t n = dhn_next_root(a, &s_root);
+    if (n < 0) break;
+    ++c_roots;
+    const int32_t r = a.row_of[n];
+    const int64_t ib = a.sp[r], ie = a.sp[r + 1];
+    const int64_t pb = a.gp[n], pe = a.gp[n + 1];
+    const int deg_out = (int)(pe - pb), deg_in = (int)(ie - ib);
+    const bool cur_ok = deg_out <= H4_DEG_CAP && deg_in <= H4_DEG_CAP;
+    const int64_t bound = a.wout[n] < (uint32_t)a.G ? (int64_t)a.wout[n] : a.G;
+    int bits = 0;
+    while (bits < H4_HBITS && (part_keys << bits) < bound) ++bits;
+    H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
+    R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
+    c_multi += R.P > 1;
+    for (int c0 = 0; c0 < d; c0 += 32) {
+      float4 acc = f4_zero(), acc_b = f4_zero();
+      if (cur_ok) {
+        for (int i = threadIdx.x; i < deg_out; i += H4_THREADS) cur_out[i] = 0;
+        for (int i = threadIdx.x; i < deg_in; i += H4_THREADS) cur_in[i] = 0;
+      }
+      __syncthreads();
+      for (uint32_t part = 0; part < R.P; ++part) {
+        R.part = part;
+        ++c_parts;
+        c_chunked += R.chunked;
+        R.deg = deg_out;
+        h4s_sweep<true, false>(a, R, keys, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c0, s_cnt,
+                               nullptr);
+        R.deg = deg_in;
+        acc = f4_add(acc, h4s_sweep<false, DUAL>(a, R, keys, S, cur_in, q_i, q_b, q_e, &q_n,
+                                                 &grab, c0, s_cnt, &acc_b));
+        // clear the occupied rows and slots for the next partition / root (the sweeps ended
+        // with a barrier, so no lane still reads the table)
+        for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) {
+          if (keys[i] != -1) {
+            float4* row = reinterpret_cast<float4*>(S + (int64_t)i * 32);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) __stcg(row + j, f4_zero());
+            keys[i] = -1;
+          }
+        }
+        __syncthreads();
+      }
+      // sum the four hit slots (lanes cq, cq + 8, cq + 16, cq + 24): lane cq < 8 then holds
+      // channels c0 + 4 cq .. + 3
+#pragma unroll
+      for (int m = 8; m < 32; m <<= 1) acc = f4_add(acc, f4_shfl_xor(acc, m));
+      if (lane < 8) *reinterpret_cast<float4*>(&s_red[warp * 32 + 4 * lane]) = acc;
+      __syncthreads();
+      if (warp == 0) {
+        float s = 0.f;
+        for (int w = 0; w < H4_WARPS; ++w) s += s_red[w * 32 + lane];
+        if (c0 + lane < d) dhn_store(a, n, c0 + lane, s);
+      }
+      __syncthreads();
+      if (DUAL) {
+#pragma unroll
+        for (int m = 8; m < 32; m <<= 1) acc_b = f4_add(acc_b, f4_shfl_xor(acc_b, m));
+        if (lane < 8) *reinterpret_cast<float4*>(&s_red[warp * 32 + 4 * lane]) = acc_b;
+        __syncthreads();
+        if (warp == 0) {
+          float s = 0.f;
+          for (int w = 0; w < H4_WARPS; ++w) s += s_red[w * 32 + lane];
+          const int64_t orow = a.out_by_row ? (int64_t)a.row_of[n] : n;
+          if (c0 + lane < d) a.out_b[orow * a.ld_out + c0 + lane] = s;
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_dhn_paths[2], c_roots);
+    atomicAdd(&g_dhn_paths[3], c_parts);
+    atomicAdd(&g_dhn_paths[4], c_chunked);
+    atomicAdd(&g_dhn_paths[5], (unsigned long long)s_cnt[0]);
+    atomicAdd(&g_dhn_paths[6], (unsigned long long)s_cnt[1]);
+    atomicAdd(&g_dhn_paths[7], c_multi);
+  }
+}
+
 // sort keys of the hash-ordered adjacency lists: (segment << 16) | top 16 bits of hash(w)
 __global__ void h4_keys_kernel(const int32_t* __restrict__ seg, const int32_t* __restrict__ val,
                                int64_t E, uint64_t* __restrict__ key, int32_t* __restrict__ out) {
@@ -1128,7 +1480,8 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
   if (P.k == 3) {
     a.mark = reinterpret_cast<int*>(b.cta);
     const int dpl = (P.d + 31) / 32;
-    const size_t smem = 2 * H3_CAP * sizeof(int) + (size_t)DHN_WARPS * dpl * 32 * sizeof(float);
+    const size_t smem = (2 * H3_CAP + H3_MAX_INDEG) * sizeof(int) +
+                        (size_t)DHN_WARPS * dpl * 32 * sizeof(float);
     auto kern = a.F1b ? (dpl == 1 ? dhn3_kernel<1, true> : dpl == 2 ? dhn3_kernel<2, true>
                          : dpl == 3 ? dhn3_kernel<3, true> : dhn3_kernel<4, true>)
                       : (dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2>
@@ -1161,6 +1514,21 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
                     aligned16(a.F3) && aligned16(a.slab);
     RNN_REQUIRE(!F2b || (v4 && aligned16(F2b)), RNN_ERR_UNSUPPORTED,
                 "dual-middle C4 walk needs the float4 path");
+    // slot-indexed walk (default); RNN_DHN_COMPACT_IDS=1 selects the compact-id walk it
+    // replaced (kept for measurement, profiles/r02/dhn)
+    const bool compact = getenv("RNN_DHN_COMPACT_IDS") != nullptr;   // read per launch (tests)
+    if (v4 && !compact) {
+      static const int part_keys = getenv("RNN_DHN_PART_KEYS") ? atoi(getenv("RNN_DHN_PART_KEYS")) : 0;
+      a.part_keys = std::min(part_keys, H4_PART);
+      const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
+                            2 * H4_DEG_CAP * sizeof(int) +
+                            H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
+      auto kern = F2b ? dhn4s_kernel<true> : dhn4s_kernel<false>;
+      RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
+      kern<<<P.n_cta, H4_THREADS, smem_s, st>>>(a);
+      RNN_LAUNCH_CHECK();
+      return RNN_OK;
+    }
     auto kern = F2b ? dhn4_kernel<true, true> : v4 ? dhn4_kernel<true> : dhn4_kernel<false>;
     RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<P.n_cta, H4_THREADS, smem, st>>>(a);

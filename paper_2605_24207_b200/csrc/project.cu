@@ -924,16 +924,21 @@ __global__ void __launch_bounds__(PT_THREADS, 1)
         if (p.relu_src) {
           // d pre = dX (.) [X > 0]: the mask row of the producing layer's output, 32 rows per
           // chunk, each load one coalesced 128-byte row segment across the warp
+          // (unpredicated loads from clamped addresses, so all 32 are in flight at once: with
+          // a predicate per load the compiler ran out of predicate registers and issued each
+          // load just before its use -- ncu: 483 vs 40 us per arxiv launch)
           const bool fok = f < p.N;
+          const float* src = p.relu_src + (fok ? f : 0);
           float mk[32];
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
             const int64_t row = r0 + c0 + q;
-            mk[q] = (fok && row < p.M) ? __ldg(p.relu_src + row * p.ld_relu + f) : 0.f;
+            mk[q] = __ldg(src + (row < p.M ? row : p.M - 1) * p.ld_relu);
           }
+          const int nvalid = fok ? (int)(p.M - (r0 + c0) < 32 ? p.M - (r0 + c0) : 32) : 0;
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const float v = mk[q] > 0.f ? __uint_as_float(r[q]) + bf : 0.f;
+            const float v = (q < nvalid && mk[q] > 0.f) ? __uint_as_float(r[q]) + bf : 0.f;
             csum += v;
             st[q * 32 + lane] = v;
           }

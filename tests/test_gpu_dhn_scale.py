@@ -168,14 +168,18 @@ def test_c3_mark_array_path(rnn):
     assert paths["c3_mark_roots"] >= 1, paths
 
 
-@pytest.fixture(params=["l2slab", "smem_s1"])
+@pytest.fixture(params=["slot", "compact_ids", "smem_s1"])
 def c4_variant(request, monkeypatch):
-    """Both C4 S1-value layouts: the L2 slab (default) and shared-memory values
-    (RNN_DHN_SMEM_S1, read by the library at every launch)."""
+    """Every C4 walk variant (switches read by the library at every launch): the
+    slot-indexed L2 slab (default), the compact-id L2 slab it replaced (RNN_DHN_COMPACT_IDS)
+    and shared-memory values (RNN_DHN_SMEM_S1)."""
+    monkeypatch.delenv("RNN_DHN_SMEM_S1", raising=False)
     if request.param == "smem_s1":
         monkeypatch.setenv("RNN_DHN_SMEM_S1", "1")
+    elif request.param == "compact_ids":
+        monkeypatch.setenv("RNN_DHN_COMPACT_IDS", "1")
     else:
-        monkeypatch.delenv("RNN_DHN_SMEM_S1", raising=False)
+        monkeypatch.delenv("RNN_DHN_COMPACT_IDS", raising=False)
     return request.param
 
 
