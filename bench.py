@@ -332,6 +332,7 @@ def run_ours(args):
             first["index_ms"] = _index_build_ms(prog, world)
             first["model"] = prog.roof_model()
             first["launches"] = count_launches(prog)
+            first["proj_flops"] = count_proj_flops(prog)
             if not args.no_e2e:
                 first["e2e"] = run_e2e(prog, args, world, dev, rows, replay)
             first["meta"] = {k: getattr(prog, k) for k in ("L", "dims") if hasattr(prog, k)}
@@ -391,6 +392,20 @@ def run_ours(args):
     # every bracketed kernel's mean launch time and its launches per step
     roof["kernel_ms"] = {k: (round(v, 5) if v else None) for k, v in per.items()}
     roof["launches_per_step"] = {k: len(v) // max(n_steps, 1) for k, v in launches_ms.items()}
+    # the projections: bound by the tensor pipe under 3xTF32
+    pf = first.get("proj_flops") or {}
+    tpk, tpk_src = tf32_peak()
+    proj = {}
+    for k in ("proj_fwd", "proj_bwd"):
+        n_l = roof["launches_per_step"].get(k, 0)
+        if pf.get(k) and per.get(k) and n_l:
+            t = per[k] * n_l * 1e-3
+            proj[k] = {"flops_per_step": int(pf[k]), "ms_per_step": round(per[k] * n_l, 5),
+                       "achieved": round(pf[k] / t / 1e12, 2),
+                       "frac": round(pf[k] / t / 1e12 / tpk, 4)}
+    if proj:
+        roof["projection"] = {"bound": "tensor", "unit": "TFLOP/s", "peak": tpk,
+                              "peak_source": tpk_src, "precision": args.prec, **proj}
     lja_ms = sum((per[k] or 0.0) * roof["launches_per_step"].get(k, 0) for k in model)
     result = None
     if rank == 0:
@@ -472,6 +487,31 @@ def run_train(prog, args):
                     "wd 5e-4) on W and b, one CUDA graph replay, L2 not flushed",
             "paper_context": "PAPER.md:876: RelaNN 6.8 +- 0.3 ms/epoch, PyG 4.9 +- 0.4 "
                              "(GCN on Cora, A40) -- other hardware and framework overheads"}
+
+
+def count_proj_flops(prog):
+    """Tensor-core flops of one step's projections as issued (rnn.FLOP_COUNTER; 3xTF32 = three
+    tf32 products per term), from one untimed eager step."""
+    import torch
+    from paper_2605_24207_b200 import rnn
+    rnn.FLOP_COUNTER = {}
+    try:
+        prog.step()
+        torch.cuda.synchronize()
+        return dict(rnn.FLOP_COUNTER)
+    finally:
+        rnn.FLOP_COUNTER = None
+
+
+def tf32_peak():
+    """Dense tf32 tensor peak: the measured bf16 matmul peak (MEASURED_PEAKS.json) x the
+    guide's nominal tf32 / bf16 ratio (1.1 / 2.25 PFLOP/s, B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16 = json.load(f)["bf16_tflops"]
+        return round(bf16 * 1.1 / 2.25, 1), "derived: measured bf16 (MEASURED_PEAKS.json) x 1.1/2.25"
+    except Exception:
+        return 1100.0, "fallback: nominal dense tf32 (B200_PROFILING.md)"
 
 
 def count_launches(prog):

@@ -195,6 +195,20 @@ rnn_status rnn_join_aggregate_fwd(const rnn_join_index* idx, const rnn_lifted_qu
                                   float* out, int64_t ld_out, float beta, float* lse,
                                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* Union over relations keeping each relation's own output (HGT: H_tilda(t) = sum_phi O_phi(t),
+ * PAPER.md:1408-1409 [src-only], Fig. 4 :917-927).  Computes the aggregate into out exactly as
+ * rnn_join_aggregate_fwd with beta = 0 (out and lse are what rnn_join_aggregate_bwd needs:
+ * the SOFTMAX backward forms D = <dOut, out> per relation), and in the same pass
+ * acc[G, ld_acc] = beta_acc * acc + out (beta_acc 0 for the first relation into a type, 1 for
+ * the others).  acc: device, 16-byte aligned, ld_acc % 4 == 0, ld_acc >= width, must not alias
+ * out.  Fused into the store of the d = 128 SOFTMAX walker; other (combine, agg) pairs add one
+ * pass over [G, width].  MEAN: RNN_ERR_UNSUPPORTED (not decomposable).  Other
+ * arguments, layouts and errors: rnn_join_aggregate_fwd. */
+rnn_status rnn_join_aggregate_fwd_union(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                        float* out, int64_t ld_out, float* lse, float* acc,
+                                        int64_t ld_acc, float beta_acc, void* workspace,
+                                        size_t workspace_bytes, void* stream);
+
 /* ===================================================================================== */
 /* A5. Backward                                                                          */
 /* ===================================================================================== */
@@ -210,6 +224,17 @@ rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rnn_lifted_qu
                                   const float* d_out, int64_t ld_dout, float* d_src,
                                   float* d_src_key, float* d_edge, float* d_dst,
                                   void* workspace, size_t workspace_bytes, void* stream);
+/* As rnn_join_aggregate_bwd, with d_dst = beta_dst * d_dst + (gradient): beta_dst = 1 sums
+ * the gradient of a group-side operand shared by several relations (HGT's per-type query
+ * QLin<L, tau_t>, reading 12) in place, rows never referenced keeping their value.
+ * beta_dst in {0, 1}; beta_dst = 1 is supported where d_dst comes from the SOFTMAX
+ * source-major backward (dim 128), else RNN_ERR_UNSUPPORTED. */
+rnn_status rnn_join_aggregate_bwd_acc(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                      const float* out, int64_t ld_out, const float* lse,
+                                      const float* d_out, int64_t ld_dout, float* d_src,
+                                      float* d_src_key, float* d_edge, float* d_dst,
+                                      float beta_dst, void* workspace, size_t workspace_bytes,
+                                      void* stream);
 
 /* MAX aggregate (PAPER.md:209 "sum, mean, or max", :755): agg
  * RNN_AGG_MAX with combine SRC, value w_p * z_s (edge: optional scalar weight, by row or by

@@ -25,14 +25,16 @@ namespace rnn {
 namespace {
 
 // C3 CTA shape (compile-time; -D overrides for measurement builds, profiles/build_variant.py)
+// (4 CTAs of 8 warps per SM: one CTA's per-root barriers overlap the others' walks;
+// 0.1-scale products C3 fwd 25.1 -> 15.8 ms against 1 x 1024, profiles/r02/c3lb)
 #ifndef DHN_THREADS_CFG
-#define DHN_THREADS_CFG 1024
+#define DHN_THREADS_CFG 256
 #endif
 #ifndef DHN_CTAS_CFG
-#define DHN_CTAS_CFG 1
+#define DHN_CTAS_CFG 4
 #endif
 #ifndef H3_CAP_CFG
-#define H3_CAP_CFG 8192
+#define H3_CAP_CFG 4096
 #endif
 constexpr int DHN_THREADS = DHN_THREADS_CFG;
 constexpr int DHN_WARPS = DHN_THREADS / 32;
@@ -136,6 +138,8 @@ __device__ __forceinline__ int hs_find(const int* keys, int cap_mask, int w) {
 // -------------------------------------------------------------------------------------
 constexpr int H3_CAP = H3_CAP_CFG;           // slots (keys + counts: 64 KB at 8,192)
 constexpr int H3_MAX_INDEG = H3_CAP / 4 * 3; // load factor <= 0.75
+constexpr int H3_LONG = 256;                 // N(v) longer than this: split over all warps
+constexpr int H3_QMAX = 256;                 // long lists queued per root (overflow: inline)
 
 template <int DPL, bool DUAL = false>
 __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnArgs a) {
@@ -144,11 +148,17 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
   int* cnt = h3 + H3_CAP;
   int* used = cnt + H3_CAP;                                  // [H3_MAX_INDEG] slots taken
   float* s_acc = reinterpret_cast<float*>(used + H3_MAX_INDEG);   // [DHN_WARPS][DPL * 32]
-  __shared__ int s_root;
+  int64_t* q_b = reinterpret_cast<int64_t*>(s_acc + DHN_WARPS * DPL * 32);   // [H3_QMAX]
+  int64_t* q_e = q_b + H3_QMAX;
+  int32_t* q_v = reinterpret_cast<int32_t*>(q_e + H3_QMAX);
+  int32_t* q_i = q_v + H3_QMAX;     // neighbour index of each queued list
+  int32_t* q_ord = q_i + H3_QMAX;   // queue slots in neighbour order
+  __shared__ int s_root, s_qn;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* mark = a.mark + (int64_t)blockIdx.x * a.cta_stride;
   const int d = a.d;
   for (int i = threadIdx.x; i < H3_CAP; i += DHN_THREADS) { keys[i] = -1; cnt[i] = 0; }
+  if (threadIdx.x == 0) s_qn = 0;
   unsigned long long c_roots = 0, c_mark = 0;   // path counters (thread 0)
   for (;;) {
     const int64_t n = dhn_next_root(a, &s_root);
@@ -171,10 +181,10 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
     float acc[DPL], acc_b[DPL];
 #pragma unroll
     for (int j = 0; j < DPL; ++j) acc[j] = acc_b[j] = 0.f;
-    const int64_t pe = a.gp[n + 1];
-    for (int64_t pos = a.gp[n] + warp; pos < pe; pos += DHN_WARPS) {
-      const int32_t v = a.nbr[pos];
-      if (v < 0) continue;
+    const int64_t pb = a.gp[n], pe = a.gp[n + 1];
+    // the wedges n -> v -> w, w in [i_beg, i_end) of N(v): two 32-entry chunks per step (both
+    // loads in flight before either probe); hits gather f1(v) (.) f2(w), 4 per round
+    auto walk_range = [&](int32_t v, int64_t i_beg, int64_t i_end) {
       float f1v[DPL], f1bv[DPL];
 #pragma unroll
       for (int j = 0; j < DPL; ++j) {
@@ -182,11 +192,9 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
         f1v[j] = c < d ? a.F1[(int64_t)v * d + c] : 0.f;
         f1bv[j] = DUAL && c < d ? a.F1b[(int64_t)v * d + c] : 0.f;
       }
-      const int64_t we = a.gp[v + 1];
-      // two 32-entry chunks of N(v) per step: both loads in flight before either probe
-      for (int64_t i0 = a.gp[v]; i0 < we; i0 += 64) {
-        const int32_t w2[2] = {i0 + lane < we ? a.nbr[i0 + lane] : -1,
-                               i0 + 32 + lane < we ? a.nbr[i0 + 32 + lane] : -1};
+      for (int64_t i0 = i_beg; i0 < i_end; i0 += 64) {
+        const int32_t w2[2] = {i0 + lane < i_end ? a.nbr[i0 + lane] : -1,
+                               i0 + 32 + lane < i_end ? a.nbr[i0 + 32 + lane] : -1};
         int m2[2] = {0, 0};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -201,44 +209,88 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
         }
 #pragma unroll
         for (int hc = 0; hc < 2; ++hc) {
-        const int32_t w = w2[hc];
-        const int m = m2[hc];
-        unsigned bal = __ballot_sync(FULL, m != 0);
-        while (bal) {
-          // up to 4 hits per round so their row loads are in flight together
-          int ww[4], mm[4], nh = 0;
+          const int32_t w = w2[hc];
+          const int m = m2[hc];
+          unsigned bal = __ballot_sync(FULL, m != 0);
+          while (bal) {
+            int ww[4], mm[4], nh = 0;
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            ww[h] = 0; mm[h] = 0;
-            if (bal) {
-              const int b = __ffs(bal) - 1;
-              bal &= bal - 1;
-              ww[h] = __shfl_sync(FULL, w, b);
-              mm[h] = __shfl_sync(FULL, m, b);
-              ++nh;
+            for (int h = 0; h < 4; ++h) {
+              ww[h] = 0; mm[h] = 0;
+              if (bal) {
+                const int b = __ffs(bal) - 1;
+                bal &= bal - 1;
+                ww[h] = __shfl_sync(FULL, w, b);
+                mm[h] = __shfl_sync(FULL, m, b);
+                ++nh;
+              }
             }
-          }
 #pragma unroll
-          for (int j = 0; j < DPL; ++j) {
-            const int c = lane + 32 * j;
-            if (c < d) {
-              float x[4];
+            for (int j = 0; j < DPL; ++j) {
+              const int c = lane + 32 * j;
+              if (c < d) {
+                float x[4];
 #pragma unroll
-              for (int h = 0; h < 4; ++h) x[h] = h < nh ? a.F2[(int64_t)ww[h] * d + c] : 0.f;
-              float t = 0.f;
+                for (int h = 0; h < 4; ++h) x[h] = h < nh ? a.F2[(int64_t)ww[h] * d + c] : 0.f;
+                float t = 0.f;
 #pragma unroll
-              for (int h = 0; h < 4; ++h) t += (float)mm[h] * x[h];
-              acc[j] += f1v[j] * t;
-              if (DUAL) acc_b[j] += f1bv[j] * t;
+                for (int h = 0; h < 4; ++h) t += (float)mm[h] * x[h];
+                acc[j] += f1v[j] * t;
+                if (DUAL) acc_b[j] += f1bv[j] * t;
+              }
             }
           }
         }
+      }
+    };
+    // phase A: neighbour i goes to warp i % WARPS (a fixed order per warp: the walk is
+    // deterministic); lists longer than H3_LONG are queued instead
+    for (int64_t i = warp; pb + i < pe; i += DHN_WARPS) {
+      const int32_t v = a.nbr[pb + i];
+      if (v < 0) continue;
+      const int64_t vb = a.gp[v], ve = a.gp[v + 1];
+      if (ve - vb > H3_LONG) {
+        int slot = 0;
+        if (lane == 0) slot = atomicAdd(&s_qn, 1);
+        slot = __shfl_sync(FULL, slot, 0);
+        if (slot < H3_QMAX) {
+          if (lane == 0) { q_v[slot] = v; q_b[slot] = vb; q_e[slot] = ve; q_i[slot] = (int)i; }
+          continue;
         }
+      }
+      walk_range(v, vb, ve);
+    }
+    __syncthreads();
+    // phase B: the queued lists in neighbour order (rank of q_i: the queue's slot order
+    // depends on timing), cut into 128-entry pieces; piece g goes to warp g % WARPS
+    const int nq = s_qn < H3_QMAX ? s_qn : H3_QMAX;
+    if (nq > 0) {
+      for (int t = threadIdx.x; t < nq; t += DHN_THREADS) {
+        int rk = 0;
+        for (int j = 0; j < nq; ++j) rk += q_i[j] < q_i[t];
+        q_ord[rk] = t;
+      }
+      __syncthreads();
+      int k = 0;
+      int64_t k_beg = 0, k_end = 0;
+      for (int g = warp;; g += DHN_WARPS) {
+        while (g >= k_end && k < nq) {
+          const int it = q_ord[k];
+          k_beg = k_end;
+          k_end += (q_e[it] - q_b[it] + 127) / 128;
+          ++k;
+        }
+        if (g >= k_end) break;
+        const int it = q_ord[k - 1];
+        const int64_t b0 = q_b[it] + (int64_t)(g - k_beg) * 128;
+        const int64_t e0 = b0 + 128 < q_e[it] ? b0 + 128 : q_e[it];
+        walk_range(q_v[it], b0, e0);
       }
     }
 #pragma unroll
     for (int j = 0; j < DPL; ++j) s_acc[warp * DPL * 32 + lane + 32 * j] = acc[j];
     __syncthreads();
+    if (threadIdx.x == 0) s_qn = 0;   // every warp is past phase B
     for (int c = threadIdx.x; c < d; c += DHN_THREADS) {
       float s = 0.f;
       for (int w = 0; w < DHN_WARPS; ++w) s += s_acc[w * DPL * 32 + c];
@@ -813,7 +865,7 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
 // Two chunks of a run are loaded per step.  The table is cleared row by row (occupied slots).
 // -------------------------------------------------------------------------------------
 #ifndef H4S_INFLIGHT
-#define H4S_INFLIGHT 2   // IN sweep: hits per lane group in flight per round (x4 per warp)
+#define H4S_INFLIGHT 4   // IN sweep: hits per lane group in flight per round (x4 per warp)
 #endif
 __device__ __forceinline__ uint32_t h4s_hash(int32_t w) { return dhn_hash((uint32_t)w ^ 0x5bd1e995u); }
 __device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w) {
@@ -857,10 +909,12 @@ __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32
     }
   } else {
     const int sl = (in && w >= 0) ? h4s_find(keys, H, w) : -1;
-    for (int q0 = 0; q0 < cnt; q0 += 4 * H4S_INFLIGHT) {
-      float4 x[H4S_INFLIGHT], y[H4S_INFLIGHT], yb[H4S_INFLIGHT];
+    // (the dual-middle walk keeps 2 in flight: a third operand row per hit spills at 4)
+    constexpr int NF = DUAL ? 2 : H4S_INFLIGHT;
+    for (int q0 = 0; q0 < cnt; q0 += 4 * NF) {
+      float4 x[NF], y[NF], yb[NF];
 #pragma unroll
-      for (int u = 0; u < H4S_INFLIGHT; ++u) {
+      for (int u = 0; u < NF; ++u) {
         const int q = q0 + 4 * u + sub;
         const int slq = __shfl_sync(FULL, sl, q & 31);
         const int wq = __shfl_sync(FULL, w, q & 31);
@@ -871,7 +925,7 @@ __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32
           yb[u] = ok ? __ldg(reinterpret_cast<const float4*>(F2bq + (int64_t)wq * d)) : f4_zero();
       }
 #pragma unroll
-      for (int u = 0; u < H4S_INFLIGHT; ++u) {
+      for (int u = 0; u < NF; ++u) {
         t4.x = fmaf(x[u].x, y[u].x, t4.x); t4.y = fmaf(x[u].y, y[u].y, t4.y);
         t4.z = fmaf(x[u].z, y[u].z, t4.z); t4.w = fmaf(x[u].w, y[u].w, t4.w);
         if (DUAL) {
@@ -1481,7 +1535,8 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     a.mark = reinterpret_cast<int*>(b.cta);
     const int dpl = (P.d + 31) / 32;
     const size_t smem = (2 * H3_CAP + H3_MAX_INDEG) * sizeof(int) +
-                        (size_t)DHN_WARPS * dpl * 32 * sizeof(float);
+                        (size_t)DHN_WARPS * dpl * 32 * sizeof(float) +
+                        H3_QMAX * (2 * sizeof(int64_t) + 3 * sizeof(int32_t));
     auto kern = a.F1b ? (dpl == 1 ? dhn3_kernel<1, true> : dpl == 2 ? dhn3_kernel<2, true>
                          : dpl == 3 ? dhn3_kernel<3, true> : dhn3_kernel<4, true>)
                       : (dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2>

@@ -658,13 +658,11 @@ extern "C" rnn_status rnn_lja_workspace_size(const rnn_join_index* idx, const rn
   return RNN_OK;
 }
 
-extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rnn_lifted_query* q,
-                                             const float* out, int64_t ld_out, const float* lse,
-                                             const float* d_out, int64_t ld_dout, float* d_src,
-                                             float* d_src_key, float* d_edge, float* d_dst,
-                                             void* workspace, size_t workspace_bytes,
-                                             void* stream) {
-  clear_error();
+static rnn_status lja_bwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q,
+                               const float* out, int64_t ld_out, const float* lse,
+                               const float* d_out, int64_t ld_dout, float* d_src,
+                               float* d_src_key, float* d_edge, float* d_dst, float beta_dst,
+                               void* workspace, size_t workspace_bytes, void* stream) {
   QueryInfo qi;
   RNN_TRY(check_query(idx, q, &qi));
   cudaStream_t st = as_stream(stream);
@@ -676,6 +674,12 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
   if (!q->src_key.data) d_src_key = nullptr;
   if (!q->edge.data) d_edge = nullptr;
   if (!q->dst.data) d_dst = nullptr;
+  const bool acc_dst = d_dst && beta_dst != 0.f;   // d_dst += (rows never referenced: + 0)
+  RNN_REQUIRE(!acc_dst || idx->n_join_rows == 0 ||   // (an empty join adds nothing)
+                  (q->agg == RNN_AGG_SOFTMAX && sm_rowsplit_ok(idx, q, qi.D) && idx->src_seg &&
+                   !getenv("RNN_SM_TWOPASS")),
+              RNN_ERR_UNSUPPORTED,
+              "beta_dst = 1 needs the SOFTMAX source-major backward (d = 128, dim/heads in {4..32})");
   const bool need_t = d_src || d_src_key;
   RNN_REQUIRE(!need_t || idx->n_groups == 0 ||
                   (idx->src_ptr && idx->src_pos && idx->src_group && idx->src_work_ptr),
@@ -698,12 +702,12 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
     RNN_TRY(zero2d(d_src_key, q->src_key.ld, q->src_key.dim, n_s));
   if (d_edge && q->edge.mode == RNN_BY_ROW)
     RNN_TRY(zero2d(d_edge, q->edge.ld, q->edge.dim, idx->n_edge_rows));
-  if (d_dst && q->dst.mode == RNN_BY_ROW && idx->n_groups < idx->n_dst_rows)
+  if (d_dst && !acc_dst && q->dst.mode == RNN_BY_ROW && idx->n_groups < idx->n_dst_rows)
     RNN_TRY(zero2d(d_dst, q->dst.ld, q->dst.dim, idx->n_dst_rows));
   if (idx->n_groups == 0) return RNN_OK;
   if (idx->n_join_rows == 0) {
     // dense groups over an empty join: every group-side gradient is 0 (no work items run)
-    if (d_dst)
+    if (d_dst && !acc_dst)
       RNN_TRY(zero2d(d_dst, q->dst.ld, q->dst.dim,
                      q->dst.mode == RNN_BY_ROW ? idx->n_dst_rows : idx->n_groups));
     return RNN_OK;
@@ -744,6 +748,7 @@ extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rn
         SmBwdBPol pb;
         pb.a = rows;
         pb.DE = DE; pb.dq = d_dst; pb.ld_dq = q->dst.ld;
+        pb.beta = acc_dst ? 1.f : 0.f;
         RSCtx c1{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
                  idx->n_work, Lw.part_fwd, qi.pstride, Lw.cnt_fwd, 1};
         RNN_TRY(launch_st_var(pb, c1, st, 2));
@@ -892,4 +897,29 @@ extern "C" rnn_status rnn_group_softmax_bwd(const rnn_join_index* idx, const flo
       idx->group_ptr, idx->n_groups, probs, d_probs, heads, d_scores);
   RNN_LAUNCH_CHECK();
   return RNN_OK;
+}
+
+extern "C" rnn_status rnn_join_aggregate_bwd(const rnn_join_index* idx, const rnn_lifted_query* q,
+                                             const float* out, int64_t ld_out, const float* lse,
+                                             const float* d_out, int64_t ld_dout, float* d_src,
+                                             float* d_src_key, float* d_edge, float* d_dst,
+                                             void* workspace, size_t workspace_bytes,
+                                             void* stream) {
+  rnn::clear_error();
+  return lja_bwd_impl(idx, q, out, ld_out, lse, d_out, ld_dout, d_src, d_src_key, d_edge,
+                           d_dst, 0.f, workspace, workspace_bytes, stream);
+}
+
+extern "C" rnn_status rnn_join_aggregate_bwd_acc(const rnn_join_index* idx,
+                                                 const rnn_lifted_query* q, const float* out,
+                                                 int64_t ld_out, const float* lse,
+                                                 const float* d_out, int64_t ld_dout,
+                                                 float* d_src, float* d_src_key, float* d_edge,
+                                                 float* d_dst, float beta_dst, void* workspace,
+                                                 size_t workspace_bytes, void* stream) {
+  rnn::clear_error();
+  RNN_REQUIRE(beta_dst == 0.f || beta_dst == 1.f, RNN_ERR_INVALID_ARGUMENT,
+              "beta_dst must be 0 or 1");
+  return lja_bwd_impl(idx, q, out, ld_out, lse, d_out, ld_dout, d_src, d_src_key, d_edge,
+                           d_dst, beta_dst, workspace, workspace_bytes, stream);
 }

@@ -441,9 +441,10 @@ rnn_status launch_softmax(const LjaArgs& a, int heads, float scale, const SegCtx
 
 }  // namespace
 
+struct Union2 { float* out; int64_t ld; float beta; bool done; };
 rnn_status lja_fwd_core(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
                         int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
-                        cudaStream_t st, const EpiD* epi, int* epi_done);
+                        cudaStream_t st, const EpiD* epi, int* epi_done, Union2* un = nullptr);
 
 rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
                         int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
@@ -466,7 +467,7 @@ rnn_status lja_fwd_impl(const rnn_join_index* idx, const rnn_lifted_query* q, fl
 
 rnn_status lja_fwd_core(const rnn_join_index* idx, const rnn_lifted_query* q, float* out,
                         int64_t ld_out, float beta, float* lse, void* ws, size_t ws_bytes,
-                        cudaStream_t st, const EpiD* epi, int* epi_done) {
+                        cudaStream_t st, const EpiD* epi, int* epi_done, Union2* un) {
   QueryInfo qi;
   RNN_TRY(check_query(idx, q, &qi));
   if (idx->n_groups == 0) return RNN_OK;
@@ -524,6 +525,10 @@ rnn_status lja_fwd_core(const rnn_join_index* idx, const rnn_lifted_query* q, fl
     SmFwdPol pol;
     pol.a = sm_rows(idx, q);
     pol.out = out; pol.ld_out = ld_out; pol.beta = beta; pol.lse = lse;
+    if (un) {   // union store fused into the walker's finish
+      pol.out2 = un->out; pol.ld_out2 = un->ld; pol.beta2 = un->beta;
+      un->done = true;
+    }
     RSCtx rx{idx->pos_group, idx->group_ptr, idx->n_groups, idx->n_join_rows, idx->work_ptr,
              idx->n_work, cx.partial, cx.pstride, cx.counter, 1};
     return launch_st_var(pol, rx, st, 0);
@@ -561,6 +566,31 @@ extern "C" rnn_status rnn_join_aggregate_fwd(const rnn_join_index* idx, const rn
   rnn::clear_error();
   return rnn::lja_fwd_impl(idx, q, out, ld_out, beta, lse, workspace, workspace_bytes,
                            rnn::as_stream(stream));
+}
+
+extern "C" rnn_status rnn_join_aggregate_fwd_union(const rnn_join_index* idx,
+                                                   const rnn_lifted_query* q, float* out,
+                                                   int64_t ld_out, float* lse, float* acc,
+                                                   int64_t ld_acc, float beta_acc,
+                                                   void* workspace, size_t workspace_bytes,
+                                                   void* stream) {
+  rnn::clear_error();
+  RNN_REQUIRE(beta_acc == 0.f || beta_acc == 1.f, RNN_ERR_INVALID_ARGUMENT,
+              "beta_acc must be 0 or 1");
+  RNN_REQUIRE(q && q->agg != RNN_AGG_MEAN, RNN_ERR_UNSUPPORTED,
+              "a union over relations of MEAN is not decomposable (PAPER.md:340)");
+  rnn::QueryInfo qi;
+  RNN_TRY(rnn::check_query(idx, q, &qi));
+  if (idx->n_groups == 0) return RNN_OK;
+  RNN_REQUIRE(acc && ld_acc >= qi.D && ld_acc % 4 == 0 && rnn::aligned16(acc) && acc != out,
+              RNN_ERR_INVALID_ARGUMENT, "acc NULL, aliasing out, unaligned or ld_acc < %d", qi.D);
+  cudaStream_t st = rnn::as_stream(stream);
+  rnn::Union2 un{acc, ld_acc, beta_acc, false};
+  RNN_TRY(rnn::lja_fwd_core(idx, q, out, ld_out, 0.f, lse, workspace, workspace_bytes, st,
+                            nullptr, nullptr, &un));
+  if (!un.done)   // paths without the fused store: one pass acc = beta_acc acc + out
+    return rnn_accumulate(acc, ld_acc, out, ld_out, idx->n_groups, qi.D, beta_acc, stream);
+  return RNN_OK;
 }
 
 extern "C" rnn_status rnn_join_aggregate_fwd_epi(const rnn_join_index* idx,

@@ -200,6 +200,7 @@ struct SmFwdPol {
   SmRows a;
   float* out; int64_t ld_out; float beta;
   float* lse;
+  float* out2 = nullptr; int64_t ld_out2 = 0; float beta2 = 0.f;   // union: out2 = beta2 out2 + x
   struct Meta { int s, t; };
   struct Row { float4 k, v, q; float sc; };
   struct State { float4 acc; float m, l; };
@@ -234,6 +235,10 @@ struct SmFwdPol {
     const int k = lane_id();
     const bool empty = s.l == 0.f;
     float4 x = empty ? f4_zero() : f4_scale(1.f / s.l, s.acc);
+    if (out2) {
+      float* o2 = out2 + g * ld_out2 + 4 * k;
+      st_f4(o2, beta2 != 0.f ? f4_add(x, ld_f4_cg(o2)) : x);
+    }
     float* o = out + g * ld_out + 4 * k;
     if (beta != 0.f) x = f4_fma(beta, ld_f4_cg(o), x);
     st_f4(o, x);
@@ -472,6 +477,7 @@ struct SmBwdBPol {
   SmRows a;
   const float* DE;                 // [E', h]
   float* dq; int64_t ld_dq;
+  float beta = 0.f;                // 1: dq accumulates (a query shared by several relations)
   struct Meta { int s; };
   struct Row { float4 k; float de; };
   struct State { float4 dq; };
@@ -493,10 +499,12 @@ struct SmBwdBPol {
     return a.q_by_group ? g : (int64_t)a.dst_row[g];
   }
   __device__ __forceinline__ void finish(const State& s, int64_t g) const {
-    st_f4(dq + qrow(g) * ld_dq + 4 * lane_id(), f4_scale(a.scale, s.dq));
+    float* o = dq + qrow(g) * ld_dq + 4 * lane_id();
+    const float4 x = f4_scale(a.scale, s.dq);
+    st_f4(o, beta != 0.f ? f4_add(x, ld_f4_cg(o)) : x);
   }
   __device__ __forceinline__ void zero(int64_t g) const {
-    st_f4(dq + qrow(g) * ld_dq + 4 * lane_id(), f4_zero());
+    if (beta == 0.f) st_f4(dq + qrow(g) * ld_dq + 4 * lane_id(), f4_zero());
   }
   __device__ __forceinline__ void save(const State& s, float* dst) const {
     __stcg(reinterpret_cast<float4*>(dst + 4 * lane_id()), s.dq);

@@ -469,13 +469,6 @@ class HGTProgram(_Program):
             n_into = sum(x["dst_type"] == tt for x in rels.values())
             self.O[name] = self.Ht[tt] if n_into == 1 else _empty(self.n[tt], d, dev)
             self.lse[name] = torch.empty(max(self.n[tt], 1), self.h, dtype=torch.float32, device=dev)
-        # dQ of the second and later relations into a target type: written here, then added
-        # onto the type's query-gradient block (the shared Q's gradient is the sum over phi).
-        # A gradient buffer takes its operand's leading dimension (rnn.h), so the scratch is a
-        # d-column view of a buffer as wide as the stacked Y[t] (only its d columns are touched).
-        self.dQ_tmp = {t: torch.empty(max(self.n[t], 1), self.Y[t].stride(0), dtype=torch.float32,
-                                      device=dev)[: self.n[t], :d]
-                       for t in self.targets if sum(r["dst_type"] == t for r in rels.values()) > 1}
         self.ws = rnn.Workspace(dev)
         self.ws_p = rnn.Workspace(dev)
 
@@ -540,11 +533,14 @@ class HGTProgram(_Program):
         for name, r in self.rels.items():
             tt = r["dst_type"]
             self._t("lja_fwd")
-            rnn.join_aggregate_fwd(self.idx[name], self.q[name], out=self.O[name],
-                                   lse=self.lse[name], ws=self.ws)
+            if self.O[name] is self.Ht[tt]:
+                rnn.join_aggregate_fwd(self.idx[name], self.q[name], out=self.O[name],
+                                       lse=self.lse[name], ws=self.ws)
+            else:   # union over the relations into tt, fused into the walker's store
+                rnn.join_aggregate_fwd_union(self.idx[name], self.q[name], self.O[name],
+                                             self.Ht[tt], beta_acc=0.0 if first[tt] else 1.0,
+                                             lse=self.lse[name], ws=self.ws)
             self._t("lja_fwd_end")
-            if self.O[name] is not self.Ht[tt]:     # union over the relations into tt
-                rnn.accumulate(self.Ht[tt], self.O[name], beta=0.0 if first[tt] else 1.0)
             first[tt] = False
         return self.Ht
 
@@ -558,15 +554,16 @@ class HGTProgram(_Program):
             _, bb = rnn.lja_workspace_size(idx, q)
             w = self.ws.get(bb)
             dm, dk = self._blk("m", name, True), self._blk("k", name, True)
-            dq = self._blk("q", tt, True) if first[tt] else self.dQ_tmp[tt]
+            dq = self._blk("q", tt, True)
             self._t("lja_bwd")
-            rnn._check(rnn.lib().rnn_join_aggregate_bwd(
+            # the shared query's gradient is the sum over the relations into tt: the first
+            # writes it, the others accumulate in place (rnn_join_aggregate_bwd_acc)
+            rnn._check(rnn.lib().rnn_join_aggregate_bwd_acc(
                 C.byref(idx.c), C.byref(q), rnn._ptr(self.O[name]), self.O[name].stride(0),
                 rnn._ptr(self.lse[name]), rnn._ptr(dO), dO.stride(0), rnn._ptr(dm), rnn._ptr(dk),
-                None, rnn._ptr(dq), rnn._ptr(w), w.numel(), rnn._stream()))
+                None, rnn._ptr(dq), 0.0 if first[tt] else 1.0, rnn._ptr(w), w.numel(),
+                rnn._stream()))
             self._t("lja_bwd_end")
-            if not first[tt]:
-                rnn.accumulate(self._blk("q", tt, True), dq, beta=1.0)
             first[tt] = False
         self._t("proj_bwd")
         for t in self.blocks:

@@ -102,6 +102,10 @@ def lib():
                                              C.c_float, vp, vp, sz, vp]
         L.rnn_join_aggregate_bwd.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp, i64, vp,
                                              vp, i64, vp, vp, vp, vp, vp, sz, vp]
+        L.rnn_join_aggregate_fwd_union.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp,
+                                                   i64, vp, vp, i64, C.c_float, vp, sz, vp]
+        L.rnn_join_aggregate_bwd_acc.argtypes = [C.POINTER(JoinIndexC), C.POINTER(QueryC), vp, i64,
+                                                 vp, vp, i64, vp, vp, vp, vp, C.c_float, vp, sz, vp]
         L.rnn_group_softmax.argtypes = [C.POINTER(JoinIndexC), vp, i32, vp, vp]
         L.rnn_group_softmax_bwd.argtypes = [C.POINTER(JoinIndexC), vp, vp, i32, vp, vp]
         L.rnn_project.argtypes = [vp, i64, i32, i64, vp, i32, i64, vp, vp, i64, C.c_int, vp]
@@ -171,6 +175,7 @@ def lib():
             getattr(L, f).restype = C.c_int
         for f in ("rnn_build_join_index", "rnn_lja_workspace_size", "rnn_join_aggregate_fwd",
                   "rnn_join_aggregate_bwd", "rnn_group_softmax", "rnn_group_softmax_bwd",
+                  "rnn_join_aggregate_fwd_union", "rnn_join_aggregate_bwd_acc",
                   "rnn_project", "rnn_project_bwd_workspace_size", "rnn_project_bwd",
                   "rnn_project_bwd_relu", "rnn_gcn_norm", "rnn_hash_partition"):
             getattr(L, f).restype = C.c_int
@@ -372,6 +377,22 @@ def join_aggregate_fwd(idx: JoinIndex, q: QueryC, out=None, beta=0.0, lse=None, 
     return (out, lse) if q.agg == AGG["softmax"] else out
 
 
+def join_aggregate_fwd_union(idx: JoinIndex, q: QueryC, out, acc, beta_acc=0.0, lse=None,
+                             ws=None, stream=None):
+    """out = the aggregate (as join_aggregate_fwd, beta 0) and, in the same pass,
+    acc = beta_acc * acc + out (rnn_join_aggregate_fwd_union: HGT's union over relations that
+    keeps each relation's own output for its backward)."""
+    dev = idx.group_ptr.device
+    if q.agg == AGG["softmax"] and lse is None:
+        lse = torch.empty(max(idx.n_groups, 1), q.heads, dtype=torch.float32, device=dev)
+    fb, _ = lja_workspace_size(idx, q)
+    w = ws.get(fb) if ws is not None else _ws(fb, dev)
+    _check(lib().rnn_join_aggregate_fwd_union(C.byref(idx.c), C.byref(q), _ptr(out), out.stride(0),
+                                              _ptr(lse), _ptr(acc), acc.stride(0), float(beta_acc),
+                                              _ptr(w), w.numel(), _stream(stream)))
+    return (out, lse) if q.agg == AGG["softmax"] else out
+
+
 def _grad_like(op: OperandC, rows, dev):
     if not op.data:
         return None
@@ -417,10 +438,23 @@ def group_softmax_bwd(idx: JoinIndex, probs, d_probs, heads, stream=None):
 # ------------------------------------------------------------------------------------------
 # A2 projection
 # ------------------------------------------------------------------------------------------
+# tensor-core work of the projections, counted when a dict is installed here (bench.py's
+# projection roofline): {"proj_fwd": flops, "proj_bwd": flops}, MMA flops as issued (3xTF32
+# issues three tf32 products per term)
+FLOP_COUNTER = None
+_MMAS = {"tf32": 1, "3xtf32": 3, "bf16": 1}
+
+
+def _count(kind, flops):
+    if FLOP_COUNTER is not None:
+        FLOP_COUNTER[kind] = FLOP_COUNTER.get(kind, 0) + flops
+
+
 def project(X, W, bias=None, out=None, prec="3xtf32", stream=None):
     """Y = X W^T + b on tcgen05 (W is [N, K] like nn.Linear.weight)."""
     M, K = X.shape
     N = W.shape[0]
+    _count("proj_fwd", 2 * M * K * N * _MMAS[prec])
     if out is None:
         out = torch.empty(M, (N + 3) // 4 * 4, dtype=torch.float32, device=X.device)[:, :N]
     _check(lib().rnn_project(_ptr(X), M, K, X.stride(0), _ptr(W), N, W.stride(0), _ptr(bias),
@@ -436,6 +470,7 @@ def project_bwd(X, W, dY, want_dx=True, want_db=False, prec="3xtf32", ws=None, s
     M, K = X.shape
     N = W.shape[0]
     dev = X.device
+    _count("proj_bwd", 2 * M * K * N * _MMAS[prec] * (2 if want_dx else 1))
     dX = None
     if want_dx:
         dX = dx_out if dx_out is not None else torch.empty(M, (K + 3) // 4 * 4, dtype=torch.float32, device=dev)[:, :K]
@@ -593,6 +628,8 @@ def dhn_bwd(adj: JoinIndex, k, f, d_out, want=None, d_f=None, ws=None, stream=No
                                        ld, DHN_SYMMETRIC_EDGE if symmetric else 0, _ptr(w),
                                        w.numel(), _stream(stream)))
         return d_f
+    if symmetric:
+        raise ValueError("symmetric=True needs walk_sum or roots (rnn_dhn_bwd takes no flags)")
     _check(lib().rnn_dhn_bwd(C.byref(adj.c), k, _dhn_ops(f), _ptr(d_out), d_out.stride(0), ptrs,
                              ld, _ptr(w), w.numel(), _stream(stream)))
     return d_f

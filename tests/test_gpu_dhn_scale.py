@@ -108,7 +108,7 @@ def test_counts_beyond_fp32(rnn):
 # ------------------------------------------------------------------------------------------
 # big-root paths of the fp32 walk kernels
 # ------------------------------------------------------------------------------------------
-def check_walks(rnn, keys, e_n, e_v, k, d, seed, ks_count=True, dyadic=False):
+def check_walks(rnn, keys, e_n, e_v, k, d, seed, ks_count=True, dyadic=False, sym=False):
     """fp32 forward + every backward operand vs the oracle; exact counts vs the oracle.
     dyadic: features k/8 in [0.5, 1.5] -- for multigraphs whose walk sums run over 10^5
     terms through ONE key: every partial sum (< 2^21 in units of 1/8) is then exact in fp32
@@ -142,6 +142,15 @@ def check_walks(rnn, keys, e_n, e_v, k, d, seed, ks_count=True, dyadic=False):
         got = np_(rnn.dhn_count(gi, k))
         ref = oracle.dhn_fwd(k, oi, keys, [np.ones((n, 1))] * k)[:, 0]
         np.testing.assert_array_equal(got[rows], ref.astype(np.int64))
+    if sym:   # symmetric Edge: the dual-middle backward (d f1 | d f3 from one walk)
+        ws_s = torch.empty((gi.n_groups, d), dtype=torch.float32, device="cuda")
+        rnn.dhn_fwd(gi, k, fg, walk_sum=ws_s)
+        rnn.dhn_path_counters(reset=True)
+        grads_s = rnn.dhn_bwd(gi, k, fg, cu(d_out), walk_sum=ws_s, symmetric=True)
+        paths_s = rnn.dhn_path_counters()
+        for i in range(k):
+            assert_close(np_(grads_s[i]), ref_g[i], FP32_TOL, f"C{k} d f{i} (sym)")
+        return paths, paths_s
     return paths
 
 
@@ -161,7 +170,7 @@ def star_graph(seed, n_leaves, extra):
 
 
 def test_c3_mark_array_path(rnn):
-    """A root with in-degree 7,000 > H3_MAX_INDEG = 6,144 keeps its in-neighbours in the
+    """A root with in-degree 7,000 > H3_MAX_INDEG (3,072) keeps its in-neighbours in the
     per-CTA global mark array instead of the shared-memory hash set."""
     keys, e_n, e_v = star_graph(1, 7000, 3000)
     paths = check_walks(rnn, keys, e_n, e_v, 3, 8, seed=5)
@@ -188,10 +197,11 @@ def test_c4_partitioned_chunked_path(rnn, c4_variant):
     itself has 8,300 neighbours (> H4_DEG_CAP: no smem cursors, binary-searched partition
     starts) and walks its neighbours 32 at a time (chunked mode)."""
     keys, e_n, e_v = star_graph(2, 8300, 1000)
-    paths = check_walks(rnn, keys, e_n, e_v, 4, 4, seed=6)
-    assert paths["c4_partitioned_roots"] >= 1, paths
-    assert paths["c4_chunked_passes"] >= 1, paths
-    assert paths["c4_passes"] > paths["c4_roots"], paths
+    paths, paths_s = check_walks(rnn, keys, e_n, e_v, 4, 4, seed=6, sym=True)
+    for p in (paths, paths_s):   # the dual-middle symmetric walk takes the same big-root paths
+        assert p["c4_partitioned_roots"] >= 1, p
+        assert p["c4_chunked_passes"] >= 1, p
+        assert p["c4_passes"] > p["c4_roots"], p
 
 
 def test_c4_long_run_overflow(rnn, c4_variant):
@@ -261,6 +271,11 @@ def test_products_full_scale_sampled(rnn, products):
     d_out = rng.standard_normal((G, d)).astype(np.float32)
     g4 = rnn.dhn_bwd(gi, 4, fg, cu(d_out), want=[False, True, False, False])[1]
     g4 = np_(g4)
+    # the symmetric Edge backward the bench runs (d f1 | d f3 from one dual-middle walk)
+    ws4 = torch.empty((G, d), dtype=torch.float32, device="cuda")
+    c4s = np_(rnn.dhn_fwd(gi, 4, fg, walk_sum=ws4))
+    g4s = np_(rnn.dhn_bwd(gi, 4, fg, cu(d_out), want=[False, True, False, True], walk_sum=ws4,
+                          symmetric=True)[1])
     assert paths["c4_roots"] == G and paths["c4_partitioned_roots"] > 0, paths
     assert paths["c4_value_overflow"] == 0, paths
     # sampled roots: 48 random + 8 of degree 200-600 (C3 also gets the 4 largest hubs)
@@ -281,6 +296,8 @@ def test_products_full_scale_sampled(rnn, products):
         ref = oracle.dhn_fwd(k, oi, keys, f[:k], sel=og)
         assert_close((c3 if k == 3 else c4)[sel], ref, FP32_TOL, f"C{k} fwd (sampled roots)")
         if k == 4:
+            assert_close(c4s[sel], ref, FP32_TOL, "C4 fwd, with walk sum (sampled roots)")
+        if k == 4:
             # d f1(x) = sum over closed walks x -> w -> p -> n -> x of f2(w) f3(p) g(n),
             # g = f0 (.) dOut by node row: the walk aggregate rooted at x, operands rotated
             row_of = np_(gi.group_dst_row)
@@ -289,5 +306,6 @@ def test_products_full_scale_sampled(rnn, products):
             rot = [np.ones((len(keys), d)), f[2], f[3], gnode]
             ref_d1 = oracle.dhn_fwd(4, oi, keys, rot, sel=og)
             assert_close(g4[row_of[sel]], ref_d1, FP32_TOL, "C4 d f1 (sampled nodes)")
+            assert_close(g4s[row_of[sel]], ref_d1, FP32_TOL, "C4 d f1, symmetric (sampled nodes)")
     np.testing.assert_array_equal(counts[2], deg)
     assert counts[3].sum() > 0 and counts[4].sum() > counts[3].sum()

@@ -530,3 +530,91 @@ def test_max_aggregate_parity(R, ora, D, wmode, dense):
     assert_close(np_(d_src), rdz, FP32_TOL, "d_src")
     if w is not None:
         assert_close(np_(d_edge).reshape(-1), rdw, FP32_TOL, "d_edge")
+
+
+@pytest.mark.parametrize("heads,D,split", [(8, 128, 32), (8, 128, 0), (2, 16, 32)])
+def test_union_fwd_and_accumulating_bwd(R, ora, heads, D, split):
+    """rnn_join_aggregate_fwd_union: out = the relation's own aggregate (what its backward
+    needs) and acc = beta acc + out in the same pass (fused for D = 128, one extra pass
+    otherwise); rnn_join_aggregate_bwd_acc: d_dst = d_dst + gradient of a query shared by two
+    relations -- the union of two relations into one target type against the oracle's sum."""
+    rng = np.random.default_rng(D + heads + split)
+    n_s, n_t = 400, 150
+    scale = 1.0 / np.sqrt(D / heads)
+    Q = (rng.standard_normal((n_t, D)) * 0.5).astype(np.float32)
+    t_key = rng.permutation(n_t).astype(np.int64) * 3 + 1
+    rels = []
+    for r in range(2):
+        s_key = rng.permutation(n_s).astype(np.int64) * 7 + r
+        # every target once (dense groups = the compact ones) plus Zipf-distributed hub rows
+        e_dst = np.concatenate([t_key, t_key[np.minimum(rng.zipf(1.5, 6000) - 1, n_t - 1)]])
+        e_src = s_key[rng.integers(0, n_s, len(e_dst))]
+        gi = R.build_join_index(cu(e_src), cu(e_dst), cu(s_key), cu(t_key), dense_groups=True,
+                                rows_per_item=split)
+        oi = ora.build_join_index(e_src, e_dst, s_key, t_key)
+        assert gi.n_groups == oi["n_groups"] == n_t
+        K = (rng.standard_normal((n_s, D)) * 0.5).astype(np.float32)
+        M = rng.standard_normal((n_s, D)).astype(np.float32)
+        rels.append((gi, oi, K, M))
+    Qd = padded(Q)
+    acc = padded(np.full((n_t, D), 123.0, np.float32))
+    dQ = padded(np.full((n_t, D), -7.0, np.float32))
+    dO = rng.standard_normal((n_t, D)).astype(np.float32)
+    ref_acc = np.zeros((n_t, D))
+    ref_dq = np.zeros((n_t, D))
+    for r, (gi, oi, K, M) in enumerate(rels):
+        q = R.make_query("src", "softmax", src=padded(M), src_key=padded(K), dst=Qd, heads=heads,
+                         scale=scale)
+        out = padded(np.zeros((n_t, D), np.float32))
+        out, lse = R.join_aggregate_fwd_union(gi, q, out, acc, beta_acc=float(r))
+        ref, _ = ora.lja_fwd(oi, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=scale)
+        assert_close(np_(out), ref, FP32_TOL, f"out[{r}]")
+        ref_acc += ref
+        if D != 128:
+            continue   # beta_dst = 1 is a D = 128 (source-major walker) feature
+        ws = R.Workspace(torch.device("cuda"))
+        _, bb = R.lja_workspace_size(gi, q)
+        w = ws.get(bb)
+        import ctypes as C
+        R._check(R.lib().rnn_join_aggregate_bwd_acc(
+            C.byref(gi.c), C.byref(q), R._ptr(out), out.stride(0), R._ptr(lse), R._ptr(padded(dO)),
+            padded(dO).stride(0), None, None, None, R._ptr(dQ), float(r), R._ptr(w), w.numel(),
+            R._stream()))
+        gr = ora.lja_bwd(oi, dO, agg="softmax", src=M, src_key=K, dst=Q, heads=heads, scale=scale)
+        ref_dq += gr["dst"]
+    assert_close(np_(acc), ref_acc, FP32_TOL, "acc = O_0 + O_1")
+    if D == 128:
+        assert_close(np_(dQ), ref_dq, FP32_TOL, "dQ = dQ_0 + dQ_1")
+
+
+def test_union_errors_and_empty(R):
+    """beta_dst = 1 outside the source-major softmax backward is refused; MEAN unions are
+    refused; an empty dense-group join leaves acc + 0 and an accumulated dQ untouched."""
+    import ctypes as C
+    keys = cu(np.arange(10, dtype=np.int64))
+    gi = R.build_join_index(cu(np.zeros(0, np.int64)), cu(np.zeros(0, np.int64)), keys, keys,
+                            dense_groups=True)
+    M = padded(np.ones((10, 128), np.float32))
+    q = R.make_query("src", "softmax", src=M, src_key=M, dst=M, heads=8, scale=1.0)
+    acc = padded(np.full((10, 128), 5.0, np.float32))
+    out = padded(np.zeros((10, 128), np.float32))
+    out, lse = R.join_aggregate_fwd_union(gi, q, out, acc, beta_acc=1.0)
+    assert np.all(np_(acc) == 5.0) and np.all(np_(out) == 0.0)
+    dQ = padded(np.full((10, 128), 3.0, np.float32))
+    dO = padded(np.ones((10, 128), np.float32))
+    w = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    R._check(R.lib().rnn_join_aggregate_bwd_acc(
+        C.byref(gi.c), C.byref(q), R._ptr(out), out.stride(0), R._ptr(lse), R._ptr(dO),
+        dO.stride(0), None, None, None, R._ptr(dQ), 1.0, R._ptr(w), w.numel(), R._stream()))
+    torch.cuda.synchronize()
+    assert np.all(np_(dQ) == 3.0)
+    with pytest.raises(R.RnnError):
+        R.join_aggregate_fwd_union(gi, R.make_query("src", "mean", src=M), out, acc)
+    # a non-empty SUM join with a group-side operand: d_dst accumulation is refused there
+    e = cu(np.arange(10, dtype=np.int64))
+    gs = R.build_join_index(e, e, keys, keys)
+    qs = R.make_query("mul", "sum", src=M, dst=M)
+    st = R.lib().rnn_join_aggregate_bwd_acc(
+        C.byref(gs.c), C.byref(qs), None, 0, None, R._ptr(dO), dO.stride(0), None, None, None,
+        R._ptr(dQ), 1.0, R._ptr(w), w.numel(), R._stream())
+    assert st != 0
