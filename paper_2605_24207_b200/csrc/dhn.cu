@@ -139,7 +139,8 @@ __device__ __forceinline__ int hs_find(const int* keys, int cap_mask, int w) {
 constexpr int H3_CAP = H3_CAP_CFG;           // slots (keys + counts: 64 KB at 8,192)
 constexpr int H3_MAX_INDEG = H3_CAP / 4 * 3; // load factor <= 0.75
 constexpr int H3_LONG = 256;                 // N(v) longer than this: split over all warps
-constexpr int H3_QMAX = 256;                 // long lists queued per root (overflow: inline)
+constexpr int H3_QMAX = 128;                 // long lists queued per root (overflow: inline)
+constexpr int H3_PRE = 256;                  // neighbours whose list extents are prefetched
 
 template <int DPL, bool DUAL = false>
 __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnArgs a) {
@@ -153,6 +154,9 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
   int32_t* q_v = reinterpret_cast<int32_t*>(q_e + H3_QMAX);
   int32_t* q_i = q_v + H3_QMAX;     // neighbour index of each queued list
   int32_t* q_ord = q_i + H3_QMAX;   // queue slots in neighbour order
+  int64_t* p_b = reinterpret_cast<int64_t*>(q_ord + H3_QMAX);     // [H3_PRE] list start of N(v)
+  int32_t* p_v = reinterpret_cast<int32_t*>(p_b + H3_PRE);        // [H3_PRE] neighbour v
+  int32_t* p_l = p_v + H3_PRE;                                      // [H3_PRE] |N(v)|
   __shared__ int s_root, s_qn;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* mark = a.mark + (int64_t)blockIdx.x * a.cta_stride;
@@ -176,6 +180,16 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
       }
     } else {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) atomicAdd(&mark[a.sg[q]], 1);
+    }
+    {   // the first H3_PRE neighbours' list extents, lane-parallel (one latency chain per root)
+      const int64_t pb0 = a.gp[n], np = a.gp[n + 1] - pb0 < H3_PRE ? a.gp[n + 1] - pb0 : H3_PRE;
+      for (int64_t i = threadIdx.x; i < np; i += DHN_THREADS) {
+        const int32_t v = a.nbr[pb0 + i];
+        const int64_t b = v >= 0 ? a.gp[v] : 0;
+        p_v[i] = v;
+        p_b[i] = b;
+        p_l[i] = v >= 0 ? (int32_t)(a.gp[v + 1] - b) : 0;
+      }
     }
     __syncthreads();
     float acc[DPL], acc_b[DPL];
@@ -246,9 +260,16 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
     // phase A: neighbour i goes to warp i % WARPS (a fixed order per warp: the walk is
     // deterministic); lists longer than H3_LONG are queued instead
     for (int64_t i = warp; pb + i < pe; i += DHN_WARPS) {
-      const int32_t v = a.nbr[pb + i];
+      int32_t v;
+      int64_t vb, ve;
+      if (i < H3_PRE) {
+        v = p_v[i]; vb = p_b[i]; ve = vb + p_l[i];
+      } else {
+        v = a.nbr[pb + i];
+        vb = v >= 0 ? a.gp[v] : 0;
+        ve = v >= 0 ? a.gp[v + 1] : 0;
+      }
       if (v < 0) continue;
-      const int64_t vb = a.gp[v], ve = a.gp[v + 1];
       if (ve - vb > H3_LONG) {
         int slot = 0;
         if (lane == 0) slot = atomicAdd(&s_qn, 1);
@@ -539,6 +560,16 @@ struct H4Root {
   uint32_t P, part;
   int sh;
   bool cur_ok, chunked;
+};
+
+// slot walk: the first H4_PRE neighbours of each side are read once per root, lane-parallel,
+// into shared memory (neighbour, list start, list length), so no partition pass repeats the
+// dependent global loads neighbour -> list extent
+constexpr int H4_PRE = 2048;
+struct H4Pre {
+  const int32_t* u;
+  const int64_t* s;
+  const int32_t* len;
 };
 
 // One side of one partition.  OUT: neighbours v = nbr[pb + i] with lists nbrh over the group
@@ -942,7 +973,7 @@ __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32
 template <bool OUT, bool DUAL>
 __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float* S, int* cur,
                             int* q_i, int64_t* q_b, int64_t* q_e, int* q_n, int* grab, int c0,
-                            int* s_cnt, float4* acc_b) {
+                            int* s_cnt, float4* acc_b, const H4Pre& pre) {
   const int lane = threadIdx.x & 31;
   const int32_t* L = OUT ? a.nbrh : a.sgh;
   const float* Fv = OUT ? a.F1 : a.F3;
@@ -971,7 +1002,11 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
     int64_t b0 = 0, e0 = 0, s0 = 0;
     bool has = false;
     if (i < R.deg && (R.chunked || lane == 0)) {
-      if (OUT) {
+      if (i < H4_PRE) {   // neighbour and list extent prefetched at root setup (shared memory)
+        u = pre.u[i];
+        s0 = pre.s[i];
+        e0 = s0 + pre.len[i];
+      } else if (OUT) {
         u = a.nbr[R.pb + i];
         if (u >= 0) { s0 = a.gp[u]; e0 = a.gp[u + 1]; }
       } else {
@@ -982,7 +1017,9 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
       }
       if (u >= 0) {
         b0 = R.cur_ok ? s0 + cur[i] : h4_lower(L, s0, e0, R.part, R.sh);
-        has = b0 < e0 && (h4_top(L[b0]) >> R.sh) == R.part;
+        // (no probe of L[b0] for the partition: a run with no entry in this partition ends
+        // at its first chunk -- one dependent global load less per neighbour)
+        has = b0 < e0;
       }
     }
     unsigned hb = __ballot_sync(FULL, has);
@@ -1088,6 +1125,10 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
   int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
   int64_t* q_e = q_b + H4_LONG_MAX;
   int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
+  int64_t* pre_s = reinterpret_cast<int64_t*>(q_i + H4_LONG_MAX);  // [2][H4_PRE]
+  int32_t* pre_u = reinterpret_cast<int32_t*>(pre_s + 2 * H4_PRE);  // [2][H4_PRE]
+  int32_t* pre_l = pre_u + 2 * H4_PRE;                              // [2][H4_PRE]
+  const H4Pre pre_out{pre_u, pre_s, pre_l}, pre_in{pre_u + H4_PRE, pre_s + H4_PRE, pre_l + H4_PRE};
   float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;          // [H4_CAP][32], zero
   __shared__ int s_root, q_n, grab;
   __shared__ int s_cnt[2];
@@ -1112,6 +1153,22 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
     H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
     R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
     c_multi += R.P > 1;
+    // neighbour metadata of both sides, lane-parallel (read by every partition pass)
+    for (int i = threadIdx.x; i < (deg_out < H4_PRE ? deg_out : H4_PRE); i += H4_THREADS) {
+      const int32_t u = a.nbr[pb + i];
+      pre_u[i] = u;
+      const int64_t b = u >= 0 ? a.gp[u] : 0;
+      pre_s[i] = b;
+      pre_l[i] = u >= 0 ? (int32_t)(a.gp[u + 1] - b) : 0;
+    }
+    for (int i = threadIdx.x; i < (deg_in < H4_PRE ? deg_in : H4_PRE); i += H4_THREADS) {
+      const int32_t u = a.sg[ib + i];
+      const int32_t ru = a.row_of[u];
+      const int64_t b = a.sp[ru];
+      pre_u[H4_PRE + i] = u;
+      pre_s[H4_PRE + i] = b;
+      pre_l[H4_PRE + i] = (int32_t)(a.sp[ru + 1] - b);
+    }
     for (int c0 = 0; c0 < d; c0 += 32) {
       float4 acc = f4_zero(), acc_b = f4_zero();
       if (cur_ok) {
@@ -1125,10 +1182,10 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
         c_chunked += R.chunked;
         R.deg = deg_out;
         h4s_sweep<true, false>(a, R, keys, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c0, s_cnt,
-                               nullptr);
+                               nullptr, pre_out);
         R.deg = deg_in;
         acc = f4_add(acc, h4s_sweep<false, DUAL>(a, R, keys, S, cur_in, q_i, q_b, q_e, &q_n,
-                                                 &grab, c0, s_cnt, &acc_b));
+                                                 &grab, c0, s_cnt, &acc_b, pre_in));
         // clear the occupied rows and slots for the next partition / root (the sweeps ended
         // with a barrier, so no lane still reads the table)
         for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) {
@@ -1536,7 +1593,8 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     const int dpl = (P.d + 31) / 32;
     const size_t smem = (2 * H3_CAP + H3_MAX_INDEG) * sizeof(int) +
                         (size_t)DHN_WARPS * dpl * 32 * sizeof(float) +
-                        H3_QMAX * (2 * sizeof(int64_t) + 3 * sizeof(int32_t));
+                        H3_QMAX * (2 * sizeof(int64_t) + 3 * sizeof(int32_t)) +
+                        H3_PRE * (sizeof(int64_t) + 2 * sizeof(int32_t));
     auto kern = a.F1b ? (dpl == 1 ? dhn3_kernel<1, true> : dpl == 2 ? dhn3_kernel<2, true>
                          : dpl == 3 ? dhn3_kernel<3, true> : dhn3_kernel<4, true>)
                       : (dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2>
@@ -1577,7 +1635,8 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
       a.part_keys = std::min(part_keys, H4_PART);
       const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4_DEG_CAP * sizeof(int) +
-                            H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
+                            H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) +
+                            2 * H4_PRE * (sizeof(int64_t) + 2 * sizeof(int32_t));
       auto kern = F2b ? dhn4s_kernel<true> : dhn4s_kernel<false>;
       RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
       kern<<<P.n_cta, H4_THREADS, smem_s, st>>>(a);

@@ -147,13 +147,34 @@ __global__ void __launch_bounds__(256) epi_bwd4_kernel(const float* __restrict__
   }
 }
 
-__global__ void epi_colsum_final(const float* __restrict__ part, int64_t chunks, int dim,
-                                 float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= dim) return;
-  float t = 0.f;
-  for (int64_t k = 0; k < chunks; ++k) t += part[k * dim + c];
-  out[c] = t;
+// out[c] = sum over the chunks' partial rows, fixed order: block = 32 columns x 8 chunk lanes,
+// lane j sums chunks j, j + 8, ... with four loads in flight, then the 8 sums in order (one
+// thread per column summing 662 rows serially took 41 us at arxiv size)
+__global__ void __launch_bounds__(256) epi_colsum_final(const float* __restrict__ part,
+                                                        int64_t chunks, int dim,
+                                                        float* __restrict__ out) {
+  __shared__ float sh[8][33];
+  const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+  if (c < dim) {
+    int64_t k = j;
+    for (; k + 24 < chunks; k += 32) {
+      t0 += part[k * dim + c];
+      t1 += part[(k + 8) * dim + c];
+      t2 += part[(k + 16) * dim + c];
+      t3 += part[(k + 24) * dim + c];
+    }
+    for (; k < chunks; k += 8) t0 += part[k * dim + c];
+  }
+  sh[j][lane] = (t0 + t1) + (t2 + t3);
+  __syncthreads();
+  if (j == 0 && c < dim) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += sh[q][lane];
+    out[c] = s;
+  }
 }
 
 __global__ void epi_sum_final(const float* __restrict__ part, int64_t n, float* __restrict__ out) {
@@ -265,7 +286,7 @@ extern "C" rnn_status rnn_epilogue_bwd(const float* dy, int64_t lddy, const floa
                                          d_gate ? part_g : nullptr);
   RNN_LAUNCH_CHECK();
   if (d_bias) {
-    epi_colsum_final<<<(unsigned)ceil_div(dim, 128), 128, 0, st>>>(part_b, chunks, dim, d_bias);
+    epi_colsum_final<<<(unsigned)ceil_div(dim, 32), 256, 0, st>>>(part_b, chunks, dim, d_bias);
     RNN_LAUNCH_CHECK();
   }
   if (d_gate) {

@@ -1043,23 +1043,46 @@ __global__ void colsum_partial(const float* __restrict__ Y, int64_t M, int N, in
     if (c < N) part[blockIdx.y * (int64_t)N + c] = s;
   }
 }
-__global__ void colsum_final(const float* __restrict__ part, int64_t chunks, int N,
-                             float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  float s = 0.f;
-  for (int64_t k = 0; k < chunks; ++k) s += part[k * N + c];
-  out[c] = s;
+// out[f] = sum_i part[(base(f) + i * stride) * N + f] over the partial rows of column f, in a
+// fixed order: block = 32 columns x 8 row lanes, lane j sums rows i = j, j + 8, ... (four
+// loads in flight), then the 8 lane sums are added in order (the serial one-thread-per-column
+// sum was latency-bound: 22-41 us for 148-662 partial rows)
+__device__ __forceinline__ void colsum8(const float* __restrict__ part, int64_t n, int64_t base,
+                                        int64_t stride, int N, float* __restrict__ out) {
+  __shared__ float sh[8][33];
+  const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
+  const int f = blockIdx.x * 32 + lane;
+  float t0 = 0.f, t1 = 0.f, t2 = 0.f, t3 = 0.f;
+  if (f < N) {
+    int64_t i = j;
+    for (; i + 24 < n; i += 32) {
+      t0 += part[(base + i * stride) * N + f];
+      t1 += part[(base + (i + 8) * stride) * N + f];
+      t2 += part[(base + (i + 16) * stride) * N + f];
+      t3 += part[(base + (i + 24) * stride) * N + f];
+    }
+    for (; i < n; i += 8) t0 += part[(base + i * stride) * N + f];
+  }
+  sh[j][lane] = (t0 + t1) + (t2 + t3);
+  __syncthreads();
+  if (j == 0 && f < N) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += sh[q][lane];
+    out[f] = s;
+  }
+}
+__global__ void __launch_bounds__(256) colsum_final(const float* __restrict__ part, int64_t chunks,
+                                                    int N, float* __restrict__ out) {
+  colsum8(part, chunks, 0, 1, N, out);
 }
 // column sums of the fused ReLU backward (tc_projt_kernel colsum): CTA c wrote the features of
 // column block c % n_tiles_n, so feature f sums the CTAs nt(f), nt(f) + n_tiles_n, ... in order
-__global__ void projt_colsum_final(const float* __restrict__ part, int grid, int n_tiles_n, int N,
-                                   float* __restrict__ out) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= N) return;
-  float s = 0.f;
-  for (int c = f / 128; c < grid; c += n_tiles_n) s += part[(int64_t)c * N + f];
-  out[f] = s;
+__global__ void __launch_bounds__(256) projt_colsum_final(const float* __restrict__ part, int grid,
+                                                          int n_tiles_n, int N,
+                                                          float* __restrict__ out) {
+  const int nt = blockIdx.x * 32 / 128;   // 32-column blocks never straddle a 128-feature block
+  colsum8(part, (grid - nt + n_tiles_n - 1) / n_tiles_n, nt, n_tiles_n, N, out);
 }
 // dX *= [X > 0] (the unfused path of rnn_project_bwd_relu)
 __global__ void relu_mask_kernel(float* __restrict__ dx, int64_t lddx, const float* __restrict__ x,
@@ -1396,12 +1419,12 @@ rnn_status project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, const 
       if (d_in_bias) {
         if (rb.fused) {
           RNN_REQUIRE(rb.grid <= RELU_PART_ROWS, RNN_ERR_UNSUPPORTED, "fused grid %d", rb.grid);
-          projt_colsum_final<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(w.rpart, rb.grid,
+          projt_colsum_final<<<(unsigned)ceil_div(K, 32), 256, 0, st>>>(w.rpart, rb.grid,
                                                                         rb.n_tiles_n, K, d_in_bias);
         } else {
           dim3 g1((unsigned)ceil_div(K, 32), (unsigned)w.chunks);
           colsum_partial<<<g1, 256, 0, st>>>(dX, M, K, lddx, 4096, w.rpart);
-          colsum_final<<<(unsigned)ceil_div(K, 128), 128, 0, st>>>(w.rpart, w.chunks, K,
+          colsum_final<<<(unsigned)ceil_div(K, 32), 256, 0, st>>>(w.rpart, w.chunks, K,
                                                                    d_in_bias);
         }
         RNN_LAUNCH_CHECK();
@@ -1478,7 +1501,7 @@ rnn_status project_bwd(const float* X, int64_t M, int32_t K, int64_t ldx, const 
     } else {
       dim3 g1((unsigned)ceil_div(N, 32), (unsigned)w.chunks);
       colsum_partial<<<g1, 256, 0, st>>>(dY, M, N, lddy, 4096, w.cpart);
-      colsum_final<<<(unsigned)ceil_div(N, 128), 128, 0, st>>>(w.cpart, w.chunks, N, db);
+      colsum_final<<<(unsigned)ceil_div(N, 32), 256, 0, st>>>(w.cpart, w.chunks, N, db);
       RNN_LAUNCH_CHECK();
     }
   }

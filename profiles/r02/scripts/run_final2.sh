@@ -30,7 +30,7 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --set full --clock-control none --import-source on \
   -k regex:'lean_kernel' -c 4 -o /tmp/ncu/prof_hyper -f \
   python bench.py --config hyper --steps 1 --warmup 1 --seeds 42 --eager --no-e2e --no-cpu-baseline > $O/ncu_full_hyper.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:'dhn3_kernel|dhn4y_kernel' -c 3 -o /tmp/ncu/prof_dhn -f \
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:'dhn3_kernel|dhn4s_kernel' -c 3 -o /tmp/ncu/prof_dhn -f \
   python bench.py --config dhn --dhn-scale 0.03 --steps 1 --warmup 0 --seeds 42 --no-cpu-baseline --no-e2e --eager > $O/ncu_full_dhn.log 2>&1
 for c in mag arxiv arxiv_l2w hyper dhn; do
   ncu -i /tmp/ncu/prof_$c.ncu-rep --page raw --csv > $O/prof_${c}_raw.csv 2>&1

@@ -46,12 +46,28 @@ if want("lja"):
     qs = rnn.make_query("src", "softmax", src=z, src_key=K, dst=Q, heads=8, scale=0.25)
     o, lse = rnn.join_aggregate_fwd(gi, qs)
     rnn.join_aggregate_bwd(gi, qs, o.contiguous(), out=o, lse=lse)
+    # union store fused into the softmax walker, accumulating query gradient (round 2)
+    acc = torch.zeros(gi.n_groups, 128, device="cuda")
+    o2 = torch.empty(gi.n_groups, 128, device="cuda")
+    o2, lse2 = rnn.join_aggregate_fwd_union(gi, qs, o2, acc, beta_acc=1.0)
+    import ctypes as C
+    dq = torch.zeros(200, 128, device="cuda")
+    dO = o2.contiguous()
+    _, bb = rnn.lja_workspace_size(gi, qs)
+    wsb = torch.empty(bb, dtype=torch.uint8, device="cuda")
+    rnn._check(rnn.lib().rnn_join_aggregate_bwd_acc(
+        C.byref(gi.c), C.byref(qs), rnn._ptr(o2), o2.stride(0), rnn._ptr(lse2), rnn._ptr(dO),
+        dO.stride(0), None, None, None, rnn._ptr(dq), 1.0, rnn._ptr(wsb), wsb.numel(),
+        rnn._stream()))
 for prec in (("tf32", "3xtf32") if want("proj") else ()):
     for (M, Kd, N) in [(1000, 128, 128), (700, 64, 384), (300, 200, 48)]:
         X = cu(rng.standard_normal((M, Kd)).astype(np.float32))
         W = cu(rng.standard_normal((N, Kd)).astype(np.float32))
         Y = rnn.project(X, W, prec=prec)
         rnn.project_bwd(X, W, Y.contiguous(), prec=prec)
+        if Kd % 4 == 0:   # the fused ReLU-input epilogue (mask + bias column sums)
+            rnn.project_bwd(X.relu(), W, Y.contiguous(), prec=prec, relu_in=True,
+                            d_in_bias=torch.empty(Kd, device="cuda"))
 # DHN: SANITIZE_DHN_N nodes (racecheck instruments every shared-memory hash probe of the
 # 1,024-thread root CTAs: a smaller graph keeps it within minutes), SANITIZE_DHN_K = one k
 NV = int(os.environ.get("SANITIZE_DHN_N", "120"))
