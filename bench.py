@@ -336,7 +336,8 @@ def run_ours(args):
             if not args.no_e2e:
                 first["e2e"] = run_e2e(prog, args, world, dev, rows, replay)
             first["meta"] = {k: getattr(prog, k) for k in ("L", "dims") if hasattr(prog, k)}
-            if hasattr(prog, "setup_training") and prog._labels is not None and not sharded:
+            if (hasattr(prog, "setup_training") and prog._labels is not None and not sharded
+                    and not args.l2_window):   # (the window is a stream attribute: no capture)
                 first["train"] = run_train(prog, args)
             first["prog"] = None
         del prog, replay

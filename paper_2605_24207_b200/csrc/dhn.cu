@@ -560,6 +560,7 @@ struct H4Root {
   uint32_t P, part;
   int sh;
   bool cur_ok, chunked;
+  uint32_t cmask = H4_CAP - 1;   // slot walk: table size - 1 for this root
 };
 
 // slot walk: the first H4_PRE neighbours of each side are read once per root, lane-parallel,
@@ -899,22 +900,26 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
 #define H4S_INFLIGHT 4   // IN sweep: hits per lane group in flight per round (x4 per warp)
 #endif
 __device__ __forceinline__ uint32_t h4s_hash(int32_t w) { return dhn_hash((uint32_t)w ^ 0x5bd1e995u); }
-__device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w) {
-  uint32_t s = H & (uint32_t)(H4_CAP - 1);
-  for (int t = 0; t < H4_CAP; ++t) {
+// cmask = table size - 1 of this root: a single-partition root (at most H4_PART keys) uses
+// the first next_pow2(2 x its out-wedge count) slots, so its value rows are a short prefix of
+// the slab that stays L2-hot from root to root (slot rows scattered over the whole 2 MB slab
+// doubled the walk's DRAM traffic, ncu); multi-partition roots use the full table
+__device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w, uint32_t cmask) {
+  uint32_t s = H & cmask;
+  for (uint32_t t = 0; t <= cmask; ++t) {
     const int prev = atomicCAS(&keys[s], -1, w);
     if (prev == -1 || prev == w) return (int)s;
-    s = (s + 1) & (uint32_t)(H4_CAP - 1);
+    s = (s + 1) & cmask;
   }
   return -1;
 }
-__device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w) {
-  uint32_t s = H & (uint32_t)(H4_CAP - 1);
-  for (int t = 0; t < H4_CAP; ++t) {
+__device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w, uint32_t cmask) {
+  uint32_t s = H & cmask;
+  for (uint32_t t = 0; t <= cmask; ++t) {
     const int k = keys[s];
     if (k == w) return (int)s;
     if (k == -1) return -1;
-    s = (s + 1) & (uint32_t)(H4_CAP - 1);
+    s = (s + 1) & cmask;
   }
   return -1;
 }
@@ -925,10 +930,11 @@ __device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w) {
 template <bool OUT, bool DUAL>
 __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32_t H, bool in,
                                           int cnt, const float4& fv4, float4& t4, float4& t4b,
-                                          int lane, const float* F2q, const float* F2bq, int d) {
+                                          int lane, const float* F2q, const float* F2bq, int d,
+                                          uint32_t cmask) {
   const int sub = lane >> 3, cq = lane & 7;
   if (OUT) {
-    const int sl = (in && w >= 0) ? h4s_insert(keys, H, w) : -1;
+    const int sl = (in && w >= 0) ? h4s_insert(keys, H, w, cmask) : -1;
     if (in && w >= 0 && sl < 0) atomicAdd(&g_dhn_paths[8], 1ull);   // table full (tests: 0)
     for (int q0 = 0; q0 < cnt; q0 += 4) {
       const int q = q0 + sub;
@@ -939,7 +945,7 @@ __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32
                      : "memory");
     }
   } else {
-    const int sl = (in && w >= 0) ? h4s_find(keys, H, w) : -1;
+    const int sl = (in && w >= 0) ? h4s_find(keys, H, w, cmask) : -1;
     // (the dual-middle walk keeps 2 in flight: a third operand row per hit spills at 4)
     constexpr int NF = DUAL ? 2 : H4S_INFLIGHT;
     for (int q0 = 0; q0 < cnt; q0 += 4 * NF) {
@@ -1058,8 +1064,9 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
         const bool inb = tb < ej && in_part(Hb);
         const unsigned ma = __ballot_sync(FULL, ina), mb = __ballot_sync(FULL, inb);
         const int ca = __popc(ma), cb = __popc(mb);
-        h4s_chunk<OUT, DUAL>(keys, S, wa, Ha, ina, ca, fv4, t4, t4b, lane, F2q, F2bq, d);
-        if (cb) h4s_chunk<OUT, DUAL>(keys, S, wb, Hb, inb, cb, fv4, t4, t4b, lane, F2q, F2bq, d);
+        h4s_chunk<OUT, DUAL>(keys, S, wa, Ha, ina, ca, fv4, t4, t4b, lane, F2q, F2bq, d, R.cmask);
+        if (cb)
+          h4s_chunk<OUT, DUAL>(keys, S, wb, Hb, inb, cb, fv4, t4, t4b, lane, F2q, F2bq, d, R.cmask);
         t0 += ca + cb;
         if (mb != FULL) break;
       }
@@ -1106,7 +1113,8 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
       const int32_t w = tt < qe ? L[tt] : -1;
       const bool in = tt < qe;
       const int cnt = __popc(__ballot_sync(FULL, in));
-      h4s_chunk<OUT, DUAL>(keys, S, w, h4s_hash(w), in, cnt, fv4, t4, t4b, lane, F2q, F2bq, d);
+      h4s_chunk<OUT, DUAL>(keys, S, w, h4s_hash(w), in, cnt, fv4, t4, t4b, lane, F2q, F2bq, d,
+                           R.cmask);
     }
   }
   __syncthreads();
@@ -1153,6 +1161,11 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
     H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
     R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
     c_multi += R.P > 1;
+    if (R.P == 1) {   // <= bound distinct keys: 2 x bound slots (load <= 1/2) suffice
+      uint32_t c = 64;
+      while (c < H4_CAP && (int64_t)c < 2 * bound) c <<= 1;
+      R.cmask = c - 1;
+    }
     // neighbour metadata of both sides, lane-parallel (read by every partition pass)
     for (int i = threadIdx.x; i < (deg_out < H4_PRE ? deg_out : H4_PRE); i += H4_THREADS) {
       const int32_t u = a.nbr[pb + i];
@@ -1188,7 +1201,7 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
                                                  &grab, c0, s_cnt, &acc_b, pre_in));
         // clear the occupied rows and slots for the next partition / root (the sweeps ended
         // with a barrier, so no lane still reads the table)
-        for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) {
+        for (int i = threadIdx.x; i <= (int)R.cmask; i += H4_THREADS) {
           if (keys[i] != -1) {
             float4* row = reinterpret_cast<float4*>(S + (int64_t)i * 32);
 #pragma unroll

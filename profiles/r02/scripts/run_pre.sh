@@ -16,3 +16,12 @@ for k in 3 4; do
 done
 CUDA_MODULE_LOADING=EAGER timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python profiles/r02/scripts/sanitize_tiny.py > $O/memcheck.log 2>&1; echo "exit $?" >> $O/memcheck.log
 SANITIZE_PART=dhn SANITIZE_DHN_N=60 timeout 900 compute-sanitizer --tool synccheck --print-limit 20 python profiles/r02/scripts/sanitize_tiny.py > $O/synccheck_dhn.log 2>&1; echo "exit $?" >> $O/synccheck_dhn.log
+timeout 900 python bench.py --config arxiv --l2-window --no-cpu-baseline --no-e2e > $O/bench_arxiv_l2w.json 2> $O/bench_arxiv_l2w.err
+timeout 900 ncu --set full --clock-control none -k regex:'lean_kernel' -c 6 -o $O/prof_arxiv_l2w -f \
+  python bench.py --config arxiv --l2-window --steps 1 --warmup 1 --seeds 42 --no-e2e --no-cpu-baseline > $O/ncu_l2w.log 2>&1
+ncu -i $O/prof_arxiv_l2w.ncu-rep --page raw --csv > $O/prof_arxiv_l2w_raw.csv 2>&1
+rm -f $O/prof_arxiv_l2w.ncu-rep
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:'dhn4s_kernel' -c 1 -o $O/prof_dhn4s -f \
+  python bench.py --config dhn --dhn-scale 0.03 --steps 1 --warmup 0 --seeds 42 --no-cpu-baseline --no-e2e --eager > $O/ncu_dhn4s.log 2>&1
+ncu -i $O/prof_dhn4s.ncu-rep --page raw --csv > $O/prof_dhn4s_raw.csv 2>&1
+rm -f $O/prof_dhn4s.ncu-rep
