@@ -72,6 +72,9 @@ struct DhnArgs {
   const float* F1b;       // k=3, optional second first-hop operand (symmetric Edge)
   float* out_b;           // its result (same layout as out, no root multiplier)
   int part_keys;          // k=4 slot-indexed walk: target distinct keys per partition (0: H4_PART)
+  int pre_n;              // k=4 slot walk: neighbours prefetched per side (<= H4_PRE)
+  int probe_part;         // k=4 slot walk: probe L[b0] for the partition before a run (1)
+  int full_table;         // k=4 slot walk: every root uses all H4_CAP slots (0: sized per root)
 };
 
 __device__ __forceinline__ void dhn_store(const DhnArgs& a, int64_t n, int c, float v) {
@@ -1008,7 +1011,7 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
     int64_t b0 = 0, e0 = 0, s0 = 0;
     bool has = false;
     if (i < R.deg && (R.chunked || lane == 0)) {
-      if (i < H4_PRE) {   // neighbour and list extent prefetched at root setup (shared memory)
+      if (i < a.pre_n) {   // neighbour and list extent prefetched at root setup (shared memory)
         u = pre.u[i];
         s0 = pre.s[i];
         e0 = s0 + pre.len[i];
@@ -1023,9 +1026,9 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
       }
       if (u >= 0) {
         b0 = R.cur_ok ? s0 + cur[i] : h4_lower(L, s0, e0, R.part, R.sh);
-        // (no probe of L[b0] for the partition: a run with no entry in this partition ends
-        // at its first chunk -- one dependent global load less per neighbour)
-        has = b0 < e0;
+        // probe_part = 0: no load of L[b0] for the partition (a run with no entry in this
+        // partition then ends at its first chunk, but a long one pays the run-end search)
+        has = b0 < e0 && (!a.probe_part || (h4_top(L[b0]) >> R.sh) == R.part);
       }
     }
     unsigned hb = __ballot_sync(FULL, has);
@@ -1161,20 +1164,20 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
     H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
     R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
     c_multi += R.P > 1;
-    if (R.P == 1) {   // <= bound distinct keys: 2 x bound slots (load <= 1/2) suffice
+    if (R.P == 1 && !a.full_table) {   // <= bound distinct keys: 2 x bound slots suffice
       uint32_t c = 64;
       while (c < H4_CAP && (int64_t)c < 2 * bound) c <<= 1;
       R.cmask = c - 1;
     }
     // neighbour metadata of both sides, lane-parallel (read by every partition pass)
-    for (int i = threadIdx.x; i < (deg_out < H4_PRE ? deg_out : H4_PRE); i += H4_THREADS) {
+    for (int i = threadIdx.x; i < (deg_out < a.pre_n ? deg_out : a.pre_n); i += H4_THREADS) {
       const int32_t u = a.nbr[pb + i];
       pre_u[i] = u;
       const int64_t b = u >= 0 ? a.gp[u] : 0;
       pre_s[i] = b;
       pre_l[i] = u >= 0 ? (int32_t)(a.gp[u + 1] - b) : 0;
     }
-    for (int i = threadIdx.x; i < (deg_in < H4_PRE ? deg_in : H4_PRE); i += H4_THREADS) {
+    for (int i = threadIdx.x; i < (deg_in < a.pre_n ? deg_in : a.pre_n); i += H4_THREADS) {
       const int32_t u = a.sg[ib + i];
       const int32_t ru = a.row_of[u];
       const int64_t b = a.sp[ru];
@@ -1646,6 +1649,10 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     if (v4 && !compact) {
       static const int part_keys = getenv("RNN_DHN_PART_KEYS") ? atoi(getenv("RNN_DHN_PART_KEYS")) : 0;
       a.part_keys = std::min(part_keys, H4_PART);
+      // measurement switches (read per launch): neighbour prefetch off, partition probe off
+      a.pre_n = getenv("RNN_DHN_NO_PREFETCH") ? 0 : H4_PRE;
+      a.probe_part = getenv("RNN_DHN_NO_PROBE") ? 0 : 1;
+      a.full_table = getenv("RNN_DHN_FULL_TABLE") ? 1 : 0;
       const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4_DEG_CAP * sizeof(int) +
                             H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) +
