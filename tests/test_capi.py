@@ -86,3 +86,22 @@ def test_dhn_saved_entry_points_host_checks(lib):
                                C.c_uint32(2), None, 0, None)
     assert st == 1 and b"flags" in lib.rnn_last_error()
     assert lib.rnn_dhn_bwd_saved.argtypes is not None
+
+
+def test_union_entry_points_host_checks(lib):
+    """rnn_join_aggregate_fwd_union / rnn_join_aggregate_bwd_acc reject a beta outside {0, 1}
+    and a MEAN union before any device work."""
+    from paper_2605_24207_b200 import rnn
+    idx = rnn.JoinIndexC()
+    q = rnn.QueryC()
+    v = C.c_void_p(16)
+    assert lib.rnn_join_aggregate_fwd_union(C.byref(idx), C.byref(q), v, 128, v, v, 128,
+                                            C.c_float(0.5), None, 0, None) == 1
+    assert b"beta_acc" in lib.rnn_last_error()
+    q.agg = rnn.AGG["mean"]
+    assert lib.rnn_join_aggregate_fwd_union(C.byref(idx), C.byref(q), v, 128, v, v, 128,
+                                            C.c_float(1.0), None, 0, None) != 0
+    assert b"MEAN" in lib.rnn_last_error() or b"decomposable" in lib.rnn_last_error()
+    assert lib.rnn_join_aggregate_bwd_acc(C.byref(idx), C.byref(q), None, 0, None, v, 128, None,
+                                          None, None, v, C.c_float(2.0), None, 0, None) == 1
+    assert b"beta_dst" in lib.rnn_last_error()
