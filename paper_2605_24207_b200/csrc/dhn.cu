@@ -1136,10 +1136,11 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
   int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
   int64_t* q_e = q_b + H4_LONG_MAX;
   int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
-  int64_t* pre_s = reinterpret_cast<int64_t*>(q_i + H4_LONG_MAX);  // [2][H4_PRE]
-  int32_t* pre_u = reinterpret_cast<int32_t*>(pre_s + 2 * H4_PRE);  // [2][H4_PRE]
-  int32_t* pre_l = pre_u + 2 * H4_PRE;                              // [2][H4_PRE]
-  const H4Pre pre_out{pre_u, pre_s, pre_l}, pre_in{pre_u + H4_PRE, pre_s + H4_PRE, pre_l + H4_PRE};
+  const int npre = a.pre_n;                                         // 0 or H4_PRE
+  int64_t* pre_s = reinterpret_cast<int64_t*>(q_i + H4_LONG_MAX);  // [2][npre]
+  int32_t* pre_u = reinterpret_cast<int32_t*>(pre_s + 2 * npre);    // [2][npre]
+  int32_t* pre_l = pre_u + 2 * npre;                                // [2][npre]
+  const H4Pre pre_out{pre_u, pre_s, pre_l}, pre_in{pre_u + npre, pre_s + npre, pre_l + npre};
   float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;          // [H4_CAP][32], zero
   __shared__ int s_root, q_n, grab;
   __shared__ int s_cnt[2];
@@ -1181,9 +1182,9 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
       const int32_t u = a.sg[ib + i];
       const int32_t ru = a.row_of[u];
       const int64_t b = a.sp[ru];
-      pre_u[H4_PRE + i] = u;
-      pre_s[H4_PRE + i] = b;
-      pre_l[H4_PRE + i] = (int32_t)(a.sp[ru + 1] - b);
+      pre_u[npre + i] = u;
+      pre_s[npre + i] = b;
+      pre_l[npre + i] = (int32_t)(a.sp[ru + 1] - b);
     }
     for (int c0 = 0; c0 < d; c0 += 32) {
       float4 acc = f4_zero(), acc_b = f4_zero();
@@ -1649,14 +1650,16 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     if (v4 && !compact) {
       static const int part_keys = getenv("RNN_DHN_PART_KEYS") ? atoi(getenv("RNN_DHN_PART_KEYS")) : 0;
       a.part_keys = std::min(part_keys, H4_PART);
-      // measurement switches (read per launch): neighbour prefetch off, partition probe off
-      a.pre_n = getenv("RNN_DHN_NO_PREFETCH") ? 0 : H4_PRE;
+      // measurement switches (read per launch): neighbour prefetch ON (its 64 KB of shared
+      // memory cost L1 capacity: 0.1-scale C4 fwd 273 -> 294 ms, profiles/r02/c4ab), partition
+      // probe off
+      a.pre_n = getenv("RNN_DHN_PREFETCH") ? H4_PRE : 0;
       a.probe_part = getenv("RNN_DHN_NO_PROBE") ? 0 : 1;
       a.full_table = getenv("RNN_DHN_FULL_TABLE") ? 1 : 0;
       const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4_DEG_CAP * sizeof(int) +
                             H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) +
-                            2 * H4_PRE * (sizeof(int64_t) + 2 * sizeof(int32_t));
+                            2 * (size_t)a.pre_n * (sizeof(int64_t) + 2 * sizeof(int32_t));
       auto kern = F2b ? dhn4s_kernel<true> : dhn4s_kernel<false>;
       RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
       kern<<<P.n_cta, H4_THREADS, smem_s, st>>>(a);
