@@ -1652,9 +1652,9 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
       a.part_keys = std::min(part_keys, H4_PART);
       // measurement switches (read per launch): neighbour prefetch ON (its 64 KB of shared
       // memory cost L1 capacity: 0.1-scale C4 fwd 273 -> 294 ms, profiles/r02/c4ab), partition
-      // probe off
+      // probe ON
       a.pre_n = getenv("RNN_DHN_PREFETCH") ? H4_PRE : 0;
-      a.probe_part = getenv("RNN_DHN_NO_PROBE") ? 0 : 1;
+      a.probe_part = getenv("RNN_DHN_PROBE") ? 1 : 0;   // off: 282 -> 276 ms (c4ab2)
       a.full_table = getenv("RNN_DHN_FULL_TABLE") ? 1 : 0;
       const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4_DEG_CAP * sizeof(int) +
