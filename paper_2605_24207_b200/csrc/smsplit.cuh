@@ -145,6 +145,11 @@ rnn_status launch_st_var(const Pol& pol, RSCtx cx, cudaStream_t st, int which) {
   if (U == 3 && B == 4) return launch_st<Pol, 3, 4>(pol, cx, st);
   if (U == 4 && B == 4) return launch_st<Pol, 4, 4>(pol, cx, st);
   if (U == 8 && B == 4) return launch_st<Pol, 8, 4>(pol, cx, st);
+  // more resident CTAs than 4 (256 threads each): fewer registers per thread
+  if (U == 4 && B == 6) return launch_st<Pol, 4, 6>(pol, cx, st);
+  if (U == 4 && B == 8) return launch_st<Pol, 4, 8>(pol, cx, st);
+  if (U == 2 && B == 6) return launch_st<Pol, 2, 6>(pol, cx, st);
+  if (U == 1 && B == 6) return launch_st<Pol, 1, 6>(pol, cx, st);
   return launch_st<Pol, 4, 3>(pol, cx, st);
 }
 

@@ -1,0 +1,7 @@
+# softmax walkers at 6 / 8 resident CTAs per SM (fewer registers per thread)
+set -u
+O=gpurun_out/r02_stvar2; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+for v in 4,3,1,4,4,4 4,3,1,4,4,6 4,3,1,4,2,6 4,3,1,4,4,8 4,3,1,6,4,4 4,3,2,6,4,4 2,6,1,4,4,4 4,6,1,4,4,4; do
+  RNN_ST_VAR=$v timeout 600 python bench.py --seeds 42 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/mag_$v.json 2> $O/mag_$v.err
+done
