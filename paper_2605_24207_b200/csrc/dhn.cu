@@ -904,9 +904,10 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
 #endif
 __device__ __forceinline__ uint32_t h4s_hash(int32_t w) { return dhn_hash((uint32_t)w ^ 0x5bd1e995u); }
 // cmask = table size - 1 of this root: a single-partition root (at most H4_PART keys) uses
-// the first next_pow2(2 x its out-wedge count) slots, so its value rows are a short prefix of
-// the slab that stays L2-hot from root to root (slot rows scattered over the whole 2 MB slab
-// doubled the walk's DRAM traffic, ncu); multi-partition roots use the full table
+// the first next_pow2(2 x its out-wedge count) slots (value rows a short prefix of the slab,
+// clears scan only those slots); multi-partition roots use the full table.  Measured neutral
+// against the full table for every root (0.1-scale C4 fwd 276.1 vs 275.5 ms, profiles/r02/c4ab3:
+// the slab's DRAM traffic comes from the big roots); RNN_DHN_FULL_TABLE=1 switches it off
 __device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w, uint32_t cmask) {
   uint32_t s = H & cmask;
   for (uint32_t t = 0; t <= cmask; ++t) {
