@@ -150,6 +150,10 @@ rnn_status launch_st_var(const Pol& pol, RSCtx cx, cudaStream_t st, int which) {
   if (U == 4 && B == 8) return launch_st<Pol, 4, 8>(pol, cx, st);
   if (U == 2 && B == 6) return launch_st<Pol, 2, 6>(pol, cx, st);
   if (U == 1 && B == 6) return launch_st<Pol, 1, 6>(pol, cx, st);
+  if (U == 2 && B == 8) return launch_st<Pol, 2, 8>(pol, cx, st);
+  if (U == 3 && B == 6) return launch_st<Pol, 3, 6>(pol, cx, st);
+  if (U == 1 && B == 8) return launch_st<Pol, 1, 8>(pol, cx, st);
+  if (U == 2 && B == 5) return launch_st<Pol, 2, 5>(pol, cx, st);
   return launch_st<Pol, 4, 3>(pol, cx, st);
 }
 
