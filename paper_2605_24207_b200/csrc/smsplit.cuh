@@ -127,7 +127,9 @@ rnn_status launch_st(const Pol& pol, RSCtx cx, cudaStream_t st) {
 struct StVar { int u[3], b[3]; };
 inline StVar st_var() {
   static StVar v = [] {
-    StVar r{{4, 1, 4}, {3, 4, 4}};   // measured best on MAG (profiles/r01/st_var, sm_src)
+    // measured best on MAG (profiles/r01/st_var, sm_src; round 2 profiles/r02/stvar: pass B
+    // at 2 rows x 6 CTAs/SM, lja_bwd 2.69 -> 2.59 ms per relation, step 20.34 -> 19.96 ms)
+    StVar r{{4, 1, 2}, {3, 4, 6}};
     if (const char* e = getenv("RNN_ST_VAR"))
       sscanf(e, "%d,%d,%d,%d,%d,%d", &r.u[0], &r.b[0], &r.u[1], &r.b[1], &r.u[2], &r.b[2]);
     return r;
