@@ -56,7 +56,10 @@ typedef enum {
   RNN_OK = 0,
   RNN_ERR_INVALID_ARGUMENT = 1,   /* null/misaligned pointer, bad size or flag            */
   RNN_ERR_SHAPE_MISMATCH = 2,     /* operand widths inconsistent      */
-  RNN_ERR_INDEX_OUT_OF_RANGE = 3, /* device-side validation found an index out of range  */
+  RNN_ERR_INDEX_OUT_OF_RANGE = 3, /* reserved: no entry point returns it in this build --
+                                    * the join index is built here (in range by construction),
+                                    * DHN root lists are filtered (out-of-range ids ignored),
+                                    * gather / scatter row lists are the caller's contract     */
   RNN_ERR_DUPLICATE_KEY = 4,      /* S or T is not a set                   */
   RNN_ERR_UNSUPPORTED = 5,        /* valid request outside this build's limits            */
   RNN_ERR_WORKSPACE_TOO_SMALL = 6,
