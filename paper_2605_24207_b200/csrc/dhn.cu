@@ -906,8 +906,9 @@ __device__ __forceinline__ uint32_t h4s_hash(int32_t w) { return dhn_hash((uint3
 // cmask = table size - 1 of this root: a single-partition root (at most H4_PART keys) uses
 // the first next_pow2(2 x its out-wedge count) slots (value rows a short prefix of the slab,
 // clears scan only those slots); multi-partition roots use the full table.  Measured neutral
-// against the full table for every root (0.1-scale C4 fwd 276.1 vs 275.5 ms, profiles/r02/c4ab3:
-// the slab's DRAM traffic comes from the big roots); RNN_DHN_FULL_TABLE=1 switches it off
+// against the full table for every root at 0.1 scale (276.1 vs 275.5 ms, profiles/r02/c4ab3)
+// and ~5 % slower on the full products graph (C4 fwd 3,458 -> 3,642 ms): opt-in through
+// RNN_DHN_ROOT_TABLE=1
 __device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w, uint32_t cmask) {
   uint32_t s = H & cmask;
   for (uint32_t t = 0; t <= cmask; ++t) {
@@ -1656,7 +1657,7 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
       // probe ON
       a.pre_n = getenv("RNN_DHN_PREFETCH") ? H4_PRE : 0;
       a.probe_part = getenv("RNN_DHN_PROBE") ? 1 : 0;   // off: 282 -> 276 ms (c4ab2)
-      a.full_table = getenv("RNN_DHN_FULL_TABLE") ? 1 : 0;
+      a.full_table = getenv("RNN_DHN_ROOT_TABLE") ? 0 : 1;   // per-root sizing: opt-in
       const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4_DEG_CAP * sizeof(int) +
                             H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) +
