@@ -72,9 +72,6 @@ struct DhnArgs {
   const float* F1b;       // k=3, optional second first-hop operand (symmetric Edge)
   float* out_b;           // its result (same layout as out, no root multiplier)
   int part_keys;          // k=4 slot-indexed walk: target distinct keys per partition (0: H4_PART)
-  int pre_n;              // k=4 slot walk: neighbours prefetched per side (<= H4_PRE)
-  int probe_part;         // k=4 slot walk: probe L[b0] for the partition before a run (1)
-  int full_table;         // k=4 slot walk: every root uses all H4_CAP slots (0: sized per root)
 };
 
 __device__ __forceinline__ void dhn_store(const DhnArgs& a, int64_t n, int c, float v) {
@@ -142,8 +139,7 @@ __device__ __forceinline__ int hs_find(const int* keys, int cap_mask, int w) {
 constexpr int H3_CAP = H3_CAP_CFG;           // slots (keys + counts: 64 KB at 8,192)
 constexpr int H3_MAX_INDEG = H3_CAP / 4 * 3; // load factor <= 0.75
 constexpr int H3_LONG = 256;                 // N(v) longer than this: split over all warps
-constexpr int H3_QMAX = 128;                 // long lists queued per root (overflow: inline)
-constexpr int H3_PRE = 256;                  // neighbours whose list extents are prefetched
+constexpr int H3_QMAX = 256;                 // long lists queued per root (overflow: inline)
 
 template <int DPL, bool DUAL = false>
 __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnArgs a) {
@@ -157,9 +153,6 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
   int32_t* q_v = reinterpret_cast<int32_t*>(q_e + H3_QMAX);
   int32_t* q_i = q_v + H3_QMAX;     // neighbour index of each queued list
   int32_t* q_ord = q_i + H3_QMAX;   // queue slots in neighbour order
-  int64_t* p_b = reinterpret_cast<int64_t*>(q_ord + H3_QMAX);     // [H3_PRE] list start of N(v)
-  int32_t* p_v = reinterpret_cast<int32_t*>(p_b + H3_PRE);        // [H3_PRE] neighbour v
-  int32_t* p_l = p_v + H3_PRE;                                      // [H3_PRE] |N(v)|
   __shared__ int s_root, s_qn;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* mark = a.mark + (int64_t)blockIdx.x * a.cta_stride;
@@ -183,16 +176,6 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
       }
     } else {
       for (int64_t q = ib + threadIdx.x; q < ie; q += DHN_THREADS) atomicAdd(&mark[a.sg[q]], 1);
-    }
-    {   // the first H3_PRE neighbours' list extents, lane-parallel (one latency chain per root)
-      const int64_t pb0 = a.gp[n], np = a.gp[n + 1] - pb0 < H3_PRE ? a.gp[n + 1] - pb0 : H3_PRE;
-      for (int64_t i = threadIdx.x; i < np; i += DHN_THREADS) {
-        const int32_t v = a.nbr[pb0 + i];
-        const int64_t b = v >= 0 ? a.gp[v] : 0;
-        p_v[i] = v;
-        p_b[i] = b;
-        p_l[i] = v >= 0 ? (int32_t)(a.gp[v + 1] - b) : 0;
-      }
     }
     __syncthreads();
     float acc[DPL], acc_b[DPL];
@@ -263,16 +246,9 @@ __global__ void __launch_bounds__(DHN_THREADS, DHN_CTAS_PER_SM) dhn3_kernel(DhnA
     // phase A: neighbour i goes to warp i % WARPS (a fixed order per warp: the walk is
     // deterministic); lists longer than H3_LONG are queued instead
     for (int64_t i = warp; pb + i < pe; i += DHN_WARPS) {
-      int32_t v;
-      int64_t vb, ve;
-      if (i < H3_PRE) {
-        v = p_v[i]; vb = p_b[i]; ve = vb + p_l[i];
-      } else {
-        v = a.nbr[pb + i];
-        vb = v >= 0 ? a.gp[v] : 0;
-        ve = v >= 0 ? a.gp[v + 1] : 0;
-      }
+      const int32_t v = a.nbr[pb + i];
       if (v < 0) continue;
+      const int64_t vb = a.gp[v], ve = a.gp[v + 1];
       if (ve - vb > H3_LONG) {
         int slot = 0;
         if (lane == 0) slot = atomicAdd(&s_qn, 1);
@@ -563,17 +539,6 @@ struct H4Root {
   uint32_t P, part;
   int sh;
   bool cur_ok, chunked;
-  uint32_t cmask = H4_CAP - 1;   // slot walk: table size - 1 for this root
-};
-
-// slot walk: the first H4_PRE neighbours of each side are read once per root, lane-parallel,
-// into shared memory (neighbour, list start, list length), so no partition pass repeats the
-// dependent global loads neighbour -> list extent
-constexpr int H4_PRE = 2048;
-struct H4Pre {
-  const int32_t* u;
-  const int64_t* s;
-  const int32_t* len;
 };
 
 // One side of one partition.  OUT: neighbours v = nbr[pb + i] with lists nbrh over the group
@@ -903,28 +868,22 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4_kernel(DhnArgs a) {
 #define H4S_INFLIGHT 4   // IN sweep: hits per lane group in flight per round (x4 per warp)
 #endif
 __device__ __forceinline__ uint32_t h4s_hash(int32_t w) { return dhn_hash((uint32_t)w ^ 0x5bd1e995u); }
-// cmask = table size - 1 of this root: a single-partition root (at most H4_PART keys) uses
-// the first next_pow2(2 x its out-wedge count) slots (value rows a short prefix of the slab,
-// clears scan only those slots); multi-partition roots use the full table.  Measured neutral
-// against the full table for every root at 0.1 scale (276.1 vs 275.5 ms, profiles/r02/c4ab3)
-// and ~5 % slower on the full products graph (C4 fwd 3,458 -> 3,642 ms): opt-in through
-// RNN_DHN_ROOT_TABLE=1
-__device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w, uint32_t cmask) {
-  uint32_t s = H & cmask;
-  for (uint32_t t = 0; t <= cmask; ++t) {
+__device__ __forceinline__ int h4s_insert(int* keys, uint32_t H, int w) {
+  uint32_t s = H & (uint32_t)(H4_CAP - 1);
+  for (int t = 0; t < H4_CAP; ++t) {
     const int prev = atomicCAS(&keys[s], -1, w);
     if (prev == -1 || prev == w) return (int)s;
-    s = (s + 1) & cmask;
+    s = (s + 1) & (uint32_t)(H4_CAP - 1);
   }
   return -1;
 }
-__device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w, uint32_t cmask) {
-  uint32_t s = H & cmask;
-  for (uint32_t t = 0; t <= cmask; ++t) {
+__device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w) {
+  uint32_t s = H & (uint32_t)(H4_CAP - 1);
+  for (int t = 0; t < H4_CAP; ++t) {
     const int k = keys[s];
     if (k == w) return (int)s;
     if (k == -1) return -1;
-    s = (s + 1) & cmask;
+    s = (s + 1) & (uint32_t)(H4_CAP - 1);
   }
   return -1;
 }
@@ -935,11 +894,10 @@ __device__ __forceinline__ int h4s_find(const int* keys, uint32_t H, int w, uint
 template <bool OUT, bool DUAL>
 __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32_t H, bool in,
                                           int cnt, const float4& fv4, float4& t4, float4& t4b,
-                                          int lane, const float* F2q, const float* F2bq, int d,
-                                          uint32_t cmask) {
+                                          int lane, const float* F2q, const float* F2bq, int d) {
   const int sub = lane >> 3, cq = lane & 7;
   if (OUT) {
-    const int sl = (in && w >= 0) ? h4s_insert(keys, H, w, cmask) : -1;
+    const int sl = (in && w >= 0) ? h4s_insert(keys, H, w) : -1;
     if (in && w >= 0 && sl < 0) atomicAdd(&g_dhn_paths[8], 1ull);   // table full (tests: 0)
     for (int q0 = 0; q0 < cnt; q0 += 4) {
       const int q = q0 + sub;
@@ -950,7 +908,7 @@ __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32
                      : "memory");
     }
   } else {
-    const int sl = (in && w >= 0) ? h4s_find(keys, H, w, cmask) : -1;
+    const int sl = (in && w >= 0) ? h4s_find(keys, H, w) : -1;
     // (the dual-middle walk keeps 2 in flight: a third operand row per hit spills at 4)
     constexpr int NF = DUAL ? 2 : H4S_INFLIGHT;
     for (int q0 = 0; q0 < cnt; q0 += 4 * NF) {
@@ -984,7 +942,7 @@ __device__ __forceinline__ void h4s_chunk(int* keys, float* S, int32_t w, uint32
 template <bool OUT, bool DUAL>
 __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float* S, int* cur,
                             int* q_i, int64_t* q_b, int64_t* q_e, int* q_n, int* grab, int c0,
-                            int* s_cnt, float4* acc_b, const H4Pre& pre) {
+                            int* s_cnt, float4* acc_b) {
   const int lane = threadIdx.x & 31;
   const int32_t* L = OUT ? a.nbrh : a.sgh;
   const float* Fv = OUT ? a.F1 : a.F3;
@@ -1013,11 +971,7 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
     int64_t b0 = 0, e0 = 0, s0 = 0;
     bool has = false;
     if (i < R.deg && (R.chunked || lane == 0)) {
-      if (i < a.pre_n) {   // neighbour and list extent prefetched at root setup (shared memory)
-        u = pre.u[i];
-        s0 = pre.s[i];
-        e0 = s0 + pre.len[i];
-      } else if (OUT) {
+      if (OUT) {
         u = a.nbr[R.pb + i];
         if (u >= 0) { s0 = a.gp[u]; e0 = a.gp[u + 1]; }
       } else {
@@ -1028,9 +982,7 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
       }
       if (u >= 0) {
         b0 = R.cur_ok ? s0 + cur[i] : h4_lower(L, s0, e0, R.part, R.sh);
-        // probe_part = 0: no load of L[b0] for the partition (a run with no entry in this
-        // partition then ends at its first chunk, but a long one pays the run-end search)
-        has = b0 < e0 && (!a.probe_part || (h4_top(L[b0]) >> R.sh) == R.part);
+        has = b0 < e0 && (h4_top(L[b0]) >> R.sh) == R.part;
       }
     }
     unsigned hb = __ballot_sync(FULL, has);
@@ -1069,9 +1021,8 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
         const bool inb = tb < ej && in_part(Hb);
         const unsigned ma = __ballot_sync(FULL, ina), mb = __ballot_sync(FULL, inb);
         const int ca = __popc(ma), cb = __popc(mb);
-        h4s_chunk<OUT, DUAL>(keys, S, wa, Ha, ina, ca, fv4, t4, t4b, lane, F2q, F2bq, d, R.cmask);
-        if (cb)
-          h4s_chunk<OUT, DUAL>(keys, S, wb, Hb, inb, cb, fv4, t4, t4b, lane, F2q, F2bq, d, R.cmask);
+        h4s_chunk<OUT, DUAL>(keys, S, wa, Ha, ina, ca, fv4, t4, t4b, lane, F2q, F2bq, d);
+        if (cb) h4s_chunk<OUT, DUAL>(keys, S, wb, Hb, inb, cb, fv4, t4, t4b, lane, F2q, F2bq, d);
         t0 += ca + cb;
         if (mb != FULL) break;
       }
@@ -1118,8 +1069,7 @@ __device__ float4 h4s_sweep(const DhnArgs& a, const H4Root& R, int* keys, float*
       const int32_t w = tt < qe ? L[tt] : -1;
       const bool in = tt < qe;
       const int cnt = __popc(__ballot_sync(FULL, in));
-      h4s_chunk<OUT, DUAL>(keys, S, w, h4s_hash(w), in, cnt, fv4, t4, t4b, lane, F2q, F2bq, d,
-                           R.cmask);
+      h4s_chunk<OUT, DUAL>(keys, S, w, h4s_hash(w), in, cnt, fv4, t4, t4b, lane, F2q, F2bq, d);
     }
   }
   __syncthreads();
@@ -1138,11 +1088,6 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
   int64_t* q_b = reinterpret_cast<int64_t*>(cur_in + H4_DEG_CAP);  // [H4_LONG_MAX]
   int64_t* q_e = q_b + H4_LONG_MAX;
   int* q_i = reinterpret_cast<int*>(q_e + H4_LONG_MAX);
-  const int npre = a.pre_n;                                         // 0 or H4_PRE
-  int64_t* pre_s = reinterpret_cast<int64_t*>(q_i + H4_LONG_MAX);  // [2][npre]
-  int32_t* pre_u = reinterpret_cast<int32_t*>(pre_s + 2 * npre);    // [2][npre]
-  int32_t* pre_l = pre_u + 2 * npre;                                // [2][npre]
-  const H4Pre pre_out{pre_u, pre_s, pre_l}, pre_in{pre_u + npre, pre_s + npre, pre_l + npre};
   float* S = a.slab + (int64_t)blockIdx.x * a.cta_stride;          // [H4_CAP][32], zero
   __shared__ int s_root, q_n, grab;
   __shared__ int s_cnt[2];
@@ -1167,27 +1112,6 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
     H4Root R{n, ib, pb, 0, 1u << bits, 0, H4_HBITS - bits, cur_ok, false};
     R.chunked = (int64_t)R.P * deg_out > (int64_t)a.wout[n];
     c_multi += R.P > 1;
-    if (R.P == 1 && !a.full_table) {   // <= bound distinct keys: 2 x bound slots suffice
-      uint32_t c = 64;
-      while (c < H4_CAP && (int64_t)c < 2 * bound) c <<= 1;
-      R.cmask = c - 1;
-    }
-    // neighbour metadata of both sides, lane-parallel (read by every partition pass)
-    for (int i = threadIdx.x; i < (deg_out < a.pre_n ? deg_out : a.pre_n); i += H4_THREADS) {
-      const int32_t u = a.nbr[pb + i];
-      pre_u[i] = u;
-      const int64_t b = u >= 0 ? a.gp[u] : 0;
-      pre_s[i] = b;
-      pre_l[i] = u >= 0 ? (int32_t)(a.gp[u + 1] - b) : 0;
-    }
-    for (int i = threadIdx.x; i < (deg_in < a.pre_n ? deg_in : a.pre_n); i += H4_THREADS) {
-      const int32_t u = a.sg[ib + i];
-      const int32_t ru = a.row_of[u];
-      const int64_t b = a.sp[ru];
-      pre_u[npre + i] = u;
-      pre_s[npre + i] = b;
-      pre_l[npre + i] = (int32_t)(a.sp[ru + 1] - b);
-    }
     for (int c0 = 0; c0 < d; c0 += 32) {
       float4 acc = f4_zero(), acc_b = f4_zero();
       if (cur_ok) {
@@ -1201,13 +1125,13 @@ __global__ void __launch_bounds__(H4_THREADS, H4_CTAS) dhn4s_kernel(DhnArgs a) {
         c_chunked += R.chunked;
         R.deg = deg_out;
         h4s_sweep<true, false>(a, R, keys, S, cur_out, q_i, q_b, q_e, &q_n, &grab, c0, s_cnt,
-                               nullptr, pre_out);
+                               nullptr);
         R.deg = deg_in;
         acc = f4_add(acc, h4s_sweep<false, DUAL>(a, R, keys, S, cur_in, q_i, q_b, q_e, &q_n,
-                                                 &grab, c0, s_cnt, &acc_b, pre_in));
+                                                 &grab, c0, s_cnt, &acc_b));
         // clear the occupied rows and slots for the next partition / root (the sweeps ended
         // with a barrier, so no lane still reads the table)
-        for (int i = threadIdx.x; i <= (int)R.cmask; i += H4_THREADS) {
+        for (int i = threadIdx.x; i < H4_CAP; i += H4_THREADS) {
           if (keys[i] != -1) {
             float4* row = reinterpret_cast<float4*>(S + (int64_t)i * 32);
 #pragma unroll
@@ -1612,8 +1536,7 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     const int dpl = (P.d + 31) / 32;
     const size_t smem = (2 * H3_CAP + H3_MAX_INDEG) * sizeof(int) +
                         (size_t)DHN_WARPS * dpl * 32 * sizeof(float) +
-                        H3_QMAX * (2 * sizeof(int64_t) + 3 * sizeof(int32_t)) +
-                        H3_PRE * (sizeof(int64_t) + 2 * sizeof(int32_t));
+                        H3_QMAX * (2 * sizeof(int64_t) + 3 * sizeof(int32_t));
     auto kern = a.F1b ? (dpl == 1 ? dhn3_kernel<1, true> : dpl == 2 ? dhn3_kernel<2, true>
                          : dpl == 3 ? dhn3_kernel<3, true> : dhn3_kernel<4, true>)
                       : (dpl == 1 ? dhn3_kernel<1> : dpl == 2 ? dhn3_kernel<2>
@@ -1652,16 +1575,9 @@ rnn_status walk(const Plan& P, const Bufs& b, const rnn_join_index* adj, const f
     if (v4 && !compact) {
       static const int part_keys = getenv("RNN_DHN_PART_KEYS") ? atoi(getenv("RNN_DHN_PART_KEYS")) : 0;
       a.part_keys = std::min(part_keys, H4_PART);
-      // measurement switches (read per launch): neighbour prefetch ON (its 64 KB of shared
-      // memory cost L1 capacity: 0.1-scale C4 fwd 273 -> 294 ms, profiles/r02/c4ab), partition
-      // probe ON
-      a.pre_n = getenv("RNN_DHN_PREFETCH") ? H4_PRE : 0;
-      a.probe_part = getenv("RNN_DHN_PROBE") ? 1 : 0;   // off: 282 -> 276 ms (c4ab2)
-      a.full_table = getenv("RNN_DHN_ROOT_TABLE") ? 0 : 1;   // per-root sizing: opt-in
       const size_t smem_s = H4_CAP * sizeof(int) + (size_t)H4_WARPS * 32 * sizeof(float) +
                             2 * H4_DEG_CAP * sizeof(int) +
-                            H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int)) +
-                            2 * (size_t)a.pre_n * (sizeof(int64_t) + 2 * sizeof(int32_t));
+                            H4_LONG_MAX * (2 * sizeof(int64_t) + sizeof(int));
       auto kern = F2b ? dhn4s_kernel<true> : dhn4s_kernel<false>;
       RNN_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_s));
       kern<<<P.n_cta, H4_THREADS, smem_s, st>>>(a);
