@@ -150,6 +150,37 @@ __global__ void __launch_bounds__(256) epi_bwd4_kernel(const float* __restrict__
   }
 }
 
+// bias-only backward (act none, no dx / d_resid / d_gate: the GCN's last layer): per-chunk
+// column partials of gate * dy -- lane = float4 column quad, warp w takes rows w, w + 8, ... of
+// the chunk four at a time (independent loads in flight), warps summed in a fixed order
+__global__ void __launch_bounds__(256) epi_colsum4_kernel(const float* __restrict__ dy,
+                                                          int64_t lddy, int64_t rows, int dim,
+                                                          float gate, float* __restrict__ part_b) {
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 128 + 4 * lane;
+  const int64_t r0 = (int64_t)blockIdx.y * EPI_VROWS;
+  const int64_t r1 = r0 + EPI_VROWS < rows ? r0 + EPI_VROWS : rows;
+  float4 a0 = f4_zero(), a1 = f4_zero(), a2 = f4_zero(), a3 = f4_zero();
+  if (c < dim) {
+    int64_t r = r0 + wp;
+    for (; r + 24 < r1; r += 32) {
+      a0 = f4_add(a0, *reinterpret_cast<const float4*>(dy + r * lddy + c));
+      a1 = f4_add(a1, *reinterpret_cast<const float4*>(dy + (r + 8) * lddy + c));
+      a2 = f4_add(a2, *reinterpret_cast<const float4*>(dy + (r + 16) * lddy + c));
+      a3 = f4_add(a3, *reinterpret_cast<const float4*>(dy + (r + 24) * lddy + c));
+    }
+    for (; r < r1; r += 8) a0 = f4_add(a0, *reinterpret_cast<const float4*>(dy + r * lddy + c));
+  }
+  __shared__ float4 sh[8][32];
+  sh[wp][lane] = f4_add(f4_add(a0, a1), f4_add(a2, a3));
+  __syncthreads();
+  if (wp == 0 && c < dim) {
+    float4 t = sh[0][lane];
+    for (int k = 1; k < 8; ++k) t = f4_add(t, sh[k][lane]);
+    *reinterpret_cast<float4*>(part_b + (int64_t)blockIdx.y * dim + c) = f4_scale(gate, t);
+  }
+}
+
 // out[c] = sum over the chunks' partial rows, fixed order: block = 32 columns x 8 chunk lanes,
 // lane j sums chunks j, j + 8, ... with four loads in flight, then the 8 sums in order (one
 // thread per column summing 662 rows serially took 41 us at arxiv size)
@@ -279,7 +310,10 @@ extern "C" rnn_status rnn_epilogue_bwd(const float* dy, int64_t lddy, const floa
   float* part_b = reinterpret_cast<float*>(workspace);
   float* part_g = part_b + chunks * dim;
   dim3 grid((unsigned)slabs, (unsigned)chunks);
-  if (vec)
+  const bool bias_only = vec && d_bias && !dx && !d_resid && !d_gate && epi->act == RNN_ACT_NONE;
+  if (bias_only)
+    epi_colsum4_kernel<<<grid, 256, 0, st>>>(dy, lddy, rows, dim, e.gate, part_b);
+  else if (vec)
     epi_bwd4_kernel<<<grid, 256, 0, st>>>(dy, lddy, y, ldy, rows, dim, e, dx, lddx, d_resid,
                                           ld_dresid, d_bias ? part_b : nullptr,
                                           d_gate ? part_g : nullptr);
