@@ -495,6 +495,9 @@ def test_epilogue_fused_parity(R, ora, D, act, gated):
     if gated:
         assert_close(np_(dres), rdr, FP32_TOL, "d_resid")
         assert abs(float(dgate.item()) - rdg) <= FP32_TOL * max(1.0, abs(rdg))
+    if act == "none" and not gated:   # the bias-only path (no dx): column sums of dy alone
+        _, dbias2, _, _ = R.epilogue_bwd(padded(dy), out, epi, want_dx=False)
+        assert_close(np_(dbias2), rdb, FP32_TOL, "d_bias (bias only)")
 
 
 @pytest.mark.parametrize("D,wmode,dense", [(16, 1, False), (128, 0, True), (7, 1, True),
